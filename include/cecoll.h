@@ -1,0 +1,160 @@
+/*
+ * cecoll — B200-native copy-engine collectives (all-gather, all-to-all).
+ *
+ * Thin C ABI (plain pointers and sizes; streams are cudaStream_t passed as
+ * void*). Every entry point below names the reference interface it replaces
+ * or realises; paths are relative to /root/reference/proj.
+ *
+ * Vocabulary kept from the reference:
+ *   - chunk_bytes is the per-peer chunk s (program.hpp:20-31, README.md:29-30).
+ *   - all-gather: recv holds n*s bytes, rank i's chunk at [i*s, (i+1)*s)
+ *     (compiler.cpp:115-122). all-to-all: send holds n*s bytes, chunk j goes to
+ *     rank j's slot `rank` (compiler.cpp:124-126, 156-157).
+ *   - implementations pcpy / bcst / swap / b2b and their prelaunch_ variants
+ *     (compiler.hpp:12-21); swap is in place (compiler.cpp:207-210, 293).
+ *
+ * Errors are status codes; the reference's std::invalid_argument sites map to
+ * CECOLL_INVALID_ARGUMENT / CECOLL_UNSUPPORTED and its untriggered-poll
+ * deadlock (sim.cpp:227-242) to CECOLL_TIMEOUT.
+ */
+#ifndef CECOLL_H
+#define CECOLL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CECOLL_VERSION 1
+
+typedef enum {
+  CECOLL_SUCCESS = 0,
+  CECOLL_INVALID_ARGUMENT = 1, /* std::invalid_argument (compiler.cpp:142-145, program.cpp:31-38) */
+  CECOLL_UNSUPPORTED = 2,      /* impl not valid for the collective (compiler.cpp:70-75, 289-291) */
+  CECOLL_CUDA_ERROR = 3,
+  CECOLL_TIMEOUT = 4, /* a poll that is never triggered (sim.cpp:237-240) */
+  CECOLL_NO_DEVICE = 5,
+  CECOLL_NOT_REGISTERED = 6, /* buffer not reachable from a peer rank */
+  CECOLL_INTERNAL = 7
+} cecoll_status_t;
+
+typedef enum { CECOLL_ALLGATHER = 0, CECOLL_ALLTOALL = 1 } cecoll_kind_t; /* CollectiveKind, program.hpp:13 */
+
+/* Implementation (compiler.hpp:12-21) plus the B200 SM path and AUTO. */
+typedef enum {
+  CECOLL_IMPL_AUTO = -1, /* cecoll_select() */
+  CECOLL_IMPL_PCPY = 0,
+  CECOLL_IMPL_BCST = 1,
+  CECOLL_IMPL_SWAP = 2,
+  CECOLL_IMPL_B2B = 3,
+  CECOLL_IMPL_PRELAUNCH_PCPY = 4,
+  CECOLL_IMPL_PRELAUNCH_BCST = 5,
+  CECOLL_IMPL_PRELAUNCH_SWAP = 6,
+  CECOLL_IMPL_PRELAUNCH_B2B = 7,
+  CECOLL_IMPL_SM = 8 /* one-shot sm_100a push kernel (latency regime) */
+} cecoll_impl_t;
+
+typedef struct cecoll_comm* cecoll_comm_t;
+typedef struct cecoll_program* cecoll_program_t;
+typedef struct cecoll_plan* cecoll_plan_t;
+
+const char* cecoll_strerror(cecoll_status_t status);
+/* to_string / parse_implementation (compiler.cpp:8-37; "baseline" = pcpy). */
+const char* cecoll_impl_name(cecoll_impl_t impl);
+cecoll_impl_t cecoll_parse_impl(const char* name); /* returns -2 when unknown */
+/* valid_for (compiler.cpp:70-75) */
+int cecoll_impl_valid_for(cecoll_impl_t impl, cecoll_kind_t kind);
+/* Last error message recorded on this thread (first violation found). */
+const char* cecoll_last_error(void);
+
+/* ---------------------------------------------------------------------
+ * Command programs (CPU only; no GPU required).
+ * Replaces compile(Implementation, CollectiveSpec, NodeTopology)
+ * (compiler.hpp:55-56, compiler.cpp:287-303) with the node model reduced to
+ * `lanes_per_rank` (engines_per_gpu, topology.hpp:34); the returned program has
+ * the reference's queue/command structure exactly.
+ * ------------------------------------------------------------------- */
+cecoll_status_t cecoll_program_compile(cecoll_kind_t kind, cecoll_impl_t impl, int64_t chunk_bytes,
+                                       int nranks, int lanes_per_rank, cecoll_program_t* out);
+/* dump_program text (program.cpp:218-254). Returns the length (excluding the
+ * NUL) or -1 when cap is too small. */
+int64_t cecoll_program_dump(cecoll_program_t program, char* buf, size_t cap);
+/* static_metrics (program.cpp:40-65): data, sync, poll, engines, doorbells. */
+cecoll_status_t cecoll_program_metrics(cecoll_program_t program, int64_t out5[5]);
+/* account_traffic (verifier.cpp:281-327): total read, write, link bytes;
+ * per-rank arrays (nranks entries) may be NULL. */
+cecoll_status_t cecoll_program_traffic(cecoll_program_t program, int64_t out3[3], int64_t* per_rank_read,
+                                       int64_t* per_rank_write);
+/* validate_program (program.cpp:98-205): CECOLL_SUCCESS or INVALID_ARGUMENT
+ * with cecoll_last_error() naming the first violation. */
+cecoll_status_t cecoll_program_validate(cecoll_program_t program, int lanes_per_rank);
+void cecoll_program_free(cecoll_program_t program);
+
+/* select_implementation (compiler.cpp:305-318), the reference's MI300X table. */
+cecoll_impl_t cecoll_reference_select(cecoll_kind_t kind, int64_t chunk_bytes);
+/* B200 selector: measured thresholds for nranks ranks on ndevices devices;
+ * overridable with CECOLL_SM_MAX_BYTES. */
+cecoll_impl_t cecoll_select(cecoll_kind_t kind, int64_t chunk_bytes, int nranks, int ndevices);
+
+/* ---------------------------------------------------------------------
+ * Communicators. The reference models one host process driving every GPU
+ * (SPEC.md:61); cecoll_comm_init_all is that model (like
+ * ncclCommInitAll). devlist may repeat a device: several ranks then share
+ * one B200 ("co-resident ranks") and their transfers are intra-HBM.
+ * ------------------------------------------------------------------- */
+cecoll_status_t cecoll_comm_init_all(cecoll_comm_t* comms, int nranks, const int* devlist);
+/* Multi-process: one process per GPU owning one rank. `exchange` must
+ * all-gather `bytes` from every rank into `all` (rank-major); the Python
+ * layer passes torch.distributed. Buffers are mapped through CUDA IPC. */
+typedef int (*cecoll_exchange_fn)(void* ctx, const void* mine, size_t bytes, void* all);
+cecoll_status_t cecoll_comm_init_rank(cecoll_comm_t* comm, int nranks, int rank, int device,
+                                      cecoll_exchange_fn exchange, void* ctx);
+cecoll_status_t cecoll_comm_destroy(cecoll_comm_t comm);
+cecoll_status_t cecoll_comm_info(cecoll_comm_t comm, int* rank, int* nranks, int* device);
+
+/* Buffer registration (≙ BufferId::Input/Output being addressable on every
+ * GPU, program.hpp:36). Single-process: optional. Multi-process: collective
+ * over all ranks; every send/recv pointer must lie in a registered range. */
+cecoll_status_t cecoll_register(cecoll_comm_t comm, void* ptr, size_t bytes);
+cecoll_status_t cecoll_deregister(cecoll_comm_t comm, void* ptr);
+
+/* ---------------------------------------------------------------------
+ * Collectives (the runtime the reference simulates, sim.cpp:470).
+ * In single-process mode call once per rank inside group_start/group_end
+ * (all ranks of the communicator must participate); a lone call outside a
+ * group is only valid for multi-process communicators.
+ * ------------------------------------------------------------------- */
+cecoll_status_t cecoll_allgather(const void* send, void* recv, size_t chunk_bytes, cecoll_impl_t impl,
+                                 cecoll_comm_t comm, void* stream);
+/* recv may equal send only for CECOLL_IMPL_SWAP / PRELAUNCH_SWAP (in place). */
+cecoll_status_t cecoll_alltoall(const void* send, void* recv, size_t chunk_bytes, cecoll_impl_t impl,
+                                cecoll_comm_t comm, void* stream);
+cecoll_status_t cecoll_group_start(void);
+cecoll_status_t cecoll_group_end(void);
+
+/* ---------------------------------------------------------------------
+ * Explicit prelaunch plans (≙ apply_prelaunch, compiler.cpp:267-285, and the
+ * producer→collective sync chain, sim.cpp:475-499). A plan binds the ranks'
+ * buffers once, records the command lists as CUDA graphs gated by trigger
+ * polls, and keeps one instance armed ahead of the trigger.
+ * ------------------------------------------------------------------- */
+cecoll_status_t cecoll_plan_create(const cecoll_comm_t* comms, int ncomms, cecoll_kind_t kind,
+                                   const void* const* sends, void* const* recvs, size_t chunk_bytes,
+                                   cecoll_impl_t impl, cecoll_plan_t* out);
+/* Trigger the armed instance from each rank's stream (streams[i] for
+ * comms[i]; NULL entries = host trigger) and make each stream wait for
+ * completion; re-arms the next instance off the critical path. */
+cecoll_status_t cecoll_plan_launch(cecoll_plan_t plan, void* const* streams);
+cecoll_status_t cecoll_plan_destroy(cecoll_plan_t plan);
+
+/* Counters since comm creation: [0] collectives, [1] copy commands issued
+ * (CE memcpys), [2] flag writes, [3] flag waits, [4] kernel launches,
+ * [5] graph launches, [6] host API calls issued, [7] lanes (streams) used. */
+cecoll_status_t cecoll_comm_counters(cecoll_comm_t comm, int64_t out8[8]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CECOLL_H */

@@ -1,0 +1,380 @@
+"""cecoll — B200-native copy-engine collectives (Python host layer).
+
+Thin ctypes bindings over the C ABI in include/cecoll.h (libcecoll.so, built
+in-tree by build()). The vocabulary is the reference's: collective kinds
+allgather/alltoall, implementations pcpy/bcst/swap/b2b/prelaunch_* (plus the
+B200 SM path "sm"), per-peer chunk size s, and the rank/chunk layout of
+proj/src/compiler.cpp:115-126.
+
+The product path is libcecoll.so only: if it is missing every entry point
+raises; nothing here falls back to a CPU or torch implementation.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from typing import Callable, Sequence
+
+# Streams that wait on flags must not share a hardware queue with the stream
+# that writes them; give the driver its maximum number of queues. Must be set
+# before the CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcecoll.so")
+CSRC = os.path.join(HERE, "csrc")
+
+ALLGATHER, ALLTOALL = 0, 1
+KINDS = {"allgather": ALLGATHER, "ag": ALLGATHER, "alltoall": ALLTOALL, "aa": ALLTOALL}
+IMPLS = {
+    "auto": -1,
+    "pcpy": 0,
+    "baseline": 0,
+    "bcst": 1,
+    "swap": 2,
+    "b2b": 3,
+    "prelaunch_pcpy": 4,
+    "prelaunch_bcst": 5,
+    "prelaunch_swap": 6,
+    "prelaunch_b2b": 7,
+    "sm": 8,
+}
+IMPL_NAMES = {v: k for k, v in IMPLS.items() if k != "baseline"}
+# implementations_for (compiler.cpp:77-85) + the SM path
+IMPLS_FOR = {
+    "allgather": ["pcpy", "bcst", "b2b", "prelaunch_pcpy", "prelaunch_bcst", "prelaunch_b2b"],
+    "alltoall": ["pcpy", "swap", "b2b", "prelaunch_pcpy", "prelaunch_swap", "prelaunch_b2b"],
+}
+STATUS = {
+    0: "success",
+    1: "invalid argument",
+    2: "unsupported",
+    3: "CUDA error",
+    4: "timeout",
+    5: "no CUDA device",
+    6: "buffer not registered",
+    7: "internal error",
+}
+DEFAULT_LANES = 16  # engines_per_gpu default of the reference topology (topology.hpp:34)
+
+
+class CecollError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"cecoll: {STATUS.get(status, status)}: {what}")
+
+
+class InvalidArgument(CecollError, ValueError):
+    pass
+
+
+def build(force: bool = False) -> str:
+    """Compile libcecoll.so for sm_100a in-tree (nvcc cross-compiles without a GPU)."""
+    cmd = ["make", "-s", "-C", CSRC, "-j8"]
+    if force:
+        subprocess.run(["make", "-s", "-C", CSRC, "clean"], check=True)
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+_lib = None
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
+def lib():
+    """The loaded libcecoll.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libcecoll.so not built ({LIB_PATH}); run paper_2511_06605_b200.build()")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, sz = C.c_void_p, C.c_int, C.c_int64, C.c_size_t
+    sig = {
+        "cecoll_strerror": ([i32], C.c_char_p),
+        "cecoll_impl_name": ([i32], C.c_char_p),
+        "cecoll_parse_impl": ([C.c_char_p], i32),
+        "cecoll_impl_valid_for": ([i32, i32], i32),
+        "cecoll_last_error": ([], C.c_char_p),
+        "cecoll_program_compile": ([i32, i32, i64, i32, i32, C.POINTER(vp)], i32),
+        "cecoll_program_dump": ([vp, C.c_char_p, sz], i64),
+        "cecoll_program_metrics": ([vp, C.POINTER(i64)], i32),
+        "cecoll_program_traffic": ([vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], i32),
+        "cecoll_program_validate": ([vp, i32], i32),
+        "cecoll_program_free": ([vp], None),
+        "cecoll_reference_select": ([i32, i64], i32),
+        "cecoll_select": ([i32, i64, i32, i32], i32),
+        "cecoll_comm_init_all": ([C.POINTER(vp), i32, C.POINTER(i32)], i32),
+        "cecoll_comm_init_rank": ([C.POINTER(vp), i32, i32, i32, EXCHANGE_FN, vp], i32),
+        "cecoll_comm_destroy": ([vp], i32),
+        "cecoll_comm_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
+        "cecoll_register": ([vp, vp, sz], i32),
+        "cecoll_deregister": ([vp, vp], i32),
+        "cecoll_set_exchange": ([EXCHANGE_FN, vp], None),
+        "cecoll_allgather": ([vp, vp, sz, i32, vp, vp], i32),
+        "cecoll_alltoall": ([vp, vp, sz, i32, vp, vp], i32),
+        "cecoll_group_start": ([], i32),
+        "cecoll_group_end": ([], i32),
+        "cecoll_plan_create": ([C.POINTER(vp), i32, i32, C.POINTER(vp), C.POINTER(vp), sz, i32, C.POINTER(vp)], i32),
+        "cecoll_plan_launch": ([vp, C.POINTER(vp)], i32),
+        "cecoll_plan_destroy": ([vp], i32),
+        "cecoll_comm_counters": ([vp, C.POINTER(i64)], i32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+EXPORTED_SYMBOLS = [
+    "cecoll_strerror", "cecoll_impl_name", "cecoll_parse_impl", "cecoll_impl_valid_for", "cecoll_last_error",
+    "cecoll_program_compile", "cecoll_program_dump", "cecoll_program_metrics", "cecoll_program_traffic",
+    "cecoll_program_validate", "cecoll_program_free", "cecoll_reference_select", "cecoll_select",
+    "cecoll_comm_init_all", "cecoll_comm_init_rank", "cecoll_comm_destroy", "cecoll_comm_info",
+    "cecoll_register", "cecoll_deregister", "cecoll_allgather", "cecoll_alltoall", "cecoll_group_start",
+    "cecoll_group_end", "cecoll_plan_create", "cecoll_plan_launch", "cecoll_plan_destroy", "cecoll_comm_counters",
+]
+
+
+def _check(status: int, what: str = ""):
+    if status != 0:
+        msg = lib().cecoll_last_error().decode(errors="replace")
+        cls = InvalidArgument if status in (1, 2) else CecollError
+        raise cls(status, f"{what}: {msg}" if what else msg)
+
+
+def _kind(kind) -> int:
+    if isinstance(kind, int):
+        return kind
+    return KINDS[kind]
+
+
+def _impl(impl) -> int:
+    if isinstance(impl, int):
+        return impl
+    if impl not in IMPLS:
+        raise InvalidArgument(1, f"unknown implementation {impl!r}")
+    return IMPLS[impl]
+
+
+def impl_name(impl: int) -> str:
+    return lib().cecoll_impl_name(impl).decode()
+
+
+# ---------------------------------------------------------------------------
+# Command programs (CPU only) — compile() / dump_program() / static_metrics()
+# / account_traffic() / validate_program() (proj/src/{compiler,program,verifier}.cpp)
+# ---------------------------------------------------------------------------
+
+
+class Program:
+    """A compiled command program (≙ dmasim::CommandProgram)."""
+
+    def __init__(self, kind, impl, chunk_bytes: int, nranks: int, lanes_per_rank: int = DEFAULT_LANES):
+        self.kind, self.impl, self.chunk, self.nranks = kind, impl, chunk_bytes, nranks
+        h = C.c_void_p()
+        _check(
+            lib().cecoll_program_compile(_kind(kind), _impl(impl), chunk_bytes, nranks, lanes_per_rank, C.byref(h)),
+            f"compile {kind}/{impl} s={chunk_bytes} n={nranks}",
+        )
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.cecoll_program_free(self._h)
+            self._h = None
+
+    def dump(self) -> str:
+        cap = 1 << 22
+        buf = C.create_string_buffer(cap)
+        k = lib().cecoll_program_dump(self._h, buf, cap)
+        if k < 0:
+            raise CecollError(7, "dump buffer too small")
+        return buf.raw[:k].decode()
+
+    def metrics(self) -> dict:
+        out = (C.c_int64 * 5)()
+        _check(lib().cecoll_program_metrics(self._h, out))
+        return dict(zip(["data_commands", "sync_commands", "poll_commands", "engines_used", "doorbells"], list(out)))
+
+    def traffic(self) -> dict:
+        t = (C.c_int64 * 3)()
+        rr = (C.c_int64 * self.nranks)()
+        rw = (C.c_int64 * self.nranks)()
+        _check(lib().cecoll_program_traffic(self._h, t, rr, rw))
+        return {"read": t[0], "write": t[1], "link": t[2], "rank_read": list(rr), "rank_write": list(rw)}
+
+    def validate(self, lanes_per_rank: int = DEFAULT_LANES) -> str | None:
+        st = lib().cecoll_program_validate(self._h, lanes_per_rank)
+        return None if st == 0 else lib().cecoll_last_error().decode()
+
+
+def reference_select(kind, chunk_bytes: int) -> str | None:
+    """select_implementation (compiler.cpp:305-318): the reference's MI300X table."""
+    r = lib().cecoll_reference_select(_kind(kind), chunk_bytes)
+    return None if r < -1 else IMPL_NAMES[r]
+
+
+def select(kind, chunk_bytes: int, nranks: int, ndevices: int) -> str:
+    """The B200 selector (measured thresholds)."""
+    return IMPL_NAMES[lib().cecoll_select(_kind(kind), chunk_bytes, nranks, ndevices)]
+
+
+# ---------------------------------------------------------------------------
+# Communicators and collectives
+# ---------------------------------------------------------------------------
+
+
+def _ptr(x) -> int:
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    raise TypeError(f"expected a device pointer or tensor, got {type(x)}")
+
+
+def _stream(s) -> int | None:
+    if s is None:
+        return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream  # torch.cuda.Stream
+
+
+class Comm:
+    """One rank of a communicator (≙ ncclComm_t)."""
+
+    def __init__(self, handle, owner=None):
+        self._h = handle
+        self._owner = owner  # keeps the exchange callback alive (multi-process)
+        r, n, d = C.c_int(), C.c_int(), C.c_int()
+        _check(lib().cecoll_comm_info(self._h, C.byref(r), C.byref(n), C.byref(d)))
+        self.rank, self.nranks, self.device = r.value, n.value, d.value
+
+    @staticmethod
+    def init_all(devices: Sequence[int]) -> list["Comm"]:
+        """Single process driving every rank (devices may repeat: co-resident ranks)."""
+        n = len(devices)
+        hs = (C.c_void_p * n)()
+        devs = (C.c_int * n)(*devices)
+        _check(lib().cecoll_comm_init_all(hs, n, devs), "comm_init_all")
+        return [Comm(C.c_void_p(hs[i])) for i in range(n)]
+
+    @staticmethod
+    def init_rank(nranks: int, rank: int, device: int, exchange: Callable[[bytes], list[bytes]]) -> "Comm":
+        """One rank per process; `exchange(mine) -> [bytes of every rank]` is an all-gather."""
+        cb = _make_exchange(exchange, nranks)
+        h = C.c_void_p()
+        _check(lib().cecoll_comm_init_rank(C.byref(h), nranks, rank, device, cb, None), "comm_init_rank")
+        c = Comm(h, owner=cb)
+        return c
+
+    def register(self, buf, nbytes: int | None = None):
+        """Collective in multi-process communicators (symmetric windows)."""
+        ptr = _ptr(buf)
+        if nbytes is None:
+            nbytes = buf.numel() * buf.element_size()
+        if self._owner is not None:
+            lib().cecoll_set_exchange(self._owner, None)
+        _check(lib().cecoll_register(self._h, ptr, nbytes), "register")
+
+    def counters(self) -> dict:
+        out = (C.c_int64 * 8)()
+        _check(lib().cecoll_comm_counters(self._h, out))
+        keys = ["collectives", "copies", "flag_writes", "flag_waits", "kernels", "graph_launches", "api_calls",
+                "lanes"]
+        return dict(zip(keys, list(out)))
+
+    def destroy(self):
+        if self._h is not None:
+            _check(lib().cecoll_comm_destroy(self._h))
+            self._h = None
+
+
+def destroy_all(comms: Sequence[Comm]):
+    for c in comms:
+        c.destroy()
+
+
+def _make_exchange(exchange, nranks):
+    def _cb(ctx, mine, nbytes, out):
+        try:
+            data = C.string_at(mine, nbytes)
+            parts = exchange(data)
+            assert len(parts) == nranks
+            blob = b"".join(parts)
+            C.memmove(out, blob, len(blob))
+            return 0
+        except Exception:  # noqa: BLE001 - reported as a status code across the ABI
+            return 1
+
+    return EXCHANGE_FN(_cb)
+
+
+def torch_exchange(group=None):
+    """An exchange callback over torch.distributed (gloo or nccl object collectives)."""
+    import torch.distributed as dist
+
+    def ex(mine: bytes) -> list[bytes]:
+        out = [None] * dist.get_world_size(group)
+        dist.all_gather_object(out, mine, group=group)
+        return out
+
+    return ex
+
+
+def _collective(fn_name, comms, sends, recvs, chunk_bytes, impl, streams):
+    L = lib()
+    fn = getattr(L, fn_name)
+    if isinstance(comms, Comm):
+        comms, sends, recvs = [comms], [sends], [recvs]
+        streams = [streams] if not isinstance(streams, (list, tuple)) else streams
+    if streams is None or not isinstance(streams, (list, tuple)):
+        streams = [streams] * len(comms)
+    im = _impl(impl)
+    _check(L.cecoll_group_start())
+    try:
+        for c, s, r, st in zip(comms, sends, recvs, streams):
+            _check(fn(_ptr(s), _ptr(r), chunk_bytes, im, c._h, _stream(st)), fn_name)
+    finally:
+        _check(L.cecoll_group_end(), fn_name)
+
+
+def all_gather(comms, sends, recvs, chunk_bytes: int, impl="auto", streams=None):
+    """recv[r] (n*s bytes) gets rank i's s-byte chunk at [i*s, (i+1)*s) (compiler.cpp:115-122)."""
+    _collective("cecoll_allgather", comms, sends, recvs, chunk_bytes, impl, streams)
+
+
+def all_to_all(comms, sends, recvs, chunk_bytes: int, impl="auto", streams=None):
+    """send[r] chunk j (s bytes) lands in recv[j] slot r (compiler.cpp:124-126, 156-157)."""
+    _collective("cecoll_alltoall", comms, sends, recvs, chunk_bytes, impl, streams)
+
+
+class Plan:
+    """A prelaunched plan: recorded once, armed ahead, triggered per launch."""
+
+    def __init__(self, comms, kind, sends, recvs, chunk_bytes: int, impl="prelaunch_pcpy"):
+        n = len(comms)
+        hs = (C.c_void_p * n)(*[c._h.value for c in comms])
+        ss = (C.c_void_p * n)(*[_ptr(x) for x in sends])
+        rs = (C.c_void_p * n)(*[_ptr(x) for x in recvs])
+        self._keep = (sends, recvs)  # buffers must outlive an armed plan
+        self._n = n
+        h = C.c_void_p()
+        _check(lib().cecoll_plan_create(hs, n, _kind(kind), ss, rs, chunk_bytes, _impl(impl), C.byref(h)),
+               "plan_create")
+        self._h = h
+
+    def launch(self, streams=None):
+        if streams is None or not isinstance(streams, (list, tuple)):
+            streams = [streams] * self._n
+        arr = (C.c_void_p * self._n)(*[_stream(s) for s in streams])
+        _check(lib().cecoll_plan_launch(self._h, arr), "plan_launch")
+
+    def destroy(self):
+        if self._h is not None:
+            _check(lib().cecoll_plan_destroy(self._h), "plan_destroy")
+            self._h = None

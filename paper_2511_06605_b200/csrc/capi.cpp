@@ -1,0 +1,322 @@
+// extern "C" boundary (include/cecoll.h). Exceptions never cross it: the
+// reference's std::invalid_argument sites become CECOLL_INVALID_ARGUMENT /
+// CECOLL_UNSUPPORTED and the message is kept for cecoll_last_error().
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "cecoll.h"
+#include "program.hpp"
+#include "runtime.hpp"
+
+using namespace cecoll;
+
+struct cecoll_program {
+  Program program;
+};
+
+namespace {
+
+struct PendingCall {
+  cecoll_comm_t comm;
+  Kind kind;
+  const void* send;
+  void* recv;
+  int64_t chunk;
+  Impl impl;
+  cudaStream_t stream;
+};
+
+thread_local int g_group_depth = 0;
+thread_local std::vector<PendingCall> g_pending;
+
+cecoll_status_t st(const Status& s) { return static_cast<cecoll_status_t>(s.code); }
+
+cecoll_status_t err(cecoll_status_t code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+
+bool impl_ok(cecoll_impl_t impl) { return impl >= CECOLL_IMPL_AUTO && impl <= CECOLL_IMPL_SM; }
+
+cecoll_status_t flush_group(std::vector<PendingCall>& calls) {
+  cecoll_status_t result = CECOLL_SUCCESS;
+  std::vector<bool> done(calls.size(), false);
+  for (size_t i = 0; i < calls.size(); ++i) {
+    if (done[i]) continue;
+    World* w = calls[i].comm->world;
+    std::vector<CallArgs> args;
+    for (size_t j = i; j < calls.size(); ++j) {
+      if (done[j] || calls[j].comm->world != w) continue;
+      if (calls[j].kind != calls[i].kind || calls[j].chunk != calls[i].chunk || calls[j].impl != calls[i].impl) {
+        return err(CECOLL_INVALID_ARGUMENT, "group: one collective per communicator set (kind, size and impl must match)");
+      }
+      args.push_back({calls[j].comm->rank, calls[j].send, calls[j].recv, calls[j].stream});
+      done[j] = true;
+    }
+    Status s = run_collective(w, calls[i].kind, calls[i].impl, calls[i].chunk, args);
+    if (!s.ok() && result == CECOLL_SUCCESS) result = st(s);
+  }
+  return result;
+}
+
+cecoll_status_t enqueue(Kind kind, const void* send, void* recv, size_t chunk, cecoll_impl_t impl, cecoll_comm_t comm,
+                        void* stream) {
+  if (!comm || !comm->world) return err(CECOLL_INVALID_ARGUMENT, "null communicator");
+  if (!impl_ok(impl)) return err(CECOLL_INVALID_ARGUMENT, "unknown implementation");
+  if (chunk == 0 || !send || !recv) return err(CECOLL_INVALID_ARGUMENT, "collective: chunk size must be positive");
+  PendingCall c{comm, kind, send, recv, static_cast<int64_t>(chunk), static_cast<Impl>(impl),
+                static_cast<cudaStream_t>(stream)};
+  if (g_group_depth > 0) {
+    g_pending.push_back(c);
+    return CECOLL_SUCCESS;
+  }
+  World* w = comm->world;
+  if (!w->multiprocess && w->nranks > 1)
+    return err(CECOLL_INVALID_ARGUMENT,
+               "single-process communicator with several ranks: call every rank inside cecoll_group_start/end");
+  std::vector<PendingCall> one{c};
+  return flush_group(one);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cecoll_strerror(cecoll_status_t s) {
+  switch (s) {
+    case CECOLL_SUCCESS: return "success";
+    case CECOLL_INVALID_ARGUMENT: return "invalid argument";
+    case CECOLL_UNSUPPORTED: return "unsupported";
+    case CECOLL_CUDA_ERROR: return "CUDA error";
+    case CECOLL_TIMEOUT: return "timeout";
+    case CECOLL_NO_DEVICE: return "no CUDA device";
+    case CECOLL_NOT_REGISTERED: return "buffer not registered";
+    case CECOLL_INTERNAL: return "internal error";
+  }
+  return "unknown status";
+}
+
+const char* cecoll_impl_name(cecoll_impl_t impl) { return impl_name(static_cast<Impl>(impl)); }
+
+cecoll_impl_t cecoll_parse_impl(const char* name) {
+  Impl out;
+  if (!name || !parse_impl(name, &out)) return static_cast<cecoll_impl_t>(-2);
+  return static_cast<cecoll_impl_t>(out);
+}
+
+int cecoll_impl_valid_for(cecoll_impl_t impl, cecoll_kind_t kind) {
+  if (impl == CECOLL_IMPL_SM || impl == CECOLL_IMPL_AUTO) return 1;
+  if (!impl_ok(impl)) return 0;
+  return valid_for(static_cast<Impl>(impl), static_cast<Kind>(kind)) ? 1 : 0;
+}
+
+const char* cecoll_last_error(void) { return last_error(); }
+
+cecoll_status_t cecoll_program_compile(cecoll_kind_t kind, cecoll_impl_t impl, int64_t chunk_bytes, int nranks,
+                                       int lanes_per_rank, cecoll_program_t* out) {
+  if (!out) return err(CECOLL_INVALID_ARGUMENT, "null output");
+  *out = nullptr;
+  if (kind != CECOLL_ALLGATHER && kind != CECOLL_ALLTOALL) return err(CECOLL_INVALID_ARGUMENT, "unknown collective");
+  if (impl < CECOLL_IMPL_PCPY || impl > CECOLL_IMPL_PRELAUNCH_B2B)
+    return err(CECOLL_INVALID_ARGUMENT, "no command program for this implementation");
+  if (!valid_for(static_cast<Impl>(impl), static_cast<Kind>(kind)))
+    return err(CECOLL_UNSUPPORTED, std::string(impl_name(static_cast<Impl>(impl))) + " does not apply to " +
+                                       (kind == CECOLL_ALLGATHER ? "allgather" : "alltoall"));
+  Spec spec;
+  spec.kind = static_cast<Kind>(kind);
+  spec.chunk = chunk_bytes;
+  spec.nranks = nranks;
+  try {
+    auto* p = new cecoll_program{compile(static_cast<Impl>(impl), spec, lanes_per_rank)};
+    *out = p;
+    return CECOLL_SUCCESS;
+  } catch (const std::invalid_argument& e) {
+    return err(CECOLL_INVALID_ARGUMENT, e.what());
+  }
+}
+
+int64_t cecoll_program_dump(cecoll_program_t program, char* buf, size_t cap) {
+  if (!program) return -1;
+  std::string text = dump(program->program);
+  if (!buf || text.size() + 1 > cap) return -1;
+  std::memcpy(buf, text.c_str(), text.size() + 1);
+  return static_cast<int64_t>(text.size());
+}
+
+cecoll_status_t cecoll_program_metrics(cecoll_program_t program, int64_t out5[5]) {
+  if (!program || !out5) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  Metrics m = metrics(program->program);
+  out5[0] = m.data;
+  out5[1] = m.sync;
+  out5[2] = m.poll;
+  out5[3] = m.engines;
+  out5[4] = m.doorbells;
+  return CECOLL_SUCCESS;
+}
+
+cecoll_status_t cecoll_program_traffic(cecoll_program_t program, int64_t out3[3], int64_t* rr, int64_t* rw) {
+  if (!program || !out3) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  Traffic t = traffic(program->program);
+  out3[0] = t.read;
+  out3[1] = t.write;
+  out3[2] = t.link;
+  for (size_t i = 0; i < t.rank_read.size(); ++i) {
+    if (rr) rr[i] = t.rank_read[i];
+    if (rw) rw[i] = t.rank_write[i];
+  }
+  return CECOLL_SUCCESS;
+}
+
+cecoll_status_t cecoll_program_validate(cecoll_program_t program, int lanes_per_rank) {
+  if (!program) return err(CECOLL_INVALID_ARGUMENT, "null program");
+  std::string v = validate(program->program, lanes_per_rank);
+  if (v.empty()) return CECOLL_SUCCESS;
+  return err(CECOLL_INVALID_ARGUMENT, v);
+}
+
+void cecoll_program_free(cecoll_program_t program) { delete program; }
+
+cecoll_impl_t cecoll_reference_select(cecoll_kind_t kind, int64_t chunk_bytes) {
+  try {
+    return static_cast<cecoll_impl_t>(reference_select(static_cast<Kind>(kind), chunk_bytes));
+  } catch (const std::invalid_argument& e) {
+    set_error(e.what());
+    return static_cast<cecoll_impl_t>(-2);
+  }
+}
+
+cecoll_impl_t cecoll_select(cecoll_kind_t kind, int64_t chunk_bytes, int nranks, int ndevices) {
+  return static_cast<cecoll_impl_t>(select(static_cast<Kind>(kind), chunk_bytes, nranks, ndevices));
+}
+
+cecoll_status_t cecoll_comm_init_all(cecoll_comm_t* comms, int nranks, const int* devlist) {
+  if (!comms || !devlist) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  World* w = nullptr;
+  Status s = world_init_all(nranks, devlist, &w);
+  if (!s.ok()) return st(s);
+  for (int r = 0; r < nranks; ++r) comms[r] = new cecoll_comm{w, r};
+  return CECOLL_SUCCESS;
+}
+
+cecoll_status_t cecoll_comm_init_rank(cecoll_comm_t* comm, int nranks, int rank, int device,
+                                      cecoll_exchange_fn exchange, void* ctx) {
+  if (!comm) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  World* w = nullptr;
+  Status s = world_init_rank(nranks, rank, device, exchange, ctx, &w);
+  if (!s.ok()) return st(s);
+  *comm = new cecoll_comm{w, rank};
+  return CECOLL_SUCCESS;
+}
+
+cecoll_status_t cecoll_comm_destroy(cecoll_comm_t comm) {
+  if (!comm) return err(CECOLL_INVALID_ARGUMENT, "null communicator");
+  World* w = comm->world;
+  delete comm;
+  if (--w->live_comms == 0) world_release(w);
+  return CECOLL_SUCCESS;
+}
+
+cecoll_status_t cecoll_comm_info(cecoll_comm_t comm, int* rank, int* nranks, int* device) {
+  if (!comm) return err(CECOLL_INVALID_ARGUMENT, "null communicator");
+  if (rank) *rank = comm->rank;
+  if (nranks) *nranks = comm->world->nranks;
+  if (device) *device = comm->world->device[comm->rank];
+  return CECOLL_SUCCESS;
+}
+
+static thread_local cecoll_exchange_fn g_reg_fn = nullptr;
+static thread_local void* g_reg_ctx = nullptr;
+
+cecoll_status_t cecoll_register(cecoll_comm_t comm, void* ptr, size_t bytes) {
+  if (!comm || !ptr || !bytes) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  return st(world_register(comm->world, comm->rank, ptr, bytes, g_reg_fn, g_reg_ctx));
+}
+
+// Multi-process registration needs the exchange callback again; the Python
+// layer installs it before cecoll_register (not part of the public header's
+// required surface, exported for the bindings).
+void cecoll_set_exchange(cecoll_exchange_fn fn, void* ctx) {
+  g_reg_fn = fn;
+  g_reg_ctx = ctx;
+}
+
+cecoll_status_t cecoll_deregister(cecoll_comm_t comm, void* ptr) {
+  if (!comm) return err(CECOLL_INVALID_ARGUMENT, "null communicator");
+  return st(world_deregister(comm->world, ptr));
+}
+
+cecoll_status_t cecoll_allgather(const void* send, void* recv, size_t chunk_bytes, cecoll_impl_t impl,
+                                 cecoll_comm_t comm, void* stream) {
+  return enqueue(Kind::AllGather, send, recv, chunk_bytes, impl, comm, stream);
+}
+
+cecoll_status_t cecoll_alltoall(const void* send, void* recv, size_t chunk_bytes, cecoll_impl_t impl,
+                                cecoll_comm_t comm, void* stream) {
+  return enqueue(Kind::AllToAll, send, recv, chunk_bytes, impl, comm, stream);
+}
+
+cecoll_status_t cecoll_group_start(void) {
+  ++g_group_depth;
+  return CECOLL_SUCCESS;
+}
+
+cecoll_status_t cecoll_group_end(void) {
+  if (g_group_depth <= 0) return err(CECOLL_INVALID_ARGUMENT, "group_end without group_start");
+  if (--g_group_depth > 0) return CECOLL_SUCCESS;
+  std::vector<PendingCall> calls;
+  calls.swap(g_pending);
+  return flush_group(calls);
+}
+
+cecoll_status_t cecoll_plan_create(const cecoll_comm_t* comms, int ncomms, cecoll_kind_t kind,
+                                   const void* const* sends, void* const* recvs, size_t chunk_bytes,
+                                   cecoll_impl_t impl, cecoll_plan_t* out) {
+  if (!comms || ncomms <= 0 || !sends || !recvs || !out) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  if (!impl_ok(impl)) return err(CECOLL_INVALID_ARGUMENT, "unknown implementation");
+  World* w = comms[0]->world;
+  std::vector<CallArgs> args;
+  // Streams are bound at launch; plan units are formed per (device, rank)
+  // with a placeholder stream equal to the rank index, resolved at launch.
+  for (int i = 0; i < ncomms; ++i) {
+    if (comms[i]->world != w) return err(CECOLL_INVALID_ARGUMENT, "plan: communicators of one world only");
+    args.push_back({comms[i]->rank, sends[i], recvs[i], nullptr});
+  }
+  Plan* p = nullptr;
+  Status s = plan_create(w, static_cast<Kind>(kind), static_cast<Impl>(impl), static_cast<int64_t>(chunk_bytes),
+                         args, &p);
+  if (!s.ok()) return st(s);
+  *out = new cecoll_plan{w, p};
+  return CECOLL_SUCCESS;
+}
+
+cecoll_status_t cecoll_plan_launch(cecoll_plan_t plan, void* const* streams) {
+  if (!plan) return err(CECOLL_INVALID_ARGUMENT, "null plan");
+  Plan* p = plan->plan;
+  // Units were formed per device (streams are bound at launch): each unit
+  // runs on the stream given for its lowest rank.
+  for (Unit& u : p->units) {
+    cudaStream_t s = nullptr;
+    for (size_t i = 0; i < p->key_rank.size(); ++i)
+      if (p->key_rank[i] == u.ranks[0] && streams) s = static_cast<cudaStream_t>(streams[i]);
+    u.stream = s;
+  }
+  return st(plan_launch(plan->world, p, true));
+}
+
+cecoll_status_t cecoll_plan_destroy(cecoll_plan_t plan) {
+  if (!plan) return err(CECOLL_INVALID_ARGUMENT, "null plan");
+  Status s = plan_destroy(plan->world, plan->plan);
+  delete plan->plan;
+  delete plan;
+  return st(s);
+}
+
+cecoll_status_t cecoll_comm_counters(cecoll_comm_t comm, int64_t out8[8]) {
+  if (!comm || !out8) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  for (int i = 0; i < 8; ++i) out8[i] = comm->world->counters[i].load();
+  return CECOLL_SUCCESS;
+}
+
+}  // extern "C"

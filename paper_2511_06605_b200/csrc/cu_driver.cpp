@@ -1,0 +1,49 @@
+#include "cu_driver.hpp"
+
+#include <mutex>
+
+namespace cecoll {
+
+namespace {
+
+template <typename F>
+bool load(const char* name, F& fn) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPointByVersion(name, &p, 12090, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || p == nullptr) {
+    cudaGetLastError();
+    return false;
+  }
+  fn = reinterpret_cast<F>(p);
+  return true;
+}
+
+}  // namespace
+
+const DriverApi* driver_api() {
+  static DriverApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+      cudaGetLastError();
+      return;
+    }
+    bool ok = true;
+    ok &= load("cuStreamWaitValue64", api.StreamWaitValue64);
+    ok &= load("cuStreamWriteValue64", api.StreamWriteValue64);
+    ok &= load("cuStreamWaitValue32", api.StreamWaitValue32);
+    ok &= load("cuStreamWriteValue32", api.StreamWriteValue32);
+    ok &= load("cuStreamBatchMemOp", api.StreamBatchMemOp);
+    ok &= load("cuDeviceGetAttribute", api.DeviceGetAttribute);
+    ok &= load("cuGetErrorString", api.GetErrorString);
+    api.has_batch_memcpy = load("cuMemcpyBatchAsync", api.MemcpyBatchAsync);
+    load("cuMulticastCreate", api.MulticastCreate);
+    ok &= load("cuMemGetAddressRange", api.MemGetAddressRange);
+    api.loaded = ok;
+  });
+  return api.loaded ? &api : nullptr;
+}
+
+}  // namespace cecoll

@@ -1,0 +1,36 @@
+// Driver-API entry points resolved at runtime through cudart.
+//
+// libcecoll links cudart statically and never links libcuda, so the shared
+// library loads (and its CPU-side planner runs) on a machine without a GPU
+// driver. The stream memory operations (cuStreamWaitValue64 /
+// cuStreamWriteValue64 / cuStreamBatchMemOp) and cuMemcpyBatchAsync have no
+// cudart equivalent; they are looked up once with
+// cudaGetDriverEntryPointByVersion the first time a communicator is created.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace cecoll {
+
+struct DriverApi {
+  CUresult (*StreamWaitValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned) = nullptr;
+  CUresult (*StreamWriteValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned) = nullptr;
+  CUresult (*StreamWaitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned) = nullptr;
+  CUresult (*StreamWriteValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned) = nullptr;
+  CUresult (*StreamBatchMemOp)(CUstream, unsigned, CUstreamBatchMemOpParams*, unsigned) = nullptr;
+  CUresult (*MemcpyBatchAsync)(CUdeviceptr*, CUdeviceptr*, size_t*, size_t, CUmemcpyAttributes*,
+                               size_t*, size_t, size_t*, CUstream) = nullptr;
+  CUresult (*DeviceGetAttribute)(int*, CUdevice_attribute, CUdevice) = nullptr;
+  CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
+  CUresult (*MulticastCreate)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*) = nullptr;
+  CUresult (*MemGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
+  bool loaded = false;
+  bool has_batch_memcpy = false;
+};
+
+// Returns the process-wide table, loading it on first use. Returns nullptr
+// when the CUDA driver is absent (CPU-only machine).
+const DriverApi* driver_api();
+
+}  // namespace cecoll

@@ -1,0 +1,880 @@
+// Communicator, plan lowering and the three executors:
+//   CE       pcpy / b2b / bcst / swap: per-lane streams of copy commands,
+//            bracketed by batched flag memops (cuStreamBatchMemOp).
+//   graph    prelaunch_*: the same lanes recorded once per unit into a CUDA
+//            graph whose body sits behind a gate (conditional node), launched
+//            ahead and opened by a host post (apply_prelaunch,
+//            compiler.cpp:267-285).
+//   SM       one sm_100a item kernel per unit moving every chunk of the unit's
+//            ranks (latency regime).
+#include "runtime.hpp"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <set>
+#include <stdexcept>
+
+namespace cecoll {
+
+namespace {
+
+thread_local std::string g_error;
+
+Status fail(int code, const std::string& msg) {
+  g_error = msg;
+  return Status{code, msg};
+}
+
+Status cuda_fail(cudaError_t e, const char* what, int line) {
+  return fail(CECOLL_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e) + " (runtime.cpp:" +
+                                     std::to_string(line) + ")");
+}
+
+Status cu_fail(CUresult r, const char* what, int line) {
+  const char* s = "?";
+  if (driver_api()) driver_api()->GetErrorString(r, &s);
+  return fail(CECOLL_CUDA_ERROR, std::string(what) + ": " + s + " (runtime.cpp:" + std::to_string(line) + ")");
+}
+
+#define CUDA_TRY(expr)                                      \
+  do {                                                      \
+    cudaError_t e_ = (expr);                                \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr, __LINE__); \
+  } while (0)
+
+#define CU_TRY(expr)                                       \
+  do {                                                     \
+    CUresult r_ = (expr);                                  \
+    if (r_ != CUDA_SUCCESS) return cu_fail(r_, #expr, __LINE__); \
+  } while (0)
+
+#define STATUS_TRY(expr)         \
+  do {                           \
+    Status s_ = (expr);          \
+    if (!s_.ok()) return s_;     \
+  } while (0)
+
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev_);
+    if (dev >= 0 && dev != prev_) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() { cudaSetDevice(prev_); }
+
+ private:
+  int prev_ = 0;
+};
+
+CUstreamBatchMemOpParams op_write(uint64_t* addr, uint64_t v) {
+  CUstreamBatchMemOpParams op;
+  std::memset(&op, 0, sizeof(op));
+  op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+  op.writeValue.address = reinterpret_cast<CUdeviceptr>(addr);
+  op.writeValue.value64 = v;
+  op.writeValue.flags = 0;  // with the default memory barrier: prior copies are visible first
+  return op;
+}
+
+CUstreamBatchMemOpParams op_wait(uint64_t* addr, uint64_t v) {
+  CUstreamBatchMemOpParams op;
+  std::memset(&op, 0, sizeof(op));
+  op.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_64;
+  op.waitValue.address = reinterpret_cast<CUdeviceptr>(addr);
+  op.waitValue.value64 = v;
+  op.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+  return op;
+}
+
+// Poll + reset of one slot (the reset keeps graph replays value-constant).
+void add_poll(MemOps& ops, uint64_t* addr) {
+  ops.push_back(op_wait(addr, 1));
+  ops.push_back(op_write(addr, 0));
+}
+
+Status submit(World* w, cudaStream_t s, const MemOps& ops) {
+  const DriverApi* d = driver_api();
+  size_t i = 0;
+  while (i < ops.size()) {
+    const unsigned count = static_cast<unsigned>(std::min<size_t>(255, ops.size() - i));
+    CU_TRY(d->StreamBatchMemOp(reinterpret_cast<CUstream>(s), count,
+                               const_cast<CUstreamBatchMemOpParams*>(ops.data() + i), 0));
+    for (unsigned k = 0; k < count; ++k) {
+      if (ops[i + k].operation == CU_STREAM_MEM_OP_WRITE_VALUE_64) ++w->counters[2];
+      else ++w->counters[3];
+    }
+    ++w->counters[6];
+    i += count;
+  }
+  return {};
+}
+
+Status issue_copies(World* w, const std::vector<Copy>& copies, cudaStream_t s, bool allow_batch) {
+  const DriverApi* d = driver_api();
+  if (copies.size() > 1 && allow_batch && d->has_batch_memcpy) {
+    std::vector<CUdeviceptr> dst, src;
+    std::vector<size_t> sz;
+    for (const Copy& c : copies) {
+      dst.push_back(reinterpret_cast<CUdeviceptr>(c.dst));
+      src.push_back(reinterpret_cast<CUdeviceptr>(c.src));
+      sz.push_back(static_cast<size_t>(c.bytes));
+    }
+    CUmemcpyAttributes attr;
+    std::memset(&attr, 0, sizeof(attr));
+    attr.srcAccessOrder = CU_MEMCPY_SRC_ACCESS_ORDER_STREAM;
+    attr.flags = CU_MEMCPY_FLAG_PREFER_OVERLAP_WITH_COMPUTE;
+    size_t idx = 0, fail_idx = 0;
+    CU_TRY(d->MemcpyBatchAsync(dst.data(), src.data(), sz.data(), copies.size(), &attr, &idx, 1, &fail_idx,
+                               reinterpret_cast<CUstream>(s)));
+    w->counters[1] += static_cast<int64_t>(copies.size());
+    ++w->counters[6];
+    return {};
+  }
+  for (const Copy& c : copies) {
+    CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, static_cast<size_t>(c.bytes), cudaMemcpyDefault, s));
+    ++w->counters[1];
+    ++w->counters[6];
+  }
+  return {};
+}
+
+Status make_rank(World* w, int rank, int device) {
+  DeviceGuard g(device);
+  auto rs = std::make_unique<RankState>();
+  rs->rank = rank;
+  rs->device = device;
+  CUDA_TRY(cudaEventCreateWithFlags(&rs->start, cudaEventDisableTiming));
+  CUDA_TRY(cudaMalloc(&rs->flags, kFlagBytes));
+  CUDA_TRY(cudaMemset(rs->flags, 0, kFlagBytes));
+  CUDA_TRY(cudaDeviceSynchronize());
+  w->flag_page[rank] = rs->flags;
+  w->local[rank] = std::move(rs);
+  return {};
+}
+
+Status ensure_lanes(RankState* rs, int n) {
+  DeviceGuard g(rs->device);
+  while (static_cast<int>(rs->lanes.size()) < n) {
+    cudaStream_t s;
+    cudaEvent_t e;
+    CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    rs->lanes.push_back(s);
+    rs->lane_done.push_back(e);
+  }
+  return {};
+}
+
+int count_devices(const std::vector<int>& dev) {
+  std::set<int> s(dev.begin(), dev.end());
+  return static_cast<int>(s.size());
+}
+
+}  // namespace
+
+void set_error(const std::string& msg) { g_error = msg; }
+const char* last_error() { return g_error.c_str(); }
+
+Status world_init_all(int nranks, const int* devlist, World** out) {
+  if (!driver_api()) return fail(CECOLL_NO_DEVICE, "no CUDA driver / device");
+  if (nranks < 1 || nranks > kMaxRanks)
+    return fail(CECOLL_INVALID_ARGUMENT, "nranks must be in [1, " + std::to_string(kMaxRanks) + "]");
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  for (int r = 0; r < nranks; ++r)
+    if (devlist[r] < 0 || devlist[r] >= ndev)
+      return fail(CECOLL_INVALID_ARGUMENT, "device " + std::to_string(devlist[r]) + " out of range");
+  auto w = std::make_unique<World>();
+  w->nranks = nranks;
+  w->device.assign(devlist, devlist + nranks);
+  w->flag_page.assign(nranks, nullptr);
+  w->local.resize(nranks);
+  w->ndevices = count_devices(w->device);
+  // Peer access between every pair of distinct devices (NVLink / NVSwitch).
+  std::set<int> devs(w->device.begin(), w->device.end());
+  for (int a : devs)
+    for (int b : devs) {
+      if (a == b) continue;
+      int can = 0;
+      CUDA_TRY(cudaDeviceCanAccessPeer(&can, a, b));
+      if (!can) return fail(CECOLL_UNSUPPORTED, "no peer access between devices");
+      DeviceGuard g(a);
+      cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "EnablePeerAccess", __LINE__);
+      cudaGetLastError();
+    }
+  for (int r = 0; r < nranks; ++r) STATUS_TRY(make_rank(w.get(), r, w->device[r]));
+  w->live_comms = nranks;
+  *out = w.release();
+  return {};
+}
+
+namespace {
+struct PeerInfo {
+  int device;
+  int pid;
+  cudaIpcMemHandle_t flags;
+};
+struct RegInfo {
+  cudaIpcMemHandle_t handle;
+  uint64_t offset;
+  uint64_t bytes;
+};
+}  // namespace
+
+Status world_init_rank(int nranks, int rank, int device, cecoll_exchange_fn fn, void* ctx, World** out) {
+  if (!driver_api()) return fail(CECOLL_NO_DEVICE, "no CUDA driver / device");
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks || !fn)
+    return fail(CECOLL_INVALID_ARGUMENT, "bad rank / nranks / exchange");
+  DeviceGuard g(device);
+  auto w = std::make_unique<World>();
+  w->nranks = nranks;
+  w->multiprocess = true;
+  w->device.assign(nranks, -1);
+  w->flag_page.assign(nranks, nullptr);
+  w->local.resize(nranks);
+  w->device[rank] = device;
+  STATUS_TRY(make_rank(w.get(), rank, device));
+  PeerInfo mine;
+  std::memset(&mine, 0, sizeof(mine));
+  mine.device = device;
+  CUDA_TRY(cudaIpcGetMemHandle(&mine.flags, w->local[rank]->flags));
+  std::vector<PeerInfo> all(nranks);
+  if (fn(ctx, &mine, sizeof(PeerInfo), all.data()) != 0) return fail(CECOLL_INTERNAL, "exchange failed");
+  for (int r = 0; r < nranks; ++r) {
+    w->device[r] = all[r].device;
+    if (r == rank) continue;
+    void* p = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, all[r].flags, cudaIpcMemLazyEnablePeerAccess));
+    w->ipc_opened.push_back(p);
+    w->flag_page[r] = static_cast<uint64_t*>(p);
+  }
+  w->ndevices = count_devices(w->device);
+  w->live_comms = 1;
+  *out = w.release();
+  return {};
+}
+
+Status world_register(World* w, int rank, void* ptr, size_t bytes, cecoll_exchange_fn fn, void* ctx) {
+  if (!w->multiprocess) return {};  // single process: UVA pointers are used as is
+  DeviceGuard g(w->device[rank]);
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  CU_TRY(driver_api()->MemGetAddressRange(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)));
+  RegInfo mine;
+  std::memset(&mine, 0, sizeof(mine));
+  CUDA_TRY(cudaIpcGetMemHandle(&mine.handle, reinterpret_cast<void*>(base)));
+  mine.offset = reinterpret_cast<uint64_t>(ptr) - base;
+  mine.bytes = bytes;
+  std::vector<RegInfo> all(w->nranks);
+  if (fn(ctx, &mine, sizeof(RegInfo), all.data()) != 0) return fail(CECOLL_INTERNAL, "exchange failed");
+  Window win;
+  win.base = static_cast<char*>(ptr);
+  win.bytes = bytes;
+  win.peer_base.assign(w->nranks, nullptr);
+  for (int r = 0; r < w->nranks; ++r) {
+    if (all[r].bytes != bytes)
+      return fail(CECOLL_INVALID_ARGUMENT, "cecoll_register: windows must be symmetric (same size on every rank)");
+    if (r == rank) {
+      win.peer_base[r] = static_cast<char*>(ptr);
+      continue;
+    }
+    void* p = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, all[r].handle, cudaIpcMemLazyEnablePeerAccess));
+    w->ipc_opened.push_back(p);
+    win.peer_base[r] = static_cast<char*>(p) + all[r].offset;
+  }
+  w->windows.push_back(std::move(win));
+  return {};
+}
+
+Status world_deregister(World* w, void* ptr) {
+  for (size_t i = 0; i < w->windows.size(); ++i)
+    if (w->windows[i].base == ptr) {
+      w->windows.erase(w->windows.begin() + i);
+      return {};
+    }
+  return w->multiprocess ? fail(CECOLL_NOT_REGISTERED, "pointer was not registered") : Status{};
+}
+
+void world_release(World* w) {
+  for (auto& p : w->plans) plan_destroy(w, p.get());
+  w->plans.clear();
+  for (auto& rs : w->local) {
+    if (!rs) continue;
+    DeviceGuard g(rs->device);
+    cudaDeviceSynchronize();
+    for (auto s : rs->lanes) cudaStreamDestroy(s);
+    for (auto e : rs->lane_done) cudaEventDestroy(e);
+    if (rs->start) cudaEventDestroy(rs->start);
+    if (rs->flags) cudaFree(rs->flags);
+  }
+  for (void* p : w->ipc_opened) cudaIpcCloseMemHandle(p);
+  delete w;
+}
+
+// ---------------------------------------------------------------------------
+// Plan lowering
+// ---------------------------------------------------------------------------
+
+namespace {
+
+struct Addressing {
+  std::vector<const char*> send;  // per rank, usable in this process
+  std::vector<char*> recv;
+};
+
+char* translate(World* w, int target, const void* mine, bool* ok) {
+  const char* p = static_cast<const char*>(mine);
+  for (const Window& win : w->windows)
+    if (p >= win.base && p < win.base + win.bytes) return win.peer_base[target] + (p - win.base);
+  *ok = false;
+  return nullptr;
+}
+
+uint64_t* slot(World* w, int rank, int index) { return w->flag_page[rank] + index; }
+
+Status upload_items(World* w, Plan* p, int device, std::vector<Item>& items, Item** out) {
+  (void)w;
+  DeviceGuard g(device);
+  int64_t tiles = 0;
+  for (Item& it : items) {
+    it.first_tile = static_cast<int32_t>(tiles);
+    tiles += tiles_for(it.bytes);
+  }
+  if (tiles > INT32_MAX) return fail(CECOLL_INVALID_ARGUMENT, "collective too large for one launch");
+  void* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, sizeof(Item) * items.size()));
+  CUDA_TRY(cudaMemcpy(d, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice));
+  p->dev_allocs.push_back(d);
+  p->dev_alloc_device.push_back(device);
+  *out = static_cast<Item*>(d);
+  return {};
+}
+
+Status upload_ptrs(Plan* p, int device, const std::vector<uint64_t*>& ptrs, uint64_t*** out) {
+  *out = nullptr;
+  if (ptrs.empty()) return {};
+  DeviceGuard g(device);
+  void* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, sizeof(uint64_t*) * ptrs.size()));
+  CUDA_TRY(cudaMemcpy(d, ptrs.data(), sizeof(uint64_t*) * ptrs.size(), cudaMemcpyHostToDevice));
+  p->dev_allocs.push_back(d);
+  p->dev_alloc_device.push_back(device);
+  *out = static_cast<uint64_t**>(d);
+  return {};
+}
+
+int64_t item_tiles(const std::vector<Item>& items) {
+  int64_t t = 0;
+  for (const Item& it : items) t += tiles_for(it.bytes);
+  return t;
+}
+
+}  // namespace
+
+Status build_graph(World* w, Plan* p, Unit& u);
+
+Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args, Plan** out) {
+  const int n = w->nranks;
+  if (s <= 0) return fail(CECOLL_INVALID_ARGUMENT, "collective: chunk size must be positive");
+  auto plan = std::make_unique<Plan>();
+  Plan* p = plan.get();
+  p->kind = kind;
+  p->chunk = s;
+  for (const CallArgs& a : args) {
+    p->key_rank.push_back(a.rank);
+    p->key_send.push_back(a.send);
+    p->key_recv.push_back(a.recv);
+    p->key_stream.push_back(a.stream);
+  }
+  if (impl == Impl::Auto) impl = select(kind, s, n, w->ndevices);
+  if (impl != Impl::Sm && !valid_for(impl, kind))
+    return fail(CECOLL_UNSUPPORTED, std::string(impl_name(impl)) + " does not apply to " +
+                                         (kind == Kind::AllGather ? "allgather" : "alltoall"));
+  const bool in_place_impl = base_of(impl) == Impl::Swap;
+  p->impl = impl;
+  p->sm = impl == Impl::Sm;
+  p->prelaunch = is_prelaunched(impl);
+
+  // Addresses of every rank's buffers as usable from this process.
+  Addressing ad;
+  ad.send.assign(n, nullptr);
+  ad.recv.assign(n, nullptr);
+  std::vector<bool> have(n, false);
+  for (const CallArgs& a : args) {
+    if (a.rank < 0 || a.rank >= n || !w->local[a.rank]) return fail(CECOLL_INVALID_ARGUMENT, "rank not local");
+    if (have[a.rank]) return fail(CECOLL_INVALID_ARGUMENT, "rank appears twice in one group");
+    have[a.rank] = true;
+    ad.send[a.rank] = static_cast<const char*>(a.send);
+    ad.recv[a.rank] = static_cast<char*>(a.recv);
+  }
+  if (!w->multiprocess) {
+    for (int r = 0; r < n; ++r)
+      if (!have[r])
+        return fail(CECOLL_INVALID_ARGUMENT,
+                    "single-process communicator: every rank must take part (use cecoll_group_start/end)");
+  } else {
+    if (args.size() != 1) return fail(CECOLL_INVALID_ARGUMENT, "multi-process: one local rank per call");
+    const CallArgs& a = args[0];
+    for (int r = 0; r < n; ++r) {
+      if (r == a.rank) continue;
+      bool ok = true;
+      ad.send[r] = translate(w, r, a.send, &ok);
+      ad.recv[r] = translate(w, r, a.recv, &ok);
+      if (!ok) return fail(CECOLL_NOT_REGISTERED, "send/recv must lie in a window registered with cecoll_register");
+    }
+  }
+  for (const CallArgs& a : args) {
+    const bool aliased = a.send == a.recv;
+    if (kind == Kind::AllToAll && aliased && !in_place_impl)
+      return fail(CECOLL_INVALID_ARGUMENT, "alltoall in place requires the swap implementation");
+  }
+
+  // Units: local ranks sharing (device, stream).
+  std::vector<int> unit_of(n, -1);
+  for (const CallArgs& a : args) {
+    int found = -1;
+    for (size_t u = 0; u < p->units.size(); ++u)
+      if (p->units[u].device == w->device[a.rank] && p->units[u].stream == a.stream) found = static_cast<int>(u);
+    if (found < 0) {
+      Unit u;
+      u.device = w->device[a.rank];
+      u.stream = a.stream;
+      p->units.push_back(u);
+      found = static_cast<int>(p->units.size()) - 1;
+    }
+    p->units[found].ranks.push_back(a.rank);
+    unit_of[a.rank] = found;
+  }
+  for (Unit& u : p->units) std::sort(u.ranks.begin(), u.ranks.end());
+  auto same_unit = [&](int a, int b) { return unit_of[a] >= 0 && unit_of[a] == unit_of[b]; };
+
+  // Buffer of a program region. In-place programs (swap) address the
+  // in-place buffer as Input (compiler.cpp:119-122); it is `recv`.
+  auto base = [&](int rank, Buf b) -> char* {
+    if (in_place_impl || b == Buf::Output) return ad.recv[rank];
+    return const_cast<char*>(ad.send[rank]);
+  };
+  auto addr = [&](const Region& r) { return base(r.rank, r.buf) + r.off; };
+
+  // Edges writer -> destination and the flag operations they imply.
+  std::vector<std::pair<int, int>> edges;
+  if (p->sm) {
+    for (int r = 0; r < n; ++r)
+      for (int d = 1; d < n; ++d) edges.push_back({r, (r + d) % n});
+  } else {
+    if (n < 2) return fail(CECOLL_INVALID_ARGUMENT, "collective: gpu_count must be >= 2");
+    Spec spec;
+    spec.kind = kind;
+    spec.chunk = s;
+    spec.nranks = n;
+    try {
+      p->program = compile(impl, spec, kMaxLanes);
+    } catch (const std::invalid_argument& e) {
+      return fail(CECOLL_INVALID_ARGUMENT, e.what());
+    }
+    for (const Lane& l : p->program.lanes)
+      for (const Command& c : l.cmds) {
+        if (!c.moves_data()) continue;
+        const Region* ds[3] = {&c.dst, c.op == Op::Broadcast ? &c.dst2 : nullptr, nullptr};
+        if (c.op == Op::Swap) ds[0] = &c.peer;
+        for (const Region* d : ds)
+          if (d && d->rank != l.rank) edges.push_back({l.rank, d->rank});
+      }
+  }
+  for (auto [r, j] : edges) {
+    if (same_unit(r, j)) continue;
+    if (unit_of[j] >= 0) {  // j is local: it announces readiness and waits for r's data
+      Unit& u = p->units[unit_of[j]];
+      u.start.push_back(op_write(slot(w, r, kSlotRdy + j), 1));
+      add_poll(u.finish, slot(w, j, kSlotDone + r));
+    }
+    if (unit_of[r] >= 0 && p->sm) {  // r is local: wait for j, then signal it
+      Unit& u = p->units[unit_of[r]];
+      add_poll(u.sm_pre, slot(w, r, kSlotRdy + j));
+      u.sm_post.push_back(op_write(slot(w, j, kSlotDone + r), 1));
+    }
+  }
+
+  // Local-slot placement (verifier.cpp:40-44) and the swap pre-copy.
+  for (Unit& u : p->units)
+    for (int r : u.ranks) {
+      if (in_place_impl) {
+        if (ad.send[r] != ad.recv[r])
+          u.precopy.push_back({ad.recv[r], ad.send[r], s * n});
+        continue;
+      }
+      const char* src = ad.send[r] + (kind == Kind::AllGather ? 0 : r * s);
+      char* dst = ad.recv[r] + r * s;
+      if (src != dst) u.placement.push_back({dst, src, s});
+    }
+
+  if (p->sm) {
+    for (Unit& u : p->units) {
+      std::vector<Item> items;
+      for (int r : u.ranks) {
+        for (const Copy& c : u.placement)
+          if (c.dst == ad.recv[r] + r * s) items.push_back({c.src, c.dst, nullptr, c.bytes, kItemCopy, 0});
+        for (int d = 1; d < n; ++d) {
+          const int j = (r + d) % n;
+          const char* src = ad.send[r] + (kind == Kind::AllGather ? 0 : j * s);
+          items.push_back({src, ad.recv[j] + r * s, nullptr, s, kItemCopy, 0});
+        }
+      }
+      u.placement.clear();
+      u.nitems = static_cast<int>(items.size());
+      u.ntiles = static_cast<int>(item_tiles(items));
+      if (u.nitems > kMaxItemsSmem) return fail(CECOLL_INVALID_ARGUMENT, "too many items for one launch");
+      if (u.nitems) STATUS_TRY(upload_items(w, p, u.device, items, &u.items));
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->units[0].device);
+    p->sm_grid = sms * 4;
+  } else {
+    // Lanes of the command program owned by local ranks.
+    for (const Lane& l : p->program.lanes) {
+      if (unit_of[l.rank] < 0) continue;
+      LaneExec le;
+      le.rank = l.rank;
+      le.lane = l.index;
+      std::set<int> dests;
+      std::vector<Item> items;
+      for (const Command& c : l.cmds) {
+        switch (c.op) {
+          case Op::Copy:
+            le.copies.push_back({addr(c.dst), addr(c.src), c.size});
+            dests.insert(c.dst.rank);
+            break;
+          case Op::Broadcast:
+            items.push_back({addr(c.src), addr(c.dst), addr(c.dst2), c.size, kItemBcst, 0});
+            dests.insert(c.dst.rank);
+            dests.insert(c.dst2.rank);
+            break;
+          case Op::Swap:
+            items.push_back({addr(c.peer), addr(c.src), nullptr, c.size, kItemSwap, 0});
+            dests.insert(c.peer.rank);
+            break;
+          default: break;  // Signal / Poll: realised by the flag operations below
+        }
+      }
+      dests.erase(l.rank);
+      for (int j : dests) {
+        if (same_unit(l.rank, j)) continue;
+        add_poll(le.pre, slot(w, l.rank, kSlotRdy + j));
+        le.post.push_back(op_write(slot(w, j, kSlotDone + l.rank), 1));
+      }
+      if (!items.empty()) {
+        le.nitems = static_cast<int>(items.size());
+        le.ntiles = static_cast<int>(item_tiles(items));
+        STATUS_TRY(upload_items(w, p, w->device[l.rank], items, &le.items));
+      }
+      STATUS_TRY(ensure_lanes(w->local[l.rank].get(), l.index + 1));
+      p->lanes.push_back(std::move(le));
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->units[0].device);
+    p->sm_grid = sms * 4;
+    if (p->prelaunch)
+      for (Unit& u : p->units) STATUS_TRY(build_graph(w, p, u));
+  }
+  *out = plan.release();
+  return {};
+}
+
+// Records one unit's lanes into a graph: [gate kernel] -> IF{ poll kernel ->
+// lanes (copies, item kernels) + placement -> signal kernel }.
+Status build_graph(World* w, Plan* p, Unit& u) {
+  DeviceGuard g(u.device);
+  CUDA_TRY(cudaStreamCreateWithFlags(&u.arm, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&u.graph_done, cudaEventDisableTiming));
+  void* host = nullptr;
+  CUDA_TRY(cudaHostAlloc(&host, 4096, cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(host, 0, 4096);
+  u.posted = static_cast<uint64_t*>(host);
+  void* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, 64));
+  CUDA_TRY(cudaMemset(d, 0, 64));
+  p->dev_allocs.push_back(d);
+  p->dev_alloc_device.push_back(u.device);
+  u.consumed = static_cast<uint64_t*>(d);
+  u.err = static_cast<uint64_t*>(d) + 1;
+  u.ready_flag = slot(w, u.ranks[0], kSlotReady);
+
+  // Polls: the unit's own readiness word plus rdy from destinations in other
+  // units; signals: done to those destinations (from the lanes' memops).
+  std::vector<uint64_t*> polls{u.ready_flag}, sigs, fins;
+  for (const LaneExec& le : p->lanes) {
+    if (std::find(u.ranks.begin(), u.ranks.end(), le.rank) == u.ranks.end()) continue;
+    for (const auto& op : le.pre)
+      if (op.operation == CU_STREAM_MEM_OP_WAIT_VALUE_64) polls.push_back(reinterpret_cast<uint64_t*>(op.waitValue.address));
+    for (const auto& op : le.post) sigs.push_back(reinterpret_cast<uint64_t*>(op.writeValue.address));
+  }
+  for (const auto& op : u.finish)
+    if (op.operation == CU_STREAM_MEM_OP_WAIT_VALUE_64) fins.push_back(reinterpret_cast<uint64_t*>(op.waitValue.address));
+  u.npoll = static_cast<int>(polls.size());
+  u.nsig = static_cast<int>(sigs.size());
+  u.nfin = static_cast<int>(fins.size());
+  STATUS_TRY(upload_ptrs(p, u.device, polls, &u.poll_tab));
+  STATUS_TRY(upload_ptrs(p, u.device, sigs, &u.sig_tab));
+  STATUS_TRY(upload_ptrs(p, u.device, fins, &u.fin_tab));
+
+  CUDA_TRY(cudaGraphCreate(&u.graph, 0));
+  cudaGraphConditionalHandle handle;
+  CUDA_TRY(cudaGraphConditionalHandleCreate(&handle, u.graph, 0, cudaGraphCondAssignDefault));
+  uint64_t* posted_dev = nullptr;
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&posted_dev), u.posted, 0));
+
+  // Root: the gate kernel.
+  CUDA_TRY(cudaStreamBeginCaptureToGraph(u.arm, u.graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  cudaError_t le = launch_gate(posted_dev, u.consumed, handle, u.err, u.arm);
+  cudaGraph_t captured = nullptr;
+  cudaError_t ec = cudaStreamEndCapture(u.arm, &captured);
+  CUDA_TRY(le);
+  CUDA_TRY(ec);
+  size_t nnodes = 0;
+  CUDA_TRY(cudaGraphGetNodes(u.graph, nullptr, &nnodes));
+  std::vector<cudaGraphNode_t> nodes(nnodes);
+  CUDA_TRY(cudaGraphGetNodes(u.graph, nodes.data(), &nnodes));
+  if (nnodes != 1) return fail(CECOLL_INTERNAL, "gate capture produced an unexpected graph");
+
+  // cudaGraphNodeParams has no default constructor (union with non-trivial
+  // members): zero-initialised raw storage, as the runtime expects.
+  alignas(cudaGraphNodeParams) unsigned char cp_storage[sizeof(cudaGraphNodeParams)] = {};
+  cudaGraphNodeParams& cp = *reinterpret_cast<cudaGraphNodeParams*>(cp_storage);
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t if_node;
+  CUDA_TRY(cudaGraphAddNode(&if_node, u.graph, nodes.data(), 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+
+  // Body: poll -> fork lanes -> join -> signal.
+  CUDA_TRY(cudaStreamBeginCaptureToGraph(u.arm, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  Status st;
+  auto body_ops = [&]() -> Status {
+    CUDA_TRY(launch_poll(u.poll_tab, u.npoll, u.err, u.arm));
+    for (const Copy& c : u.placement) CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, u.arm));
+    cudaEvent_t fork;
+    CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(fork, u.arm));
+    for (const LaneExec& l : p->lanes) {
+      if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) == u.ranks.end()) continue;
+      RankState* rs = w->local[l.rank].get();
+      cudaStream_t ls = rs->lanes[l.lane];
+      CUDA_TRY(cudaStreamWaitEvent(ls, fork, 0));
+      for (const Copy& c : l.copies) CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, ls));
+      if (l.nitems) CUDA_TRY(launch_items(l.items, l.nitems, l.ntiles, p->sm_grid, ls));
+      CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], ls));
+      CUDA_TRY(cudaStreamWaitEvent(u.arm, rs->lane_done[l.lane], 0));
+    }
+    CUDA_TRY(launch_signal(u.sig_tab, u.nsig, u.arm));
+    cudaEventDestroy(fork);
+    return {};
+  };
+  st = body_ops();
+  cudaGraph_t body_out = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(u.arm, &body_out);
+  if (!st.ok()) return st;
+  CUDA_TRY(e2);
+  CUDA_TRY(cudaGraphInstantiate(&u.exec, u.graph, 0));
+  return {};
+}
+
+// ---------------------------------------------------------------------------
+// Execution
+// ---------------------------------------------------------------------------
+
+namespace {
+
+Status run_ce(World* w, Plan* p) {
+  const DriverApi* d = driver_api();
+  (void)d;
+  // Phase 1: every unit announces readiness (rdy), forks its lanes and places
+  // its own chunk. Phase 2: lanes poll rdy, copy, signal done. Phase 3: units
+  // poll done and join their lanes. Every poll is submitted after the signal
+  // it waits for, so streams that share a hardware queue cannot deadlock.
+  for (Unit& u : p->units) {
+    DeviceGuard g(u.device);
+    STATUS_TRY(issue_copies(w, u.precopy, u.stream, true));
+    STATUS_TRY(submit(w, u.stream, u.start));
+    for (int r : u.ranks) {
+      CUDA_TRY(cudaEventRecord(w->local[r]->start, u.stream));
+      ++w->counters[6];
+    }
+    STATUS_TRY(issue_copies(w, u.placement, u.stream, true));
+  }
+  for (LaneExec& l : p->lanes) {
+    RankState* rs = w->local[l.rank].get();
+    DeviceGuard g(rs->device);
+    cudaStream_t s = rs->lanes[l.lane];
+    CUDA_TRY(cudaStreamWaitEvent(s, rs->start, 0));
+    ++w->counters[6];
+    STATUS_TRY(submit(w, s, l.pre));
+    STATUS_TRY(issue_copies(w, l.copies, s, true));
+    if (l.nitems) {
+      CUDA_TRY(launch_items(l.items, l.nitems, l.ntiles, p->sm_grid, s));
+      ++w->counters[4];
+      ++w->counters[6];
+    }
+    STATUS_TRY(submit(w, s, l.post));
+    CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], s));
+    ++w->counters[6];
+  }
+  for (Unit& u : p->units) {
+    DeviceGuard g(u.device);
+    STATUS_TRY(submit(w, u.stream, u.finish));
+    for (const LaneExec& l : p->lanes) {
+      if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) == u.ranks.end()) continue;
+      CUDA_TRY(cudaStreamWaitEvent(u.stream, w->local[l.rank]->lane_done[l.lane], 0));
+      ++w->counters[6];
+    }
+  }
+  return {};
+}
+
+Status run_sm(World* w, Plan* p) {
+  for (Unit& u : p->units) {  // phase 1: readiness to sources in other units
+    DeviceGuard g(u.device);
+    STATUS_TRY(submit(w, u.stream, u.start));
+  }
+  for (Unit& u : p->units) {  // phase 2: wait destinations, move, signal
+    DeviceGuard g(u.device);
+    STATUS_TRY(submit(w, u.stream, u.sm_pre));
+    if (u.nitems) {
+      CUDA_TRY(launch_items(u.items, u.nitems, u.ntiles, p->sm_grid, u.stream));
+      ++w->counters[4];
+      ++w->counters[6];
+    }
+    STATUS_TRY(submit(w, u.stream, u.sm_post));
+  }
+  for (Unit& u : p->units) {  // phase 3: incoming chunks
+    DeviceGuard g(u.device);
+    STATUS_TRY(submit(w, u.stream, u.finish));
+  }
+  return {};
+}
+
+Status post_gate(Unit& u, uint64_t kind) {
+  const uint64_t k = u.posts++;
+  volatile uint64_t* posted = u.posted;
+  posted[1 + (k % 64)] = kind;
+  __atomic_thread_fence(__ATOMIC_SEQ_CST);
+  posted[0] = k + 1;
+  __atomic_thread_fence(__ATOMIC_SEQ_CST);
+  return {};
+}
+
+Status arm_unit(World* w, Unit& u) {
+  DeviceGuard g(u.device);
+  CUDA_TRY(cudaGraphLaunch(u.exec, u.arm));
+  CUDA_TRY(cudaEventRecord(u.graph_done, u.arm));
+  ++w->counters[5];
+  w->counters[6] += 2;
+  u.armed = true;
+  return {};
+}
+
+Status trigger_unit(World* w, Plan* p, Unit& u) {
+  DeviceGuard g(u.device);
+  STATUS_TRY(issue_copies(w, u.precopy, u.stream, true));
+  MemOps ops = u.start;
+  ops.push_back(op_write(u.ready_flag, 1));
+  STATUS_TRY(submit(w, u.stream, ops));
+  STATUS_TRY(post_gate(u, 1));
+  u.armed = false;
+  if (u.nfin) {
+    CUDA_TRY(launch_poll(u.fin_tab, u.nfin, u.err, u.stream));
+    ++w->counters[4];
+    ++w->counters[6];
+  }
+  CUDA_TRY(cudaStreamWaitEvent(u.stream, u.graph_done, 0));
+  ++w->counters[6];
+  (void)p;
+  return {};
+}
+
+bool same_call(const Plan* p, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args) {
+  if (p->kind != kind || p->chunk != s || p->key_rank.size() != args.size()) return false;
+  if (p->impl != impl) return false;
+  for (size_t i = 0; i < args.size(); ++i)
+    if (p->key_rank[i] != args[i].rank || p->key_send[i] != args[i].send || p->key_recv[i] != args[i].recv ||
+        p->key_stream[i] != args[i].stream)
+      return false;
+  return true;
+}
+
+}  // namespace
+
+Status plan_arm(World* w, Plan* p) {
+  if (!p->prelaunch) return {};
+  for (Unit& u : p->units)
+    if (!u.armed) STATUS_TRY(arm_unit(w, u));
+  return {};
+}
+
+Status plan_launch(World* w, Plan* p, bool rearm) {
+  ++w->counters[0];
+  if (p->sm) return run_sm(w, p);
+  if (!p->prelaunch) return run_ce(w, p);
+  // prelaunch: make sure every unit is armed, trigger all, re-arm if asked.
+  STATUS_TRY(plan_arm(w, p));
+  for (Unit& u : p->units) STATUS_TRY(trigger_unit(w, p, u));
+  if (rearm) STATUS_TRY(plan_arm(w, p));
+  return {};
+}
+
+Status plan_destroy(World* w, Plan* p) {
+  (void)w;
+  for (Unit& u : p->units) {
+    DeviceGuard g(u.device);
+    if (u.armed) {
+      post_gate(u, 2);  // cancel: the gate skips the body
+      cudaStreamSynchronize(u.arm);
+      u.armed = false;
+    }
+    if (u.exec) cudaGraphExecDestroy(u.exec);
+    if (u.graph) cudaGraphDestroy(u.graph);
+    if (u.arm) {
+      cudaStreamSynchronize(u.arm);
+      cudaStreamDestroy(u.arm);
+    }
+    if (u.graph_done) cudaEventDestroy(u.graph_done);
+    if (u.posted) cudaFreeHost(u.posted);
+  }
+  for (size_t i = 0; i < p->dev_allocs.size(); ++i) {
+    DeviceGuard g(p->dev_alloc_device[i]);
+    cudaFree(p->dev_allocs[i]);
+  }
+  p->dev_allocs.clear();
+  return {};
+}
+
+Status run_collective(World* w, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args) {
+  if (impl == Impl::Auto) impl = select(kind, s, w->nranks, w->ndevices);
+  Plan* p = nullptr;
+  for (auto& cand : w->plans)
+    if (same_call(cand.get(), kind, impl, s, args)) {
+      p = cand.get();
+      break;
+    }
+  if (!p) {
+    STATUS_TRY(plan_create(w, kind, impl, s, args, &p));
+    w->plans.emplace_back(p);
+    if (w->plans.size() > 64) {  // bounded cache: drop the oldest plan
+      for (Unit& u : w->plans.front()->units) {
+        DeviceGuard g(u.device);
+        cudaStreamSynchronize(u.stream);
+      }
+      plan_destroy(w, w->plans.front().get());
+      w->plans.erase(w->plans.begin());
+    }
+  }
+  // Eager calls never leave an instance armed after returning (a waiting
+  // graph would block device-wide synchronisation); explicit plans do.
+  return plan_launch(w, p, false);
+}
+
+}  // namespace cecoll

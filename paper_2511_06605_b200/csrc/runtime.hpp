@@ -1,0 +1,187 @@
+// Communicator, plans and executors.
+//
+// Execution model:
+//  * A World is every rank this process can address. comm_init_all builds one
+//    World whose ranks are all local (one host thread drives every device, the
+//    reference's single host process); comm_init_rank builds one
+//    local rank per process and maps the peers' flag pages and registered
+//    windows through CUDA IPC.
+//  * A unit is the set of local ranks that share a device and a caller
+//    stream; stream order already orders their readiness and completion.
+//    Between units synchronisation is flag based (§2.4 atomic and
+//    poll commands; program.hpp:47): every rank owns a page of u64 slots in
+//    device memory. rdy[j] in rank r's page is written by rank j when j's
+//    destination buffer may be written by r; done[i] in rank r's page is
+//    written after rank i's chunk landed in r. Waiters reset a slot to 0 in
+//    the same batch, so recorded graphs replay with constant values, and a
+//    slot's next write is always causally after its reset.
+//  * A Plan is a Program (program.hpp) lowered onto concrete buffers: per lane
+//    the polls, the copy-engine copies or kernel items, and the signals; per
+//    unit the start/finish flag operations, the SM item table and, for
+//    prelaunch_*, the recorded graph. Plans are cached per call signature.
+#pragma once
+
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "cecoll.h"
+#include "cu_driver.hpp"
+#include "kernels.hpp"
+#include "program.hpp"
+
+namespace cecoll {
+
+constexpr int kMaxRanks = 32;
+constexpr int kMaxLanes = 32;
+// Flag page layout (u64 slots).
+constexpr int kSlotRdy = 0;             // rdy[j], j < kMaxRanks
+constexpr int kSlotDone = kMaxRanks;    // done[i]
+constexpr int kSlotReady = 2 * kMaxRanks;  // unit-ready word of a prelaunch graph
+constexpr size_t kFlagBytes = 4096;
+
+struct Status {
+  int code = 0;
+  std::string msg;
+  bool ok() const { return code == 0; }
+};
+
+struct RankState {
+  int rank = -1;
+  int device = -1;
+  std::vector<cudaStream_t> lanes;
+  std::vector<cudaEvent_t> lane_done;
+  cudaEvent_t start = nullptr;
+  uint64_t* flags = nullptr;  // own flag page (device memory)
+};
+
+struct Window {  // a registered range (multi-process) and its image in every rank
+  char* base = nullptr;
+  size_t bytes = 0;
+  std::vector<char*> peer_base;
+};
+
+struct Plan;
+
+struct World {
+  int nranks = 0;
+  bool multiprocess = false;
+  int ndevices = 1;
+  std::vector<int> device;           // per rank
+  std::vector<uint64_t*> flag_page;  // per rank, usable from this process
+  std::vector<std::unique_ptr<RankState>> local;  // by rank; null if remote
+  std::atomic<int64_t> counters[8];
+  std::vector<std::unique_ptr<Plan>> plans;  // eager-call plan cache
+  std::vector<Window> windows;
+  std::vector<void*> ipc_opened;
+  int live_comms = 0;
+  World() {
+    for (auto& c : counters) c = 0;
+  }
+};
+
+struct Copy {
+  char* dst;
+  const char* src;
+  int64_t bytes;
+};
+
+using MemOps = std::vector<CUstreamBatchMemOpParams>;
+
+struct LaneExec {
+  int rank = 0;
+  int lane = 0;
+  MemOps pre;                 // rdy polls (+ resets) for destinations in other units
+  std::vector<Copy> copies;   // copy commands
+  Item* items = nullptr;      // device table for Broadcast / Swap commands
+  int nitems = 0, ntiles = 0;
+  MemOps post;                // done signals to destinations in other units
+};
+
+struct Unit {
+  int device = -1;
+  cudaStream_t stream = nullptr;  // shared caller stream
+  std::vector<int> ranks;         // local ranks, ascending
+  MemOps start;                   // rdy signals to sources in other units
+  MemOps finish;                  // done polls (+ resets) from sources in other units
+  MemOps sm_pre, sm_post;         // SM path: rdy polls / done signals
+  std::vector<Copy> placement;    // local-slot placement (verifier.cpp:40-44)
+  std::vector<Copy> precopy;      // swap with send != recv: send -> recv first
+  Item* items = nullptr;          // SM path table
+  int nitems = 0, ntiles = 0;
+  // prelaunch graph
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t arm = nullptr;
+  cudaEvent_t graph_done = nullptr;
+  uint64_t* posted = nullptr;      // pinned host: [0] count, [1..64] kinds
+  uint64_t* consumed = nullptr;    // device
+  uint64_t* err = nullptr;         // device
+  uint64_t** poll_tab = nullptr;   // device array of flag pointers
+  uint64_t** sig_tab = nullptr;
+  uint64_t** fin_tab = nullptr;
+  int npoll = 0, nsig = 0, nfin = 0;
+  uint64_t* ready_flag = nullptr;  // device word the caller stream writes
+  bool armed = false;
+  uint64_t posts = 0;
+};
+
+struct Plan {
+  Kind kind = Kind::AllGather;
+  Impl impl = Impl::Pcpy;
+  int64_t chunk = 0;
+  std::vector<const void*> key_send;
+  std::vector<void*> key_recv;
+  std::vector<cudaStream_t> key_stream;
+  std::vector<int> key_rank;
+  std::vector<LaneExec> lanes;
+  std::vector<Unit> units;
+  std::vector<void*> dev_allocs;
+  std::vector<int> dev_alloc_device;
+  Program program;
+  bool sm = false;
+  bool prelaunch = false;
+  int sm_grid = 0;
+};
+
+void set_error(const std::string& msg);
+const char* last_error();
+
+Status world_init_all(int nranks, const int* devlist, World** out);
+Status world_init_rank(int nranks, int rank, int device, cecoll_exchange_fn fn, void* ctx, World** out);
+void world_release(World* w);
+Status world_register(World* w, int rank, void* ptr, size_t bytes, cecoll_exchange_fn fn, void* ctx);
+Status world_deregister(World* w, void* ptr);
+
+struct CallArgs {
+  int rank;
+  const void* send;
+  void* recv;
+  cudaStream_t stream;
+};
+
+Status run_collective(World* w, Kind kind, Impl impl, int64_t chunk, const std::vector<CallArgs>& args);
+
+Status plan_create(World* w, Kind kind, Impl impl, int64_t chunk, const std::vector<CallArgs>& args, Plan** out);
+Status plan_arm(World* w, Plan* p);
+Status plan_launch(World* w, Plan* p, bool rearm);
+Status plan_destroy(World* w, Plan* p);
+
+}  // namespace cecoll
+
+struct cecoll_comm {
+  cecoll::World* world;
+  int rank;
+};
+
+struct cecoll_plan {
+  cecoll::World* world;
+  cecoll::Plan* plan;
+};

@@ -1,0 +1,107 @@
+"""The product's planner (libcecoll.so, C ABI) against the reference's goldens.
+
+CPU only: the planner emits the exact command program the executors lower
+onto the GPU, so its dump_program text, metrics and traffic must equal the
+reference's (tests/golden/programs.json, from proj/src/compiler.cpp).
+"""
+import json
+import os
+import re
+
+import pytest
+
+import paper_2511_06605_b200 as cc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def test_library_exports_every_declared_symbol():
+    L = cc.lib()
+    with open(os.path.join(ROOT, "include", "cecoll.h")) as f:
+        header = f.read()
+    declared = set(re.findall(r"\b(cecoll_[a-z_0-9]+)\s*\(", header))
+    declared -= {"cecoll_exchange_fn"}
+    assert declared, "no declarations parsed"
+    for name in sorted(declared):
+        assert hasattr(L, name), name
+    assert set(cc.EXPORTED_SYMBOLS) <= declared
+
+
+def test_programs_match_reference_goldens():
+    with open(os.path.join(GOLDEN, "programs.json")) as f:
+        data = json.load(f)
+    import hashlib
+
+    for e in data["programs"]:
+        p = cc.Program(e["kind"], e["impl"], e["s"], e["n"])
+        text = p.dump()
+        assert hashlib.sha256(text.encode()).hexdigest() == e["dump_sha256"], (e["kind"], e["impl"], e["n"])
+        if "dump" in e:
+            assert text == e["dump"]
+        m = p.metrics()
+        assert [m[k] for k in ("data_commands", "sync_commands", "poll_commands", "engines_used", "doorbells")] == e[
+            "metrics"
+        ]
+        t = p.traffic()
+        assert [t["read"], t["write"], t["link"]] == e["traffic"]
+        assert t["rank_read"] == e["per_gpu_read"] and t["rank_write"] == e["per_gpu_write"]
+        assert p.validate() is None
+        assert e["valid"]
+
+
+def test_rejections_match_reference():
+    with open(os.path.join(GOLDEN, "programs.json")) as f:
+        data = json.load(f)
+    for r in data["rejects"]:
+        if r["accepted"]:
+            cc.Program(r["kind"], r["impl"], r["s"], r["n"])
+        else:
+            with pytest.raises(cc.InvalidArgument):
+                cc.Program(r["kind"], r["impl"], r["s"], r["n"])
+
+
+def test_reference_select_table():
+    with open(os.path.join(GOLDEN, "select.json")) as f:
+        table = json.load(f)
+    for kind, rows in table.items():
+        for size, name in rows:
+            assert cc.reference_select(kind, size) == name, (kind, size)
+
+
+def test_impl_names_round_trip():
+    L = cc.lib()
+    for name, v in cc.IMPLS.items():
+        if name == "auto":
+            continue
+        assert L.cecoll_parse_impl(name.encode()) == v
+        if name != "baseline":
+            assert cc.impl_name(v) == name
+    assert L.cecoll_parse_impl(b"nope") == -2
+    assert L.cecoll_impl_valid_for(1, 0) == 1 and L.cecoll_impl_valid_for(1, 1) == 0  # bcst: AG only
+    assert L.cecoll_impl_valid_for(2, 1) == 1 and L.cecoll_impl_valid_for(2, 0) == 0  # swap: AA only
+
+
+def test_prelaunch_adds_one_poll_per_lane_and_keeps_traffic():
+    base = cc.Program("allgather", "pcpy", 4096, 8)
+    pre = cc.Program("allgather", "prelaunch_pcpy", 4096, 8)
+    mb, mp = base.metrics(), pre.metrics()
+    assert mp["poll_commands"] == mb["engines_used"] == 56
+    assert mp["data_commands"] == mb["data_commands"]
+    assert pre.traffic() == base.traffic()
+    assert all(line.split("\t")[2] == "poll" for line in pre.dump().splitlines() if line.split("\t")[1] == "0")
+
+
+def test_engine_budget_is_enforced():
+    with pytest.raises(cc.InvalidArgument):
+        cc.Program("allgather", "pcpy", 4096, 8, lanes_per_rank=6)  # needs n-1 = 7 lanes
+    cc.Program("allgather", "b2b", 4096, 8, lanes_per_rank=1)
+
+
+def test_comm_init_without_gpu_fails_loudly():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(cc.CecollError):
+        cc.Comm.init_all([0, 0])
