@@ -1,0 +1,343 @@
+"""cecoll benchmark (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): all-to-all over 8 ranks with a 64 MiB
+send buffer per rank (per-peer chunk s = 8 MiB, SURVEY.md §8 sizing). With
+one GPU the 8 ranks are co-resident on it (comm_init_all with a repeated
+device), so every chunk transfer is an HBM->HBM copy through the executor.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--algo auto|sm|pcpy|b2b|prelaunch_pcpy|...] [--sweep]
+
+A step is one collective over the synthetic inputs. `value` is the
+nccl-tests bus bandwidth of the 8-rank collective, busBW = (n-1)*s/t, with
+inputs resident in HBM; `e2e` is the same metric through the public API with
+the inputs copied from pinned host memory and the results copied back inside
+the timed region. `--impl reference` times the reference's CPU path (the
+reference's own compile() from oracle/_ref plus the byte executor) on the
+host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import paper_2511_06605_b200 as cc  # noqa: E402  (sets CUDA_DEVICE_MAX_CONNECTIONS first)
+
+NRANKS = 8
+SEND_PER_RANK = 64 << 20
+CHUNK = SEND_PER_RANK // NRANKS  # s = 8 MiB
+METRIC = "alltoall_busbw_8ranks_x_64MiB"
+WORKLOAD = "alltoall, 8 ranks x 64 MiB send/rank (s = 8 MiB per peer), BASELINE configs[1]"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+def load_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_items_kernel.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index=0):
+        self.proc = None
+        self.lines = []
+        self.gpu = gpu_index
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def busbw(n, s, seconds):
+    return (n - 1) * s / seconds / 1e9
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's CPU path on the host cores
+# ---------------------------------------------------------------------------
+
+
+def cpu_reference_step(kind="alltoall", n=NRANKS, s=CHUNK, impl="pcpy", budget_s=None):
+    """One CPU collective over the full workload; returns (seconds, kind, cores, sample)."""
+    import numpy as np
+
+    from oracle import oracle as ora
+
+    in_bytes = s if kind == "allgather" else n * s
+    ins = [ora.splitmix_pattern(in_bytes, r) for r in range(n)]
+    outs = [np.empty(n * s, dtype=np.uint8) for _ in range(n)]
+    if os.path.exists(ora.REF_LIB):
+        R = ora.Reference()
+        ptr_in = ora._ptrs(ins)
+        ptr_out = ora._ptrs(outs)
+
+        def once():
+            rc = R.L.ref_execute(kind.encode(), impl.encode(), s, n, ptr_in, ptr_out)
+            assert rc == 0
+
+        label = "reference"
+    else:
+        O = ora.Oracle()
+        p = O.compile(kind, impl, s, n)
+
+        def once():
+            O.execute(p, ins, outs)
+
+        label = "port"
+    once()  # warm the pages
+    t0 = time.perf_counter()
+    once()
+    dt = time.perf_counter() - t0
+    return dt, label, 1, f"{kind} {impl} n={n} s={s} (full workload, reference compile() + byte executor)"
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    times = []
+    for _ in range(args.warmup):
+        cpu_reference_step()
+    label, cores, sample = None, 1, ""
+    for _ in range(args.steps):
+        dt, label, cores, sample = cpu_reference_step()
+        times.append(dt)
+    t = sum(times) / len(times)
+    v = busbw(NRANKS, CHUNK, t)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(v, 3),
+        "unit": "GB/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3, 3),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic splitmix64 pattern",
+        "config": {"workload": WORKLOAD, "ranks": NRANKS, "chunk_bytes": CHUNK, "device": "host CPU"},
+        "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": cores, "kind": label, "sample": sample},
+        "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        return run_ours_multiprocess(args)
+    dev = 0
+    torch.cuda.set_device(dev)
+    n, s = NRANKS, CHUNK
+    comms = cc.Comm.init_all([dev] * n)
+    stream = torch.cuda.Stream()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    sends = [torch.randint(0, 256, (n * s,), dtype=torch.uint8, device="cuda", generator=g) for _ in range(n)]
+    recvs = [torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    impl = args.algo
+    chosen = cc.select("alltoall", s, n, 1) if impl == "auto" else impl
+    torch.cuda.synchronize()
+
+    def step():
+        cc.all_to_all(comms, sends, recvs, s, impl=chosen, streams=stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, args.warmup)):
+            step()
+    torch.cuda.synchronize()
+    c0 = comms[0].counters()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clocks:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    c1 = comms[0].counters()
+    ms = e0.elapsed_time(e1) / args.steps
+    value = busbw(n, s, ms / 1e3)
+
+    # Parity of the timed buffers against the definition (cheap device check).
+    ok = all(torch.equal(recvs[j][i * s:(i + 1) * s], sends[i][j * s:(j + 1) * s])
+             for i in range(n) for j in (0, n - 1))
+
+    # Roofline of the dominant kernel: one launch moves every chunk (n*n*s
+    # bytes read + written; the local placement included).
+    peak, peak_kind = load_peaks()
+    alg_bytes = 2 * n * n * s
+    achieved = alg_bytes / (ms / 1e3) / 1e9
+    kernels_per_step = (c1["kernels"] - c0["kernels"]) / args.steps
+    graphs_per_step = (c1["graph_launches"] - c0["graph_launches"]) / args.steps
+
+    # e2e: pinned host inputs -> HBM -> collective -> HBM -> pinned host results.
+    host_in = [torch.empty(n * s, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
+    host_out = [torch.empty(n * s, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
+    for h, d in zip(host_in, sends):
+        h.copy_(d)
+    e2e_steps = max(2, min(args.steps, 5))
+
+    def e2e_step():
+        for h, d in zip(host_in, sends):
+            d.copy_(h, non_blocking=True)
+        step()
+        for h, d in zip(host_out, recvs):
+            h.copy_(d, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        e2e_step()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    e2e_value = busbw(n, s, e2e_ms / 1e3)
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        dt, label, cores, sample = cpu_reference_step()
+        cpu = {"value": round(busbw(n, s, dt), 3), "unit": "GB/s", "cores": cores, "kind": label,
+               "sample": sample + f"; {dt * 1e3:.1f} ms"}
+
+    line = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "GB/s",
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": max(3, args.warmup),
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic (torch.randint bytes)",
+        "config": {
+            "workload": WORKLOAD,
+            "ranks": n,
+            "ranks_per_gpu": n,
+            "chunk_bytes": s,
+            "impl": chosen,
+            "l2": "inputs larger than L2 (1 GiB touched per step vs 126 MB L2)",
+            "aggregate_gbs": round(n * value, 3),
+            "algbw_gbs": round(n * s / (ms / 1e3) / 1e9, 3),
+        },
+        "parity_ok": bool(ok),
+        "roofline": {
+            "bound": "hbm",
+            "achieved": round(achieved, 1),
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": load_traffic(),
+            "peak_source": peak_kind + " hbm_gbs (copy, read+write)",
+            "algorithmic_bytes_per_launch": alg_bytes,
+        },
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": n * n * s,
+                "d2h_bytes_per_step": n * n * s, "ms_per_step": round(e2e_ms, 3)},
+        "gpu_launches": int(round((kernels_per_step + 4 * graphs_per_step) * args.steps)),
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    cc.destroy_all(comms)
+
+
+def run_ours_multiprocess(args):
+    raise SystemExit("multi-GPU bench: see DESIGN.md §6 (not measured this round)")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--algo", default="auto")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

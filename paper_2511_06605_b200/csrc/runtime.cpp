@@ -112,7 +112,9 @@ Status submit(World* w, cudaStream_t s, const MemOps& ops) {
 
 Status issue_copies(World* w, const std::vector<Copy>& copies, cudaStream_t s, bool allow_batch) {
   const DriverApi* d = driver_api();
-  if (copies.size() > 1 && allow_batch && d->has_batch_memcpy) {
+  // cuMemcpyBatchAsync rejects the legacy NULL stream.
+  const bool legacy = s == nullptr || s == cudaStreamLegacy;
+  if (copies.size() > 1 && allow_batch && d->has_batch_memcpy && !legacy) {
     std::vector<CUdeviceptr> dst, src;
     std::vector<size_t> sz;
     for (const Copy& c : copies) {
