@@ -91,6 +91,13 @@ cecoll_status_t cecoll_program_traffic(cecoll_program_t program, int64_t out3[3]
  * with cecoll_last_error() naming the first violation. */
 cecoll_status_t cecoll_program_validate(cecoll_program_t program, int lanes_per_rank);
 void cecoll_program_free(cecoll_program_t program);
+/* Inverse of dump: reads dump_program text (program.cpp:218-254) produced by
+ * the reference's own compile() — or any hand-made program — so that the
+ * exact reference program can be executed with cecoll_plan_create_program.
+ * The program is validated (validate_program rules, buffer bounds) at plan
+ * creation. */
+cecoll_status_t cecoll_program_parse(const char* dump_text, cecoll_kind_t kind, int64_t chunk_bytes, int nranks,
+                                     cecoll_program_t* out);
 
 /* select_implementation (compiler.cpp:305-318), the reference's MI300X table. */
 cecoll_impl_t cecoll_reference_select(cecoll_kind_t kind, int64_t chunk_bytes);
@@ -143,6 +150,10 @@ cecoll_status_t cecoll_group_end(void);
 cecoll_status_t cecoll_plan_create(const cecoll_comm_t* comms, int ncomms, cecoll_kind_t kind,
                                    const void* const* sends, void* const* recvs, size_t chunk_bytes,
                                    cecoll_impl_t impl, cecoll_plan_t* out);
+/* A plan that executes a given command program (the reference's interpreter
+ * seam: simulate(program) / verify_collective(program) → run on hardware). */
+cecoll_status_t cecoll_plan_create_program(const cecoll_comm_t* comms, int ncomms, cecoll_program_t program,
+                                           const void* const* sends, void* const* recvs, cecoll_plan_t* out);
 /* Trigger the armed instance from each rank's stream (streams[i] for
  * comms[i]; NULL entries = host trigger) and make each stream wait for
  * completion; re-arms the next instance off the critical path. */

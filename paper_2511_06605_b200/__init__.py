@@ -103,6 +103,8 @@ def lib():
         "cecoll_program_traffic": ([vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], i32),
         "cecoll_program_validate": ([vp, i32], i32),
         "cecoll_program_free": ([vp], None),
+        "cecoll_program_parse": ([C.c_char_p, i32, i64, i32, C.POINTER(vp)], i32),
+        "cecoll_plan_create_program": ([C.POINTER(vp), i32, vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)], i32),
         "cecoll_reference_select": ([i32, i64], i32),
         "cecoll_select": ([i32, i64, i32, i32], i32),
         "cecoll_comm_init_all": ([C.POINTER(vp), i32, C.POINTER(i32)], i32),
@@ -136,6 +138,7 @@ EXPORTED_SYMBOLS = [
     "cecoll_comm_init_all", "cecoll_comm_init_rank", "cecoll_comm_destroy", "cecoll_comm_info",
     "cecoll_register", "cecoll_deregister", "cecoll_allgather", "cecoll_alltoall", "cecoll_group_start",
     "cecoll_group_end", "cecoll_plan_create", "cecoll_plan_launch", "cecoll_plan_destroy", "cecoll_comm_counters",
+    "cecoll_program_parse", "cecoll_plan_create_program",
 ]
 
 
@@ -173,14 +176,26 @@ def impl_name(impl: int) -> str:
 class Program:
     """A compiled command program (≙ dmasim::CommandProgram)."""
 
-    def __init__(self, kind, impl, chunk_bytes: int, nranks: int, lanes_per_rank: int = DEFAULT_LANES):
+    def __init__(self, kind, impl, chunk_bytes: int, nranks: int, lanes_per_rank: int = DEFAULT_LANES,
+                 _handle=None):
         self.kind, self.impl, self.chunk, self.nranks = kind, impl, chunk_bytes, nranks
+        if _handle is not None:
+            self._h = _handle
+            return
         h = C.c_void_p()
         _check(
             lib().cecoll_program_compile(_kind(kind), _impl(impl), chunk_bytes, nranks, lanes_per_rank, C.byref(h)),
             f"compile {kind}/{impl} s={chunk_bytes} n={nranks}",
         )
         self._h = h
+
+    @classmethod
+    def parse(cls, dump_text: str, kind, chunk_bytes: int, nranks: int) -> "Program":
+        """Read the reference's dump_program text (e.g. `dmasim compile` output)."""
+        h = C.c_void_p()
+        _check(lib().cecoll_program_parse(dump_text.encode(), _kind(kind), chunk_bytes, nranks, C.byref(h)),
+               "program_parse")
+        return cls(kind, None, chunk_bytes, nranks, _handle=h)
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
@@ -356,16 +371,20 @@ def all_to_all(comms, sends, recvs, chunk_bytes: int, impl="auto", streams=None)
 class Plan:
     """A prelaunched plan: recorded once, armed ahead, triggered per launch."""
 
-    def __init__(self, comms, kind, sends, recvs, chunk_bytes: int, impl="prelaunch_pcpy"):
+    def __init__(self, comms, kind, sends, recvs, chunk_bytes: int = 0, impl="prelaunch_pcpy",
+                 program: Program | None = None):
         n = len(comms)
         hs = (C.c_void_p * n)(*[c._h.value for c in comms])
         ss = (C.c_void_p * n)(*[_ptr(x) for x in sends])
         rs = (C.c_void_p * n)(*[_ptr(x) for x in recvs])
-        self._keep = (sends, recvs)  # buffers must outlive an armed plan
+        self._keep = (sends, recvs, program)  # buffers must outlive an armed plan
         self._n = n
         h = C.c_void_p()
-        _check(lib().cecoll_plan_create(hs, n, _kind(kind), ss, rs, chunk_bytes, _impl(impl), C.byref(h)),
-               "plan_create")
+        if program is not None:
+            _check(lib().cecoll_plan_create_program(hs, n, program._h, ss, rs, C.byref(h)), "plan_create_program")
+        else:
+            _check(lib().cecoll_plan_create(hs, n, _kind(kind), ss, rs, chunk_bytes, _impl(impl), C.byref(h)),
+                   "plan_create")
         self._h = h
 
     def launch(self, streams=None):

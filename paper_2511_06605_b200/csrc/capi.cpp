@@ -178,6 +178,19 @@ cecoll_status_t cecoll_program_validate(cecoll_program_t program, int lanes_per_
 
 void cecoll_program_free(cecoll_program_t program) { delete program; }
 
+cecoll_status_t cecoll_program_parse(const char* text, cecoll_kind_t kind, int64_t chunk_bytes, int nranks,
+                                     cecoll_program_t* out) {
+  if (!text || !out) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (kind != CECOLL_ALLGATHER && kind != CECOLL_ALLTOALL) return err(CECOLL_INVALID_ARGUMENT, "unknown collective");
+  try {
+    *out = new cecoll_program{parse_dump(text, static_cast<Kind>(kind), chunk_bytes, nranks)};
+    return CECOLL_SUCCESS;
+  } catch (const std::invalid_argument& e) {
+    return err(CECOLL_INVALID_ARGUMENT, e.what());
+  }
+}
+
 cecoll_impl_t cecoll_reference_select(cecoll_kind_t kind, int64_t chunk_bytes) {
   try {
     return static_cast<cecoll_impl_t>(reference_select(static_cast<Kind>(kind), chunk_bytes));
@@ -286,6 +299,24 @@ cecoll_status_t cecoll_plan_create(const cecoll_comm_t* comms, int ncomms, cecol
   Plan* p = nullptr;
   Status s = plan_create(w, static_cast<Kind>(kind), static_cast<Impl>(impl), static_cast<int64_t>(chunk_bytes),
                          args, &p);
+  if (!s.ok()) return st(s);
+  *out = new cecoll_plan{w, p};
+  return CECOLL_SUCCESS;
+}
+
+cecoll_status_t cecoll_plan_create_program(const cecoll_comm_t* comms, int ncomms, cecoll_program_t program,
+                                           const void* const* sends, void* const* recvs, cecoll_plan_t* out) {
+  if (!comms || ncomms <= 0 || !program || !sends || !recvs || !out)
+    return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  World* w = comms[0]->world;
+  std::vector<CallArgs> args;
+  for (int i = 0; i < ncomms; ++i) {
+    if (comms[i]->world != w) return err(CECOLL_INVALID_ARGUMENT, "plan: communicators of one world only");
+    args.push_back({comms[i]->rank, sends[i], recvs[i], nullptr});
+  }
+  const Program& prog = program->program;
+  Plan* p = nullptr;
+  Status s = plan_create(w, prog.spec.kind, prog.impl, prog.spec.chunk, args, &p, &prog);
   if (!s.ok()) return st(s);
   *out = new cecoll_plan{w, p};
   return CECOLL_SUCCESS;

@@ -1,14 +1,11 @@
-// sm_100a item mover: copies, two-destination broadcasts and in-place swaps.
+// sm_100a item movers (copies, two-destination broadcasts, in-place swaps)
+// and the flag kernels of recorded graphs.
 //
 // Roofline: pure data movement, bound by HBM (same-device destinations) or by
 // NVLink (peer destinations). Algorithmic bytes per item: copy 2*bytes
 // (1 read + 1 write), bcst 3*bytes (1 read + 2 writes), swap 4*bytes.
-//
-// Each CTA of 256 threads moves 32 KiB tiles: every thread issues eight
-// independent 128-bit loads before its eight 128-bit stores, so 128 KiB per SM
-// (at 4 CTAs/SM) are in flight, enough to cover HBM and NVLink latency.
-// Source loads bypass L1 (ld.global.nc.L1::no_allocate); the data is touched
-// once.
+// Variant choice (tile shape, occupancy, TMA vs registers) was measured with
+// tools/copy_bench.cu on the bench workload (profiles/copy_bench_r01.txt).
 #include <cstdint>
 
 #include "kernels.hpp"
@@ -17,8 +14,13 @@ namespace cecoll {
 
 namespace {
 
-constexpr int kVecPerThread = static_cast<int>(kTileBytes / 16 / kCopyThreads);  // 8
-static_assert(kVecPerThread * 16 * kCopyThreads == kTileBytes, "tile shape");
+// ---------------------------------------------------------------------------
+// Register mover
+// ---------------------------------------------------------------------------
+
+constexpr int kRegThreads = 512;
+constexpr int kRegVec = 8;  // 16-byte vectors per thread per tile
+constexpr int64_t kRegTile = int64_t{kRegThreads} * kRegVec * 16;  // 64 KiB
 
 __device__ __forceinline__ int4 ld_stream(const int4* p) {
   int4 r;
@@ -30,9 +32,7 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
 
 __device__ __forceinline__ int4 ld_plain(const int4* p) {
   int4 r;
-  asm volatile("ld.global.v4.s32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+  asm volatile("ld.global.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
 
@@ -41,25 +41,27 @@ __device__ __forceinline__ void st_vec(int4* p, const int4& v) {
                : "memory");
 }
 
-// Full, 16-byte aligned tile body: nvec vectors starting at vector 0.
+// 16-byte aligned body of nvec vectors.
+template <int kKinds>
 __device__ __forceinline__ void move_vectors(const Item& it, int64_t off, int64_t nvec) {
   const int t = threadIdx.x;
-  if (it.kind == kItemSwap) {
+  const bool full = nvec == kRegTile / 16;
+  if ((kKinds & (1 << kItemSwap)) && it.kind == kItemSwap) {
     int4* a = reinterpret_cast<int4*>(it.dst + off);
     int4* b = reinterpret_cast<int4*>(const_cast<char*>(it.src) + off);
-    int4 va[kVecPerThread], vb[kVecPerThread];
+    int4 va[kRegVec], vb[kRegVec];
 #pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) {
-      const int64_t v = t + (int64_t)k * kCopyThreads;
-      if (v < nvec) {
+    for (int k = 0; k < kRegVec; ++k) {
+      const int64_t v = t + int64_t{k} * kRegThreads;
+      if (full || v < nvec) {
         va[k] = ld_plain(a + v);
         vb[k] = ld_plain(b + v);
       }
     }
 #pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) {
-      const int64_t v = t + (int64_t)k * kCopyThreads;
-      if (v < nvec) {
+    for (int k = 0; k < kRegVec; ++k) {
+      const int64_t v = t + int64_t{k} * kRegThreads;
+      if (full || v < nvec) {
         st_vec(a + v, vb[k]);
         st_vec(b + v, va[k]);
       }
@@ -68,43 +70,31 @@ __device__ __forceinline__ void move_vectors(const Item& it, int64_t off, int64_
   }
   const int4* s = reinterpret_cast<const int4*>(it.src + off);
   int4* d = reinterpret_cast<int4*>(it.dst + off);
-  int4 r[kVecPerThread];
-  if (nvec == kTileBytes / 16) {
+  int4 r[kRegVec];
 #pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) r[k] = ld_stream(s + t + k * kCopyThreads);
-#pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) st_vec(d + t + k * kCopyThreads, r[k]);
-    if (it.kind == kItemBcst) {
-      int4* d2 = reinterpret_cast<int4*>(it.dst2 + off);
-#pragma unroll
-      for (int k = 0; k < kVecPerThread; ++k) st_vec(d2 + t + k * kCopyThreads, r[k]);
-    }
-    return;
+  for (int k = 0; k < kRegVec; ++k) {
+    const int64_t v = t + int64_t{k} * kRegThreads;
+    if (full || v < nvec) r[k] = ld_stream(s + v);
   }
 #pragma unroll
-  for (int k = 0; k < kVecPerThread; ++k) {
-    const int64_t v = t + (int64_t)k * kCopyThreads;
-    if (v < nvec) r[k] = ld_stream(s + v);
+  for (int k = 0; k < kRegVec; ++k) {
+    const int64_t v = t + int64_t{k} * kRegThreads;
+    if (full || v < nvec) st_vec(d + v, r[k]);
   }
-#pragma unroll
-  for (int k = 0; k < kVecPerThread; ++k) {
-    const int64_t v = t + (int64_t)k * kCopyThreads;
-    if (v < nvec) st_vec(d + v, r[k]);
-  }
-  if (it.kind == kItemBcst) {
+  if ((kKinds & (1 << kItemBcst)) && it.kind == kItemBcst) {
     int4* d2 = reinterpret_cast<int4*>(it.dst2 + off);
 #pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) {
-      const int64_t v = t + (int64_t)k * kCopyThreads;
-      if (v < nvec) st_vec(d2 + v, r[k]);
+    for (int k = 0; k < kRegVec; ++k) {
+      const int64_t v = t + int64_t{k} * kRegThreads;
+      if (full || v < nvec) st_vec(d2 + v, r[k]);
     }
   }
 }
 
-// Byte-granular path for [off, off+len) (misaligned heads/tails, or items
-// whose source and destination disagree modulo 16).
+// Byte-granular path for [off, off+len): unaligned heads/tails, or items
+// whose source and destination disagree modulo 16.
 __device__ __forceinline__ void move_bytes(const Item& it, int64_t off, int64_t len) {
-  for (int64_t b = threadIdx.x; b < len; b += kCopyThreads) {
+  for (int64_t b = threadIdx.x; b < len; b += kRegThreads) {
     const int64_t o = off + b;
     if (it.kind == kItemSwap) {
       char* a = it.dst + o;
@@ -120,6 +110,7 @@ __device__ __forceinline__ void move_bytes(const Item& it, int64_t off, int64_t 
   }
 }
 
+template <int kKinds>
 __device__ __forceinline__ void move_tile(const Item& it, int64_t off, int64_t len) {
   const uintptr_t d = reinterpret_cast<uintptr_t>(it.dst + off);
   const uintptr_t s = reinterpret_cast<uintptr_t>(it.src + off);
@@ -129,29 +120,109 @@ __device__ __forceinline__ void move_tile(const Item& it, int64_t off, int64_t l
     move_bytes(it, off, len);
     return;
   }
-  const int64_t head = static_cast<int64_t>((16 - (d & 15)) & 15) < len ? static_cast<int64_t>((16 - (d & 15)) & 15)
-                                                                         : len;
+  int64_t head = static_cast<int64_t>((16 - (d & 15)) & 15);
+  if (head > len) head = len;
   if (head) move_bytes(it, off, head);
-  const int64_t body = (len - head) & ~static_cast<int64_t>(15);
-  if (body) move_vectors(it, off + head, body / 16);
+  const int64_t body = (len - head) & ~int64_t{15};
+  if (body) move_vectors<kKinds>(it, off + head, body / 16);
   const int64_t tail = len - head - body;
   if (tail) move_bytes(it, off + head + body, tail);
 }
 
-__global__ void __launch_bounds__(kCopyThreads) items_kernel(const Item* __restrict__ items, int nitems,
-                                                              int ntiles) {
+template <int kKinds, int kMinBlocks>
+__global__ void __launch_bounds__(kRegThreads, kMinBlocks)
+    reg_items_kernel(const Item* __restrict__ items, int nitems, int ntiles) {
   __shared__ int first[kMaxItemsSmem];
-  for (int i = threadIdx.x; i < nitems; i += kCopyThreads) first[i] = items[i].first_tile;
+  for (int i = threadIdx.x; i < nitems; i += kRegThreads) first[i] = items[i].first_tile;
   __syncthreads();
   int cur = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     while (cur + 1 < nitems && first[cur + 1] <= tile) ++cur;
     const Item it = items[cur];
-    const int64_t off = static_cast<int64_t>(tile - it.first_tile) * kTileBytes;
+    const int64_t off = static_cast<int64_t>(tile - it.first_tile) * kRegTile;
     const int64_t rem = it.bytes - off;
-    move_tile(it, off, rem < kTileBytes ? rem : kTileBytes);
+    move_tile<kKinds>(it, off, rem < kRegTile ? rem : kRegTile);
   }
 }
+
+// ---------------------------------------------------------------------------
+// TMA bulk mover (copy items, 16-byte aligned, sizes multiple of 16)
+// ---------------------------------------------------------------------------
+
+constexpr int kTmaStages = 4;
+constexpr int kTmaTile = 32 * 1024;
+constexpr int kTmaSmem = kTmaStages * kTmaTile;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict__ items, int nitems, int ntiles) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[kTmaStages];
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < kTmaStages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[i])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+
+  const int mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  int cur = 0;
+  // Tile k of this CTA is global tile blockIdx.x + k * gridDim.x.
+  auto locate = [&](int k, const char** src, char** dst, uint32_t* bytes) {
+    const int tile = blockIdx.x + k * gridDim.x;
+    while (cur + 1 < nitems && items[cur + 1].first_tile <= tile) ++cur;
+    const Item& it = items[cur];
+    const int64_t off = static_cast<int64_t>(tile - it.first_tile) * kTmaTile;
+    const int64_t rem = it.bytes - off;
+    *src = it.src + off;
+    *dst = it.dst + off;
+    *bytes = static_cast<uint32_t>(rem < kTmaTile ? rem : kTmaTile);
+  };
+  auto load = [&](int stage, const char* src, uint32_t bytes) {
+    const uint32_t bar = smem_addr(&full[stage]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(ring + stage * kTmaTile)),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+  };
+  char* dst[kTmaStages];
+  uint32_t nbytes[kTmaStages];
+  int issued = 0;
+  for (; issued < kTmaStages && issued < mine; ++issued) {
+    const char* src;
+    locate(issued, &src, &dst[issued], &nbytes[issued]);
+    load(issued, src, nbytes[issued]);
+  }
+  uint32_t phase = 0;
+  for (int k = 0; k < mine; ++k) {
+    const int st = k % kTmaStages;
+    const uint32_t bar = smem_addr(&full[st]);
+    const uint32_t parity = (phase >> st) & 1u;
+    asm volatile(
+        "{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+    phase ^= 1u << st;
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst[st]),
+                 "r"(smem_addr(ring + st * kTmaTile)), "r"(nbytes[st])
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (issued < mine) {
+      // The stage is refilled once its store has finished reading it.
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      const char* src;
+      locate(issued, &src, &dst[st], &nbytes[st]);
+      load(st, src, nbytes[st]);
+      ++issued;
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Flag kernels
+// ---------------------------------------------------------------------------
 
 constexpr unsigned long long kPollTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
 
@@ -212,6 +283,40 @@ __global__ void gate_kernel(volatile uint64_t* posted, uint64_t* consumed, cudaG
 
 }  // namespace
 
+int64_t mover_tile_bytes(Mover m) { return m == Mover::Tma ? kTmaTile : kRegTile; }
+
+int64_t tiles_for(int64_t bytes, Mover m) {
+  const int64_t t = mover_tile_bytes(m);
+  return (bytes + t - 1) / t;
+}
+
+int mover_grid(Mover m, int sms) { return m == Mover::Tma ? 2 * sms : 2 * sms; }
+
+cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream) {
+  if (t.nitems <= 0 || t.ntiles <= 0) return cudaSuccess;
+  if (t.nitems > kMaxItemsSmem) return cudaErrorInvalidValue;
+  if (grid > t.ntiles) grid = t.ntiles;
+  if (t.mover == Mover::Tma) {
+    static bool configured[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !configured[dev]) {
+      cudaError_t e = cudaFuncSetAttribute(tma_items_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+      if (e != cudaSuccess) return e;
+      configured[dev] = true;
+    }
+    tma_items_kernel<<<grid, 32, kTmaSmem, stream>>>(t.items, t.nitems, t.ntiles);
+  } else if (t.kinds == (1 << kItemCopy)) {
+    reg_items_kernel<(1 << kItemCopy), 2><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems, t.ntiles);
+  } else if (!(t.kinds & (1 << kItemSwap))) {
+    reg_items_kernel<(1 << kItemCopy) | (1 << kItemBcst), 2><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems,
+                                                                                              t.ntiles);
+  } else {
+    reg_items_kernel<7, 1><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems, t.ntiles);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_poll(uint64_t* const* flags, int n, uint64_t* err, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   poll_kernel<<<(n + 127) / 128, 128, 0, stream>>>(flags, n, err);
@@ -227,16 +332,6 @@ cudaError_t launch_signal(uint64_t* const* flags, int n, cudaStream_t stream) {
 cudaError_t launch_gate(volatile uint64_t* posted, uint64_t* consumed, cudaGraphConditionalHandle handle,
                         uint64_t* err, cudaStream_t stream) {
   gate_kernel<<<1, 32, 0, stream>>>(posted, consumed, handle, err);
-  return cudaGetLastError();
-}
-
-int64_t tiles_for(int64_t bytes) { return (bytes + kTileBytes - 1) / kTileBytes; }
-
-cudaError_t launch_items(const Item* items, int nitems, int ntiles, int grid, cudaStream_t stream) {
-  if (nitems <= 0 || ntiles <= 0) return cudaSuccess;
-  if (nitems > kMaxItemsSmem) return cudaErrorInvalidValue;
-  if (grid > ntiles) grid = ntiles;
-  items_kernel<<<grid, kCopyThreads, 0, stream>>>(items, nitems, ntiles);
   return cudaGetLastError();
 }
 

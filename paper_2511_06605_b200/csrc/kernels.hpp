@@ -1,6 +1,6 @@
 // sm_100a data-movement kernels shared by the SM path and by the command
 // types a copy engine cannot execute (two-destination broadcast, in-place
-// swap; compiler.cpp:166-239).
+// swap; compiler.cpp:166-239), plus the flag kernels of recorded graphs.
 #pragma once
 
 #include <cstdint>
@@ -23,16 +23,32 @@ struct Item {
   int32_t first_tile;  // prefix sum of tiles over the item table
 };
 
-// Bytes per tile: one CTA moves one tile per step (256 threads x 8 x 16 B).
-constexpr int64_t kTileBytes = 32 * 1024;
-constexpr int kCopyThreads = 256;
+// Which kernel moves a table:
+//  Reg: 512-thread CTAs, 64 KiB tiles staged through registers (eight 16-byte
+//       loads in flight per thread), any alignment, any item kind.
+//  Tma: copy-only tables whose items are 16-byte aligned with sizes that are
+//       multiples of 16: one elected thread per CTA streams 32 KiB tiles
+//       through a 4-stage shared-memory ring with cp.async.bulk
+//       (global->shared on an mbarrier, shared->global as a bulk group).
+enum class Mover : int { Reg = 0, Tma = 1 };
+
+struct ItemTable {
+  Item* items = nullptr;  // device memory
+  int nitems = 0;
+  int ntiles = 0;
+  Mover mover = Mover::Reg;
+  int kinds = 1;  // bitmask of (1 << ItemKind) present
+};
+
 constexpr int kMaxItemsSmem = 1024;
 
-// Moves every item of `items` (device-resident table) with a grid-stride loop
-// over tiles. `ntiles` is items[nitems-1].first_tile + tiles of the last item.
-cudaError_t launch_items(const Item* items, int nitems, int ntiles, int grid, cudaStream_t stream);
+int64_t mover_tile_bytes(Mover m);
+// Tiles of one item under mover m.
+int64_t tiles_for(int64_t bytes, Mover m);
+// Grid that fills the device for mover m (multiple of the SM count).
+int mover_grid(Mover m, int sms);
 
-int64_t tiles_for(int64_t bytes);
+cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream);
 
 // Flag kernels used inside recorded (prelaunch) graphs, where stream memory
 // operations are not allowed in conditional bodies.

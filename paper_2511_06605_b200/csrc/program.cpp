@@ -8,6 +8,7 @@
 #include "program.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <set>
@@ -410,6 +411,113 @@ std::string validate(const Program& p, int lanes_per_rank) {
   if (std::set<int>(p.trigger_slots.begin(), p.trigger_slots.end()) != polls)
     return "trigger_slots do not match the poll slots used";
   return std::string();
+}
+
+namespace {
+
+Region parse_region(const std::string& tok) {
+  // g<rank>.in[<off>+<len>] | g<rank>.out[<off>+<len>]
+  Region r;
+  long long rank = 0, off = 0, len = 0;
+  char buf[8] = {0};
+  if (std::sscanf(tok.c_str(), "g%lld.%3[a-z][%lld+%lld]", &rank, buf, &off, &len) != 4)
+    throw std::invalid_argument("parse_dump: bad region '" + tok + "'");
+  const std::string b(buf);
+  if (b != "in" && b != "out") throw std::invalid_argument("parse_dump: bad buffer '" + tok + "'");
+  r.rank = static_cast<int>(rank);
+  r.buf = b == "in" ? Buf::Input : Buf::Output;
+  r.off = off;
+  r.len = len;
+  return r;
+}
+
+std::vector<std::string> split(const std::string& s, char sep) {
+  std::vector<std::string> out;
+  std::string cur;
+  for (char c : s) {
+    if (c == sep) {
+      out.push_back(cur);
+      cur.clear();
+    } else {
+      cur += c;
+    }
+  }
+  out.push_back(cur);
+  return out;
+}
+
+}  // namespace
+
+Program parse_dump(const std::string& text, Kind kind, int64_t chunk, int nranks) {
+  Program p;
+  p.spec.kind = kind;
+  p.spec.chunk = chunk;
+  p.spec.nranks = nranks;
+  int last_q = -1;
+  for (const std::string& line : split(text, '\n')) {
+    if (line.empty()) continue;
+    const auto f = split(line, '\t');
+    if (f.size() != 7) throw std::invalid_argument("parse_dump: expected 7 fields: " + line);
+    int q = -1, g = -1, e = -1;
+    if (std::sscanf(f[0].c_str(), "q%d(g%de%d)", &q, &g, &e) != 3)
+      throw std::invalid_argument("parse_dump: bad queue '" + f[0] + "'");
+    if (q != last_q) {
+      if (q != last_q + 1) throw std::invalid_argument("parse_dump: queues must be listed in order");
+      Lane l;
+      l.rank = g;
+      l.index = e;
+      p.lanes.push_back(l);
+      last_q = q;
+    }
+    Command c;
+    const std::string& op = f[2];
+    if (op == "copy") {
+      c.op = Op::Copy;
+      c.src = parse_region(f[3]);
+      c.dst = parse_region(f[4]);
+    } else if (op == "broadcast") {
+      c.op = Op::Broadcast;
+      c.src = parse_region(f[3]);
+      const auto d = split(f[4], ',');
+      if (d.size() != 2) throw std::invalid_argument("parse_dump: broadcast needs two destinations");
+      c.dst = parse_region(d[0]);
+      c.dst2 = parse_region(d[1]);
+    } else if (op == "swap") {
+      c.op = Op::Swap;
+      c.src = parse_region(f[3]);
+      c.peer = parse_region(f[4]);
+      p.spec.in_place = true;
+    } else if (op == "signal") {
+      c.op = Op::Signal;
+      c.signal_slot = std::atoi(f[6].c_str());
+      p.completion_signals.push_back(c.signal_slot);
+    } else if (op == "poll") {
+      c.op = Op::Poll;
+      c.poll_slot = std::atoi(f[6].c_str());
+      c.expected = 1;
+      p.trigger_slots.push_back(c.poll_slot);
+      p.prelaunched = true;
+    } else if (op == "timestamp") {
+      c.op = Op::Timestamp;
+    } else {
+      throw std::invalid_argument("parse_dump: unknown command '" + op + "'");
+    }
+    c.size = std::atoll(f[5].c_str());
+    p.lanes.back().cmds.push_back(c);
+  }
+  bool bcst = false, swap = false, multi = false;
+  for (const Lane& l : p.lanes) {
+    int data = 0;
+    for (const Command& c : l.cmds) {
+      bcst |= c.op == Op::Broadcast;
+      swap |= c.op == Op::Swap;
+      data += c.moves_data();
+    }
+    multi |= data > 1;
+  }
+  Impl base = swap ? Impl::Swap : bcst ? Impl::Bcst : multi ? Impl::B2b : Impl::Pcpy;
+  p.impl = p.prelaunched ? static_cast<Impl>(static_cast<int>(base) + 4) : base;
+  return p;
 }
 
 // The reference's prescribed table (compiler.cpp:305-318, PAPER Tables 1-2).

@@ -98,6 +98,10 @@ Metrics metrics(const Program& p);
 Traffic traffic(const Program& p);
 // Empty string when valid, else the first violation (program.cpp:98-205).
 std::string validate(const Program& p, int lanes_per_rank);
+// Inverse of dump(): reads the reference's dump_program text (any program the
+// reference's compile() produced, or a hand-made one) so that it can be
+// executed as is. Throws std::invalid_argument on malformed text.
+Program parse_dump(const std::string& text, Kind kind, int64_t chunk, int nranks);
 
 Impl reference_select(Kind kind, int64_t size);
 Impl select(Kind kind, int64_t size, int nranks, int ndevices);

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 #include <stdexcept>
@@ -337,13 +338,28 @@ char* translate(World* w, int target, const void* mine, bool* ok) {
 
 uint64_t* slot(World* w, int rank, int index) { return w->flag_page[rank] + index; }
 
-Status upload_items(World* w, Plan* p, int device, std::vector<Item>& items, Item** out) {
-  (void)w;
+// Chooses the mover (TMA for aligned copy-only tables unless
+// CECOLL_MOVER=reg), numbers the tiles and uploads the table.
+Status upload_items(Plan* p, int device, std::vector<Item>& items, ItemTable* out) {
+  if (items.empty()) return {};
+  if (items.size() > static_cast<size_t>(kMaxItemsSmem))
+    return fail(CECOLL_INVALID_ARGUMENT, "too many chunk transfers for one launch");
   DeviceGuard g(device);
+  bool tma = true;
+  int kinds = 0;
+  for (const Item& it : items) {
+    kinds |= 1 << it.kind;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(it.src) | reinterpret_cast<uintptr_t>(it.dst);
+    tma &= it.kind == kItemCopy && (a & 15) == 0 && (it.bytes & 15) == 0;
+  }
+  const char* env = std::getenv("CECOLL_MOVER");
+  if (env && std::string(env) == "reg") tma = false;
+  out->mover = tma ? Mover::Tma : Mover::Reg;
+  out->kinds = kinds;
   int64_t tiles = 0;
   for (Item& it : items) {
     it.first_tile = static_cast<int32_t>(tiles);
-    tiles += tiles_for(it.bytes);
+    tiles += tiles_for(it.bytes, out->mover);
   }
   if (tiles > INT32_MAX) return fail(CECOLL_INVALID_ARGUMENT, "collective too large for one launch");
   void* d = nullptr;
@@ -351,7 +367,9 @@ Status upload_items(World* w, Plan* p, int device, std::vector<Item>& items, Ite
   CUDA_TRY(cudaMemcpy(d, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice));
   p->dev_allocs.push_back(d);
   p->dev_alloc_device.push_back(device);
-  *out = static_cast<Item*>(d);
+  out->items = static_cast<Item*>(d);
+  out->nitems = static_cast<int>(items.size());
+  out->ntiles = static_cast<int>(tiles);
   return {};
 }
 
@@ -368,17 +386,13 @@ Status upload_ptrs(Plan* p, int device, const std::vector<uint64_t*>& ptrs, uint
   return {};
 }
 
-int64_t item_tiles(const std::vector<Item>& items) {
-  int64_t t = 0;
-  for (const Item& it : items) t += tiles_for(it.bytes);
-  return t;
-}
 
 }  // namespace
 
 Status build_graph(World* w, Plan* p, Unit& u);
 
-Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args, Plan** out) {
+Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args, Plan** out,
+                   const Program* given) {
   const int n = w->nranks;
   if (s <= 0) return fail(CECOLL_INVALID_ARGUMENT, "collective: chunk size must be positive");
   auto plan = std::make_unique<Plan>();
@@ -390,6 +404,13 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
     p->key_send.push_back(a.send);
     p->key_recv.push_back(a.recv);
     p->key_stream.push_back(a.stream);
+  }
+  if (given) {
+    if (given->spec.kind != kind || given->spec.chunk != s || given->spec.nranks != n)
+      return fail(CECOLL_INVALID_ARGUMENT, "program spec does not match the communicator / call");
+    const std::string v = validate(*given, kMaxLanes);
+    if (!v.empty()) return fail(CECOLL_INVALID_ARGUMENT, "program rejected: " + v);
+    impl = given->impl;
   }
   if (impl == Impl::Auto) impl = select(kind, s, n, w->ndevices);
   if (impl != Impl::Sm && !valid_for(impl, kind))
@@ -473,7 +494,7 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
     spec.chunk = s;
     spec.nranks = n;
     try {
-      p->program = compile(impl, spec, kMaxLanes);
+      p->program = given ? *given : compile(impl, spec, kMaxLanes);
     } catch (const std::invalid_argument& e) {
       return fail(CECOLL_INVALID_ARGUMENT, e.what());
     }
@@ -526,14 +547,11 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
         }
       }
       u.placement.clear();
-      u.nitems = static_cast<int>(items.size());
-      u.ntiles = static_cast<int>(item_tiles(items));
-      if (u.nitems > kMaxItemsSmem) return fail(CECOLL_INVALID_ARGUMENT, "too many items for one launch");
-      if (u.nitems) STATUS_TRY(upload_items(w, p, u.device, items, &u.items));
+      STATUS_TRY(upload_items(p, u.device, items, &u.table));
     }
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->units[0].device);
-    p->sm_grid = sms * 4;
+    p->sms = sms;
   } else {
     // Lanes of the command program owned by local ranks.
     for (const Lane& l : p->program.lanes) {
@@ -567,17 +585,13 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
         add_poll(le.pre, slot(w, l.rank, kSlotRdy + j));
         le.post.push_back(op_write(slot(w, j, kSlotDone + l.rank), 1));
       }
-      if (!items.empty()) {
-        le.nitems = static_cast<int>(items.size());
-        le.ntiles = static_cast<int>(item_tiles(items));
-        STATUS_TRY(upload_items(w, p, w->device[l.rank], items, &le.items));
-      }
+      STATUS_TRY(upload_items(p, w->device[l.rank], items, &le.table));
       STATUS_TRY(ensure_lanes(w->local[l.rank].get(), l.index + 1));
       p->lanes.push_back(std::move(le));
     }
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->units[0].device);
-    p->sm_grid = sms * 4;
+    p->sms = sms;
     if (p->prelaunch)
       for (Unit& u : p->units) STATUS_TRY(build_graph(w, p, u));
   }
@@ -668,7 +682,7 @@ Status build_graph(World* w, Plan* p, Unit& u) {
       cudaStream_t ls = rs->lanes[l.lane];
       CUDA_TRY(cudaStreamWaitEvent(ls, fork, 0));
       for (const Copy& c : l.copies) CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, ls));
-      if (l.nitems) CUDA_TRY(launch_items(l.items, l.nitems, l.ntiles, p->sm_grid, ls));
+      if (l.table.nitems) CUDA_TRY(launch_items(l.table, mover_grid(l.table.mover, p->sms), ls));
       CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], ls));
       CUDA_TRY(cudaStreamWaitEvent(u.arm, rs->lane_done[l.lane], 0));
     }
@@ -716,8 +730,8 @@ Status run_ce(World* w, Plan* p) {
     ++w->counters[6];
     STATUS_TRY(submit(w, s, l.pre));
     STATUS_TRY(issue_copies(w, l.copies, s, true));
-    if (l.nitems) {
-      CUDA_TRY(launch_items(l.items, l.nitems, l.ntiles, p->sm_grid, s));
+    if (l.table.nitems) {
+      CUDA_TRY(launch_items(l.table, mover_grid(l.table.mover, p->sms), s));
       ++w->counters[4];
       ++w->counters[6];
     }
@@ -745,8 +759,8 @@ Status run_sm(World* w, Plan* p) {
   for (Unit& u : p->units) {  // phase 2: wait destinations, move, signal
     DeviceGuard g(u.device);
     STATUS_TRY(submit(w, u.stream, u.sm_pre));
-    if (u.nitems) {
-      CUDA_TRY(launch_items(u.items, u.nitems, u.ntiles, p->sm_grid, u.stream));
+    if (u.table.nitems) {
+      CUDA_TRY(launch_items(u.table, mover_grid(u.table.mover, p->sms), u.stream));
       ++w->counters[4];
       ++w->counters[6];
     }

@@ -100,8 +100,7 @@ struct LaneExec {
   int lane = 0;
   MemOps pre;                 // rdy polls (+ resets) for destinations in other units
   std::vector<Copy> copies;   // copy commands
-  Item* items = nullptr;      // device table for Broadcast / Swap commands
-  int nitems = 0, ntiles = 0;
+  ItemTable table;            // Broadcast / Swap commands (no copy-engine form)
   MemOps post;                // done signals to destinations in other units
 };
 
@@ -114,8 +113,7 @@ struct Unit {
   MemOps sm_pre, sm_post;         // SM path: rdy polls / done signals
   std::vector<Copy> placement;    // local-slot placement (verifier.cpp:40-44)
   std::vector<Copy> precopy;      // swap with send != recv: send -> recv first
-  Item* items = nullptr;          // SM path table
-  int nitems = 0, ntiles = 0;
+  ItemTable table;                // SM path: every chunk of the unit's ranks
   // prelaunch graph
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -148,7 +146,7 @@ struct Plan {
   Program program;
   bool sm = false;
   bool prelaunch = false;
-  int sm_grid = 0;
+  int sms = 148;
 };
 
 void set_error(const std::string& msg);
@@ -169,7 +167,10 @@ struct CallArgs {
 
 Status run_collective(World* w, Kind kind, Impl impl, int64_t chunk, const std::vector<CallArgs>& args);
 
-Status plan_create(World* w, Kind kind, Impl impl, int64_t chunk, const std::vector<CallArgs>& args, Plan** out);
+// `given`: execute this program (e.g. parsed from the reference's
+// dump_program text) instead of compiling one.
+Status plan_create(World* w, Kind kind, Impl impl, int64_t chunk, const std::vector<CallArgs>& args, Plan** out,
+                   const Program* given = nullptr);
 Status plan_arm(World* w, Plan* p);
 Status plan_launch(World* w, Plan* p, bool rearm);
 Status plan_destroy(World* w, Plan* p);

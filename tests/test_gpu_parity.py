@@ -206,3 +206,27 @@ def test_counters_track_commands():
         torch.cuda.synchronize()
     finally:
         cc.destroy_all(cs)
+
+
+with open(os.path.join(GOLDEN, "programs.json")) as _f:
+    REF_DUMPS = [e for e in json.load(_f)["programs"] if "dump" in e]
+
+
+@pytest.mark.parametrize("e", REF_DUMPS, ids=lambda e: f"{e['kind']}-{e['impl']}-n{e['n']}")
+def test_executes_the_reference_program_text(e):
+    """The reference's own compile() output (dump_program text, golden) run as
+    is on the GPU through cecoll_program_parse + cecoll_plan_create_program."""
+    kind, n, s = e["kind"], e["n"], e["s"]
+    prog = cc.Program.parse(e["dump"], kind, s, n)
+    in_place = e["impl"].endswith("swap")
+    in_bytes = s if kind == "allgather" else n * s
+    host_in = [ora.splitmix_pattern(in_bytes, r, 11) for r in range(n)]
+    sends = [torch.from_numpy(h).cuda() for h in host_in]
+    recvs = sends if in_place else [torch.full((n * s,), 0xA5, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    plan = cc.Plan(comms(n), kind, sends, recvs, program=prog)
+    plan.launch([torch.cuda.current_stream()] * n)
+    torch.cuda.current_stream().synchronize()
+    res = [t.cpu().numpy() for t in recvs]
+    plan.destroy()
+    torch.cuda.synchronize()
+    assert ora.Oracle().check(kind, s, n, in_place, host_in, res) == -1

@@ -105,3 +105,32 @@ def test_comm_init_without_gpu_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(cc.CecollError):
         cc.Comm.init_all([0, 0])
+
+
+def test_parse_reference_dump_round_trips():
+    with open(os.path.join(GOLDEN, "programs.json")) as f:
+        data = json.load(f)
+    seen = 0
+    for e in data["programs"]:
+        if "dump" not in e:
+            continue
+        p = cc.Program.parse(e["dump"], e["kind"], e["s"], e["n"])
+        assert p.dump() == e["dump"]
+        m = p.metrics()
+        assert [m[k] for k in ("data_commands", "sync_commands", "poll_commands", "engines_used", "doorbells")] == e[
+            "metrics"
+        ]
+        assert p.validate() is None
+        seen += 1
+    assert seen == 48
+
+
+def test_parse_rejects_malformed_text():
+    with pytest.raises(cc.InvalidArgument):
+        cc.Program.parse("q0(g0e0)\t0\tfrobnicate\t-\t-\t0\t-\n", "allgather", 1024, 2)
+    with pytest.raises(cc.InvalidArgument):
+        cc.Program.parse("q0(g0e0)\t0\tcopy\tg0.in[0+1024]\n", "allgather", 1024, 2)
+    # Out-of-bounds programs parse but do not validate (program.cpp:85-94).
+    bad = cc.Program.parse("q0(g0e0)\t0\tcopy\tg0.in[0+1024]\tg1.out[4096+1024]\t1024\t-\n"
+                           "q0(g0e0)\t1\tsignal\t-\t-\t0\t0\n", "allgather", 1024, 2)
+    assert "out of declared bounds" in bad.validate()
