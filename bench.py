@@ -324,6 +324,147 @@ def run_ours_multiprocess(args):
     raise SystemExit("multi-GPU bench: see DESIGN.md §6 (not measured this round)")
 
 
+# ---------------------------------------------------------------------------
+# sweep (run_sweep analog, sweep.cpp:71-184): every implementation x size
+# ---------------------------------------------------------------------------
+
+def alg_hbm_bytes(kind, impl, s, n):
+    """Algorithmic HBM bytes (read + write) of one collective with co-resident
+    ranks: the program's account_traffic (verifier.cpp:281-327) plus the local
+    placement (verifier.cpp:40-44) for out-of-place programs. The SM path's
+    all-gather reads each source once (fan item)."""
+    if impl == "sm":
+        return (n * s + n * n * s) if kind == "allgather" else 2 * n * n * s
+    t = cc.Program(kind, impl, s, n).traffic()
+    extra = 0 if impl.endswith("swap") else 2 * n * s
+    return t["read"] + t["write"] + extra
+
+
+SWEEP_COLUMNS = ["impl", "api", "collective", "gpus", "size_bytes", "total_ns", "control_ns", "schedule_ns", "copy_ns",
+                 "sync_ns", "trigger_ns", "ranks", "isolated_ns", "busbw_gbs", "hbm_gbs", "roofline_frac",
+                 "api_calls", "kernels", "graphs", "parity"]
+
+
+def run_sweep(args):
+    """CSV with the reference's schema (sim.cpp:546-569) plus measured columns.
+
+    total_ns    device time per collective, back to back (throughput view)
+    isolated_ns device time of one collective issued on an idle stream
+    control_ns  host time spent inside the API call (the paper's control phase)
+    """
+    import torch
+
+    from oracle import oracle as ora
+
+    n = args.ranks
+    torch.cuda.set_device(0)
+    comms = cc.Comm.init_all([0] * n)
+    peak, _ = load_peaks()
+    stream = torch.cuda.Stream()
+    rows = []
+    sizes = [4096 << (2 * k) for k in range(10)]  # 4 KiB .. 1 GiB
+    out_path = args.sweep_out
+    O = ora.Oracle()
+    for kind in ("allgather", "alltoall"):
+        impls = ["sm"] + cc.IMPLS_FOR[kind]
+        for s in sizes:
+            in_bytes = s if kind == "allgather" else n * s
+            if n * (in_bytes + n * s) > args.max_bytes:
+                continue
+            sends = [torch.randint(0, 256, (in_bytes,), dtype=torch.uint8, device="cuda") for _ in range(n)]
+            recvs = [torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+            for impl in impls:
+                in_place = impl.endswith("swap")
+                if in_place:
+                    work = [t.clone() if t.numel() == n * s else None for t in sends]
+                    rb = work
+                else:
+                    work, rb = sends, recvs
+                fn = cc.all_gather if kind == "allgather" else cc.all_to_all
+                plan = None
+                if args.api == "plan":
+                    plan = cc.Plan(comms, kind, work, rb, s, impl=impl)
+
+                    def call():
+                        plan.launch(stream)
+                else:
+                    def call():
+                        fn(comms, work, rb, s, impl=impl, streams=stream)
+
+                with torch.cuda.stream(stream):
+                    for _ in range(3):
+                        call()
+                stream.synchronize()
+                # parity on a small sample of chunks (device compare)
+                parity = True
+                if not in_place:
+                    for i, j in ((0, n - 1), (n - 1, 0), (1, 2 % n)):
+                        src = sends[i][:s] if kind == "allgather" else sends[i][j * s:(j + 1) * s]
+                        parity &= bool(torch.equal(recvs[j][i * s:(i + 1) * s], src))
+                iters = int(max(5, min(500, 4e9 / (2 * n * n * s))))
+                c0 = comms[0].counters()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                host = 0.0
+                e0.record(stream)
+                for _ in range(iters):
+                    t0 = time.perf_counter()
+                    call()
+                    host += time.perf_counter() - t0
+                e1.record(stream)
+                stream.synchronize()
+                c1 = comms[0].counters()
+                total_ms = e0.elapsed_time(e1) / iters
+                iso = []
+                for _ in range(5):
+                    stream.synchronize()
+                    e0.record(stream)
+                    call()
+                    e1.record(stream)
+                    stream.synchronize()
+                    iso.append(e0.elapsed_time(e1))
+                iso.sort()
+                if plan is not None:
+                    plan.destroy()
+                torch.cuda.synchronize()
+                bw = busbw(n, s, total_ms / 1e3)
+                hbm = alg_hbm_bytes(kind, impl, s, n) / (total_ms / 1e3) / 1e9
+                rows.append({
+                    "impl": impl, "api": args.api, "collective": kind, "gpus": 1, "size_bytes": s,
+                    "total_ns": round(total_ms * 1e6), "control_ns": round(host / iters * 1e9),
+                    "schedule_ns": "", "copy_ns": "", "sync_ns": "", "trigger_ns": "", "ranks": n,
+                    "isolated_ns": round(iso[len(iso) // 2] * 1e6), "busbw_gbs": round(bw, 3),
+                    "hbm_gbs": round(hbm, 1), "roofline_frac": round(hbm / peak, 4),
+                    "api_calls": round((c1["api_calls"] - c0["api_calls"]) / iters, 1),
+                    "kernels": round((c1["kernels"] - c0["kernels"]) / iters, 2),
+                    "graphs": round((c1["graph_launches"] - c0["graph_launches"]) / iters, 2),
+                    "parity": parity,
+                })
+                print(",".join(str(rows[-1][c]) for c in SWEEP_COLUMNS), flush=True)
+            del sends, recvs
+            torch.cuda.empty_cache()
+    # CPU reference at the small sizes (the reference's compile() + byte executor).
+    cpu_rows = []
+    for kind in ("allgather", "alltoall"):
+        for s in sizes[:6]:
+            dt, label, cores, _ = cpu_reference_step(kind, n, s)
+            cpu_rows.append({"impl": f"cpu_{label}", "collective": kind, "gpus": 0, "size_bytes": s,
+                             "total_ns": round(dt * 1e9), "ranks": n, "busbw_gbs": round(busbw(n, s, dt), 3)})
+    with open(out_path, "w") as f:
+        f.write(",".join(SWEEP_COLUMNS) + "\n")
+        for r in rows + cpu_rows:
+            f.write(",".join(str(r.get(c, "")) for c in SWEEP_COLUMNS) + "\n")
+    # winner grid (winner_grid, sweep.cpp:186-218)
+    best = {}
+    for r in rows:
+        key = (r["collective"], r["size_bytes"])
+        if key not in best or r["total_ns"] < best[key]["total_ns"]:
+            best[key] = r
+    for (kind, s), r in sorted(best.items()):
+        print(f"winner {kind} s={s}: {r['impl']} {r['total_ns']} ns", flush=True)
+    cc.destroy_all(comms)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -332,8 +473,16 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--algo", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="size sweep of every implementation (CSV)")
+    ap.add_argument("--ranks", type=int, default=NRANKS)
+    ap.add_argument("--sweep-out", default=os.path.join(ROOT, "gpurun_out", "sweep.csv"))
+    ap.add_argument("--max-bytes", type=float, default=96e9)
+    ap.add_argument("--api", default="eager", choices=["eager", "plan"],
+                    help="sweep through the collective calls or through explicit plans")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.sweep:
+        run_sweep(args)
+    elif args.impl == "reference":
         run_reference_arm(args)
     else:
         run_ours(args)

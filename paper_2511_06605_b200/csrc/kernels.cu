@@ -89,6 +89,16 @@ __device__ __forceinline__ void move_vectors(const Item& it, int64_t off, int64_
       if (full || v < nvec) st_vec(d2 + v, r[k]);
     }
   }
+  if ((kKinds & (1 << kItemFan)) && it.kind == kItemFan) {
+    for (int f = 1; f < it.nfan; ++f) {  // fan[0] is it.dst, already written
+      int4* df = reinterpret_cast<int4*>(it.fan[f] + off);
+#pragma unroll
+      for (int k = 0; k < kRegVec; ++k) {
+        const int64_t v = t + int64_t{k} * kRegThreads;
+        if (full || v < nvec) st_vec(df + v, r[k]);
+      }
+    }
+  }
 }
 
 // Byte-granular path for [off, off+len): unaligned heads/tails, or items
@@ -106,6 +116,8 @@ __device__ __forceinline__ void move_bytes(const Item& it, int64_t off, int64_t 
       const char x = it.src[o];
       it.dst[o] = x;
       if (it.kind == kItemBcst) it.dst2[o] = x;
+      if (it.kind == kItemFan)
+        for (int f = 1; f < it.nfan; ++f) it.fan[f][o] = x;
     }
   }
 }
@@ -116,6 +128,8 @@ __device__ __forceinline__ void move_tile(const Item& it, int64_t off, int64_t l
   const uintptr_t s = reinterpret_cast<uintptr_t>(it.src + off);
   uintptr_t mis = (d ^ s) & 15;
   if (it.kind == kItemBcst) mis |= (d ^ reinterpret_cast<uintptr_t>(it.dst2 + off)) & 15;
+  if (it.kind == kItemFan)
+    for (int f = 1; f < it.nfan; ++f) mis |= (d ^ reinterpret_cast<uintptr_t>(it.fan[f] + off)) & 15;
   if (mis) {
     move_bytes(it, off, len);
     return;
@@ -167,14 +181,15 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
   const int mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   int cur = 0;
   // Tile k of this CTA is global tile blockIdx.x + k * gridDim.x.
-  auto locate = [&](int k, const char** src, char** dst, uint32_t* bytes) {
+  auto locate = [&](int k, const char** src, int* item, int64_t* off_out, uint32_t* bytes) {
     const int tile = blockIdx.x + k * gridDim.x;
     while (cur + 1 < nitems && items[cur + 1].first_tile <= tile) ++cur;
     const Item& it = items[cur];
     const int64_t off = static_cast<int64_t>(tile - it.first_tile) * kTmaTile;
     const int64_t rem = it.bytes - off;
     *src = it.src + off;
-    *dst = it.dst + off;
+    *item = cur;
+    *off_out = off;
     *bytes = static_cast<uint32_t>(rem < kTmaTile ? rem : kTmaTile);
   };
   auto load = [&](int stage, const char* src, uint32_t bytes) {
@@ -186,12 +201,13 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
         "l"(src), "r"(bytes), "r"(bar)
         : "memory");
   };
-  char* dst[kTmaStages];
+  int sitem[kTmaStages];
+  int64_t soff[kTmaStages];
   uint32_t nbytes[kTmaStages];
   int issued = 0;
   for (; issued < kTmaStages && issued < mine; ++issued) {
     const char* src;
-    locate(issued, &src, &dst[issued], &nbytes[issued]);
+    locate(issued, &src, &sitem[issued], &soff[issued], &nbytes[issued]);
     load(issued, src, nbytes[issued]);
   }
   uint32_t phase = 0;
@@ -204,15 +220,22 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
         "r"(parity)
         : "memory");
     phase ^= 1u << st;
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst[st]),
-                 "r"(smem_addr(ring + st * kTmaTile)), "r"(nbytes[st])
+    const Item& it = items[sitem[st]];
+    const uint32_t from = smem_addr(ring + st * kTmaTile);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(it.dst + soff[st]), "r"(from),
+                 "r"(nbytes[st])
                  : "memory");
+    if (it.kind == kItemFan)
+      for (int f = 1; f < it.nfan; ++f)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(it.fan[f] + soff[st]),
+                     "r"(from), "r"(nbytes[st])
+                     : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     if (issued < mine) {
       // The stage is refilled once its store has finished reading it.
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       const char* src;
-      locate(issued, &src, &dst[st], &nbytes[st]);
+      locate(issued, &src, &sitem[st], &soff[st], &nbytes[st]);
       load(st, src, nbytes[st]);
       ++issued;
     }
@@ -308,11 +331,11 @@ cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream) {
     tma_items_kernel<<<grid, 32, kTmaSmem, stream>>>(t.items, t.nitems, t.ntiles);
   } else if (t.kinds == (1 << kItemCopy)) {
     reg_items_kernel<(1 << kItemCopy), 2><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems, t.ntiles);
-  } else if (!(t.kinds & (1 << kItemSwap))) {
+  } else if (!(t.kinds & ((1 << kItemSwap) | (1 << kItemFan)))) {
     reg_items_kernel<(1 << kItemCopy) | (1 << kItemBcst), 2><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems,
                                                                                               t.ntiles);
   } else {
-    reg_items_kernel<7, 1><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems, t.ntiles);
+    reg_items_kernel<15, 1><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems, t.ntiles);
   }
   return cudaGetLastError();
 }

@@ -8,28 +8,36 @@
 
 namespace cecoll {
 
-enum ItemKind : int32_t { kItemCopy = 0, kItemBcst = 1, kItemSwap = 2 };
+enum ItemKind : int32_t { kItemCopy = 0, kItemBcst = 1, kItemSwap = 2, kItemFan = 3 };
 
 // One transfer. Copy: src -> dst. Bcst: src -> dst and dst2 (one read).
 // Swap: dst <-> src exchanged in place (both read before either is written,
 // per element, so the exchange has no observable intermediate state,
-// verifier.cpp:126-137).
+// verifier.cpp:126-137). Fan: src -> fan[0..nfan) with one read — the
+// all-gather source chunk written to every rank's slot (the n-destination
+// generalisation of the reference's two-destination broadcast,
+// compiler.cpp:166-205; on a multi-GPU node the NVLS multicast analog).
 struct Item {
   const char* src;
   char* dst;
   char* dst2;
+  char* const* fan;  // device array of nfan destinations (kItemFan)
   int64_t bytes;
   int32_t kind;
   int32_t first_tile;  // prefix sum of tiles over the item table
+  int32_t nfan;
+  int32_t pad;
 };
+constexpr int kMaxFan = 32;
 
 // Which kernel moves a table:
 //  Reg: 512-thread CTAs, 64 KiB tiles staged through registers (eight 16-byte
 //       loads in flight per thread), any alignment, any item kind.
-//  Tma: copy-only tables whose items are 16-byte aligned with sizes that are
-//       multiples of 16: one elected thread per CTA streams 32 KiB tiles
+//  Tma: copy / fan tables whose items are 16-byte aligned with sizes that
+//       are multiples of 16: one elected thread per CTA streams 32 KiB tiles
 //       through a 4-stage shared-memory ring with cp.async.bulk
-//       (global->shared on an mbarrier, shared->global as a bulk group).
+//       (global->shared on an mbarrier, shared->global as a bulk group; a
+//       fan tile is loaded once and stored once per destination).
 enum class Mover : int { Reg = 0, Tma = 1 };
 
 struct ItemTable {

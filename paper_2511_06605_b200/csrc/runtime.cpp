@@ -338,28 +338,70 @@ char* translate(World* w, int target, const void* mine, bool* ok) {
 
 uint64_t* slot(World* w, int rank, int index) { return w->flag_page[rank] + index; }
 
-// Chooses the mover (TMA for aligned copy-only tables unless
-// CECOLL_MOVER=reg), numbers the tiles and uploads the table.
-Status upload_items(Plan* p, int device, std::vector<Item>& items, ItemTable* out) {
-  if (items.empty()) return {};
-  if (items.size() > static_cast<size_t>(kMaxItemsSmem))
+Item make_item(ItemKind kind, const char* src, char* dst, char* dst2, int64_t bytes) {
+  Item it;
+  std::memset(&it, 0, sizeof(it));
+  it.kind = kind;
+  it.src = src;
+  it.dst = dst;
+  it.dst2 = dst2;
+  it.bytes = bytes;
+  return it;
+}
+
+// A host-side item plus, for kItemFan, its destination list.
+struct HostItem {
+  Item item;
+  std::vector<char*> fan;
+};
+
+// Chooses the mover (TMA for aligned copy/fan tables unless
+// CECOLL_MOVER=reg), numbers the tiles, uploads the fan lists and the table.
+Status upload_items(Plan* p, int device, std::vector<HostItem>& host, ItemTable* out) {
+  if (host.empty()) return {};
+  if (host.size() > static_cast<size_t>(kMaxItemsSmem))
     return fail(CECOLL_INVALID_ARGUMENT, "too many chunk transfers for one launch");
   DeviceGuard g(device);
   bool tma = true;
   int kinds = 0;
-  for (const Item& it : items) {
+  size_t nfan = 0;
+  for (const HostItem& h : host) {
+    const Item& it = h.item;
     kinds |= 1 << it.kind;
-    const uintptr_t a = reinterpret_cast<uintptr_t>(it.src) | reinterpret_cast<uintptr_t>(it.dst);
-    tma &= it.kind == kItemCopy && (a & 15) == 0 && (it.bytes & 15) == 0;
+    uintptr_t a = reinterpret_cast<uintptr_t>(it.src) | reinterpret_cast<uintptr_t>(it.dst);
+    for (char* f : h.fan) a |= reinterpret_cast<uintptr_t>(f);
+    tma &= (it.kind == kItemCopy || it.kind == kItemFan) && (a & 15) == 0 && (it.bytes & 15) == 0;
+    nfan += h.fan.size();
   }
   const char* env = std::getenv("CECOLL_MOVER");
   if (env && std::string(env) == "reg") tma = false;
   out->mover = tma ? Mover::Tma : Mover::Reg;
   out->kinds = kinds;
+  char** fan_dev = nullptr;
+  if (nfan) {
+    std::vector<char*> flat;
+    for (const HostItem& h : host) flat.insert(flat.end(), h.fan.begin(), h.fan.end());
+    void* d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, sizeof(char*) * flat.size()));
+    CUDA_TRY(cudaMemcpy(d, flat.data(), sizeof(char*) * flat.size(), cudaMemcpyHostToDevice));
+    p->dev_allocs.push_back(d);
+    p->dev_alloc_device.push_back(device);
+    fan_dev = static_cast<char**>(d);
+  }
+  std::vector<Item> items;
   int64_t tiles = 0;
-  for (Item& it : items) {
+  size_t fan_at = 0;
+  for (HostItem& h : host) {
+    Item it = h.item;
     it.first_tile = static_cast<int32_t>(tiles);
     tiles += tiles_for(it.bytes, out->mover);
+    if (it.kind == kItemFan) {
+      it.fan = fan_dev + fan_at;
+      it.nfan = static_cast<int32_t>(h.fan.size());
+      it.dst = h.fan[0];
+      fan_at += h.fan.size();
+    }
+    items.push_back(it);
   }
   if (tiles > INT32_MAX) return fail(CECOLL_INVALID_ARGUMENT, "collective too large for one launch");
   void* d = nullptr;
@@ -536,14 +578,26 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
 
   if (p->sm) {
     for (Unit& u : p->units) {
-      std::vector<Item> items;
+      std::vector<HostItem> items;
       for (int r : u.ranks) {
+        if (kind == Kind::AllGather) {
+          // One read of the source chunk, one write per rank's slot r (local
+          // slot first, then the pcpy rotation): n*s + n*n*s bytes instead
+          // of 2*n*n*s for n separate copies.
+          HostItem h{make_item(kItemFan, ad.send[r], nullptr, nullptr, s), {}};
+          for (int d = 0; d < n; ++d) {
+            char* dst = ad.recv[(r + d) % n] + r * s;
+            if (dst != ad.send[r]) h.fan.push_back(dst);
+          }
+          if (h.fan.size() == 1) h.item = make_item(kItemCopy, ad.send[r], h.fan[0], nullptr, s), h.fan.clear();
+          if (!h.fan.empty() || h.item.kind == kItemCopy) items.push_back(h);
+          continue;
+        }
         for (const Copy& c : u.placement)
-          if (c.dst == ad.recv[r] + r * s) items.push_back({c.src, c.dst, nullptr, c.bytes, kItemCopy, 0});
+          if (c.dst == ad.recv[r] + r * s) items.push_back({make_item(kItemCopy, c.src, c.dst, nullptr, c.bytes), {}});
         for (int d = 1; d < n; ++d) {
           const int j = (r + d) % n;
-          const char* src = ad.send[r] + (kind == Kind::AllGather ? 0 : j * s);
-          items.push_back({src, ad.recv[j] + r * s, nullptr, s, kItemCopy, 0});
+          items.push_back({make_item(kItemCopy, ad.send[r] + j * s, ad.recv[j] + r * s, nullptr, s), {}});
         }
       }
       u.placement.clear();
@@ -560,7 +614,7 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
       le.rank = l.rank;
       le.lane = l.index;
       std::set<int> dests;
-      std::vector<Item> items;
+      std::vector<HostItem> items;
       for (const Command& c : l.cmds) {
         switch (c.op) {
           case Op::Copy:
@@ -568,12 +622,12 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
             dests.insert(c.dst.rank);
             break;
           case Op::Broadcast:
-            items.push_back({addr(c.src), addr(c.dst), addr(c.dst2), c.size, kItemBcst, 0});
+            items.push_back({make_item(kItemBcst, addr(c.src), addr(c.dst), addr(c.dst2), c.size), {}});
             dests.insert(c.dst.rank);
             dests.insert(c.dst2.rank);
             break;
           case Op::Swap:
-            items.push_back({addr(c.peer), addr(c.src), nullptr, c.size, kItemSwap, 0});
+            items.push_back({make_item(kItemSwap, addr(c.peer), addr(c.src), nullptr, c.size), {}});
             dests.insert(c.peer.rank);
             break;
           default: break;  // Signal / Poll: realised by the flag operations below
