@@ -270,6 +270,8 @@ def run_ours(args):
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     e2e_value = busbw(n, s, e2e_ms / 1e3)
 
+    energy = None if args.no_energy else measure_energy(step, stream, n, s)
+
     cpu = None
     if not args.no_cpu_baseline:
         dt, label, cores, sample = cpu_reference_step()
@@ -314,9 +316,129 @@ def run_ours(args):
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": n * n * s,
                 "d2h_bytes_per_step": n * n * s, "ms_per_step": round(e2e_ms, 3)},
         "gpu_launches": int(round((kernels_per_step + 4 * graphs_per_step) * args.steps)),
+        "energy": energy,
         "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)
+    cc.destroy_all(comms)
+
+
+def measure_energy(step, stream, n, s, seconds=1.5, dev=0):
+    """NVML energy per transferred GB over a >= `seconds` loop of `step`
+    (J/GB = dE / (n(n-1)s bytes per collective x collectives / 1e9))."""
+    try:
+        import pynvml
+    except Exception:  # noqa: BLE001
+        return None
+    import torch
+
+    try:
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0 = pynvml.nvmlDeviceGetTotalEnergyConsumption(h)
+        count = 0
+        while time.perf_counter() - t0 < seconds:
+            for _ in range(20):
+                step()
+            count += 20
+            stream.synchronize()
+        torch.cuda.synchronize()
+        e1 = pynvml.nvmlDeviceGetTotalEnergyConsumption(h)
+        dt = time.perf_counter() - t0
+        joules = (e1 - e0) / 1e3
+        gb = n * (n - 1) * s * count / 1e9
+        return {"j_per_gb": round(joules / gb, 5), "joules": round(joules, 3), "seconds": round(dt, 3),
+                "avg_power_w": round(joules / dt, 1), "collectives": count,
+                "note": "NVML total energy of the GPU over the loop / link-equivalent bytes n(n-1)s"}
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)}
+
+
+def run_interference(args):
+    """C4 (BASELINE configs[4]): an all-gather loop of bf16 shards beside a
+    back-to-back cuBLAS bf16 8192^3 GEMM; reports the GEMM slowdown and the
+    collective slowdown per implementation (ranks co-resident on one GPU)."""
+    import torch
+
+    torch.cuda.set_device(0)
+    n = args.ranks
+    s = args.interference_chunk
+    comms = cc.Comm.init_all([0] * n)
+    elems = s // 2
+    g = torch.Generator(device="cuda").manual_seed(0)
+    sends = [torch.randn(elems, generator=g, device="cuda").to(torch.bfloat16) for _ in range(n)]
+    recvs = [torch.empty(n * elems, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
+    N = 8192
+    a = torch.randn(N, N, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(N, N, device="cuda", dtype=torch.bfloat16)
+    c = torch.empty(N, N, device="cuda", dtype=torch.bfloat16)
+    gemm_s = torch.cuda.Stream()
+    coll_s = torch.cuda.Stream()
+    flops = 2 * N ** 3
+
+    def gemm_loop(iters):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+        with torch.cuda.stream(gemm_s):
+            for e0, e1 in ev:
+                e0.record(gemm_s)
+                torch.matmul(a, b, out=c)
+                e1.record(gemm_s)
+        return ev
+
+    def times(ev):
+        return sorted(e0.elapsed_time(e1) for e0, e1 in ev)
+
+    # GEMM alone
+    gemm_loop(5)
+    torch.cuda.synchronize()
+    alone = times(gemm_loop(args.gemm_iters))
+    gemm_alone_ms = alone[len(alone) // 2]
+    out = {"workload": f"all-gather {n} ranks x {s >> 20} MiB bf16 shards (co-resident on 1 GPU) beside "
+                       f"cuBLAS bf16 {N}^3 GEMM", "gemm_alone_ms": round(gemm_alone_ms, 4),
+           "gemm_alone_tflops": round(flops / gemm_alone_ms / 1e9, 1), "impls": {}}
+    for impl in args.interference_impls.split(","):
+        plan = cc.Plan(comms, "allgather", sends, recvs, s, impl=impl)
+        # collective alone
+        for _ in range(3):
+            plan.launch(coll_s)
+        coll_s.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(coll_s)
+        for _ in range(5):
+            plan.launch(coll_s)
+        e1.record(coll_s)
+        coll_s.synchronize()
+        coll_alone = e0.elapsed_time(e1) / 5
+        # concurrent: enqueue the GEMM loop, then keep the collective busy
+        ev = gemm_loop(args.gemm_iters)
+        ce0, ce1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ce0.record(coll_s)
+        k = max(1, int(args.gemm_iters * gemm_alone_ms / max(coll_alone, 1e-3)))
+        for _ in range(k):
+            plan.launch(coll_s)
+        ce1.record(coll_s)
+        coll_s.synchronize()
+        gemm_s.synchronize()
+        plan.destroy()
+        torch.cuda.synchronize()
+        t = times(ev)
+        gemm_with = t[len(t) // 2]
+        coll_with = ce0.elapsed_time(ce1) / k
+        out["impls"][impl] = {
+            "collective_alone_ms": round(coll_alone, 4),
+            "collective_with_gemm_ms": round(coll_with, 4),
+            "collective_slowdown": round(coll_with / coll_alone, 3),
+            "gemm_with_collective_ms": round(gemm_with, 4),
+            "gemm_slowdown": round(gemm_with / gemm_alone_ms, 3),
+            "gemm_tflops_with_collective": round(flops / gemm_with / 1e9, 1),
+        }
+        print(impl, out["impls"][impl], flush=True)
+    print(json.dumps(out), flush=True)
+    if args.interference_out:
+        with open(args.interference_out, "w") as f:
+            json.dump(out, f, indent=1)
     cc.destroy_all(comms)
 
 
@@ -473,14 +595,22 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--algo", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-energy", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="size sweep of every implementation (CSV)")
     ap.add_argument("--ranks", type=int, default=NRANKS)
     ap.add_argument("--sweep-out", default=os.path.join(ROOT, "gpurun_out", "sweep.csv"))
     ap.add_argument("--max-bytes", type=float, default=96e9)
     ap.add_argument("--api", default="eager", choices=["eager", "plan"],
                     help="sweep through the collective calls or through explicit plans")
+    ap.add_argument("--interference", action="store_true", help="C4: all-gather beside a bf16 GEMM")
+    ap.add_argument("--interference-chunk", type=int, default=256 << 20)
+    ap.add_argument("--interference-impls", default="sm,pcpy,b2b,prelaunch_pcpy,bcst")
+    ap.add_argument("--interference-out", default=os.path.join(ROOT, "gpurun_out", "interference.json"))
+    ap.add_argument("--gemm-iters", type=int, default=30)
     args = ap.parse_args()
-    if args.sweep:
+    if args.interference:
+        run_interference(args)
+    elif args.sweep:
         run_sweep(args)
     elif args.impl == "reference":
         run_reference_arm(args)

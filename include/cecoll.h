@@ -118,12 +118,24 @@ cecoll_status_t cecoll_comm_init_all(cecoll_comm_t* comms, int nranks, const int
 typedef int (*cecoll_exchange_fn)(void* ctx, const void* mine, size_t bytes, void* all);
 cecoll_status_t cecoll_comm_init_rank(cecoll_comm_t* comm, int nranks, int rank, int device,
                                       cecoll_exchange_fn exchange, void* ctx);
+/* A process owning `nlocal` consecutive ranks [first_rank, first_rank+nlocal)
+ * on `device` (every process owns the same count). comms receives nlocal
+ * handles. The exchange callback is kept for cecoll_register and must stay
+ * valid for the communicator's lifetime. */
+cecoll_status_t cecoll_comm_init_ranks(cecoll_comm_t* comms, int nranks, int first_rank, int nlocal, int device,
+                                       cecoll_exchange_fn exchange, void* ctx);
+/* Host-only check of the init exchange (no CUDA): validates that the
+ * processes' rank ranges tile [0, nranks) and writes every rank's device. */
+cecoll_status_t cecoll_exchange_check(int nranks, int first_rank, int nlocal, int device, cecoll_exchange_fn exchange,
+                                      void* ctx, int32_t* out_devices);
 cecoll_status_t cecoll_comm_destroy(cecoll_comm_t comm);
 cecoll_status_t cecoll_comm_info(cecoll_comm_t comm, int* rank, int* nranks, int* device);
 
 /* Buffer registration (≙ BufferId::Input/Output being addressable on every
- * GPU, program.hpp:36). Single-process: optional. Multi-process: collective
- * over all ranks; every send/recv pointer must lie in a registered range. */
+ * GPU, program.hpp:36). Single-process: optional no-op. Multi-process:
+ * collective (each process registers its local ranks in the same order);
+ * windows are symmetric — same size on every rank — and a collective's
+ * buffers must sit at the same offset inside every rank's window. */
 cecoll_status_t cecoll_register(cecoll_comm_t comm, void* ptr, size_t bytes);
 cecoll_status_t cecoll_deregister(cecoll_comm_t comm, void* ptr);
 

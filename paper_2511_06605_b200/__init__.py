@@ -109,11 +109,12 @@ def lib():
         "cecoll_select": ([i32, i64, i32, i32], i32),
         "cecoll_comm_init_all": ([C.POINTER(vp), i32, C.POINTER(i32)], i32),
         "cecoll_comm_init_rank": ([C.POINTER(vp), i32, i32, i32, EXCHANGE_FN, vp], i32),
+        "cecoll_comm_init_ranks": ([C.POINTER(vp), i32, i32, i32, i32, EXCHANGE_FN, vp], i32),
+        "cecoll_exchange_check": ([i32, i32, i32, i32, EXCHANGE_FN, vp, C.POINTER(C.c_int32)], i32),
         "cecoll_comm_destroy": ([vp], i32),
         "cecoll_comm_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
         "cecoll_register": ([vp, vp, sz], i32),
         "cecoll_deregister": ([vp, vp], i32),
-        "cecoll_set_exchange": ([EXCHANGE_FN, vp], None),
         "cecoll_allgather": ([vp, vp, sz, i32, vp, vp], i32),
         "cecoll_alltoall": ([vp, vp, sz, i32, vp, vp], i32),
         "cecoll_group_start": ([], i32),
@@ -138,7 +139,7 @@ EXPORTED_SYMBOLS = [
     "cecoll_comm_init_all", "cecoll_comm_init_rank", "cecoll_comm_destroy", "cecoll_comm_info",
     "cecoll_register", "cecoll_deregister", "cecoll_allgather", "cecoll_alltoall", "cecoll_group_start",
     "cecoll_group_end", "cecoll_plan_create", "cecoll_plan_launch", "cecoll_plan_destroy", "cecoll_comm_counters",
-    "cecoll_program_parse", "cecoll_plan_create_program",
+    "cecoll_program_parse", "cecoll_plan_create_program", "cecoll_comm_init_ranks", "cecoll_exchange_check",
 ]
 
 
@@ -280,20 +281,23 @@ class Comm:
 
     @staticmethod
     def init_rank(nranks: int, rank: int, device: int, exchange: Callable[[bytes], list[bytes]]) -> "Comm":
-        """One rank per process; `exchange(mine) -> [bytes of every rank]` is an all-gather."""
-        cb = _make_exchange(exchange, nranks)
-        h = C.c_void_p()
-        _check(lib().cecoll_comm_init_rank(C.byref(h), nranks, rank, device, cb, None), "comm_init_rank")
-        c = Comm(h, owner=cb)
-        return c
+        """One rank per process; `exchange(mine) -> [bytes of every process]` is an all-gather."""
+        return Comm.init_ranks(nranks, rank, 1, device, exchange)[0]
+
+    @staticmethod
+    def init_ranks(nranks: int, first: int, nlocal: int, device: int,
+                   exchange: Callable[[bytes], list[bytes]]) -> list["Comm"]:
+        """This process owns ranks [first, first+nlocal) on `device` (co-resident)."""
+        cb = _make_exchange(exchange, nranks // nlocal)
+        hs = (C.c_void_p * nlocal)()
+        _check(lib().cecoll_comm_init_ranks(hs, nranks, first, nlocal, device, cb, None), "comm_init_ranks")
+        return [Comm(C.c_void_p(hs[k]), owner=cb) for k in range(nlocal)]
 
     def register(self, buf, nbytes: int | None = None):
         """Collective in multi-process communicators (symmetric windows)."""
         ptr = _ptr(buf)
         if nbytes is None:
             nbytes = buf.numel() * buf.element_size()
-        if self._owner is not None:
-            lib().cecoll_set_exchange(self._owner, None)
         _check(lib().cecoll_register(self._h, ptr, nbytes), "register")
 
     def counters(self) -> dict:
@@ -314,12 +318,13 @@ def destroy_all(comms: Sequence[Comm]):
         c.destroy()
 
 
-def _make_exchange(exchange, nranks):
+def _make_exchange(exchange, nprocs):
     def _cb(ctx, mine, nbytes, out):
         try:
             data = C.string_at(mine, nbytes)
             parts = exchange(data)
-            assert len(parts) == nranks
+            if len(parts) != nprocs or any(len(p) != nbytes for p in parts):
+                return 1
             blob = b"".join(parts)
             C.memmove(out, blob, len(blob))
             return 0
@@ -327,6 +332,14 @@ def _make_exchange(exchange, nranks):
             return 1
 
     return EXCHANGE_FN(_cb)
+
+
+def exchange_check(nranks: int, first: int, nlocal: int, device: int, exchange) -> list[int]:
+    """Run only the init exchange (host, no CUDA): every rank's device."""
+    cb = _make_exchange(exchange, nranks // nlocal)
+    out = (C.c_int32 * nranks)()
+    _check(lib().cecoll_exchange_check(nranks, first, nlocal, device, cb, None, out), "exchange_check")
+    return list(out)
 
 
 def torch_exchange(group=None):

@@ -215,11 +215,27 @@ cecoll_status_t cecoll_comm_init_all(cecoll_comm_t* comms, int nranks, const int
 
 cecoll_status_t cecoll_comm_init_rank(cecoll_comm_t* comm, int nranks, int rank, int device,
                                       cecoll_exchange_fn exchange, void* ctx) {
-  if (!comm) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  return cecoll_comm_init_ranks(comm, nranks, rank, 1, device, exchange, ctx);
+}
+
+cecoll_status_t cecoll_comm_init_ranks(cecoll_comm_t* comms, int nranks, int first_rank, int nlocal, int device,
+                                       cecoll_exchange_fn exchange, void* ctx) {
+  if (!comms) return err(CECOLL_INVALID_ARGUMENT, "null argument");
   World* w = nullptr;
-  Status s = world_init_rank(nranks, rank, device, exchange, ctx, &w);
+  Status s = world_init_ranks(nranks, first_rank, nlocal, device, exchange, ctx, &w);
   if (!s.ok()) return st(s);
-  *comm = new cecoll_comm{w, rank};
+  for (int k = 0; k < nlocal; ++k) comms[k] = new cecoll_comm{w, first_rank + k};
+  return CECOLL_SUCCESS;
+}
+
+cecoll_status_t cecoll_exchange_check(int nranks, int first_rank, int nlocal, int device, cecoll_exchange_fn exchange,
+                                      void* ctx, int32_t* out_devices) {
+  std::vector<ProcInfoView> procs;
+  Status s = gather_procs(nranks, first_rank, nlocal, device, nullptr, exchange, ctx, &procs);
+  if (!s.ok()) return st(s);
+  if (out_devices)
+    for (const ProcInfoView& p : procs)
+      for (int k = 0; k < p.nlocal; ++k) out_devices[p.first + k] = p.device;
   return CECOLL_SUCCESS;
 }
 
@@ -239,20 +255,10 @@ cecoll_status_t cecoll_comm_info(cecoll_comm_t comm, int* rank, int* nranks, int
   return CECOLL_SUCCESS;
 }
 
-static thread_local cecoll_exchange_fn g_reg_fn = nullptr;
-static thread_local void* g_reg_ctx = nullptr;
-
 cecoll_status_t cecoll_register(cecoll_comm_t comm, void* ptr, size_t bytes) {
   if (!comm || !ptr || !bytes) return err(CECOLL_INVALID_ARGUMENT, "null argument");
-  return st(world_register(comm->world, comm->rank, ptr, bytes, g_reg_fn, g_reg_ctx));
-}
-
-// Multi-process registration needs the exchange callback again; the Python
-// layer installs it before cecoll_register (not part of the public header's
-// required surface, exported for the bindings).
-void cecoll_set_exchange(cecoll_exchange_fn fn, void* ctx) {
-  g_reg_fn = fn;
-  g_reg_ctx = ctx;
+  World* w = comm->world;
+  return st(world_register(w, comm->rank, ptr, bytes, w->exchange, w->exchange_ctx));
 }
 
 cecoll_status_t cecoll_deregister(cecoll_comm_t comm, void* ptr) {

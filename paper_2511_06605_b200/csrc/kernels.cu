@@ -143,13 +143,25 @@ __device__ __forceinline__ void move_tile(const Item& it, int64_t off, int64_t l
   if (tail) move_bytes(it, off + head + body, tail);
 }
 
+// Last item whose first tile is <= tile (binary search over the prefix in
+// shared memory; CTAs then advance monotonically).
+__device__ __forceinline__ int find_item(const int* first, int nitems, int tile) {
+  int lo = 0, hi = nitems - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (first[mid] <= tile) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
 template <int kKinds, int kMinBlocks>
 __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
     reg_items_kernel(const Item* __restrict__ items, int nitems, int ntiles) {
   __shared__ int first[kMaxItemsSmem];
   for (int i = threadIdx.x; i < nitems; i += kRegThreads) first[i] = items[i].first_tile;
   __syncthreads();
-  int cur = 0;
+  int cur = find_item(first, nitems, blockIdx.x);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     while (cur + 1 < nitems && first[cur + 1] <= tile) ++cur;
     const Item it = items[cur];
@@ -174,16 +186,19 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict__ items, int nitems, int ntiles) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
+  __shared__ int first[kMaxItemsSmem];
+  for (int i = threadIdx.x; i < nitems; i += 32) first[i] = items[i].first_tile;
+  __syncwarp();
   if (threadIdx.x != 0) return;
   for (int i = 0; i < kTmaStages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[i])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 
   const int mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  int cur = 0;
+  int cur = find_item(first, nitems, blockIdx.x);
   // Tile k of this CTA is global tile blockIdx.x + k * gridDim.x.
   auto locate = [&](int k, const char** src, int* item, int64_t* off_out, uint32_t* bytes) {
     const int tile = blockIdx.x + k * gridDim.x;
-    while (cur + 1 < nitems && items[cur + 1].first_tile <= tile) ++cur;
+    while (cur + 1 < nitems && first[cur + 1] <= tile) ++cur;
     const Item& it = items[cur];
     const int64_t off = static_cast<int64_t>(tile - it.first_tile) * kTmaTile;
     const int64_t rem = it.bytes - off;

@@ -60,12 +60,17 @@ struct RankState {
   std::vector<cudaEvent_t> lane_done;
   cudaEvent_t start = nullptr;
   uint64_t* flags = nullptr;  // own flag page (device memory)
+  bool owns_flags = true;
 };
 
-struct Window {  // a registered range (multi-process) and its image in every rank
-  char* base = nullptr;
+struct Window {  // a symmetric registered window: its base in every rank, as mapped here
   size_t bytes = 0;
-  std::vector<char*> peer_base;
+  std::vector<char*> rank_base;
+};
+
+struct ProcInfoView {
+  int first = 0, nlocal = 0, device = -1;
+  cudaIpcMemHandle_t flags;
 };
 
 struct Plan;
@@ -80,7 +85,13 @@ struct World {
   std::atomic<int64_t> counters[8];
   std::vector<std::unique_ptr<Plan>> plans;  // eager-call plan cache
   std::vector<Window> windows;
+  std::vector<int> reg_rounds;  // per local index
   std::vector<void*> ipc_opened;
+  std::map<std::string, void*> ipc_by_handle;
+  void* flag_block = nullptr;
+  int first_local = 0, nlocal = 0;
+  cecoll_exchange_fn exchange = nullptr;  // multi-process: kept for registration
+  void* exchange_ctx = nullptr;
   int live_comms = 0;
   World() {
     for (auto& c : counters) c = 0;
@@ -153,7 +164,12 @@ void set_error(const std::string& msg);
 const char* last_error();
 
 Status world_init_all(int nranks, const int* devlist, World** out);
-Status world_init_rank(int nranks, int rank, int device, cecoll_exchange_fn fn, void* ctx, World** out);
+Status world_init_ranks(int nranks, int first, int nlocal, int device, cecoll_exchange_fn fn, void* ctx,
+                        World** out);
+// The init exchange on its own (host only; no CUDA calls): validates that the
+// processes' rank ranges tile [0, nranks) and returns them.
+Status gather_procs(int nranks, int first, int nlocal, int device, const cudaIpcMemHandle_t* flags,
+                    cecoll_exchange_fn fn, void* ctx, std::vector<ProcInfoView>* out);
 void world_release(World* w);
 Status world_register(World* w, int rank, void* ptr, size_t bytes, cecoll_exchange_fn fn, void* ctx);
 Status world_deregister(World* w, void* ptr);

@@ -1,0 +1,147 @@
+"""One process per GPU (comm_init_rank / comm_init_ranks).
+
+CPU: the init exchange over torch.distributed (gloo, world size 2) — blob
+marshaling through the C callback and validation of the processes' rank
+ranges — runs without a GPU (cecoll_exchange_check).
+GPU: two processes on cuda:0 owning two ranks each (4 ranks), flag pages and
+symmetric windows mapped through CUDA IPC across the processes, every
+implementation checked against the oracle.
+"""
+import os
+import socket
+import traceback
+
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _init(rank, world, port):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    return dist
+
+
+def _exchange_worker(rank, world, port, out):
+    try:
+        dist = _init(rank, world, port)
+        import paper_2511_06605_b200 as cc
+
+        ex = cc.torch_exchange()
+        devs = cc.exchange_check(4, rank * 2, 2, 10 + rank, ex)
+        # Overlapping ranges are rejected on every process (no hang: the
+        # exchange completes, validation fails everywhere).
+        try:
+            cc.exchange_check(4, 0, 2, 0, ex)
+            bad = "accepted"
+        except cc.InvalidArgument as e:
+            bad = str(e)
+        # Uneven ownership is rejected before the exchange.
+        try:
+            cc.exchange_check(4, 0, 3, 0, ex)
+            uneven = "accepted"
+        except cc.InvalidArgument:
+            uneven = "rejected"
+        out.put((rank, devs, bad, uneven))
+        dist.destroy_process_group()
+    except Exception:  # noqa: BLE001
+        out.put((rank, traceback.format_exc(), None, None))
+
+
+def test_exchange_over_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank, devs, bad, uneven in res:
+        assert devs == [10, 10, 11, 11], devs
+        assert "owned by two processes" in bad or "owned by no process" in bad, bad
+        assert uneven == "rejected"
+
+
+def _gpu_worker(rank, world, port, out):
+    try:
+        dist = _init(rank, world, port)
+        import numpy as np
+        import torch
+
+        import paper_2511_06605_b200 as cc
+        from oracle import oracle as ora
+
+        nranks, nlocal = 4, 2
+        first = rank * nlocal
+        comms = cc.Comm.init_ranks(nranks, first, nlocal, 0, cc.torch_exchange())
+        O = ora.Oracle()
+        s = 65536 + 64
+        results = []
+        for kind, impls in (("alltoall", ["sm", "pcpy", "b2b", "prelaunch_pcpy", "swap"]),
+                            ("allgather", ["sm", "pcpy", "bcst", "prelaunch_b2b"])):
+            in_bytes = s if kind == "allgather" else nranks * s
+            # One symmetric window per rank: [send | recv].
+            wins = [torch.full((in_bytes + nranks * s,), 0xA5, dtype=torch.uint8, device="cuda") for _ in comms]
+            for c, w in zip(comms, wins):
+                c.register(w)
+            for it, impl in enumerate(impls):
+                seed = 40 + it
+                host_all = [ora.splitmix_pattern(in_bytes, r, seed) for r in range(nranks)]
+                sends, recvs = [], []
+                for k, w in enumerate(wins):
+                    w[:in_bytes].copy_(torch.from_numpy(host_all[first + k]))
+                    w[in_bytes:].fill_(0xA5)
+                    sends.append(w[:in_bytes])
+                    recvs.append(sends[-1] if impl.endswith("swap") else w[in_bytes:])
+                torch.cuda.synchronize()
+                dist.barrier()
+                fn = cc.all_gather if kind == "allgather" else cc.all_to_all
+                fn(comms, sends, recvs, s, impl=impl, streams=torch.cuda.current_stream())
+                torch.cuda.synchronize()
+                dist.barrier()
+                mine = [t.cpu().numpy() for t in recvs]
+                # Check this process's ranks against the oracle's full result.
+                full = [np.zeros(nranks * s, np.uint8) for _ in range(nranks)]
+                O.reference_result(kind, s, nranks, host_all, full)
+                ok = all(np.array_equal(mine[k], full[first + k]) for k in range(nlocal))
+                results.append((kind, impl, ok))
+        out.put((rank, results))
+        torch.cuda.synchronize()
+        for c in comms:
+            c.destroy()
+        dist.destroy_process_group()
+    except Exception:  # noqa: BLE001
+        out.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.gpu
+def test_two_processes_share_one_gpu_through_ipc():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, results in res:
+        assert isinstance(results, list), results
+        bad = [r for r in results if not r[2]]
+        assert not bad, (rank, bad)
+        assert len(results) == 9
