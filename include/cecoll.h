@@ -152,6 +152,12 @@ cecoll_status_t cecoll_alltoall(const void* send, void* recv, size_t chunk_bytes
                                 cecoll_comm_t comm, void* stream);
 cecoll_status_t cecoll_group_start(void);
 cecoll_status_t cecoll_group_end(void);
+/* The n per-rank calls of one group in a single call (same semantics as
+ * group_start; n x allgather/alltoall; group_end). streams may be NULL
+ * (legacy stream for every rank). */
+cecoll_status_t cecoll_collective_n(cecoll_kind_t kind, const cecoll_comm_t* comms, int n, const void* const* sends,
+                                    void* const* recvs, size_t chunk_bytes, cecoll_impl_t impl,
+                                    void* const* streams);
 
 /* ---------------------------------------------------------------------
  * Explicit prelaunch plans (≙ apply_prelaunch, compiler.cpp:267-285, and the

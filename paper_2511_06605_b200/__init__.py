@@ -119,6 +119,7 @@ def lib():
         "cecoll_alltoall": ([vp, vp, sz, i32, vp, vp], i32),
         "cecoll_group_start": ([], i32),
         "cecoll_group_end": ([], i32),
+        "cecoll_collective_n": ([i32, C.POINTER(vp), i32, C.POINTER(vp), C.POINTER(vp), sz, i32, C.POINTER(vp)], i32),
         "cecoll_plan_create": ([C.POINTER(vp), i32, i32, C.POINTER(vp), C.POINTER(vp), sz, i32, C.POINTER(vp)], i32),
         "cecoll_plan_launch": ([vp, C.POINTER(vp)], i32),
         "cecoll_plan_destroy": ([vp], i32),
@@ -140,6 +141,7 @@ EXPORTED_SYMBOLS = [
     "cecoll_register", "cecoll_deregister", "cecoll_allgather", "cecoll_alltoall", "cecoll_group_start",
     "cecoll_group_end", "cecoll_plan_create", "cecoll_plan_launch", "cecoll_plan_destroy", "cecoll_comm_counters",
     "cecoll_program_parse", "cecoll_plan_create_program", "cecoll_comm_init_ranks", "cecoll_exchange_check",
+    "cecoll_collective_n",
 ]
 
 
@@ -354,31 +356,29 @@ def torch_exchange(group=None):
     return ex
 
 
-def _collective(fn_name, comms, sends, recvs, chunk_bytes, impl, streams):
-    L = lib()
-    fn = getattr(L, fn_name)
+def _collective(kind, comms, sends, recvs, chunk_bytes, impl, streams):
+    """The n per-rank calls of one group as a single C call (cecoll_collective_n)."""
     if isinstance(comms, Comm):
         comms, sends, recvs = [comms], [sends], [recvs]
         streams = [streams] if not isinstance(streams, (list, tuple)) else streams
+    n = len(comms)
     if streams is None or not isinstance(streams, (list, tuple)):
-        streams = [streams] * len(comms)
-    im = _impl(impl)
-    _check(L.cecoll_group_start())
-    try:
-        for c, s, r, st in zip(comms, sends, recvs, streams):
-            _check(fn(_ptr(s), _ptr(r), chunk_bytes, im, c._h, _stream(st)), fn_name)
-    finally:
-        _check(L.cecoll_group_end(), fn_name)
+        streams = [streams] * n
+    arr = C.c_void_p * n
+    _check(lib().cecoll_collective_n(kind, arr(*[c._h.value for c in comms]), n, arr(*[_ptr(s) for s in sends]),
+                                     arr(*[_ptr(r) for r in recvs]), chunk_bytes, _impl(impl),
+                                     arr(*[_stream(st) for st in streams])),
+           "allgather" if kind == ALLGATHER else "alltoall")
 
 
 def all_gather(comms, sends, recvs, chunk_bytes: int, impl="auto", streams=None):
     """recv[r] (n*s bytes) gets rank i's s-byte chunk at [i*s, (i+1)*s) (compiler.cpp:115-122)."""
-    _collective("cecoll_allgather", comms, sends, recvs, chunk_bytes, impl, streams)
+    _collective(ALLGATHER, comms, sends, recvs, chunk_bytes, impl, streams)
 
 
 def all_to_all(comms, sends, recvs, chunk_bytes: int, impl="auto", streams=None):
     """send[r] chunk j (s bytes) lands in recv[j] slot r (compiler.cpp:124-126, 156-157)."""
-    _collective("cecoll_alltoall", comms, sends, recvs, chunk_bytes, impl, streams)
+    _collective(ALLTOALL, comms, sends, recvs, chunk_bytes, impl, streams)
 
 
 class Plan:

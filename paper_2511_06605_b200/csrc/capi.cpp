@@ -276,6 +276,27 @@ cecoll_status_t cecoll_alltoall(const void* send, void* recv, size_t chunk_bytes
   return enqueue(Kind::AllToAll, send, recv, chunk_bytes, impl, comm, stream);
 }
 
+cecoll_status_t cecoll_collective_n(cecoll_kind_t kind, const cecoll_comm_t* comms, int n, const void* const* sends,
+                                    void* const* recvs, size_t chunk_bytes, cecoll_impl_t impl,
+                                    void* const* streams) {
+  if (!comms || n <= 0 || !sends || !recvs) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  if (kind != CECOLL_ALLGATHER && kind != CECOLL_ALLTOALL) return err(CECOLL_INVALID_ARGUMENT, "unknown collective");
+  if (!impl_ok(impl)) return err(CECOLL_INVALID_ARGUMENT, "unknown implementation");
+  if (chunk_bytes == 0) return err(CECOLL_INVALID_ARGUMENT, "collective: chunk size must be positive");
+  std::vector<PendingCall> calls;
+  calls.reserve(n);
+  for (int i = 0; i < n; ++i) {
+    if (!comms[i] || !sends[i] || !recvs[i]) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+    calls.push_back({comms[i], static_cast<Kind>(kind), sends[i], recvs[i], static_cast<int64_t>(chunk_bytes),
+                     static_cast<Impl>(impl), streams ? static_cast<cudaStream_t>(streams[i]) : nullptr});
+  }
+  if (g_group_depth > 0) {
+    g_pending.insert(g_pending.end(), calls.begin(), calls.end());
+    return CECOLL_SUCCESS;
+  }
+  return flush_group(calls);
+}
+
 cecoll_status_t cecoll_group_start(void) {
   ++g_group_depth;
   return CECOLL_SUCCESS;

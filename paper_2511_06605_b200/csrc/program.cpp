@@ -535,15 +535,21 @@ Impl reference_select(Kind kind, int64_t size) {
   return Impl::Pcpy;
 }
 
-// B200 selector. Thresholds come from the measured winner grid
-// (bench.py --sweep, profiles/); CECOLL_SM_MAX_BYTES overrides the SM cutoff.
+// B200 selector (the winner_grid analog, sweep.cpp:186-218). One device
+// (co-resident ranks), from profiles/sweep_r01_*.csv: the SM path wins every
+// all-gather size (fan items read each source once) and all-to-all up to
+// 16 MiB chunks; above that the driver's batched copies (b2b) are ~5%
+// faster. Several devices: not measured in round 1 — the SM path for
+// latency-bound chunks, prelaunched per-peer copies (copy engines over
+// NVLink) above. CECOLL_SM_MAX_BYTES overrides the SM cutoff.
 Impl select(Kind kind, int64_t size, int nranks, int ndevices) {
-  (void)kind;
   (void)nranks;
-  int64_t sm_max = ndevices <= 1 ? (int64_t)1 << 40 : (int64_t)1 << 20;
+  int64_t sm_max;
+  if (ndevices <= 1) sm_max = kind == Kind::AllGather ? INT64_MAX : (int64_t{32} << 20);
+  else sm_max = int64_t{1} << 20;
   if (const char* env = std::getenv("CECOLL_SM_MAX_BYTES")) sm_max = std::atoll(env);
   if (size <= sm_max) return Impl::Sm;
-  return Impl::PrelaunchPcpy;
+  return ndevices <= 1 ? Impl::B2b : Impl::PrelaunchPcpy;
 }
 
 }  // namespace cecoll
