@@ -121,38 +121,46 @@ def busbw(n, s, seconds):
 # ---------------------------------------------------------------------------
 
 
-def cpu_reference_step(kind="alltoall", n=NRANKS, s=CHUNK, impl="pcpy", budget_s=None):
-    """One CPU collective over the full workload; returns (seconds, kind, cores, sample)."""
+def cpu_reference_step(kind="alltoall", n=NRANKS, s=CHUNK, impl="pcpy", threads=None):
+    """One CPU collective over the full workload with every host thread;
+    returns (seconds, kind, threads, sample)."""
+    import ctypes as C
+
     import numpy as np
 
     from oracle import oracle as ora
 
+    threads = threads or os.cpu_count() or 1
     in_bytes = s if kind == "allgather" else n * s
     ins = [ora.splitmix_pattern(in_bytes, r) for r in range(n)]
     outs = [np.empty(n * s, dtype=np.uint8) for _ in range(n)]
     if os.path.exists(ora.REF_LIB):
         R = ora.Reference()
+        R.L.ref_execute_mt.argtypes = [C.c_char_p, C.c_char_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
         ptr_in = ora._ptrs(ins)
         ptr_out = ora._ptrs(outs)
 
         def once():
-            rc = R.L.ref_execute(kind.encode(), impl.encode(), s, n, ptr_in, ptr_out)
+            rc = R.L.ref_execute_mt(kind.encode(), impl.encode(), s, n, ptr_in, ptr_out, threads)
             assert rc == 0
 
         label = "reference"
+        what = "the reference's compile() (oracle/_ref) + byte executor, queues over host threads"
     else:
         O = ora.Oracle()
-        p = O.compile(kind, impl, s, n)
 
         def once():
-            O.execute(p, ins, outs)
+            O.reference_result(kind, s, n, ins, outs, threads)
 
         label = "port"
+        what = "oracle restatement (oracle/cecoll_oracle.c), destinations over host threads"
     once()  # warm the pages
-    t0 = time.perf_counter()
-    once()
-    dt = time.perf_counter() - t0
-    return dt, label, 1, f"{kind} {impl} n={n} s={s} (full workload, reference compile() + byte executor)"
+    best = float("inf")
+    for _ in range(3):
+        t0 = time.perf_counter()
+        once()
+        best = min(best, time.perf_counter() - t0)
+    return best, label, threads, f"{kind} {impl} n={n} s={s}: full workload, {what}, best of 3"
 
 
 def run_reference_arm(args):
@@ -399,7 +407,9 @@ def run_interference(args):
     a = torch.randn(N, N, device="cuda", dtype=torch.bfloat16)
     b = torch.randn(N, N, device="cuda", dtype=torch.bfloat16)
     c = torch.empty(N, N, device="cuda", dtype=torch.bfloat16)
-    gemm_s = torch.cuda.Stream()
+    # --gemm-priority high: the GEMM stream gets the highest stream priority,
+    # the collective the lowest (the block scheduler then prefers GEMM CTAs).
+    gemm_s = torch.cuda.Stream(priority=-5 if args.gemm_priority == "high" else 0)
     coll_s = torch.cuda.Stream()
     flops = 2 * N ** 3
 
@@ -438,25 +448,45 @@ def run_interference(args):
         e1.record(coll_s)
         coll_s.synchronize()
         coll_alone = e0.elapsed_time(e1) / 5
-        # concurrent: enqueue the GEMM loop, then keep the collective busy
-        ev = gemm_loop(args.gemm_iters)
-        ce0, ce1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ce0.record(coll_s)
-        k = max(1, int(args.gemm_iters * gemm_alone_ms / max(coll_alone, 1e-3)))
-        for _ in range(k):
+        # Concurrent window: the GEMM stream holds args.gemm_iters GEMMs; the
+        # collective stream is kept busy (<= 3 in flight) until the last GEMM
+        # ends, so every GEMM overlaps collectives. Rates are taken inside the
+        # window: GEMM time = GEMM window / iters; collective time = the
+        # collectives that finished inside the window.
+        g_start, g_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        coll_ev = []
+        g_start.record(gemm_s)
+        with torch.cuda.stream(gemm_s):
+            for _ in range(args.gemm_iters):
+                torch.matmul(a, b, out=c)
+        g_end.record(gemm_s)
+        while True:
+            if len(coll_ev) >= 3:
+                coll_ev[-3][1].synchronize()
+            e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e_a.record(coll_s)
             plan.launch(coll_s)
-        ce1.record(coll_s)
+            e_b.record(coll_s)
+            coll_ev.append((e_a, e_b))
+            if g_end.query():
+                break
         coll_s.synchronize()
         gemm_s.synchronize()
         plan.destroy()
         torch.cuda.synchronize()
-        t = times(ev)
-        gemm_with = t[len(t) // 2]
-        coll_with = ce0.elapsed_time(ce1) / k
+        window = g_start.elapsed_time(g_end)
+        gemm_with = window / args.gemm_iters
+        inside = [(a_, b_) for a_, b_ in coll_ev if g_start.elapsed_time(b_) <= window and
+                  g_start.elapsed_time(a_) >= 0]
+        if len(inside) >= 2:
+            coll_with = inside[0][0].elapsed_time(inside[-1][1]) / len(inside)
+        else:
+            coll_with = None
         out["impls"][impl] = {
             "collective_alone_ms": round(coll_alone, 4),
-            "collective_with_gemm_ms": round(coll_with, 4),
-            "collective_slowdown": round(coll_with / coll_alone, 3),
+            "collective_with_gemm_ms": None if coll_with is None else round(coll_with, 4),
+            "collective_slowdown": None if coll_with is None else round(coll_with / coll_alone, 3),
+            "collectives_in_window": len(inside),
             "gemm_with_collective_ms": round(gemm_with, 4),
             "gemm_slowdown": round(gemm_with / gemm_alone_ms, 3),
             "gemm_tflops_with_collective": round(flops / gemm_with / 1e9, 1),
@@ -706,7 +736,8 @@ def main():
     ap.add_argument("--interference-chunk", type=int, default=256 << 20)
     ap.add_argument("--interference-impls", default="sm,pcpy,b2b,prelaunch_pcpy,bcst")
     ap.add_argument("--interference-out", default=os.path.join(ROOT, "gpurun_out", "interference.json"))
-    ap.add_argument("--gemm-iters", type=int, default=30)
+    ap.add_argument("--gemm-iters", type=int, default=200)
+    ap.add_argument("--gemm-priority", default="same", choices=["same", "high"])
     args = ap.parse_args()
     if args.interference:
         run_interference(args)

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "dmasim/compiler.hpp"
@@ -114,35 +115,63 @@ int ref_select(const char* kind, std::int64_t size, char* buf, std::size_t cap) 
   }
 }
 
-int ref_execute(const char* kind, const char* impl, std::int64_t s, int n, std::uint8_t** in,
-                std::uint8_t** out) {
+namespace {
+
+void run_queue(const CommandProgram& p, const CommandQueue& q, std::uint8_t** in, std::uint8_t** out,
+               std::vector<std::uint8_t>& tmp) {
+  for (const auto& c : q.commands) {
+    switch (c.kind) {
+      case CommandKind::Copy:
+        std::memcpy(region(p, in, out, c.dst), region(p, in, out, c.src), c.size);
+        break;
+      case CommandKind::Broadcast:
+        std::memcpy(region(p, in, out, c.dst), region(p, in, out, c.src), c.size);
+        std::memcpy(region(p, in, out, c.dst2), region(p, in, out, c.src), c.size);
+        break;
+      case CommandKind::Swap:
+        tmp.resize(c.size);
+        std::memcpy(tmp.data(), region(p, in, out, c.src), c.size);
+        std::memcpy(region(p, in, out, c.src), region(p, in, out, c.peer), c.size);
+        std::memcpy(region(p, in, out, c.peer), tmp.data(), c.size);
+        break;
+      default:
+        break;
+    }
+  }
+}
+
+}  // namespace
+
+// Executes the reference's program with `nthreads` host threads: queues are
+// independent (every destination region has one writer, verifier.cpp:202-235),
+// so they are distributed round-robin, like the reference's own thread pool
+// over independent work (sweep.cpp:113-124).
+int ref_execute_mt(const char* kind, const char* impl, std::int64_t s, int n, std::uint8_t** in,
+                   std::uint8_t** out, int nthreads) {
   CommandProgram p;
   if (!build(kind, impl, s, n, p)) return -1;
   const CollectiveSpec& spec = p.metadata.spec;
-  if (!spec.in_place)
-    for (int g = 0; g < n; ++g)
-      std::memcpy(out[g] + g * s, in[g] + (spec.kind == CollectiveKind::AllGather ? 0 : g * s), s);
-  std::vector<std::uint8_t> tmp(s);
-  for (const auto& q : p.queues)
-    for (const auto& c : q.commands) {
-      switch (c.kind) {
-        case CommandKind::Copy:
-          std::memcpy(region(p, in, out, c.dst), region(p, in, out, c.src), c.size);
-          break;
-        case CommandKind::Broadcast:
-          std::memcpy(region(p, in, out, c.dst), region(p, in, out, c.src), c.size);
-          std::memcpy(region(p, in, out, c.dst2), region(p, in, out, c.src), c.size);
-          break;
-        case CommandKind::Swap:
-          std::memcpy(tmp.data(), region(p, in, out, c.src), c.size);
-          std::memcpy(region(p, in, out, c.src), region(p, in, out, c.peer), c.size);
-          std::memcpy(region(p, in, out, c.peer), tmp.data(), c.size);
-          break;
-        default:
-          break;
-      }
-    }
+  if (nthreads < 1) nthreads = 1;
+  auto work = [&](int t) {
+    std::vector<std::uint8_t> tmp;
+    if (!spec.in_place)
+      for (int g = t; g < n; g += nthreads)
+        std::memcpy(out[g] + g * s, in[g] + (spec.kind == CollectiveKind::AllGather ? 0 : g * s), s);
+    for (size_t qi = t; qi < p.queues.size(); qi += nthreads) run_queue(p, p.queues[qi], in, out, tmp);
+  };
+  if (nthreads == 1) {
+    work(0);
+    return 0;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nthreads; ++t) pool.emplace_back(work, t);
+  for (auto& th : pool) th.join();
   return 0;
+}
+
+int ref_execute(const char* kind, const char* impl, std::int64_t s, int n, std::uint8_t** in,
+                std::uint8_t** out) {
+  return ref_execute_mt(kind, impl, s, n, in, out, 1);
 }
 
 }  // extern "C"

@@ -7,6 +7,7 @@
 // Variant choice (tile shape, occupancy, TMA vs registers) was measured with
 // tools/copy_bench.cu on the bench workload (profiles/copy_bench_r01.txt).
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -328,7 +329,29 @@ int64_t tiles_for(int64_t bytes, Mover m) {
   return (bytes + t - 1) / t;
 }
 
-int mover_grid(Mover m, int sms) { return m == Mover::Tma ? 2 * sms : 2 * sms; }
+// Default: a persistent grid of 2 CTAs per SM (fastest alone; the TMA ring
+// holds 128 KiB of shared memory per CTA). Beside compute, the mover's SM
+// footprint is a policy: CECOLL_SM_GRID=<ctas> caps the grid (SM budget),
+// CECOLL_SM_TILES_PER_CTA=<k> launches short-lived CTAs of k tiles so the
+// block scheduler can interleave a higher-priority stream's CTAs
+// (profiles/interference_r01.json).
+int mover_grid(Mover m, int sms) {
+  (void)m;
+  static const int cap = [] {
+    const char* e = std::getenv("CECOLL_SM_GRID");
+    return e ? std::atoi(e) : 0;
+  }();
+  return cap > 0 ? cap : 2 * sms;
+}
+
+int mover_grid_for(const ItemTable& t, int sms) {
+  static const int per_cta = [] {
+    const char* e = std::getenv("CECOLL_SM_TILES_PER_CTA");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (per_cta > 0) return (t.ntiles + per_cta - 1) / per_cta;
+  return mover_grid(t.mover, sms);
+}
 
 cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream) {
   if (t.nitems <= 0 || t.ntiles <= 0) return cudaSuccess;

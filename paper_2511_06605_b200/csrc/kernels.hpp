@@ -55,6 +55,8 @@ int64_t mover_tile_bytes(Mover m);
 int64_t tiles_for(int64_t bytes, Mover m);
 // Grid that fills the device for mover m (multiple of the SM count).
 int mover_grid(Mover m, int sms);
+// Grid for one table (honours CECOLL_SM_TILES_PER_CTA).
+int mover_grid_for(const ItemTable& t, int sms);
 
 cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream);
 

@@ -552,7 +552,11 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
     if (!v.empty()) return fail(CECOLL_INVALID_ARGUMENT, "program rejected: " + v);
     impl = given->impl;
   }
-  if (impl == Impl::Auto) impl = select(kind, s, n, w->ndevices);
+  if (impl == Impl::Auto) {
+    bool in_place = kind == Kind::AllToAll;
+    for (const CallArgs& a : args) in_place &= a.send == a.recv;
+    impl = in_place ? Impl::Swap : select(kind, s, n, w->ndevices);
+  }
   if (impl != Impl::Sm && !valid_for(impl, kind))
     return fail(CECOLL_UNSUPPORTED, std::string(impl_name(impl)) + " does not apply to " +
                                          (kind == Kind::AllGather ? "allgather" : "alltoall"));
@@ -835,7 +839,7 @@ Status build_graph(World* w, Plan* p, Unit& u) {
       cudaStream_t ls = rs->lanes[l.lane];
       CUDA_TRY(cudaStreamWaitEvent(ls, fork, 0));
       for (const Copy& c : l.copies) CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, ls));
-      if (l.table.nitems) CUDA_TRY(launch_items(l.table, mover_grid(l.table.mover, p->sms), ls));
+      if (l.table.nitems) CUDA_TRY(launch_items(l.table, mover_grid_for(l.table, p->sms), ls));
       CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], ls));
       CUDA_TRY(cudaStreamWaitEvent(u.arm, rs->lane_done[l.lane], 0));
     }
@@ -884,7 +888,7 @@ Status run_ce(World* w, Plan* p) {
     STATUS_TRY(submit(w, s, l.pre));
     STATUS_TRY(issue_copies(w, l.copies, s, true));
     if (l.table.nitems) {
-      CUDA_TRY(launch_items(l.table, mover_grid(l.table.mover, p->sms), s));
+      CUDA_TRY(launch_items(l.table, mover_grid_for(l.table, p->sms), s));
       ++w->counters[4];
       ++w->counters[6];
     }
@@ -913,7 +917,7 @@ Status run_sm(World* w, Plan* p) {
     DeviceGuard g(u.device);
     STATUS_TRY(submit(w, u.stream, u.sm_pre));
     if (u.table.nitems) {
-      CUDA_TRY(launch_items(u.table, mover_grid(u.table.mover, p->sms), u.stream));
+      CUDA_TRY(launch_items(u.table, mover_grid_for(u.table, p->sms), u.stream));
       ++w->counters[4];
       ++w->counters[6];
     }
@@ -1022,7 +1026,11 @@ Status plan_destroy(World* w, Plan* p) {
 }
 
 Status run_collective(World* w, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args) {
-  if (impl == Impl::Auto) impl = select(kind, s, w->nranks, w->ndevices);
+  if (impl == Impl::Auto) {
+    bool in_place = kind == Kind::AllToAll;
+    for (const CallArgs& a : args) in_place &= a.send == a.recv;
+    impl = in_place ? Impl::Swap : select(kind, s, w->nranks, w->ndevices);
+  }
   Plan* p = nullptr;
   for (auto& cand : w->plans)
     if (same_call(cand.get(), kind, impl, s, args)) {

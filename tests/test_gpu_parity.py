@@ -230,3 +230,25 @@ def test_executes_the_reference_program_text(e):
     plan.destroy()
     torch.cuda.synchronize()
     assert ora.Oracle().check(kind, s, n, in_place, host_in, res) == -1
+
+
+def test_auto_picks_swap_for_inplace_alltoall():
+    n, s = 4, 4096
+    O = ora.Oracle()
+    host_in = [ora.splitmix_pattern(n * s, r, 77) for r in range(n)]
+    bufs = [torch.from_numpy(h).cuda() for h in host_in]
+    cc.all_to_all(comms(n), bufs, bufs, s, impl="auto")
+    torch.cuda.synchronize()
+    assert O.check("alltoall", s, n, True, host_in, [b.cpu().numpy() for b in bufs]) == -1
+
+
+@pytest.mark.parametrize("impl", ["sm", "pcpy", "b2b", "prelaunch_b2b", "bcst", "swap"])
+@pytest.mark.parametrize("n", [16, 32])
+def test_many_ranks(impl, n):
+    """Up to kMaxRanks co-resident ranks (the reference tests n up to 16,
+    acceptance.cpp:89-143); per-rank streams exercise every flag pair."""
+    kind = "allgather" if impl == "bcst" else "alltoall"
+    s = 4096 + 48
+    O = ora.Oracle()
+    host_in, res, _, _ = run(kind, impl, s, n, seed=3, stream_mode="per_rank" if n == 16 else "shared")
+    assert O.check(kind, s, n, impl.endswith("swap"), host_in, res) == -1

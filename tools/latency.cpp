@@ -1,0 +1,114 @@
+// Small-message latency of every implementation through the C ABI, from C++
+// (no Python in the loop): the library's own control cost per collective.
+//
+//   tools/latency [nranks] [iters]      (GPU box; ranks co-resident on GPU 0)
+//
+// Prints CSV: api,impl,collective,size_bytes,device_us_b2b,device_us_isolated,host_us
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "../include/cecoll.h"
+
+#define CK(x)                                                                             \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess) {                                                              \
+      std::printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      std::exit(1);                                                                       \
+    }                                                                                     \
+  } while (0)
+#define CC(x)                                                                                \
+  do {                                                                                       \
+    cecoll_status_t s_ = (x);                                                                \
+    if (s_ != CECOLL_SUCCESS) {                                                              \
+      std::printf("cecoll error %s (%s) at %s:%d\n", cecoll_strerror(s_), cecoll_last_error(), \
+                  __FILE__, __LINE__);                                                       \
+      std::exit(1);                                                                          \
+    }                                                                                        \
+  } while (0)
+
+int main(int argc, char** argv) {
+  const int n = argc > 1 ? std::atoi(argv[1]) : 8;
+  const int iters = argc > 2 ? std::atoi(argv[2]) : 500;
+  CK(cudaSetDevice(0));
+  std::vector<int> devs(n, 0);
+  std::vector<cecoll_comm_t> comms(n);
+  CC(cecoll_comm_init_all(comms.data(), n, devs.data()));
+  cudaStream_t stream;
+  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  std::vector<void*> streams(n, stream);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const size_t max_s = 1 << 20;
+  std::vector<void*> send(n), recv(n);
+  for (int r = 0; r < n; ++r) {
+    CK(cudaMalloc(&send[r], n * max_s));
+    CK(cudaMalloc(&recv[r], n * max_s));
+    CK(cudaMemset(send[r], r, n * max_s));
+  }
+  std::printf("api,impl,collective,size_bytes,device_us_b2b,device_us_isolated,host_us\n");
+  const char* names[] = {"sm", "pcpy", "b2b", "bcst", "swap", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_bcst",
+                         "prelaunch_swap"};
+  for (int kind = 0; kind < 2; ++kind) {
+    for (size_t s = 4096; s <= max_s; s *= 4) {
+      for (const char* name : names) {
+        const cecoll_impl_t impl = cecoll_parse_impl(name);
+        if (!cecoll_impl_valid_for(impl, static_cast<cecoll_kind_t>(kind))) continue;
+        const bool in_place = std::string(name).find("swap") != std::string::npos;
+        std::vector<void*> rv = in_place ? send : recv;
+        for (int api = 0; api < 2; ++api) {  // 0: plan, 1: eager collective_n
+          cecoll_plan_t plan = nullptr;
+          auto call = [&]() {
+            if (api == 0) {
+              CC(cecoll_plan_launch(plan, streams.data()));
+            } else {
+              CC(cecoll_collective_n(static_cast<cecoll_kind_t>(kind), comms.data(), n, send.data(), rv.data(), s,
+                                     impl, streams.data()));
+            }
+          };
+          if (api == 0)
+            CC(cecoll_plan_create(comms.data(), n, static_cast<cecoll_kind_t>(kind), send.data(), rv.data(), s, impl,
+                                  &plan));
+          for (int i = 0; i < 10; ++i) call();
+          CK(cudaStreamSynchronize(stream));
+          auto h0 = std::chrono::steady_clock::now();
+          CK(cudaEventRecord(e0, stream));
+          for (int i = 0; i < iters; ++i) call();
+          CK(cudaEventRecord(e1, stream));
+          auto h1 = std::chrono::steady_clock::now();
+          CK(cudaStreamSynchronize(stream));
+          float ms_b2b = 0;
+          CK(cudaEventElapsedTime(&ms_b2b, e0, e1));
+          std::vector<float> iso;
+          for (int i = 0; i < 20; ++i) {
+            CK(cudaStreamSynchronize(stream));
+            CK(cudaEventRecord(e0, stream));
+            call();
+            CK(cudaEventRecord(e1, stream));
+            CK(cudaStreamSynchronize(stream));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            iso.push_back(ms);
+          }
+          std::sort(iso.begin(), iso.end());
+          const double host_us = std::chrono::duration<double, std::micro>(h1 - h0).count() / iters;
+          std::printf("%s,%s,%s,%zu,%.2f,%.2f,%.2f\n", api == 0 ? "plan" : "eager", name,
+                      kind == 0 ? "allgather" : "alltoall", s, ms_b2b * 1000 / iters, iso[iso.size() / 2] * 1000,
+                      host_us);
+          std::fflush(stdout);
+          if (plan) CC(cecoll_plan_destroy(plan));
+          CK(cudaStreamSynchronize(stream));
+        }
+      }
+    }
+  }
+  for (auto c : comms) CC(cecoll_comm_destroy(c));
+  return 0;
+}
