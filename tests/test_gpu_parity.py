@@ -252,3 +252,36 @@ def test_many_ranks(impl, n):
     O = ora.Oracle()
     host_in, res, _, _ = run(kind, impl, s, n, seed=3, stream_mode="per_rank" if n == 16 else "shared")
     assert O.check(kind, s, n, impl.endswith("swap"), host_in, res) == -1
+
+
+@pytest.mark.parametrize("impl", ["sm", "pcpy", "b2b", "prelaunch_pcpy", "swap", "prelaunch_swap"])
+def test_flag_protocol_under_random_delays(impl):
+    """Stress of the rdy/done protocol: one stream per rank,
+    random spin delays injected into random ranks' streams before each
+    collective, 25 back-to-back collectives on the same buffers, every result
+    checked. A lost or early flag shows up as a mismatch (or a hang, bounded
+    by the test timeout)."""
+    import random
+
+    n, s = 6, 12288
+    cs = comms(n)
+    O = ora.Oracle()
+    rng = random.Random(impl)
+    streams = [torch.cuda.Stream() for _ in range(n)]
+    sends = [torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    recvs = sends if impl.endswith("swap") else [torch.empty(n * s, dtype=torch.uint8, device="cuda")
+                                                 for _ in range(n)]
+    for it in range(25):
+        host_in = [ora.splitmix_pattern(n * s, r, 1000 + it) for r in range(n)]
+        torch.cuda.synchronize()
+        for t, h in zip(sends, host_in):
+            t.copy_(torch.from_numpy(h))
+        torch.cuda.synchronize()
+        for st in streams:
+            if rng.random() < 0.5:
+                with torch.cuda.stream(st):
+                    torch.cuda._sleep(rng.randint(1000, 200000))
+        cc.all_to_all(cs, sends, recvs, s, impl=impl, streams=streams)
+        torch.cuda.synchronize()
+        res = [t.cpu().numpy() for t in recvs]
+        assert O.check("alltoall", s, n, impl.endswith("swap"), host_in, res) == -1, it
