@@ -499,6 +499,78 @@ def run_interference(args):
     cc.destroy_all(comms)
 
 
+def run_sync_chain(args):
+    """Producer GEMM -> all-gather synchronisation (simulate_sync_chain,
+    sim.cpp:475-499; §4.3). overhead = T(GEMM then collective on one
+    stream) - T(GEMM) - T(collective). Modes: `stream` (collective enqueued
+    behind the GEMM, no host involvement), `prelaunch` (armed plan triggered
+    by a stream write when the GEMM ends), `host` (the host waits for the GEMM
+    and then issues the collective: the CPU-forwarded chain of the paper)."""
+    import torch
+
+    torch.cuda.set_device(0)
+    n = args.ranks
+    comms = cc.Comm.init_all([0] * n)
+    N = args.sync_gemm
+    a = torch.randn(N, N, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(N, N, device="cuda", dtype=torch.bfloat16)
+    c = torch.empty(N, N, device="cuda", dtype=torch.bfloat16)
+    S = torch.cuda.Stream()
+    res = {"gemm": f"bf16 {N}^3", "ranks": n, "cases": []}
+
+    def timed(fn, iters=20):
+        for _ in range(3):
+            fn()
+        S.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ts = []
+        for _ in range(iters):
+            S.synchronize()
+            e0.record(S)
+            fn()
+            e1.record(S)
+            S.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ts.sort()
+        return ts[len(ts) // 2]
+
+    def gemm():
+        with torch.cuda.stream(S):
+            torch.matmul(a, b, out=c)
+
+    t_gemm = timed(gemm)
+    for s in (1 << 20, 16 << 20, 256 << 20):
+        sends = [torch.empty(s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+        recvs = [torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+        for mode, impl in (("stream", "sm"), ("stream", "b2b"), ("prelaunch", "prelaunch_b2b"),
+                           ("prelaunch", "prelaunch_pcpy"), ("host", "sm")):
+            plan = cc.Plan(comms, "allgather", sends, recvs, s, impl=impl)
+
+            def coll():
+                plan.launch(S)
+
+            def chain():
+                gemm()
+                if mode == "host":
+                    S.synchronize()  # the CPU observes the GEMM, then issues
+                coll()
+
+            t_coll = timed(coll)
+            t_chain = timed(chain)
+            plan.destroy()
+            torch.cuda.synchronize()
+            row = {"s": s, "mode": mode, "impl": impl, "gemm_ms": round(t_gemm, 4), "collective_ms": round(t_coll, 4),
+                   "chain_ms": round(t_chain, 4), "overhead_us": round((t_chain - t_gemm - t_coll) * 1e3, 2)}
+            res["cases"].append(row)
+            print(row, flush=True)
+        del sends, recvs
+        torch.cuda.empty_cache()
+    print(json.dumps(res), flush=True)
+    with open(args.sync_out, "w") as f:
+        json.dump(res, f, indent=1)
+    cc.destroy_all(comms)
+
+
 def run_ours_multiprocess(args):
     """torchrun, one process per GPU: the same 8-rank collective with 8/N
     ranks co-resident on each GPU (strong scaling: total work fixed). Flag
@@ -738,8 +810,13 @@ def main():
     ap.add_argument("--interference-out", default=os.path.join(ROOT, "gpurun_out", "interference.json"))
     ap.add_argument("--gemm-iters", type=int, default=200)
     ap.add_argument("--gemm-priority", default="same", choices=["same", "high"])
+    ap.add_argument("--sync-chain", action="store_true", help="producer GEMM -> all-gather chain overhead")
+    ap.add_argument("--sync-gemm", type=int, default=4096)
+    ap.add_argument("--sync-out", default=os.path.join(ROOT, "gpurun_out", "sync_chain.json"))
     args = ap.parse_args()
-    if args.interference:
+    if args.sync_chain:
+        run_sync_chain(args)
+    elif args.interference:
         run_interference(args)
     elif args.sweep:
         run_sweep(args)

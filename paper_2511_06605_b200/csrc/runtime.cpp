@@ -447,10 +447,14 @@ Item make_item(ItemKind kind, const char* src, char* dst, char* dst2, int64_t by
   return it;
 }
 
-// A host-side item plus, for kItemFan, its destination list.
+// A host-side item plus, for kItemFan, its destination list. `remote`: some
+// destination is another device's memory (NVLink); such tables use the
+// register mover (plain st.global to peer-mapped addresses) rather than TMA
+// bulk stores.
 struct HostItem {
   Item item;
   std::vector<char*> fan;
+  bool remote = false;
 };
 
 // Chooses the mover (TMA for aligned copy/fan tables unless
@@ -468,7 +472,7 @@ Status upload_items(Plan* p, int device, std::vector<HostItem>& host, ItemTable*
     kinds |= 1 << it.kind;
     uintptr_t a = reinterpret_cast<uintptr_t>(it.src) | reinterpret_cast<uintptr_t>(it.dst);
     for (char* f : h.fan) a |= reinterpret_cast<uintptr_t>(f);
-    tma &= (it.kind == kItemCopy || it.kind == kItemFan) && (a & 15) == 0 && (it.bytes & 15) == 0;
+    tma &= (it.kind == kItemCopy || it.kind == kItemFan) && (a & 15) == 0 && (it.bytes & 15) == 0 && !h.remote;
     nfan += h.fan.size();
   }
   const char* env = std::getenv("CECOLL_MOVER");
@@ -691,6 +695,7 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
           for (int d = 0; d < n; ++d) {
             char* dst = ad.recv[(r + d) % n] + r * s;
             if (dst != ad.send[r]) h.fan.push_back(dst);
+            h.remote |= w->device[(r + d) % n] != u.device;
           }
           if (h.fan.size() == 1) h.item = make_item(kItemCopy, ad.send[r], h.fan[0], nullptr, s), h.fan.clear();
           if (!h.fan.empty() || h.item.kind == kItemCopy) items.push_back(h);
@@ -700,7 +705,8 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
           if (c.dst == ad.recv[r] + r * s) items.push_back({make_item(kItemCopy, c.src, c.dst, nullptr, c.bytes), {}});
         for (int d = 1; d < n; ++d) {
           const int j = (r + d) % n;
-          items.push_back({make_item(kItemCopy, ad.send[r] + j * s, ad.recv[j] + r * s, nullptr, s), {}});
+          items.push_back({make_item(kItemCopy, ad.send[r] + j * s, ad.recv[j] + r * s, nullptr, s), {},
+                           w->device[j] != u.device});
         }
       }
       u.placement.clear();
@@ -725,12 +731,15 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
             dests.insert(c.dst.rank);
             break;
           case Op::Broadcast:
-            items.push_back({make_item(kItemBcst, addr(c.src), addr(c.dst), addr(c.dst2), c.size), {}});
+            items.push_back({make_item(kItemBcst, addr(c.src), addr(c.dst), addr(c.dst2), c.size), {},
+                             w->device[c.dst.rank] != w->device[l.rank] ||
+                                 w->device[c.dst2.rank] != w->device[l.rank]});
             dests.insert(c.dst.rank);
             dests.insert(c.dst2.rank);
             break;
           case Op::Swap:
-            items.push_back({make_item(kItemSwap, addr(c.peer), addr(c.src), nullptr, c.size), {}});
+            items.push_back({make_item(kItemSwap, addr(c.peer), addr(c.src), nullptr, c.size), {},
+                             w->device[c.peer.rank] != w->device[l.rank]});
             dests.insert(c.peer.rank);
             break;
           default: break;  // Signal / Poll: realised by the flag operations below
