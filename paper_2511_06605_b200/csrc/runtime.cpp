@@ -1010,12 +1010,20 @@ Status plan_launch(World* w, Plan* p, bool rearm) {
 
 Status plan_destroy(World* w, Plan* p) {
   (void)w;
+  Status result;
   for (Unit& u : p->units) {
     DeviceGuard g(u.device);
     if (u.armed) {
       post_gate(u, 2);  // cancel: the gate skips the body
       cudaStreamSynchronize(u.arm);
       u.armed = false;
+    }
+    if (u.err) {  // kernel-side polls report timeouts here (kernels.cu poll_kernel)
+      if (u.arm) cudaStreamSynchronize(u.arm);
+      uint64_t err = 0;
+      if (cudaMemcpy(&err, u.err, sizeof(err), cudaMemcpyDeviceToHost) == cudaSuccess && err && result.ok())
+        result = fail(CECOLL_TIMEOUT, (err & 1) ? "a flag poll timed out (20 s): a peer never signalled"
+                                                : "gate received an unknown post");
     }
     if (u.exec) cudaGraphExecDestroy(u.exec);
     if (u.graph) cudaGraphDestroy(u.graph);
@@ -1031,7 +1039,7 @@ Status plan_destroy(World* w, Plan* p) {
     cudaFree(p->dev_allocs[i]);
   }
   p->dev_allocs.clear();
-  return {};
+  return result;
 }
 
 Status run_collective(World* w, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args) {
