@@ -716,6 +716,21 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->units[0].device);
     p->sms = sms;
   } else {
+    // A recorded (prelaunch) graph moves its same-device chunks with one item
+    // kernel per unit instead of one memcpy node per copy: the driver runs
+    // same-device memcpy on SMs anyway (profiles/ce_probe2_r01.txt) and every
+    // graph node costs launch latency. Cross-device copies stay memcpy nodes
+    // (copy engines over NVLink). CECOLL_GRAPH_MEMCPY=1 keeps every copy a
+    // memcpy node.
+    const char* gm = std::getenv("CECOLL_GRAPH_MEMCPY");
+    const bool merge = p->prelaunch && !(gm && std::string(gm) == "1");
+    std::vector<std::vector<HostItem>> unit_items(p->units.size());
+    if (merge)
+      for (size_t ui = 0; ui < p->units.size(); ++ui) {
+        for (const Copy& c : p->units[ui].placement)
+          unit_items[ui].push_back({make_item(kItemCopy, c.src, c.dst, nullptr, c.bytes), {}});
+        p->units[ui].placement.clear();
+      }
     // Lanes of the command program owned by local ranks.
     for (const Lane& l : p->program.lanes) {
       if (unit_of[l.rank] < 0) continue;
@@ -724,22 +739,25 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
       le.lane = l.index;
       std::set<int> dests;
       std::vector<HostItem> items;
+      const int dev = w->device[l.rank];
       for (const Command& c : l.cmds) {
+        const bool local_cmd = w->device[c.src.rank] == dev && w->device[c.dst.rank] == dev &&
+                               (c.op != Op::Broadcast || w->device[c.dst2.rank] == dev) &&
+                               (c.op != Op::Swap || w->device[c.peer.rank] == dev);
+        std::vector<HostItem>& sink = merge && local_cmd ? unit_items[unit_of[l.rank]] : items;
         switch (c.op) {
           case Op::Copy:
-            le.copies.push_back({addr(c.dst), addr(c.src), c.size});
+            if (merge && local_cmd) sink.push_back({make_item(kItemCopy, addr(c.src), addr(c.dst), nullptr, c.size), {}});
+            else le.copies.push_back({addr(c.dst), addr(c.src), c.size});
             dests.insert(c.dst.rank);
             break;
           case Op::Broadcast:
-            items.push_back({make_item(kItemBcst, addr(c.src), addr(c.dst), addr(c.dst2), c.size), {},
-                             w->device[c.dst.rank] != w->device[l.rank] ||
-                                 w->device[c.dst2.rank] != w->device[l.rank]});
+            sink.push_back({make_item(kItemBcst, addr(c.src), addr(c.dst), addr(c.dst2), c.size), {}, !local_cmd});
             dests.insert(c.dst.rank);
             dests.insert(c.dst2.rank);
             break;
           case Op::Swap:
-            items.push_back({make_item(kItemSwap, addr(c.peer), addr(c.src), nullptr, c.size), {},
-                             w->device[c.peer.rank] != w->device[l.rank]});
+            sink.push_back({make_item(kItemSwap, addr(c.peer), addr(c.src), nullptr, c.size), {}, !local_cmd});
             dests.insert(c.peer.rank);
             break;
           default: break;  // Signal / Poll: realised by the flag operations below
@@ -758,6 +776,8 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->units[0].device);
     p->sms = sms;
+    for (size_t ui = 0; ui < p->units.size(); ++ui)
+      STATUS_TRY(upload_items(p, p->units[ui].device, unit_items[ui], &p->units[ui].table));
     if (p->prelaunch)
       for (Unit& u : p->units) STATUS_TRY(build_graph(w, p, u));
   }
@@ -842,16 +862,22 @@ Status build_graph(World* w, Plan* p, Unit& u) {
     cudaEvent_t fork;
     CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     CUDA_TRY(cudaEventRecord(fork, u.arm));
+    std::vector<const LaneExec*> busy;
     for (const LaneExec& l : p->lanes) {
       if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) == u.ranks.end()) continue;
+      if (l.copies.empty() && !l.table.nitems) continue;  // its chunks are in the unit kernel
       RankState* rs = w->local[l.rank].get();
       cudaStream_t ls = rs->lanes[l.lane];
       CUDA_TRY(cudaStreamWaitEvent(ls, fork, 0));
       for (const Copy& c : l.copies) CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, ls));
       if (l.table.nitems) CUDA_TRY(launch_items(l.table, mover_grid_for(l.table, p->sms), ls));
       CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], ls));
-      CUDA_TRY(cudaStreamWaitEvent(u.arm, rs->lane_done[l.lane], 0));
+      busy.push_back(&l);
     }
+    // Same-device chunks of every lane of the unit: one item kernel.
+    if (u.table.nitems) CUDA_TRY(launch_items(u.table, mover_grid_for(u.table, p->sms), u.arm));
+    for (const LaneExec* l : busy)
+      CUDA_TRY(cudaStreamWaitEvent(u.arm, w->local[l->rank]->lane_done[l->lane], 0));
     CUDA_TRY(launch_signal(u.sig_tab, u.nsig, u.arm));
     cudaEventDestroy(fork);
     return {};
