@@ -134,3 +134,57 @@ def test_parse_rejects_malformed_text():
     bad = cc.Program.parse("q0(g0e0)\t0\tcopy\tg0.in[0+1024]\tg1.out[4096+1024]\t1024\t-\n"
                            "q0(g0e0)\t1\tsignal\t-\t-\t0\t0\n", "allgather", 1024, 2)
     assert "out of declared bounds" in bad.validate()
+
+
+def _ref_dump(kind, impl, s, n):
+    with open(os.path.join(GOLDEN, "programs.json")) as f:
+        for e in json.load(f)["programs"]:
+            if (e["kind"], e["impl"], e["s"], e["n"]) == (kind, impl, s, n) and "dump" in e:
+                return e["dump"]
+    raise KeyError((kind, impl, s, n))
+
+
+def _mutate(text, fn):
+    lines = [line.split("\t") for line in text.splitlines()]
+    fn(lines)
+    return "\n".join("\t".join(f) for f in lines) + "\n"
+
+
+def test_validate_catches_engine_overflow_and_duplicates():
+    # test_program.cpp:94-110: engine index past the budget; two queues on one engine.
+    text = _ref_dump("allgather", "pcpy", 4096, 8)
+    over = _mutate(text, lambda ls: [f.__setitem__(0, "q0(g0e16)") for f in ls if f[0] == "q0(g0e0)"])
+    assert "engine overflow" in cc.Program.parse(over, "allgather", 4096, 8).validate(16)
+    dup = _mutate(text, lambda ls: [f.__setitem__(0, "q1(g0e0)") for f in ls if f[0] == "q1(g0e1)"])
+    assert "share one engine" in cc.Program.parse(dup, "allgather", 4096, 8).validate(16)
+
+
+def test_validate_requires_trailing_signal_and_matching_triggers():
+    # test_program.cpp:112-138: dropped AtomicSignal; trigger slots vs polls.
+    text = _ref_dump("allgather", "pcpy", 4096, 8)
+    dropped = _mutate(text, lambda ls: ls.remove(next(f for f in ls if f[0].startswith("q3(") and f[2] == "signal")))
+    assert "unsignaled queue" in cc.Program.parse(dropped, "allgather", 4096, 8).validate(16)
+    pre = _ref_dump("allgather", "prelaunch_pcpy", 4096, 8)
+    assert cc.Program.parse(pre, "allgather", 4096, 8).validate(16) is None
+    late_poll = _mutate(pre, lambda ls: ls.insert(2, ["q0(g0e0)", "1", "poll", "-", "-", "0", "100999"]))
+    assert "poll must precede" in cc.Program.parse(late_poll, "allgather", 4096, 8).validate(16)
+
+
+def test_validate_rejects_overlap_and_same_gpu_swap():
+    text = _ref_dump("alltoall", "pcpy", 4096, 4)
+    overlap = _mutate(text, lambda ls: [f.__setitem__(4, f[3].replace(".in[", ".in[")) for f in ls
+                                        if f[0] == "q0(g0e0)" and f[2] == "copy"])
+    assert "overlap" in cc.Program.parse(overlap, "alltoall", 4096, 4).validate(16)
+    swap = _ref_dump("alltoall", "swap", 4096, 4)
+    same = _mutate(swap, lambda ls: [f.__setitem__(4, f[3]) for f in ls if f[2] == "swap"][:1])
+    assert "distinct gpus" in cc.Program.parse(same, "alltoall", 4096, 4).validate(16)
+
+
+def test_b200_selector_is_total_and_valid():
+    for kind in ("allgather", "alltoall"):
+        for ndev in (1, 2, 8):
+            for k in range(10, 33):
+                impl = cc.select(kind, 1 << k, 8, ndev)
+                assert impl == "sm" or impl in cc.IMPLS_FOR[kind]
+    assert cc.select("allgather", 1 << 30, 8, 1) == "sm"
+    assert cc.select("alltoall", 4096, 8, 8) == "sm"
