@@ -176,6 +176,12 @@ cecoll_status_t cecoll_plan_create_program(const cecoll_comm_t* comms, int ncomm
  * comms[i]; NULL entries = host trigger) and make each stream wait for
  * completion; re-arms the next instance off the critical path. */
 cecoll_status_t cecoll_plan_launch(cecoll_plan_t plan, void* const* streams);
+/* Cancels the armed instance (the next launch re-arms). While a plan is
+ * armed its gate kernel waits on the device, so device-wide synchronisation
+ * (cudaDeviceSynchronize) only returns after disarm, destroy or a launch. */
+cecoll_status_t cecoll_plan_disarm(cecoll_plan_t plan);
+/* Destroy plans before their communicators; cecoll_comm_destroy cancels any
+ * plan still armed (its handle must not be used afterwards). */
 cecoll_status_t cecoll_plan_destroy(cecoll_plan_t plan);
 
 /* Counters since comm creation: [0] collectives, [1] copy commands issued

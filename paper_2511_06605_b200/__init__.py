@@ -123,6 +123,7 @@ def lib():
         "cecoll_plan_create": ([C.POINTER(vp), i32, i32, C.POINTER(vp), C.POINTER(vp), sz, i32, C.POINTER(vp)], i32),
         "cecoll_plan_launch": ([vp, C.POINTER(vp)], i32),
         "cecoll_plan_destroy": ([vp], i32),
+        "cecoll_plan_disarm": ([vp], i32),
         "cecoll_comm_counters": ([vp, C.POINTER(i64)], i32),
     }
     for name, (args, res) in sig.items():
@@ -141,7 +142,7 @@ EXPORTED_SYMBOLS = [
     "cecoll_register", "cecoll_deregister", "cecoll_allgather", "cecoll_alltoall", "cecoll_group_start",
     "cecoll_group_end", "cecoll_plan_create", "cecoll_plan_launch", "cecoll_plan_destroy", "cecoll_comm_counters",
     "cecoll_program_parse", "cecoll_plan_create_program", "cecoll_comm_init_ranks", "cecoll_exchange_check",
-    "cecoll_collective_n",
+    "cecoll_collective_n", "cecoll_plan_disarm",
 ]
 
 
@@ -405,6 +406,10 @@ class Plan:
             streams = [streams] * self._n
         arr = (C.c_void_p * self._n)(*[_stream(s) for s in streams])
         _check(lib().cecoll_plan_launch(self._h, arr), "plan_launch")
+
+    def disarm(self):
+        """Cancel the armed instance (needed before torch.cuda.synchronize())."""
+        _check(lib().cecoll_plan_disarm(self._h), "plan_disarm")
 
     def destroy(self):
         if self._h is not None:

@@ -1,6 +1,7 @@
 // extern "C" boundary (include/cecoll.h). Exceptions never cross it: the
 // reference's std::invalid_argument sites become CECOLL_INVALID_ARGUMENT /
 // CECOLL_UNSUPPORTED and the message is kept for cecoll_last_error().
+#include <algorithm>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -327,6 +328,7 @@ cecoll_status_t cecoll_plan_create(const cecoll_comm_t* comms, int ncomms, cecol
   Status s = plan_create(w, static_cast<Kind>(kind), static_cast<Impl>(impl), static_cast<int64_t>(chunk_bytes),
                          args, &p);
   if (!s.ok()) return st(s);
+  w->explicit_plans.push_back(p);
   *out = new cecoll_plan{w, p};
   return CECOLL_SUCCESS;
 }
@@ -345,6 +347,7 @@ cecoll_status_t cecoll_plan_create_program(const cecoll_comm_t* comms, int ncomm
   Plan* p = nullptr;
   Status s = plan_create(w, prog.spec.kind, prog.impl, prog.spec.chunk, args, &p, &prog);
   if (!s.ok()) return st(s);
+  w->explicit_plans.push_back(p);
   *out = new cecoll_plan{w, p};
   return CECOLL_SUCCESS;
 }
@@ -365,10 +368,17 @@ cecoll_status_t cecoll_plan_launch(cecoll_plan_t plan, void* const* streams) {
 
 cecoll_status_t cecoll_plan_destroy(cecoll_plan_t plan) {
   if (!plan) return err(CECOLL_INVALID_ARGUMENT, "null plan");
+  auto& v = plan->world->explicit_plans;
+  v.erase(std::remove(v.begin(), v.end(), plan->plan), v.end());
   Status s = plan_destroy(plan->world, plan->plan);
   delete plan->plan;
   delete plan;
   return st(s);
+}
+
+cecoll_status_t cecoll_plan_disarm(cecoll_plan_t plan) {
+  if (!plan) return err(CECOLL_INVALID_ARGUMENT, "null plan");
+  return st(plan_disarm(plan->world, plan->plan));
 }
 
 cecoll_status_t cecoll_comm_counters(cecoll_comm_t comm, int64_t out8[8]) {

@@ -208,13 +208,17 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
     *off_out = off;
     *bytes = static_cast<uint32_t>(rem < kTmaTile ? rem : kTmaTile);
   };
+  // Streamed data is touched once: evict-first in L2 for loads and stores
+  // (profiles/copy_bench2_r01.txt: +1-5% at 1-8 MiB chunks, neutral above).
+  uint64_t policy;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
   auto load = [&](int stage, const char* src, uint32_t bytes) {
     const uint32_t bar = smem_addr(&full[stage]);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_addr(ring + stage * kTmaTile)),
-        "l"(src), "r"(bytes), "r"(bar)
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_addr(ring + stage * kTmaTile)),
+        "l"(src), "r"(bytes), "r"(bar), "l"(policy)
         : "memory");
   };
   int sitem[kTmaStages];
@@ -238,13 +242,15 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
     phase ^= 1u << st;
     const Item& it = items[sitem[st]];
     const uint32_t from = smem_addr(ring + st * kTmaTile);
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(it.dst + soff[st]), "r"(from),
-                 "r"(nbytes[st])
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                     it.dst + soff[st]),
+                 "r"(from), "r"(nbytes[st]), "l"(policy)
                  : "memory");
     if (it.kind == kItemFan)
       for (int f = 1; f < it.nfan; ++f)
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(it.fan[f] + soff[st]),
-                     "r"(from), "r"(nbytes[st])
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                         it.fan[f] + soff[st]),
+                     "r"(from), "r"(nbytes[st]), "l"(policy)
                      : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     if (issued < mine) {

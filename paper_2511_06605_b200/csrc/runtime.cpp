@@ -397,6 +397,11 @@ Status world_deregister(World* w, void* ptr) {
 void world_release(World* w) {
   for (auto& p : w->plans) plan_destroy(w, p.get());
   w->plans.clear();
+  // Armed explicit plans would keep their gate kernels waiting (and the
+  // device synchronisation below would never return): cancel them. Their
+  // cecoll_plan handles must not be used afterwards.
+  for (Plan* p : w->explicit_plans) plan_destroy(w, p);
+  w->explicit_plans.clear();
   for (auto& rs : w->local) {
     if (!rs) continue;
     DeviceGuard g(rs->device);
@@ -1015,6 +1020,20 @@ bool same_call(const Plan* p, Kind kind, Impl impl, int64_t s, const std::vector
 }
 
 }  // namespace
+
+// Cancels armed instances (the next launch re-arms): after this, device-wide
+// synchronisation returns.
+Status plan_disarm(World* w, Plan* p) {
+  (void)w;
+  for (Unit& u : p->units) {
+    if (!u.armed) continue;
+    DeviceGuard g(u.device);
+    STATUS_TRY(post_gate(u, 2));
+    CUDA_TRY(cudaStreamSynchronize(u.arm));
+    u.armed = false;
+  }
+  return {};
+}
 
 Status plan_arm(World* w, Plan* p) {
   if (!p->prelaunch) return {};

@@ -84,6 +84,7 @@ struct World {
   std::vector<std::unique_ptr<RankState>> local;  // by rank; null if remote
   std::atomic<int64_t> counters[8];
   std::vector<std::unique_ptr<Plan>> plans;  // eager-call plan cache
+  std::vector<Plan*> explicit_plans;         // cecoll_plan_create; cancelled at release
   std::vector<Window> windows;
   std::vector<int> reg_rounds;  // per local index
   std::vector<void*> ipc_opened;
@@ -188,6 +189,7 @@ Status run_collective(World* w, Kind kind, Impl impl, int64_t chunk, const std::
 Status plan_create(World* w, Kind kind, Impl impl, int64_t chunk, const std::vector<CallArgs>& args, Plan** out,
                    const Program* given = nullptr);
 Status plan_arm(World* w, Plan* p);
+Status plan_disarm(World* w, Plan* p);
 Status plan_launch(World* w, Plan* p, bool rearm);
 Status plan_destroy(World* w, Plan* p);
 
