@@ -499,6 +499,53 @@ def run_interference(args):
     cc.destroy_all(comms)
 
 
+def run_sweep_rs(args):
+    """Reduce-scatter sweep (bf16 sum, co-resident ranks): busBW = (n-1)*chunk/t
+    (nccl-tests convention) and HBM roofline of the SM path (n+1 chunk
+    transfers per rank: n reads and one write)."""
+    import torch
+
+    n = args.ranks
+    torch.cuda.set_device(0)
+    comms = cc.Comm.init_all([0] * n)
+    peak, _ = load_peaks()
+    stream = torch.cuda.Stream()
+    rows = []
+    for count in [2048 << (2 * k) for k in range(9)]:  # 4 KiB .. 256 MiB bf16 chunks
+        s = count * 2
+        sends = [torch.randn(n * count, device="cuda").to(torch.bfloat16) for _ in range(n)]
+        recvs = [torch.empty(count, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
+        for impl in ("sm", "pcpy", "b2b", "prelaunch_pcpy"):
+            def call():
+                cc.reduce_scatter(comms, sends, recvs, count, dtype="bf16", op="sum", impl=impl, streams=stream)
+
+            for _ in range(3):
+                call()
+            stream.synchronize()
+            iters = int(max(5, min(300, 2e9 / (n * (n + 1) * s))))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(iters):
+                call()
+            e1.record(stream)
+            stream.synchronize()
+            ms = e0.elapsed_time(e1) / iters
+            hbm = n * (n + 1) * s / (ms / 1e3) / 1e9
+            row = {"impl": impl, "collective": "reduce_scatter_bf16_sum", "ranks": n, "size_bytes": s,
+                   "total_ns": round(ms * 1e6), "busbw_gbs": round(busbw(n, s, ms / 1e3), 3),
+                   "hbm_gbs": round(hbm, 1), "roofline_frac": round(hbm / peak, 4)}
+            rows.append(row)
+            print(row, flush=True)
+        del sends, recvs
+        torch.cuda.empty_cache()
+    with open(args.sweep_out, "w") as f:
+        cols = list(rows[0].keys())
+        f.write(",".join(cols) + "\n")
+        for r in rows:
+            f.write(",".join(str(r[c]) for c in cols) + "\n")
+    cc.destroy_all(comms)
+
+
 def run_sync_chain(args):
     """Producer GEMM -> all-gather synchronisation (simulate_sync_chain,
     sim.cpp:475-499; §4.3). overhead = T(GEMM then collective on one
@@ -813,8 +860,11 @@ def main():
     ap.add_argument("--sync-chain", action="store_true", help="producer GEMM -> all-gather chain overhead")
     ap.add_argument("--sync-gemm", type=int, default=4096)
     ap.add_argument("--sync-out", default=os.path.join(ROOT, "gpurun_out", "sync_chain.json"))
+    ap.add_argument("--sweep-rs", action="store_true", help="reduce-scatter sweep (bf16 sum)")
     args = ap.parse_args()
-    if args.sync_chain:
+    if args.sweep_rs:
+        run_sweep_rs(args)
+    elif args.sync_chain:
         run_sync_chain(args)
     elif args.interference:
         run_interference(args)

@@ -152,6 +152,22 @@ cecoll_status_t cecoll_alltoall(const void* send, void* recv, size_t chunk_bytes
                                 cecoll_comm_t comm, void* stream);
 cecoll_status_t cecoll_group_start(void);
 cecoll_status_t cecoll_group_end(void);
+
+/* Reduce-scatter — the third collective (§6.1; not in
+ * the reference). send holds n*count elements, recv count
+ * elements: recv of rank j = op over ranks i = 0..n-1 (in rank order) of
+ * send_i[j*count, (j+1)*count), accumulated in fp32 with one
+ * round-to-nearest-even, so results are deterministic and bit-exact against
+ * the oracle. impl: CECOLL_IMPL_SM / AUTO (one kernel reading every rank's
+ * chunk), or PCPY / B2B / PRELAUNCH_PCPY / PRELAUNCH_B2B (copy-engine gather
+ * into a staging buffer, then an SM reduction; single-process). */
+typedef enum { CECOLL_F32 = 0, CECOLL_BF16 = 1, CECOLL_F16 = 2 } cecoll_dtype_t;
+typedef enum { CECOLL_SUM = 0, CECOLL_MAX = 1, CECOLL_MIN = 2 } cecoll_redop_t;
+cecoll_status_t cecoll_reduce_scatter(const void* send, void* recv, size_t count, cecoll_dtype_t dtype,
+                                      cecoll_redop_t op, cecoll_impl_t impl, cecoll_comm_t comm, void* stream);
+cecoll_status_t cecoll_reduce_scatter_n(const cecoll_comm_t* comms, int n, const void* const* sends,
+                                        void* const* recvs, size_t count, cecoll_dtype_t dtype, cecoll_redop_t op,
+                                        cecoll_impl_t impl, void* const* streams);
 /* The n per-rank calls of one group in a single call (same semantics as
  * group_start; n x allgather/alltoall; group_end). streams may be NULL
  * (legacy stream for every rank). */

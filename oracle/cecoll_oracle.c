@@ -48,12 +48,6 @@ int ora_valid_for(int impl, int kind) {
   return 1;
 }
 
-/* CollectiveSpec::input_bytes / output_bytes (program.hpp:26-30) */
-static int64_t input_bytes(const ora_program* p) {
-  return p->kind == ORA_ALLGATHER ? p->chunk_size : p->chunk_size * p->gpu_count;
-}
-static int64_t output_bytes(const ora_program* p) { return p->chunk_size * p->gpu_count; }
-
 /* Builder (compiler.cpp:93-113): queues opened per GPU in ascending engine
  * order, each sealed with an AtomicSignal on the next signal slot. */
 typedef struct {
@@ -632,4 +626,58 @@ void ora_reference_result(int kind, int64_t s, int n, uint8_t* const* in, uint8_
   }
   if (nthreads > 1)
     for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+}
+
+/* ---- reduce-scatter (fp32 accumulation in rank order, one rounding) ---- */
+
+static float ld_elem(const uint8_t* p, int dtype, int64_t e) {
+  if (dtype == ORA_F32) {
+    float f;
+    memcpy(&f, p + 4 * e, 4);
+    return f;
+  }
+  uint16_t h;
+  memcpy(&h, p + 2 * e, 2);
+  if (dtype == ORA_BF16) {
+    uint32_t u = (uint32_t)h << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+  }
+  _Float16 x;
+  memcpy(&x, &h, 2);
+  return (float)x;
+}
+
+static void st_elem(uint8_t* p, int dtype, int64_t e, float f) {
+  if (dtype == ORA_F32) {
+    memcpy(p + 4 * e, &f, 4);
+    return;
+  }
+  uint16_t h;
+  if (dtype == ORA_BF16) {
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x007fffffu)) h = (uint16_t)((u >> 16) | 0x40); /* quiet NaN */
+    else h = (uint16_t)((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+  } else {
+    _Float16 x = (_Float16)f; /* IEEE round to nearest even */
+    memcpy(&h, &x, 2);
+  }
+  memcpy(p + 2 * e, &h, 2);
+}
+
+void ora_reduce_scatter(int dtype, int op, int64_t count, int n, uint8_t* const* in, uint8_t* const* out) {
+  const int es = dtype == ORA_F32 ? 4 : 2;
+  for (int j = 0; j < n; ++j)
+    for (int64_t e = 0; e < count; ++e) {
+      float acc = ld_elem(in[0] + (int64_t)j * count * es, dtype, e);
+      for (int i = 1; i < n; ++i) {
+        const float x = ld_elem(in[i] + (int64_t)j * count * es, dtype, e);
+        if (op == ORA_SUM) acc = acc + x;
+        else if (op == ORA_MAX) acc = (x > acc) ? x : acc;
+        else acc = (x < acc) ? x : acc;
+      }
+      st_elem(out[j], dtype, e, acc);
+    }
 }

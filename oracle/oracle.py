@@ -115,6 +115,7 @@ class Oracle:
         L.ora_check.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
         L.ora_check.restype = C.c_int64
         L.ora_reference_result.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
+        L.ora_reduce_scatter.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_void_p, C.c_void_p]
         L.ora_parse_impl.argtypes = [C.c_char_p]
         L.ora_impl_name.restype = C.c_char_p
 
@@ -167,6 +168,14 @@ class Oracle:
 
     def reference_result(self, kind, s, n, ins, outs, nthreads=1):
         self.L.ora_reference_result(KINDS[kind], s, n, _ptrs(ins), _ptrs(outs), nthreads)
+
+    def reduce_scatter(self, dtype: int, op: int, count: int, ins):
+        """ora_reduce_scatter over byte buffers ins[i] (n*count elements each)."""
+        n = len(ins)
+        es = 4 if dtype == 0 else 2
+        outs = [np.zeros(count * es, dtype=np.uint8) for _ in range(n)]
+        self.L.ora_reduce_scatter(dtype, op, count, n, _ptrs(ins), _ptrs(outs))
+        return outs
 
     def run(self, kind: str, impl: str, s: int, n: int, seed: int = 0):
         """Compile + byte-execute on pattern inputs; returns (inputs, results)."""

@@ -120,6 +120,9 @@ def lib():
         "cecoll_group_start": ([], i32),
         "cecoll_group_end": ([], i32),
         "cecoll_collective_n": ([i32, C.POINTER(vp), i32, C.POINTER(vp), C.POINTER(vp), sz, i32, C.POINTER(vp)], i32),
+        "cecoll_reduce_scatter": ([vp, vp, sz, i32, i32, i32, vp, vp], i32),
+        "cecoll_reduce_scatter_n": ([C.POINTER(vp), i32, C.POINTER(vp), C.POINTER(vp), sz, i32, i32, i32,
+                                     C.POINTER(vp)], i32),
         "cecoll_plan_create": ([C.POINTER(vp), i32, i32, C.POINTER(vp), C.POINTER(vp), sz, i32, C.POINTER(vp)], i32),
         "cecoll_plan_launch": ([vp, C.POINTER(vp)], i32),
         "cecoll_plan_destroy": ([vp], i32),
@@ -142,8 +145,10 @@ EXPORTED_SYMBOLS = [
     "cecoll_register", "cecoll_deregister", "cecoll_allgather", "cecoll_alltoall", "cecoll_group_start",
     "cecoll_group_end", "cecoll_plan_create", "cecoll_plan_launch", "cecoll_plan_destroy", "cecoll_comm_counters",
     "cecoll_program_parse", "cecoll_plan_create_program", "cecoll_comm_init_ranks", "cecoll_exchange_check",
-    "cecoll_collective_n", "cecoll_plan_disarm",
+    "cecoll_collective_n", "cecoll_plan_disarm", "cecoll_reduce_scatter", "cecoll_reduce_scatter_n",
 ]
+DTYPES = {"f32": 0, "float32": 0, "bf16": 1, "bfloat16": 1, "f16": 2, "float16": 2}
+REDOPS = {"sum": 0, "max": 1, "min": 2}
 
 
 def _check(status: int, what: str = ""):
@@ -380,6 +385,30 @@ def all_gather(comms, sends, recvs, chunk_bytes: int, impl="auto", streams=None)
 def all_to_all(comms, sends, recvs, chunk_bytes: int, impl="auto", streams=None):
     """send[r] chunk j (s bytes) lands in recv[j] slot r (compiler.cpp:124-126, 156-157)."""
     _collective(ALLTOALL, comms, sends, recvs, chunk_bytes, impl, streams)
+
+
+def _dtype(dtype) -> int:
+    if isinstance(dtype, int):
+        return dtype
+    name = str(dtype).replace("torch.", "")
+    if name not in DTYPES:
+        raise InvalidArgument(1, f"unsupported reduce-scatter dtype {dtype!r}")
+    return DTYPES[name]
+
+
+def reduce_scatter(comms, sends, recvs, count: int, dtype="bf16", op="sum", impl="auto", streams=None):
+    """recv[j] (count elements) = op over ranks i, in rank order, of send[i][j*count:(j+1)*count]
+    (fp32 accumulation, one round-to-nearest-even)."""
+    if isinstance(comms, Comm):
+        comms, sends, recvs = [comms], [sends], [recvs]
+        streams = [streams] if not isinstance(streams, (list, tuple)) else streams
+    n = len(comms)
+    if streams is None or not isinstance(streams, (list, tuple)):
+        streams = [streams] * n
+    arr = C.c_void_p * n
+    _check(lib().cecoll_reduce_scatter_n(arr(*[c._h.value for c in comms]), n, arr(*[_ptr(s) for s in sends]),
+                                         arr(*[_ptr(r) for r in recvs]), count, _dtype(dtype), REDOPS[op],
+                                         _impl(impl), arr(*[_stream(st) for st in streams])), "reduce_scatter")
 
 
 class Plan:

@@ -24,9 +24,11 @@ struct PendingCall {
   Kind kind;
   const void* send;
   void* recv;
-  int64_t chunk;
+  int64_t chunk;  // bytes (AG/AA) or elements (reduce-scatter)
   Impl impl;
   cudaStream_t stream;
+  int dtype = 0;
+  int op = 0;
 };
 
 thread_local int g_group_depth = 0;
@@ -50,25 +52,28 @@ cecoll_status_t flush_group(std::vector<PendingCall>& calls) {
     std::vector<CallArgs> args;
     for (size_t j = i; j < calls.size(); ++j) {
       if (done[j] || calls[j].comm->world != w) continue;
-      if (calls[j].kind != calls[i].kind || calls[j].chunk != calls[i].chunk || calls[j].impl != calls[i].impl) {
+      if (calls[j].kind != calls[i].kind || calls[j].chunk != calls[i].chunk || calls[j].impl != calls[i].impl ||
+          calls[j].dtype != calls[i].dtype || calls[j].op != calls[i].op) {
         return err(CECOLL_INVALID_ARGUMENT, "group: one collective per communicator set (kind, size and impl must match)");
       }
       args.push_back({calls[j].comm->rank, calls[j].send, calls[j].recv, calls[j].stream});
       done[j] = true;
     }
-    Status s = run_collective(w, calls[i].kind, calls[i].impl, calls[i].chunk, args);
+    Status s = calls[i].kind == Kind::ReduceScatter
+                   ? run_reduce_scatter(w, calls[i].impl, calls[i].chunk, calls[i].dtype, calls[i].op, args)
+                   : run_collective(w, calls[i].kind, calls[i].impl, calls[i].chunk, args);
     if (!s.ok() && result == CECOLL_SUCCESS) result = st(s);
   }
   return result;
 }
 
 cecoll_status_t enqueue(Kind kind, const void* send, void* recv, size_t chunk, cecoll_impl_t impl, cecoll_comm_t comm,
-                        void* stream) {
+                        void* stream, int dtype = 0, int op = 0) {
   if (!comm || !comm->world) return err(CECOLL_INVALID_ARGUMENT, "null communicator");
   if (!impl_ok(impl)) return err(CECOLL_INVALID_ARGUMENT, "unknown implementation");
   if (chunk == 0 || !send || !recv) return err(CECOLL_INVALID_ARGUMENT, "collective: chunk size must be positive");
-  PendingCall c{comm, kind, send, recv, static_cast<int64_t>(chunk), static_cast<Impl>(impl),
-                static_cast<cudaStream_t>(stream)};
+  PendingCall c{comm,   kind, send, recv, static_cast<int64_t>(chunk), static_cast<Impl>(impl),
+                static_cast<cudaStream_t>(stream), dtype, op};
   if (g_group_depth > 0) {
     g_pending.push_back(c);
     return CECOLL_SUCCESS;
@@ -275,6 +280,34 @@ cecoll_status_t cecoll_allgather(const void* send, void* recv, size_t chunk_byte
 cecoll_status_t cecoll_alltoall(const void* send, void* recv, size_t chunk_bytes, cecoll_impl_t impl,
                                 cecoll_comm_t comm, void* stream) {
   return enqueue(Kind::AllToAll, send, recv, chunk_bytes, impl, comm, stream);
+}
+
+cecoll_status_t cecoll_reduce_scatter(const void* send, void* recv, size_t count, cecoll_dtype_t dtype,
+                                      cecoll_redop_t op, cecoll_impl_t impl, cecoll_comm_t comm, void* stream) {
+  if (dtype < CECOLL_F32 || dtype > CECOLL_F16 || op < CECOLL_SUM || op > CECOLL_MIN)
+    return err(CECOLL_INVALID_ARGUMENT, "reduce-scatter: unknown dtype or op");
+  return enqueue(Kind::ReduceScatter, send, recv, count, impl, comm, stream, dtype, op);
+}
+
+cecoll_status_t cecoll_reduce_scatter_n(const cecoll_comm_t* comms, int n, const void* const* sends,
+                                        void* const* recvs, size_t count, cecoll_dtype_t dtype, cecoll_redop_t op,
+                                        cecoll_impl_t impl, void* const* streams) {
+  if (!comms || n <= 0 || !sends || !recvs) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  if (dtype < CECOLL_F32 || dtype > CECOLL_F16 || op < CECOLL_SUM || op > CECOLL_MIN)
+    return err(CECOLL_INVALID_ARGUMENT, "reduce-scatter: unknown dtype or op");
+  if (!impl_ok(impl)) return err(CECOLL_INVALID_ARGUMENT, "unknown implementation");
+  if (count == 0) return err(CECOLL_INVALID_ARGUMENT, "reduce-scatter: count must be positive");
+  std::vector<PendingCall> calls;
+  for (int i = 0; i < n; ++i) {
+    if (!comms[i] || !sends[i] || !recvs[i]) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+    calls.push_back({comms[i], Kind::ReduceScatter, sends[i], recvs[i], static_cast<int64_t>(count),
+                     static_cast<Impl>(impl), streams ? static_cast<cudaStream_t>(streams[i]) : nullptr, dtype, op});
+  }
+  if (g_group_depth > 0) {
+    g_pending.insert(g_pending.end(), calls.begin(), calls.end());
+    return CECOLL_SUCCESS;
+  }
+  return flush_group(calls);
 }
 
 cecoll_status_t cecoll_collective_n(cecoll_kind_t kind, const cecoll_comm_t* comms, int n, const void* const* sends,

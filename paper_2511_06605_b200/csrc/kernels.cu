@@ -184,7 +184,8 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict__ items, int nitems, int ntiles) {
+__global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict__ items, int nitems, int ntiles,
+                                                          int evict_first) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ int first[kMaxItemsSmem];
@@ -211,7 +212,10 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
   // Streamed data is touched once: evict-first in L2 for loads and stores
   // (profiles/copy_bench2_r01.txt: +1-5% at 1-8 MiB chunks, neutral above).
   uint64_t policy;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  if (evict_first)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
   auto load = [&](int stage, const char* src, uint32_t bytes) {
     const uint32_t bar = smem_addr(&full[stage]);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
@@ -372,7 +376,11 @@ cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream) {
       if (e != cudaSuccess) return e;
       configured[dev] = true;
     }
-    tma_items_kernel<<<grid, 32, kTmaSmem, stream>>>(t.items, t.nitems, t.ntiles);
+    static const int evict_first = [] {
+      const char* e = std::getenv("CECOLL_TMA_EVICT_FIRST");
+      return e ? std::atoi(e) : 0;
+    }();
+    tma_items_kernel<<<grid, 32, kTmaSmem, stream>>>(t.items, t.nitems, t.ntiles, evict_first);
   } else if (t.kinds == (1 << kItemCopy)) {
     reg_items_kernel<(1 << kItemCopy), 2><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems, t.ntiles);
   } else if (!(t.kinds & ((1 << kItemSwap) | (1 << kItemFan)))) {

@@ -60,6 +60,35 @@ int mover_grid_for(const ItemTable& t, int sms);
 
 cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream);
 
+// Reduce-scatter reduction: dst[e] = op over srcs[0..nsrc)
+// in source order of src[e], accumulated in fp32 and rounded once (RNE) to
+// the element type — the same order as the oracle (ora_reduce_scatter).
+enum Dtype : int32_t { kF32 = 0, kBF16 = 1, kF16 = 2 };
+enum RedOp : int32_t { kSum = 0, kMax = 1, kMin = 2 };
+
+inline int dtype_bytes(int dtype) { return dtype == kF32 ? 4 : 2; }
+
+struct RedItem {
+  const char* const* srcs;  // device array of nsrc pointers
+  char* dst;
+  int64_t elems;
+  int32_t nsrc;
+  int32_t first_tile;
+  int32_t vec;  // all pointers 16-byte aligned: vectorised body
+  int32_t pad;
+};
+
+struct RedTable {
+  RedItem* items = nullptr;
+  int nitems = 0;
+  int ntiles = 0;
+  int dtype = kF32;
+  int op = kSum;
+};
+
+constexpr int64_t kRedTileElems = 4096;
+cudaError_t launch_reduce(const RedTable& t, int grid, cudaStream_t stream);
+
 // Flag kernels used inside recorded (prelaunch) graphs, where stream memory
 // operations are not allowed in conditional bodies.
 //  poll:   every flags[i] >= 1, then reset to 0 (ld.acquire.sys spin with a

@@ -13,7 +13,8 @@
 
 namespace cecoll {
 
-enum class Kind : int { AllGather = 0, AllToAll = 1 };
+// ReduceScatter is the B200 extension of SURVEY §8(f)4 (no reference program).
+enum class Kind : int { AllGather = 0, AllToAll = 1, ReduceScatter = 2 };
 
 // Implementation ids follow compiler.hpp:12-21; Sm is the B200 SM path.
 enum class Impl : int {

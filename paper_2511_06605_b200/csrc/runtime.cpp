@@ -790,6 +790,223 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
   return {};
 }
 
+namespace {
+
+// Uploads a reduction table: the items plus one flat array of source pointers.
+Status upload_red(Plan* p, int device, std::vector<RedItem>& items, const std::vector<std::vector<const char*>>& srcs,
+                  int dtype, int op, RedTable* out) {
+  if (items.empty()) return {};
+  if (items.size() > static_cast<size_t>(kMaxItemsSmem))
+    return fail(CECOLL_INVALID_ARGUMENT, "too many reductions for one launch");
+  DeviceGuard g(device);
+  std::vector<const char*> flat;
+  for (const auto& v : srcs) flat.insert(flat.end(), v.begin(), v.end());
+  void* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, sizeof(char*) * flat.size()));
+  CUDA_TRY(cudaMemcpy(d, flat.data(), sizeof(char*) * flat.size(), cudaMemcpyHostToDevice));
+  p->dev_allocs.push_back(d);
+  p->dev_alloc_device.push_back(device);
+  int64_t tiles = 0;
+  size_t at = 0;
+  for (size_t i = 0; i < items.size(); ++i) {
+    items[i].srcs = static_cast<const char* const*>(d) + at;
+    at += srcs[i].size();
+    items[i].first_tile = static_cast<int32_t>(tiles);
+    tiles += (items[i].elems + kRedTileElems - 1) / kRedTileElems;
+  }
+  if (tiles > INT32_MAX) return fail(CECOLL_INVALID_ARGUMENT, "reduce-scatter too large for one launch");
+  void* t = nullptr;
+  CUDA_TRY(cudaMalloc(&t, sizeof(RedItem) * items.size()));
+  CUDA_TRY(cudaMemcpy(t, items.data(), sizeof(RedItem) * items.size(), cudaMemcpyHostToDevice));
+  p->dev_allocs.push_back(t);
+  p->dev_alloc_device.push_back(device);
+  out->items = static_cast<RedItem*>(t);
+  out->nitems = static_cast<int>(items.size());
+  out->ntiles = static_cast<int>(tiles);
+  out->dtype = dtype;
+  out->op = op;
+  return {};
+}
+
+RedItem make_red(char* dst, int64_t elems, const std::vector<const char*>& srcs, int esize) {
+  RedItem r;
+  std::memset(&r, 0, sizeof(r));
+  r.dst = dst;
+  r.elems = elems;
+  r.nsrc = static_cast<int32_t>(srcs.size());
+  uintptr_t a = reinterpret_cast<uintptr_t>(dst);
+  for (const char* s : srcs) a |= reinterpret_cast<uintptr_t>(s);
+  r.vec = (a & 15) == 0 && esize > 0;
+  return r;
+}
+
+}  // namespace
+
+Status plan_create_rs(World* w, Impl impl, int64_t count, int dtype, int op, const std::vector<CallArgs>& args,
+                      Plan** out) {
+  const int n = w->nranks;
+  if (count <= 0) return fail(CECOLL_INVALID_ARGUMENT, "reduce-scatter: count must be positive");
+  if (dtype < kF32 || dtype > kF16 || op < kSum || op > kMin)
+    return fail(CECOLL_INVALID_ARGUMENT, "reduce-scatter: unknown dtype or op");
+  if (impl == Impl::Auto) impl = Impl::Sm;
+  if (impl != Impl::Sm && impl != Impl::Pcpy && impl != Impl::B2b && impl != Impl::PrelaunchPcpy &&
+      impl != Impl::PrelaunchB2b)
+    return fail(CECOLL_UNSUPPORTED, "reduce-scatter: sm, pcpy, b2b, prelaunch_pcpy or prelaunch_b2b");
+  const int esize = dtype_bytes(dtype);
+  const int64_t s = count * esize;
+  auto plan = std::make_unique<Plan>();
+  Plan* p = plan.get();
+  p->kind = Kind::ReduceScatter;
+  p->impl = impl;
+  p->chunk = s;
+  p->dtype = dtype;
+  p->op = op;
+  p->sm = impl == Impl::Sm;
+  for (const CallArgs& a : args) {
+    p->key_rank.push_back(a.rank);
+    p->key_send.push_back(a.send);
+    p->key_recv.push_back(a.recv);
+    p->key_stream.push_back(a.stream);
+  }
+  std::vector<const char*> send(n, nullptr);
+  std::vector<char*> recv(n, nullptr);
+  std::vector<bool> have(n, false);
+  for (const CallArgs& a : args) {
+    if (a.rank < 0 || a.rank >= n || !w->local[a.rank]) return fail(CECOLL_INVALID_ARGUMENT, "rank not local");
+    if (have[a.rank]) return fail(CECOLL_INVALID_ARGUMENT, "rank appears twice in one group");
+    have[a.rank] = true;
+    send[a.rank] = static_cast<const char*>(a.send);
+    recv[a.rank] = static_cast<char*>(a.recv);
+  }
+  if (!w->multiprocess) {
+    for (int r = 0; r < n; ++r)
+      if (!have[r])
+        return fail(CECOLL_INVALID_ARGUMENT,
+                    "single-process communicator: every rank must take part (use cecoll_group_start/end)");
+  } else {
+    if (static_cast<int>(args.size()) != w->nlocal)
+      return fail(CECOLL_INVALID_ARGUMENT, "multi-process: every local rank must take part (group calls)");
+    if (!p->sm) return fail(CECOLL_UNSUPPORTED, "reduce-scatter over copy engines needs a single-process communicator");
+    for (int r = 0; r < n; ++r) {
+      if (have[r]) continue;
+      bool ok = true;
+      send[r] = translate(w, args[0].rank, r, args[0].send, &ok);
+      if (!ok) return fail(CECOLL_NOT_REGISTERED, "send must lie in a window registered with cecoll_register");
+    }
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, w->device[args[0].rank]);
+  p->sms = sms;
+
+  if (!p->sm) {
+    // Copy-engine gather: chunk j of every rank lands in rank j's staging
+    // slot i (an all-to-all into staging), then rank j reduces its staging.
+    std::vector<CallArgs> inner_args;
+    std::vector<char*> staging(n, nullptr);
+    for (const CallArgs& a : args) {
+      DeviceGuard g(w->device[a.rank]);
+      void* d = nullptr;
+      CUDA_TRY(cudaMalloc(&d, static_cast<size_t>(s) * n));
+      p->dev_allocs.push_back(d);
+      p->dev_alloc_device.push_back(w->device[a.rank]);
+      staging[a.rank] = static_cast<char*>(d);
+      inner_args.push_back({a.rank, a.send, d, a.stream});
+    }
+    Plan* inner = nullptr;
+    STATUS_TRY(plan_create(w, Kind::AllToAll, impl, s, inner_args, &inner));
+    p->inner.reset(inner);
+    for (const Unit& iu : inner->units) {
+      Unit u;
+      u.device = iu.device;
+      u.stream = iu.stream;
+      u.ranks = iu.ranks;
+      std::vector<RedItem> items;
+      std::vector<std::vector<const char*>> srcs;
+      for (int j : u.ranks) {
+        std::vector<const char*> v;
+        for (int i = 0; i < n; ++i) v.push_back(staging[j] + i * s);
+        items.push_back(make_red(recv[j], count, v, esize));
+        srcs.push_back(v);
+      }
+      STATUS_TRY(upload_red(p, u.device, items, srcs, dtype, op, &u.red));
+      p->units.push_back(std::move(u));
+    }
+    *out = plan.release();
+    return {};
+  }
+
+  // SM path: units, flags (rank j reads every rank i's send), reductions.
+  std::vector<int> unit_of(n, -1);
+  for (const CallArgs& a : args) {
+    int found = -1;
+    for (size_t u = 0; u < p->units.size(); ++u)
+      if (p->units[u].device == w->device[a.rank] && p->units[u].stream == a.stream) found = static_cast<int>(u);
+    if (found < 0) {
+      Unit u;
+      u.device = w->device[a.rank];
+      u.stream = a.stream;
+      p->units.push_back(u);
+      found = static_cast<int>(p->units.size()) - 1;
+    }
+    p->units[found].ranks.push_back(a.rank);
+    unit_of[a.rank] = found;
+  }
+  for (Unit& u : p->units) std::sort(u.ranks.begin(), u.ranks.end());
+  for (int r = 0; r < n; ++r)
+    for (int d = 1; d < n; ++d) {
+      const int j = (r + d) % n;  // r reads j's send
+      if (unit_of[r] >= 0 && unit_of[r] == unit_of[j]) continue;
+      if (unit_of[j] >= 0) {
+        Unit& u = p->units[unit_of[j]];
+        u.start.push_back(op_write(slot(w, r, kSlotRdy + j), 1));
+        add_poll(u.finish, slot(w, j, kSlotDone + r));
+      }
+      if (unit_of[r] >= 0) {
+        Unit& u = p->units[unit_of[r]];
+        add_poll(u.sm_pre, slot(w, r, kSlotRdy + j));
+        u.sm_post.push_back(op_write(slot(w, j, kSlotDone + r), 1));
+      }
+    }
+  for (Unit& u : p->units) {
+    std::vector<RedItem> items;
+    std::vector<std::vector<const char*>> srcs;
+    for (int j : u.ranks) {
+      std::vector<const char*> v;
+      for (int i = 0; i < n; ++i) v.push_back(send[i] + j * s);
+      items.push_back(make_red(recv[j], count, v, esize));
+      srcs.push_back(v);
+    }
+    STATUS_TRY(upload_red(p, u.device, items, srcs, dtype, op, &u.red));
+  }
+  *out = plan.release();
+  return {};
+}
+
+Status run_reduce_scatter(World* w, Impl impl, int64_t count, int dtype, int op, const std::vector<CallArgs>& args) {
+  if (impl == Impl::Auto) impl = Impl::Sm;
+  const int64_t s = count * dtype_bytes(dtype);
+  Plan* p = nullptr;
+  for (auto& cand : w->plans) {
+    Plan* c = cand.get();
+    if (c->kind != Kind::ReduceScatter || c->impl != impl || c->chunk != s || c->dtype != dtype || c->op != op ||
+        c->key_rank.size() != args.size())
+      continue;
+    bool same = true;
+    for (size_t i = 0; i < args.size() && same; ++i)
+      same = c->key_rank[i] == args[i].rank && c->key_send[i] == args[i].send && c->key_recv[i] == args[i].recv &&
+             c->key_stream[i] == args[i].stream;
+    if (same) {
+      p = c;
+      break;
+    }
+  }
+  if (!p) {
+    STATUS_TRY(plan_create_rs(w, impl, count, dtype, op, args, &p));
+    w->plans.emplace_back(p);
+  }
+  return plan_launch(w, p, false);
+}
+
 // Records one unit's lanes into a graph: [gate kernel] -> IF{ poll kernel ->
 // lanes (copies, item kernels) + placement -> signal kernel }.
 Status build_graph(World* w, Plan* p, Unit& u) {
@@ -961,6 +1178,11 @@ Status run_sm(World* w, Plan* p) {
       ++w->counters[4];
       ++w->counters[6];
     }
+    if (u.red.nitems) {
+      CUDA_TRY(launch_reduce(u.red, 4 * p->sms, u.stream));
+      ++w->counters[4];
+      ++w->counters[6];
+    }
     STATUS_TRY(submit(w, u.stream, u.sm_post));
   }
   for (Unit& u : p->units) {  // phase 3: incoming chunks
@@ -1024,7 +1246,7 @@ bool same_call(const Plan* p, Kind kind, Impl impl, int64_t s, const std::vector
 // Cancels armed instances (the next launch re-arms): after this, device-wide
 // synchronisation returns.
 Status plan_disarm(World* w, Plan* p) {
-  (void)w;
+  if (p->inner) STATUS_TRY(plan_disarm(w, p->inner.get()));
   for (Unit& u : p->units) {
     if (!u.armed) continue;
     DeviceGuard g(u.device);
@@ -1036,6 +1258,7 @@ Status plan_disarm(World* w, Plan* p) {
 }
 
 Status plan_arm(World* w, Plan* p) {
+  if (p->inner) return plan_arm(w, p->inner.get());
   if (!p->prelaunch) return {};
   for (Unit& u : p->units)
     if (!u.armed) STATUS_TRY(arm_unit(w, u));
@@ -1043,6 +1266,17 @@ Status plan_arm(World* w, Plan* p) {
 }
 
 Status plan_launch(World* w, Plan* p, bool rearm) {
+  if (p->inner) {  // reduce-scatter over copy engines: gather, then reduce
+    for (size_t i = 0; i < p->units.size(); ++i) p->inner->units[i].stream = p->units[i].stream;
+    STATUS_TRY(plan_launch(w, p->inner.get(), rearm));
+    for (Unit& u : p->units) {
+      DeviceGuard g(u.device);
+      CUDA_TRY(launch_reduce(u.red, 4 * p->sms, u.stream));
+      ++w->counters[4];
+      ++w->counters[6];
+    }
+    return {};
+  }
   ++w->counters[0];
   if (p->sm) return run_sm(w, p);
   if (!p->prelaunch) return run_ce(w, p);
@@ -1054,8 +1288,8 @@ Status plan_launch(World* w, Plan* p, bool rearm) {
 }
 
 Status plan_destroy(World* w, Plan* p) {
-  (void)w;
   Status result;
+  if (p->inner) result = plan_destroy(w, p->inner.get());
   for (Unit& u : p->units) {
     DeviceGuard g(u.device);
     if (u.armed) {

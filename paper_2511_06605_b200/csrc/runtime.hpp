@@ -126,6 +126,7 @@ struct Unit {
   std::vector<Copy> placement;    // local-slot placement (verifier.cpp:40-44)
   std::vector<Copy> precopy;      // swap with send != recv: send -> recv first
   ItemTable table;                // SM path: every chunk of the unit's ranks
+  RedTable red;                   // reduce-scatter: one reduction per local rank
   // prelaunch graph
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -159,6 +160,8 @@ struct Plan {
   bool sm = false;
   bool prelaunch = false;
   int sms = 148;
+  int dtype = 0, op = 0;          // reduce-scatter element type / operator
+  std::unique_ptr<Plan> inner;    // reduce-scatter over copy engines: the all-to-all into staging
 };
 
 void set_error(const std::string& msg);
@@ -188,6 +191,13 @@ Status run_collective(World* w, Kind kind, Impl impl, int64_t chunk, const std::
 // dump_program text) instead of compiling one.
 Status plan_create(World* w, Kind kind, Impl impl, int64_t chunk, const std::vector<CallArgs>& args, Plan** out,
                    const Program* given = nullptr);
+// Reduce-scatter: count elements of `dtype` per rank chunk.
+// impl Sm: one kernel per unit reads every rank's chunk (peer loads over
+// NVLink); pcpy / b2b / prelaunch_*: an all-to-all over the copy engines into
+// a per-rank staging buffer, then one reduction kernel per unit (§6.1).
+Status plan_create_rs(World* w, Impl impl, int64_t count, int dtype, int op, const std::vector<CallArgs>& args,
+                      Plan** out);
+Status run_reduce_scatter(World* w, Impl impl, int64_t count, int dtype, int op, const std::vector<CallArgs>& args);
 Status plan_arm(World* w, Plan* p);
 Status plan_disarm(World* w, Plan* p);
 Status plan_launch(World* w, Plan* p, bool rearm);
