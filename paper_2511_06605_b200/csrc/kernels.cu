@@ -209,8 +209,10 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
     *off_out = off;
     *bytes = static_cast<uint32_t>(rem < kTmaTile ? rem : kTmaTile);
   };
-  // Streamed data is touched once: evict-first in L2 for loads and stores
-  // (profiles/copy_bench2_r01.txt: +1-5% at 1-8 MiB chunks, neutral above).
+  // L2 policy of the bulk copies. Evict-first helped the isolated mover by
+  // 1-5% at 1-8 MiB chunks (profiles/copy_bench2_r01.txt) but cost 3-4% in
+  // the bench step (profiles/tma_hint_ab_r01.txt), so evict-normal is the
+  // default; CECOLL_TMA_EVICT_FIRST=1 selects evict-first.
   uint64_t policy;
   if (evict_first)
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
