@@ -93,23 +93,30 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        """Median SM clock over samples taken under load (power above idle +
+        100 W; all samples if none qualify) and every throttle reason seen."""
+        rows, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.lines:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 9:
                 continue
             try:
-                sm.append(float(parts[1]))
+                rows.append((float(parts[1]), float(parts[3])))
                 mx = float(parts[2])
             except ValueError:
                 continue
             for nm, v in zip(names, parts[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
-        sm.sort()
-        med = sm[len(sm) // 2] if sm else None
-        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
+        idle = min(p for _, p in rows)
+        loaded = [c for c, p in rows if p > idle + 100] or [c for c, _ in rows]
+        loaded.sort()
+        return {"sm_mhz": loaded[len(loaded) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(rows), "samples_under_load": len(loaded),
+                "power_w_max": max(p for _, p in rows)}
 
 
 def busbw(n, s, seconds):
@@ -230,6 +237,9 @@ def run_ours(args):
     c0 = comms[0].counters()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    # nvidia-smi samples every 100 ms while the timed region (a few ms) runs
+    # and then while the same step keeps running for the >= 1.5 s NVML energy
+    # loop, so the clocks reported are clocks under this load.
     with ClockSampler(dev) as clocks:
         torch.cuda.synchronize()
         e0.record(stream)
@@ -237,7 +247,8 @@ def run_ours(args):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
-    c1 = comms[0].counters()
+        c1 = comms[0].counters()
+        energy = None if args.no_energy else measure_energy(step, stream, n, s)
     ms = e0.elapsed_time(e1) / args.steps
     value = busbw(n, s, ms / 1e3)
 
@@ -301,8 +312,6 @@ def run_ours(args):
     e2e_value = busbw(n, s, e2e_ms / 1e3)
     e2e_ok = all(torch.equal(host_outs[(e2e_steps - 1) % 2][j][i * s:(i + 1) * s], host_in[i][j * s:(j + 1) * s])
                  for i in range(n) for j in (0, n - 1))
-
-    energy = None if args.no_energy else measure_energy(step, stream, n, s)
 
     cpu = None
     if not args.no_cpu_baseline:

@@ -535,6 +535,60 @@ Status upload_ptrs(Plan* p, int device, const std::vector<uint64_t*>& ptrs, uint
   return {};
 }
 
+// Device holding the flag page that contains addr (-1 if none).
+int flag_device(World* w, const uint64_t* addr) {
+  for (int r = 0; r < w->nranks; ++r) {
+    const uint64_t* b = w->flag_page[r];
+    if (b && addr >= b && addr < b + kFlagBytes / sizeof(uint64_t)) return w->device[r];
+  }
+  return -1;
+}
+
+// Moves the writes in `ops` that target another device's flag page into
+// `remote`: those are issued by a signal kernel (st.release.sys to the
+// peer-mapped page) rather than a stream memory operation, the portable way
+// to signal across NVLink. Same-device pages (also across processes) keep
+// the memop.
+void split_writes(World* w, int device, MemOps& ops, std::vector<uint64_t*>& remote) {
+  MemOps keep;
+  for (const auto& op : ops) {
+    if (op.operation == CU_STREAM_MEM_OP_WRITE_VALUE_64) {
+      uint64_t* a = reinterpret_cast<uint64_t*>(op.writeValue.address);
+      const int d = flag_device(w, a);
+      if (d >= 0 && d != device) {
+        remote.push_back(a);
+        continue;
+      }
+    }
+    keep.push_back(op);
+  }
+  ops.swap(keep);
+}
+
+Status split_remote(World* w, Plan* p) {
+  for (Unit& u : p->units) {
+    split_writes(w, u.device, u.start, u.start_remote);
+    split_writes(w, u.device, u.sm_post, u.sm_post_remote);
+    STATUS_TRY(upload_ptrs(p, u.device, u.start_remote, &u.start_remote_tab));
+    STATUS_TRY(upload_ptrs(p, u.device, u.sm_post_remote, &u.sm_post_remote_tab));
+  }
+  for (LaneExec& l : p->lanes) {
+    const int dev = w->device[l.rank];
+    split_writes(w, dev, l.post, l.post_remote);
+    STATUS_TRY(upload_ptrs(p, dev, l.post_remote, &l.post_remote_tab));
+  }
+  return {};
+}
+
+// Stream memops, then the signal kernel for other-device flags.
+Status signal_remote(World* w, uint64_t** tab, size_t n, cudaStream_t s) {
+  if (!n) return {};
+  CUDA_TRY(launch_signal(tab, static_cast<int>(n), s));
+  ++w->counters[4];
+  ++w->counters[6];
+  w->counters[2] += static_cast<int64_t>(n);
+  return {};
+}
 
 }  // namespace
 
@@ -783,9 +837,25 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
     p->sms = sms;
     for (size_t ui = 0; ui < p->units.size(); ++ui)
       STATUS_TRY(upload_items(p, p->units[ui].device, unit_items[ui], &p->units[ui].table));
-    if (p->prelaunch)
-      for (Unit& u : p->units) STATUS_TRY(build_graph(w, p, u));
   }
+  STATUS_TRY(split_remote(w, p));
+  if (p->prelaunch)
+    for (Unit& u : p->units) {
+      const Status gs = build_graph(w, p, u);
+      if (gs.ok()) continue;
+      if (given) return gs;  // a given program keeps its polls: no eager form
+      // A graph this driver cannot record or instantiate (e.g. a copy-engine
+      // memcpy node between devices inside a conditional body): run the same
+      // command program without prelaunch rather than fail the collective.
+      std::string why = gs.msg;
+      plan_destroy(w, p);
+      Plan* eager = nullptr;
+      STATUS_TRY(plan_create(w, kind, base_of(impl), s, args, &eager, given));
+      eager->impl = impl;
+      eager->graph_fallback = why;
+      *out = eager;
+      return {};
+    }
   *out = plan.release();
   return {};
 }
@@ -978,6 +1048,7 @@ Status plan_create_rs(World* w, Impl impl, int64_t count, int dtype, int op, con
     }
     STATUS_TRY(upload_red(p, u.device, items, srcs, dtype, op, &u.red));
   }
+  STATUS_TRY(split_remote(w, p));
   *out = plan.release();
   return {};
 }
@@ -1034,6 +1105,7 @@ Status build_graph(World* w, Plan* p, Unit& u) {
     for (const auto& op : le.pre)
       if (op.operation == CU_STREAM_MEM_OP_WAIT_VALUE_64) polls.push_back(reinterpret_cast<uint64_t*>(op.waitValue.address));
     for (const auto& op : le.post) sigs.push_back(reinterpret_cast<uint64_t*>(op.writeValue.address));
+    sigs.insert(sigs.end(), le.post_remote.begin(), le.post_remote.end());
   }
   for (const auto& op : u.finish)
     if (op.operation == CU_STREAM_MEM_OP_WAIT_VALUE_64) fins.push_back(reinterpret_cast<uint64_t*>(op.waitValue.address));
@@ -1130,6 +1202,7 @@ Status run_ce(World* w, Plan* p) {
     DeviceGuard g(u.device);
     STATUS_TRY(issue_copies(w, u.precopy, u.stream, true));
     STATUS_TRY(submit(w, u.stream, u.start));
+    STATUS_TRY(signal_remote(w, u.start_remote_tab, u.start_remote.size(), u.stream));
     for (int r : u.ranks) {
       CUDA_TRY(cudaEventRecord(w->local[r]->start, u.stream));
       ++w->counters[6];
@@ -1150,6 +1223,7 @@ Status run_ce(World* w, Plan* p) {
       ++w->counters[6];
     }
     STATUS_TRY(submit(w, s, l.post));
+    STATUS_TRY(signal_remote(w, l.post_remote_tab, l.post_remote.size(), s));
     CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], s));
     ++w->counters[6];
   }
@@ -1169,6 +1243,7 @@ Status run_sm(World* w, Plan* p) {
   for (Unit& u : p->units) {  // phase 1: readiness to sources in other units
     DeviceGuard g(u.device);
     STATUS_TRY(submit(w, u.stream, u.start));
+    STATUS_TRY(signal_remote(w, u.start_remote_tab, u.start_remote.size(), u.stream));
   }
   for (Unit& u : p->units) {  // phase 2: wait destinations, move, signal
     DeviceGuard g(u.device);
@@ -1184,6 +1259,7 @@ Status run_sm(World* w, Plan* p) {
       ++w->counters[6];
     }
     STATUS_TRY(submit(w, u.stream, u.sm_post));
+    STATUS_TRY(signal_remote(w, u.sm_post_remote_tab, u.sm_post_remote.size(), u.stream));
   }
   for (Unit& u : p->units) {  // phase 3: incoming chunks
     DeviceGuard g(u.device);
@@ -1218,6 +1294,7 @@ Status trigger_unit(World* w, Plan* p, Unit& u) {
   MemOps ops = u.start;
   ops.push_back(op_write(u.ready_flag, 1));
   STATUS_TRY(submit(w, u.stream, ops));
+  STATUS_TRY(signal_remote(w, u.start_remote_tab, u.start_remote.size(), u.stream));
   STATUS_TRY(post_gate(u, 1));
   u.armed = false;
   if (u.nfin) {

@@ -114,6 +114,10 @@ struct LaneExec {
   std::vector<Copy> copies;   // copy commands
   ItemTable table;            // Broadcast / Swap commands (no copy-engine form)
   MemOps post;                // done signals to destinations in other units
+  // Signals whose flag page lives on another device are written by a signal
+  // kernel (st.release.sys over NVLink) instead of a stream memory operation.
+  std::vector<uint64_t*> post_remote;
+  uint64_t** post_remote_tab = nullptr;
 };
 
 struct Unit {
@@ -123,6 +127,9 @@ struct Unit {
   MemOps start;                   // rdy signals to sources in other units
   MemOps finish;                  // done polls (+ resets) from sources in other units
   MemOps sm_pre, sm_post;         // SM path: rdy polls / done signals
+  std::vector<uint64_t*> start_remote, sm_post_remote;  // other-device flags (signal kernel)
+  uint64_t** start_remote_tab = nullptr;
+  uint64_t** sm_post_remote_tab = nullptr;
   std::vector<Copy> placement;    // local-slot placement (verifier.cpp:40-44)
   std::vector<Copy> precopy;      // swap with send != recv: send -> recv first
   ItemTable table;                // SM path: every chunk of the unit's ranks
@@ -162,6 +169,7 @@ struct Plan {
   int sms = 148;
   int dtype = 0, op = 0;          // reduce-scatter element type / operator
   std::unique_ptr<Plan> inner;    // reduce-scatter over copy engines: the all-to-all into staging
+  std::string graph_fallback;     // why a prelaunch plan runs without its graph (empty: it has one)
 };
 
 void set_error(const std::string& msg);
