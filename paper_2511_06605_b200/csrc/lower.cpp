@@ -1,424 +1,15 @@
-// Communicator, plan lowering and the three executors:
-//   CE       pcpy / b2b / bcst / swap: per-lane streams of copy commands,
-//            bracketed by batched flag memops (cuStreamBatchMemOp).
-//   graph    prelaunch_*: the same lanes recorded once per unit into a CUDA
-//            graph whose body sits behind a gate (conditional node), launched
-//            ahead and opened by a host post (apply_prelaunch,
-//            compiler.cpp:267-285).
-//   SM       one sm_100a item kernel per unit moving every chunk of the unit's
-//            ranks (latency regime).
-#include "runtime.hpp"
-
+// Plan lowering: a command program (program.hpp) or the SM path onto
+// concrete buffers — lanes, flag operations, item / reduction tables and the
+// prelaunch graphs.
 #include <algorithm>
-#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <set>
 #include <stdexcept>
 
+#include "internal.hpp"
+
 namespace cecoll {
-
-namespace {
-
-thread_local std::string g_error;
-
-Status fail(int code, const std::string& msg) {
-  g_error = msg;
-  return Status{code, msg};
-}
-
-Status cuda_fail(cudaError_t e, const char* what, int line) {
-  return fail(CECOLL_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e) + " (runtime.cpp:" +
-                                     std::to_string(line) + ")");
-}
-
-Status cu_fail(CUresult r, const char* what, int line) {
-  const char* s = "?";
-  if (driver_api()) driver_api()->GetErrorString(r, &s);
-  return fail(CECOLL_CUDA_ERROR, std::string(what) + ": " + s + " (runtime.cpp:" + std::to_string(line) + ")");
-}
-
-#define CUDA_TRY(expr)                                      \
-  do {                                                      \
-    cudaError_t e_ = (expr);                                \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #expr, __LINE__); \
-  } while (0)
-
-#define CU_TRY(expr)                                       \
-  do {                                                     \
-    CUresult r_ = (expr);                                  \
-    if (r_ != CUDA_SUCCESS) return cu_fail(r_, #expr, __LINE__); \
-  } while (0)
-
-#define STATUS_TRY(expr)         \
-  do {                           \
-    Status s_ = (expr);          \
-    if (!s_.ok()) return s_;     \
-  } while (0)
-
-class DeviceGuard {
- public:
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev_);
-    if (dev >= 0 && dev != prev_) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() { cudaSetDevice(prev_); }
-
- private:
-  int prev_ = 0;
-};
-
-CUstreamBatchMemOpParams op_write(uint64_t* addr, uint64_t v) {
-  CUstreamBatchMemOpParams op;
-  std::memset(&op, 0, sizeof(op));
-  op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
-  op.writeValue.address = reinterpret_cast<CUdeviceptr>(addr);
-  op.writeValue.value64 = v;
-  op.writeValue.flags = 0;  // with the default memory barrier: prior copies are visible first
-  return op;
-}
-
-CUstreamBatchMemOpParams op_wait(uint64_t* addr, uint64_t v) {
-  CUstreamBatchMemOpParams op;
-  std::memset(&op, 0, sizeof(op));
-  op.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_64;
-  op.waitValue.address = reinterpret_cast<CUdeviceptr>(addr);
-  op.waitValue.value64 = v;
-  op.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
-  return op;
-}
-
-// Poll + reset of one slot (the reset keeps graph replays value-constant).
-void add_poll(MemOps& ops, uint64_t* addr) {
-  ops.push_back(op_wait(addr, 1));
-  ops.push_back(op_write(addr, 0));
-}
-
-Status submit(World* w, cudaStream_t s, const MemOps& ops) {
-  const DriverApi* d = driver_api();
-  size_t i = 0;
-  while (i < ops.size()) {
-    const unsigned count = static_cast<unsigned>(std::min<size_t>(255, ops.size() - i));
-    CU_TRY(d->StreamBatchMemOp(reinterpret_cast<CUstream>(s), count,
-                               const_cast<CUstreamBatchMemOpParams*>(ops.data() + i), 0));
-    for (unsigned k = 0; k < count; ++k) {
-      if (ops[i + k].operation == CU_STREAM_MEM_OP_WRITE_VALUE_64) ++w->counters[2];
-      else ++w->counters[3];
-    }
-    ++w->counters[6];
-    i += count;
-  }
-  return {};
-}
-
-Status issue_copies(World* w, const std::vector<Copy>& copies, cudaStream_t s, bool allow_batch) {
-  const DriverApi* d = driver_api();
-  // cuMemcpyBatchAsync rejects the legacy NULL stream.
-  const bool legacy = s == nullptr || s == cudaStreamLegacy;
-  if (copies.size() > 1 && allow_batch && d->has_batch_memcpy && !legacy) {
-    std::vector<CUdeviceptr> dst, src;
-    std::vector<size_t> sz;
-    for (const Copy& c : copies) {
-      dst.push_back(reinterpret_cast<CUdeviceptr>(c.dst));
-      src.push_back(reinterpret_cast<CUdeviceptr>(c.src));
-      sz.push_back(static_cast<size_t>(c.bytes));
-    }
-    CUmemcpyAttributes attr;
-    std::memset(&attr, 0, sizeof(attr));
-    attr.srcAccessOrder = CU_MEMCPY_SRC_ACCESS_ORDER_STREAM;
-    attr.flags = CU_MEMCPY_FLAG_PREFER_OVERLAP_WITH_COMPUTE;
-    size_t idx = 0, fail_idx = 0;
-    CU_TRY(d->MemcpyBatchAsync(dst.data(), src.data(), sz.data(), copies.size(), &attr, &idx, 1, &fail_idx,
-                               reinterpret_cast<CUstream>(s)));
-    w->counters[1] += static_cast<int64_t>(copies.size());
-    ++w->counters[6];
-    return {};
-  }
-  for (const Copy& c : copies) {
-    CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, static_cast<size_t>(c.bytes), cudaMemcpyDefault, s));
-    ++w->counters[1];
-    ++w->counters[6];
-  }
-  return {};
-}
-
-Status make_rank(World* w, int rank, int device, uint64_t* page = nullptr) {
-  DeviceGuard g(device);
-  auto rs = std::make_unique<RankState>();
-  rs->rank = rank;
-  rs->device = device;
-  CUDA_TRY(cudaEventCreateWithFlags(&rs->start, cudaEventDisableTiming));
-  if (page) {
-    rs->flags = page;
-    rs->owns_flags = false;
-  } else {
-    CUDA_TRY(cudaMalloc(&rs->flags, kFlagBytes));
-    CUDA_TRY(cudaMemset(rs->flags, 0, kFlagBytes));
-    CUDA_TRY(cudaDeviceSynchronize());
-  }
-  w->flag_page[rank] = rs->flags;
-  w->local[rank] = std::move(rs);
-  return {};
-}
-
-Status ensure_lanes(RankState* rs, int n) {
-  DeviceGuard g(rs->device);
-  while (static_cast<int>(rs->lanes.size()) < n) {
-    cudaStream_t s;
-    cudaEvent_t e;
-    CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    rs->lanes.push_back(s);
-    rs->lane_done.push_back(e);
-  }
-  return {};
-}
-
-int count_devices(const std::vector<int>& dev) {
-  std::set<int> s(dev.begin(), dev.end());
-  return static_cast<int>(s.size());
-}
-
-}  // namespace
-
-void set_error(const std::string& msg) { g_error = msg; }
-const char* last_error() { return g_error.c_str(); }
-
-Status world_init_all(int nranks, const int* devlist, World** out) {
-  if (!driver_api()) return fail(CECOLL_NO_DEVICE, "no CUDA driver / device");
-  if (nranks < 1 || nranks > kMaxRanks)
-    return fail(CECOLL_INVALID_ARGUMENT, "nranks must be in [1, " + std::to_string(kMaxRanks) + "]");
-  int ndev = 0;
-  CUDA_TRY(cudaGetDeviceCount(&ndev));
-  for (int r = 0; r < nranks; ++r)
-    if (devlist[r] < 0 || devlist[r] >= ndev)
-      return fail(CECOLL_INVALID_ARGUMENT, "device " + std::to_string(devlist[r]) + " out of range");
-  auto w = std::make_unique<World>();
-  w->nranks = nranks;
-  w->device.assign(devlist, devlist + nranks);
-  w->flag_page.assign(nranks, nullptr);
-  w->local.resize(nranks);
-  w->ndevices = count_devices(w->device);
-  // Peer access between every pair of distinct devices (NVLink / NVSwitch).
-  std::set<int> devs(w->device.begin(), w->device.end());
-  for (int a : devs)
-    for (int b : devs) {
-      if (a == b) continue;
-      int can = 0;
-      CUDA_TRY(cudaDeviceCanAccessPeer(&can, a, b));
-      if (!can) return fail(CECOLL_UNSUPPORTED, "no peer access between devices");
-      DeviceGuard g(a);
-      cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
-      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "EnablePeerAccess", __LINE__);
-      cudaGetLastError();
-    }
-  for (int r = 0; r < nranks; ++r) STATUS_TRY(make_rank(w.get(), r, w->device[r]));
-  w->live_comms = nranks;
-  w->first_local = 0;
-  w->nlocal = nranks;
-  *out = w.release();
-  return {};
-}
-
-namespace {
-
-// One blob per process in the init exchange.
-struct ProcInfo {
-  int32_t first;   // first global rank owned by the process
-  int32_t nlocal;  // ranks owned (consecutive)
-  int32_t device;
-  int32_t pid;
-  cudaIpcMemHandle_t flags;  // nlocal flag pages, kFlagBytes apart
-};
-
-// One blob per process in a registration round.
-struct RegInfo {
-  int32_t rank;
-  int32_t pad;
-  uint64_t offset;  // of the window inside its allocation
-  uint64_t bytes;
-  cudaIpcMemHandle_t handle;  // of the allocation
-};
-
-Status open_ipc(World* w, const cudaIpcMemHandle_t& h, void** out) {
-  std::string key(reinterpret_cast<const char*>(&h), sizeof(h));
-  auto it = w->ipc_by_handle.find(key);
-  if (it != w->ipc_by_handle.end()) {
-    *out = it->second;
-    return {};
-  }
-  CUDA_TRY(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
-  w->ipc_opened.push_back(*out);
-  w->ipc_by_handle[key] = *out;
-  return {};
-}
-
-}  // namespace
-
-Status gather_procs(int nranks, int first, int nlocal, int device, const cudaIpcMemHandle_t* flags,
-                    cecoll_exchange_fn fn, void* ctx, std::vector<ProcInfoView>* out) {
-  if (nranks < 1 || nranks > kMaxRanks || nlocal < 1 || first < 0 || first + nlocal > nranks || !fn)
-    return fail(CECOLL_INVALID_ARGUMENT, "bad rank range / exchange");
-  if (nranks % nlocal != 0)
-    return fail(CECOLL_INVALID_ARGUMENT, "every process must own the same number of ranks");
-  const int procs = nranks / nlocal;
-  ProcInfo mine;
-  std::memset(&mine, 0, sizeof(mine));
-  mine.first = first;
-  mine.nlocal = nlocal;
-  mine.device = device;
-  if (flags) mine.flags = *flags;
-  std::vector<ProcInfo> all(procs);
-  if (fn(ctx, &mine, sizeof(ProcInfo), all.data()) != 0) return fail(CECOLL_INTERNAL, "exchange failed");
-  std::vector<int> owner(nranks, -1);
-  out->clear();
-  for (int p = 0; p < procs; ++p) {
-    const ProcInfo& pi = all[p];
-    if (pi.nlocal != nlocal || pi.first < 0 || pi.first + pi.nlocal > nranks)
-      return fail(CECOLL_INVALID_ARGUMENT, "inconsistent rank ranges across processes");
-    for (int k = 0; k < pi.nlocal; ++k) {
-      if (owner[pi.first + k] >= 0) return fail(CECOLL_INVALID_ARGUMENT, "a rank is owned by two processes");
-      owner[pi.first + k] = p;
-    }
-    ProcInfoView v;
-    v.first = pi.first;
-    v.nlocal = pi.nlocal;
-    v.device = pi.device;
-    std::memcpy(&v.flags, &pi.flags, sizeof(v.flags));
-    out->push_back(v);
-  }
-  for (int r = 0; r < nranks; ++r)
-    if (owner[r] < 0) return fail(CECOLL_INVALID_ARGUMENT, "rank " + std::to_string(r) + " is owned by no process");
-  return {};
-}
-
-Status world_init_ranks(int nranks, int first, int nlocal, int device, cecoll_exchange_fn fn, void* ctx,
-                        World** out) {
-  if (!driver_api()) return fail(CECOLL_NO_DEVICE, "no CUDA driver / device");
-  if (nranks < 1 || nranks > kMaxRanks || nlocal < 1 || first < 0 || first + nlocal > nranks || !fn)
-    return fail(CECOLL_INVALID_ARGUMENT, "bad rank range / exchange");
-  DeviceGuard g(device);
-  auto w = std::make_unique<World>();
-  w->nranks = nranks;
-  w->multiprocess = true;
-  w->first_local = first;
-  w->nlocal = nlocal;
-  w->device.assign(nranks, -1);
-  w->flag_page.assign(nranks, nullptr);
-  w->local.resize(nranks);
-  // One allocation holds the flag pages of every local rank (one IPC handle).
-  void* block = nullptr;
-  CUDA_TRY(cudaMalloc(&block, kFlagBytes * nlocal));
-  CUDA_TRY(cudaMemset(block, 0, kFlagBytes * nlocal));
-  CUDA_TRY(cudaDeviceSynchronize());
-  w->flag_block = block;
-  for (int k = 0; k < nlocal; ++k)
-    STATUS_TRY(make_rank(w.get(), first + k, device,
-                         reinterpret_cast<uint64_t*>(static_cast<char*>(block) + k * kFlagBytes)));
-  cudaIpcMemHandle_t h;
-  CUDA_TRY(cudaIpcGetMemHandle(&h, block));
-  std::vector<ProcInfoView> procs;
-  STATUS_TRY(gather_procs(nranks, first, nlocal, device, &h, fn, ctx, &procs));
-  for (const ProcInfoView& pv : procs) {
-    char* base = nullptr;
-    if (pv.first != first) {
-      void* opened = nullptr;
-      STATUS_TRY(open_ipc(w.get(), pv.flags, &opened));
-      base = static_cast<char*>(opened);
-    }
-    for (int k = 0; k < pv.nlocal; ++k) {
-      const int r = pv.first + k;
-      w->device[r] = pv.device;
-      if (pv.first != first) w->flag_page[r] = reinterpret_cast<uint64_t*>(base + k * kFlagBytes);
-    }
-  }
-  w->ndevices = count_devices(w->device);
-  w->live_comms = nlocal;
-  w->reg_rounds.assign(nlocal, 0);
-  w->exchange = fn;
-  w->exchange_ctx = ctx;
-  *out = w.release();
-  return {};
-}
-
-// Registration is collective: each process registers its local ranks in the
-// same order; round i of local index k fills window i for ranks first_p + k
-// of every process p. Windows are symmetric (same size on every rank) and a
-// collective's buffers must sit at the same offset in every rank's window.
-Status world_register(World* w, int rank, void* ptr, size_t bytes, cecoll_exchange_fn fn, void* ctx) {
-  if (!w->multiprocess) return {};  // single process: UVA pointers are used as is
-  if (!fn) return fail(CECOLL_INVALID_ARGUMENT, "multi-process registration needs the exchange callback");
-  DeviceGuard g(w->device[rank]);
-  const int k = rank - w->first_local;
-  const int round = w->reg_rounds[k]++;
-  if (static_cast<int>(w->windows.size()) <= round) {
-    Window win;
-    win.bytes = bytes;
-    win.rank_base.assign(w->nranks, nullptr);
-    w->windows.push_back(win);
-  }
-  Window& win = w->windows[round];
-  if (win.bytes != bytes)
-    return fail(CECOLL_INVALID_ARGUMENT, "cecoll_register: windows must be symmetric (same size on every rank)");
-  CUdeviceptr base = 0;
-  size_t size = 0;
-  CU_TRY(driver_api()->MemGetAddressRange(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)));
-  RegInfo mine;
-  std::memset(&mine, 0, sizeof(mine));
-  mine.rank = rank;
-  mine.offset = reinterpret_cast<uint64_t>(ptr) - base;
-  mine.bytes = bytes;
-  CUDA_TRY(cudaIpcGetMemHandle(&mine.handle, reinterpret_cast<void*>(base)));
-  const int procs = w->nranks / w->nlocal;
-  std::vector<RegInfo> all(procs);
-  if (fn(ctx, &mine, sizeof(RegInfo), all.data()) != 0) return fail(CECOLL_INTERNAL, "exchange failed");
-  for (const RegInfo& ri : all) {
-    if (ri.bytes != bytes)
-      return fail(CECOLL_INVALID_ARGUMENT, "cecoll_register: windows must be symmetric (same size on every rank)");
-    if (ri.rank < 0 || ri.rank >= w->nranks) return fail(CECOLL_INVALID_ARGUMENT, "bad rank in registration");
-    if (ri.rank == rank) {
-      win.rank_base[ri.rank] = static_cast<char*>(ptr);
-      continue;
-    }
-    void* opened = nullptr;
-    STATUS_TRY(open_ipc(w, ri.handle, &opened));
-    win.rank_base[ri.rank] = static_cast<char*>(opened) + ri.offset;
-  }
-  return {};
-}
-
-Status world_deregister(World* w, void* ptr) {
-  (void)ptr;
-  // Windows stay mapped until the communicator is destroyed (mappings are
-  // shared by every plan built on them).
-  return w->multiprocess ? Status{} : Status{};
-}
-
-void world_release(World* w) {
-  for (auto& p : w->plans) plan_destroy(w, p.get());
-  w->plans.clear();
-  // Armed explicit plans would keep their gate kernels waiting (and the
-  // device synchronisation below would never return): cancel them. Their
-  // cecoll_plan handles must not be used afterwards.
-  for (Plan* p : w->explicit_plans) plan_destroy(w, p);
-  w->explicit_plans.clear();
-  for (auto& rs : w->local) {
-    if (!rs) continue;
-    DeviceGuard g(rs->device);
-    cudaDeviceSynchronize();
-    for (auto s : rs->lanes) cudaStreamDestroy(s);
-    for (auto e : rs->lane_done) cudaEventDestroy(e);
-    if (rs->start) cudaEventDestroy(rs->start);
-    if (rs->flags && rs->owns_flags) cudaFree(rs->flags);
-  }
-  for (void* p : w->ipc_opened) cudaIpcCloseMemHandle(p);
-  if (w->flag_block) cudaFree(w->flag_block);
-  delete w;
-}
-
-// ---------------------------------------------------------------------------
-// Plan lowering
-// ---------------------------------------------------------------------------
 
 namespace {
 
@@ -535,6 +126,14 @@ Status upload_ptrs(Plan* p, int device, const std::vector<uint64_t*>& ptrs, uint
   return {};
 }
 
+struct PlanReleaser {
+  World* w;
+  void operator()(Plan* p) const {
+    plan_destroy(w, p);
+    delete p;
+  }
+};
+
 // Device holding the flag page that contains addr (-1 if none).
 int flag_device(World* w, const uint64_t* addr) {
   for (int r = 0; r < w->nranks; ++r) {
@@ -580,25 +179,16 @@ Status split_remote(World* w, Plan* p) {
   return {};
 }
 
-// Stream memops, then the signal kernel for other-device flags.
-Status signal_remote(World* w, uint64_t** tab, size_t n, cudaStream_t s) {
-  if (!n) return {};
-  CUDA_TRY(launch_signal(tab, static_cast<int>(n), s));
-  ++w->counters[4];
-  ++w->counters[6];
-  w->counters[2] += static_cast<int64_t>(n);
-  return {};
-}
 
 }  // namespace
 
-Status build_graph(World* w, Plan* p, Unit& u);
 
 Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args, Plan** out,
                    const Program* given) {
   const int n = w->nranks;
   if (s <= 0) return fail(CECOLL_INVALID_ARGUMENT, "collective: chunk size must be positive");
-  auto plan = std::make_unique<Plan>();
+  // Frees device allocations, graphs and pinned pages if creation fails.
+  std::unique_ptr<Plan, PlanReleaser> plan(new Plan, PlanReleaser{w});
   Plan* p = plan.get();
   p->kind = kind;
   p->chunk = s;
@@ -848,8 +438,7 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
       // memcpy node between devices inside a conditional body): run the same
       // command program without prelaunch rather than fail the collective.
       std::string why = gs.msg;
-      plan_destroy(w, p);
-      Plan* eager = nullptr;
+      Plan* eager = nullptr;  // `plan` (the failed one) is released on return
       STATUS_TRY(plan_create(w, kind, base_of(impl), s, args, &eager, given));
       eager->impl = impl;
       eager->graph_fallback = why;
@@ -924,7 +513,8 @@ Status plan_create_rs(World* w, Impl impl, int64_t count, int dtype, int op, con
     return fail(CECOLL_UNSUPPORTED, "reduce-scatter: sm, pcpy, b2b, prelaunch_pcpy or prelaunch_b2b");
   const int esize = dtype_bytes(dtype);
   const int64_t s = count * esize;
-  auto plan = std::make_unique<Plan>();
+  // Frees device allocations, graphs and pinned pages if creation fails.
+  std::unique_ptr<Plan, PlanReleaser> plan(new Plan, PlanReleaser{w});
   Plan* p = plan.get();
   p->kind = Kind::ReduceScatter;
   p->impl = impl;
@@ -1053,31 +643,6 @@ Status plan_create_rs(World* w, Impl impl, int64_t count, int dtype, int op, con
   return {};
 }
 
-Status run_reduce_scatter(World* w, Impl impl, int64_t count, int dtype, int op, const std::vector<CallArgs>& args) {
-  if (impl == Impl::Auto) impl = Impl::Sm;
-  const int64_t s = count * dtype_bytes(dtype);
-  Plan* p = nullptr;
-  for (auto& cand : w->plans) {
-    Plan* c = cand.get();
-    if (c->kind != Kind::ReduceScatter || c->impl != impl || c->chunk != s || c->dtype != dtype || c->op != op ||
-        c->key_rank.size() != args.size())
-      continue;
-    bool same = true;
-    for (size_t i = 0; i < args.size() && same; ++i)
-      same = c->key_rank[i] == args[i].rank && c->key_send[i] == args[i].send && c->key_recv[i] == args[i].recv &&
-             c->key_stream[i] == args[i].stream;
-    if (same) {
-      p = c;
-      break;
-    }
-  }
-  if (!p) {
-    STATUS_TRY(plan_create_rs(w, impl, count, dtype, op, args, &p));
-    w->plans.emplace_back(p);
-  }
-  return plan_launch(w, p, false);
-}
-
 // Records one unit's lanes into a graph: [gate kernel] -> IF{ poll kernel ->
 // lanes (copies, item kernels) + placement -> signal kernel }.
 Status build_graph(World* w, Plan* p, Unit& u) {
@@ -1183,248 +748,6 @@ Status build_graph(World* w, Plan* p, Unit& u) {
   CUDA_TRY(e2);
   CUDA_TRY(cudaGraphInstantiate(&u.exec, u.graph, 0));
   return {};
-}
-
-// ---------------------------------------------------------------------------
-// Execution
-// ---------------------------------------------------------------------------
-
-namespace {
-
-Status run_ce(World* w, Plan* p) {
-  const DriverApi* d = driver_api();
-  (void)d;
-  // Phase 1: every unit announces readiness (rdy), forks its lanes and places
-  // its own chunk. Phase 2: lanes poll rdy, copy, signal done. Phase 3: units
-  // poll done and join their lanes. Every poll is submitted after the signal
-  // it waits for, so streams that share a hardware queue cannot deadlock.
-  for (Unit& u : p->units) {
-    DeviceGuard g(u.device);
-    STATUS_TRY(issue_copies(w, u.precopy, u.stream, true));
-    STATUS_TRY(submit(w, u.stream, u.start));
-    STATUS_TRY(signal_remote(w, u.start_remote_tab, u.start_remote.size(), u.stream));
-    for (int r : u.ranks) {
-      CUDA_TRY(cudaEventRecord(w->local[r]->start, u.stream));
-      ++w->counters[6];
-    }
-    STATUS_TRY(issue_copies(w, u.placement, u.stream, true));
-  }
-  for (LaneExec& l : p->lanes) {
-    RankState* rs = w->local[l.rank].get();
-    DeviceGuard g(rs->device);
-    cudaStream_t s = rs->lanes[l.lane];
-    CUDA_TRY(cudaStreamWaitEvent(s, rs->start, 0));
-    ++w->counters[6];
-    STATUS_TRY(submit(w, s, l.pre));
-    STATUS_TRY(issue_copies(w, l.copies, s, true));
-    if (l.table.nitems) {
-      CUDA_TRY(launch_items(l.table, mover_grid_for(l.table, p->sms), s));
-      ++w->counters[4];
-      ++w->counters[6];
-    }
-    STATUS_TRY(submit(w, s, l.post));
-    STATUS_TRY(signal_remote(w, l.post_remote_tab, l.post_remote.size(), s));
-    CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], s));
-    ++w->counters[6];
-  }
-  for (Unit& u : p->units) {
-    DeviceGuard g(u.device);
-    STATUS_TRY(submit(w, u.stream, u.finish));
-    for (const LaneExec& l : p->lanes) {
-      if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) == u.ranks.end()) continue;
-      CUDA_TRY(cudaStreamWaitEvent(u.stream, w->local[l.rank]->lane_done[l.lane], 0));
-      ++w->counters[6];
-    }
-  }
-  return {};
-}
-
-Status run_sm(World* w, Plan* p) {
-  for (Unit& u : p->units) {  // phase 1: readiness to sources in other units
-    DeviceGuard g(u.device);
-    STATUS_TRY(submit(w, u.stream, u.start));
-    STATUS_TRY(signal_remote(w, u.start_remote_tab, u.start_remote.size(), u.stream));
-  }
-  for (Unit& u : p->units) {  // phase 2: wait destinations, move, signal
-    DeviceGuard g(u.device);
-    STATUS_TRY(submit(w, u.stream, u.sm_pre));
-    if (u.table.nitems) {
-      CUDA_TRY(launch_items(u.table, mover_grid_for(u.table, p->sms), u.stream));
-      ++w->counters[4];
-      ++w->counters[6];
-    }
-    if (u.red.nitems) {
-      CUDA_TRY(launch_reduce(u.red, 4 * p->sms, u.stream));
-      ++w->counters[4];
-      ++w->counters[6];
-    }
-    STATUS_TRY(submit(w, u.stream, u.sm_post));
-    STATUS_TRY(signal_remote(w, u.sm_post_remote_tab, u.sm_post_remote.size(), u.stream));
-  }
-  for (Unit& u : p->units) {  // phase 3: incoming chunks
-    DeviceGuard g(u.device);
-    STATUS_TRY(submit(w, u.stream, u.finish));
-  }
-  return {};
-}
-
-Status post_gate(Unit& u, uint64_t kind) {
-  const uint64_t k = u.posts++;
-  volatile uint64_t* posted = u.posted;
-  posted[1 + (k % 64)] = kind;
-  __atomic_thread_fence(__ATOMIC_SEQ_CST);
-  posted[0] = k + 1;
-  __atomic_thread_fence(__ATOMIC_SEQ_CST);
-  return {};
-}
-
-Status arm_unit(World* w, Unit& u) {
-  DeviceGuard g(u.device);
-  CUDA_TRY(cudaGraphLaunch(u.exec, u.arm));
-  CUDA_TRY(cudaEventRecord(u.graph_done, u.arm));
-  ++w->counters[5];
-  w->counters[6] += 2;
-  u.armed = true;
-  return {};
-}
-
-Status trigger_unit(World* w, Plan* p, Unit& u) {
-  DeviceGuard g(u.device);
-  STATUS_TRY(issue_copies(w, u.precopy, u.stream, true));
-  MemOps ops = u.start;
-  ops.push_back(op_write(u.ready_flag, 1));
-  STATUS_TRY(submit(w, u.stream, ops));
-  STATUS_TRY(signal_remote(w, u.start_remote_tab, u.start_remote.size(), u.stream));
-  STATUS_TRY(post_gate(u, 1));
-  u.armed = false;
-  if (u.nfin) {
-    CUDA_TRY(launch_poll(u.fin_tab, u.nfin, u.err, u.stream));
-    ++w->counters[4];
-    ++w->counters[6];
-  }
-  CUDA_TRY(cudaStreamWaitEvent(u.stream, u.graph_done, 0));
-  ++w->counters[6];
-  (void)p;
-  return {};
-}
-
-bool same_call(const Plan* p, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args) {
-  if (p->kind != kind || p->chunk != s || p->key_rank.size() != args.size()) return false;
-  if (p->impl != impl) return false;
-  for (size_t i = 0; i < args.size(); ++i)
-    if (p->key_rank[i] != args[i].rank || p->key_send[i] != args[i].send || p->key_recv[i] != args[i].recv ||
-        p->key_stream[i] != args[i].stream)
-      return false;
-  return true;
-}
-
-}  // namespace
-
-// Cancels armed instances (the next launch re-arms): after this, device-wide
-// synchronisation returns.
-Status plan_disarm(World* w, Plan* p) {
-  if (p->inner) STATUS_TRY(plan_disarm(w, p->inner.get()));
-  for (Unit& u : p->units) {
-    if (!u.armed) continue;
-    DeviceGuard g(u.device);
-    STATUS_TRY(post_gate(u, 2));
-    CUDA_TRY(cudaStreamSynchronize(u.arm));
-    u.armed = false;
-  }
-  return {};
-}
-
-Status plan_arm(World* w, Plan* p) {
-  if (p->inner) return plan_arm(w, p->inner.get());
-  if (!p->prelaunch) return {};
-  for (Unit& u : p->units)
-    if (!u.armed) STATUS_TRY(arm_unit(w, u));
-  return {};
-}
-
-Status plan_launch(World* w, Plan* p, bool rearm) {
-  if (p->inner) {  // reduce-scatter over copy engines: gather, then reduce
-    for (size_t i = 0; i < p->units.size(); ++i) p->inner->units[i].stream = p->units[i].stream;
-    STATUS_TRY(plan_launch(w, p->inner.get(), rearm));
-    for (Unit& u : p->units) {
-      DeviceGuard g(u.device);
-      CUDA_TRY(launch_reduce(u.red, 4 * p->sms, u.stream));
-      ++w->counters[4];
-      ++w->counters[6];
-    }
-    return {};
-  }
-  ++w->counters[0];
-  if (p->sm) return run_sm(w, p);
-  if (!p->prelaunch) return run_ce(w, p);
-  // prelaunch: make sure every unit is armed, trigger all, re-arm if asked.
-  STATUS_TRY(plan_arm(w, p));
-  for (Unit& u : p->units) STATUS_TRY(trigger_unit(w, p, u));
-  if (rearm) STATUS_TRY(plan_arm(w, p));
-  return {};
-}
-
-Status plan_destroy(World* w, Plan* p) {
-  Status result;
-  if (p->inner) result = plan_destroy(w, p->inner.get());
-  for (Unit& u : p->units) {
-    DeviceGuard g(u.device);
-    if (u.armed) {
-      post_gate(u, 2);  // cancel: the gate skips the body
-      cudaStreamSynchronize(u.arm);
-      u.armed = false;
-    }
-    if (u.err) {  // kernel-side polls report timeouts here (kernels.cu poll_kernel)
-      if (u.arm) cudaStreamSynchronize(u.arm);
-      uint64_t err = 0;
-      if (cudaMemcpy(&err, u.err, sizeof(err), cudaMemcpyDeviceToHost) == cudaSuccess && err && result.ok())
-        result = fail(CECOLL_TIMEOUT, (err & 1) ? "a flag poll timed out (20 s): a peer never signalled"
-                                                : "gate received an unknown post");
-    }
-    if (u.exec) cudaGraphExecDestroy(u.exec);
-    if (u.graph) cudaGraphDestroy(u.graph);
-    if (u.arm) {
-      cudaStreamSynchronize(u.arm);
-      cudaStreamDestroy(u.arm);
-    }
-    if (u.graph_done) cudaEventDestroy(u.graph_done);
-    if (u.posted) cudaFreeHost(u.posted);
-  }
-  for (size_t i = 0; i < p->dev_allocs.size(); ++i) {
-    DeviceGuard g(p->dev_alloc_device[i]);
-    cudaFree(p->dev_allocs[i]);
-  }
-  p->dev_allocs.clear();
-  return result;
-}
-
-Status run_collective(World* w, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args) {
-  if (impl == Impl::Auto) {
-    bool in_place = kind == Kind::AllToAll;
-    for (const CallArgs& a : args) in_place &= a.send == a.recv;
-    impl = in_place ? Impl::Swap : select(kind, s, w->nranks, w->ndevices);
-  }
-  Plan* p = nullptr;
-  for (auto& cand : w->plans)
-    if (same_call(cand.get(), kind, impl, s, args)) {
-      p = cand.get();
-      break;
-    }
-  if (!p) {
-    STATUS_TRY(plan_create(w, kind, impl, s, args, &p));
-    w->plans.emplace_back(p);
-    if (w->plans.size() > 64) {  // bounded cache: drop the oldest plan
-      for (Unit& u : w->plans.front()->units) {
-        DeviceGuard g(u.device);
-        cudaStreamSynchronize(u.stream);
-      }
-      plan_destroy(w, w->plans.front().get());
-      w->plans.erase(w->plans.begin());
-    }
-  }
-  // Eager calls never leave an instance armed after returning (a waiting
-  // graph would block device-wide synchronisation); explicit plans do.
-  return plan_launch(w, p, false);
 }
 
 }  // namespace cecoll

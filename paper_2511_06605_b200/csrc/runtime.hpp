@@ -1,4 +1,4 @@
-// Communicator, plans and executors.
+// Communicator, plans and executors (world.cpp, lower.cpp, exec.cpp).
 //
 // Execution model:
 //  * A World is every rank this process can address. comm_init_all builds one

@@ -1,0 +1,272 @@
+// Communicators: single-process worlds (every rank local, the reference's
+// single host process) and multi-process worlds (CUDA IPC
+// mapping of flag pages and symmetric registered windows).
+#include <algorithm>
+#include <cstring>
+#include <set>
+
+#include "internal.hpp"
+
+namespace cecoll {
+
+namespace {
+
+Status make_rank(World* w, int rank, int device, uint64_t* page = nullptr) {
+  DeviceGuard g(device);
+  auto rs = std::make_unique<RankState>();
+  rs->rank = rank;
+  rs->device = device;
+  CUDA_TRY(cudaEventCreateWithFlags(&rs->start, cudaEventDisableTiming));
+  if (page) {
+    rs->flags = page;
+    rs->owns_flags = false;
+  } else {
+    CUDA_TRY(cudaMalloc(&rs->flags, kFlagBytes));
+    CUDA_TRY(cudaMemset(rs->flags, 0, kFlagBytes));
+    CUDA_TRY(cudaDeviceSynchronize());
+  }
+  w->flag_page[rank] = rs->flags;
+  w->local[rank] = std::move(rs);
+  return {};
+}
+
+int count_devices(const std::vector<int>& dev) {
+  std::set<int> s(dev.begin(), dev.end());
+  return static_cast<int>(s.size());
+}
+
+}  // namespace
+
+Status world_init_all(int nranks, const int* devlist, World** out) {
+  if (!driver_api()) return fail(CECOLL_NO_DEVICE, "no CUDA driver / device");
+  if (nranks < 1 || nranks > kMaxRanks)
+    return fail(CECOLL_INVALID_ARGUMENT, "nranks must be in [1, " + std::to_string(kMaxRanks) + "]");
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  for (int r = 0; r < nranks; ++r)
+    if (devlist[r] < 0 || devlist[r] >= ndev)
+      return fail(CECOLL_INVALID_ARGUMENT, "device " + std::to_string(devlist[r]) + " out of range");
+  auto w = std::make_unique<World>();
+  w->nranks = nranks;
+  w->device.assign(devlist, devlist + nranks);
+  w->flag_page.assign(nranks, nullptr);
+  w->local.resize(nranks);
+  w->ndevices = count_devices(w->device);
+  // Peer access between every pair of distinct devices (NVLink / NVSwitch).
+  std::set<int> devs(w->device.begin(), w->device.end());
+  for (int a : devs)
+    for (int b : devs) {
+      if (a == b) continue;
+      int can = 0;
+      CUDA_TRY(cudaDeviceCanAccessPeer(&can, a, b));
+      if (!can) return fail(CECOLL_UNSUPPORTED, "no peer access between devices");
+      DeviceGuard g(a);
+      cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "EnablePeerAccess", __FILE__, __LINE__);
+      cudaGetLastError();
+    }
+  for (int r = 0; r < nranks; ++r) STATUS_TRY(make_rank(w.get(), r, w->device[r]));
+  w->live_comms = nranks;
+  w->first_local = 0;
+  w->nlocal = nranks;
+  *out = w.release();
+  return {};
+}
+
+namespace {
+
+// One blob per process in the init exchange.
+struct ProcInfo {
+  int32_t first;   // first global rank owned by the process
+  int32_t nlocal;  // ranks owned (consecutive)
+  int32_t device;
+  int32_t pid;
+  cudaIpcMemHandle_t flags;  // nlocal flag pages, kFlagBytes apart
+};
+
+// One blob per process in a registration round.
+struct RegInfo {
+  int32_t rank;
+  int32_t pad;
+  uint64_t offset;  // of the window inside its allocation
+  uint64_t bytes;
+  cudaIpcMemHandle_t handle;  // of the allocation
+};
+
+Status open_ipc(World* w, const cudaIpcMemHandle_t& h, void** out) {
+  std::string key(reinterpret_cast<const char*>(&h), sizeof(h));
+  auto it = w->ipc_by_handle.find(key);
+  if (it != w->ipc_by_handle.end()) {
+    *out = it->second;
+    return {};
+  }
+  CUDA_TRY(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  w->ipc_opened.push_back(*out);
+  w->ipc_by_handle[key] = *out;
+  return {};
+}
+
+}  // namespace
+
+Status gather_procs(int nranks, int first, int nlocal, int device, const cudaIpcMemHandle_t* flags,
+                    cecoll_exchange_fn fn, void* ctx, std::vector<ProcInfoView>* out) {
+  if (nranks < 1 || nranks > kMaxRanks || nlocal < 1 || first < 0 || first + nlocal > nranks || !fn)
+    return fail(CECOLL_INVALID_ARGUMENT, "bad rank range / exchange");
+  if (nranks % nlocal != 0)
+    return fail(CECOLL_INVALID_ARGUMENT, "every process must own the same number of ranks");
+  const int procs = nranks / nlocal;
+  ProcInfo mine;
+  std::memset(&mine, 0, sizeof(mine));
+  mine.first = first;
+  mine.nlocal = nlocal;
+  mine.device = device;
+  if (flags) mine.flags = *flags;
+  std::vector<ProcInfo> all(procs);
+  if (fn(ctx, &mine, sizeof(ProcInfo), all.data()) != 0) return fail(CECOLL_INTERNAL, "exchange failed");
+  std::vector<int> owner(nranks, -1);
+  out->clear();
+  for (int p = 0; p < procs; ++p) {
+    const ProcInfo& pi = all[p];
+    if (pi.nlocal != nlocal || pi.first < 0 || pi.first + pi.nlocal > nranks)
+      return fail(CECOLL_INVALID_ARGUMENT, "inconsistent rank ranges across processes");
+    for (int k = 0; k < pi.nlocal; ++k) {
+      if (owner[pi.first + k] >= 0) return fail(CECOLL_INVALID_ARGUMENT, "a rank is owned by two processes");
+      owner[pi.first + k] = p;
+    }
+    ProcInfoView v;
+    v.first = pi.first;
+    v.nlocal = pi.nlocal;
+    v.device = pi.device;
+    std::memcpy(&v.flags, &pi.flags, sizeof(v.flags));
+    out->push_back(v);
+  }
+  for (int r = 0; r < nranks; ++r)
+    if (owner[r] < 0) return fail(CECOLL_INVALID_ARGUMENT, "rank " + std::to_string(r) + " is owned by no process");
+  return {};
+}
+
+Status world_init_ranks(int nranks, int first, int nlocal, int device, cecoll_exchange_fn fn, void* ctx,
+                        World** out) {
+  if (!driver_api()) return fail(CECOLL_NO_DEVICE, "no CUDA driver / device");
+  if (nranks < 1 || nranks > kMaxRanks || nlocal < 1 || first < 0 || first + nlocal > nranks || !fn)
+    return fail(CECOLL_INVALID_ARGUMENT, "bad rank range / exchange");
+  DeviceGuard g(device);
+  auto w = std::make_unique<World>();
+  w->nranks = nranks;
+  w->multiprocess = true;
+  w->first_local = first;
+  w->nlocal = nlocal;
+  w->device.assign(nranks, -1);
+  w->flag_page.assign(nranks, nullptr);
+  w->local.resize(nranks);
+  // One allocation holds the flag pages of every local rank (one IPC handle).
+  void* block = nullptr;
+  CUDA_TRY(cudaMalloc(&block, kFlagBytes * nlocal));
+  CUDA_TRY(cudaMemset(block, 0, kFlagBytes * nlocal));
+  CUDA_TRY(cudaDeviceSynchronize());
+  w->flag_block = block;
+  for (int k = 0; k < nlocal; ++k)
+    STATUS_TRY(make_rank(w.get(), first + k, device,
+                         reinterpret_cast<uint64_t*>(static_cast<char*>(block) + k * kFlagBytes)));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, block));
+  std::vector<ProcInfoView> procs;
+  STATUS_TRY(gather_procs(nranks, first, nlocal, device, &h, fn, ctx, &procs));
+  for (const ProcInfoView& pv : procs) {
+    char* base = nullptr;
+    if (pv.first != first) {
+      void* opened = nullptr;
+      STATUS_TRY(open_ipc(w.get(), pv.flags, &opened));
+      base = static_cast<char*>(opened);
+    }
+    for (int k = 0; k < pv.nlocal; ++k) {
+      const int r = pv.first + k;
+      w->device[r] = pv.device;
+      if (pv.first != first) w->flag_page[r] = reinterpret_cast<uint64_t*>(base + k * kFlagBytes);
+    }
+  }
+  w->ndevices = count_devices(w->device);
+  w->live_comms = nlocal;
+  w->reg_rounds.assign(nlocal, 0);
+  w->exchange = fn;
+  w->exchange_ctx = ctx;
+  *out = w.release();
+  return {};
+}
+
+// Registration is collective: each process registers its local ranks in the
+// same order; round i of local index k fills window i for ranks first_p + k
+// of every process p. Windows are symmetric (same size on every rank) and a
+// collective's buffers must sit at the same offset in every rank's window.
+Status world_register(World* w, int rank, void* ptr, size_t bytes, cecoll_exchange_fn fn, void* ctx) {
+  if (!w->multiprocess) return {};  // single process: UVA pointers are used as is
+  if (!fn) return fail(CECOLL_INVALID_ARGUMENT, "multi-process registration needs the exchange callback");
+  DeviceGuard g(w->device[rank]);
+  const int k = rank - w->first_local;
+  const int round = w->reg_rounds[k]++;
+  if (static_cast<int>(w->windows.size()) <= round) {
+    Window win;
+    win.bytes = bytes;
+    win.rank_base.assign(w->nranks, nullptr);
+    w->windows.push_back(win);
+  }
+  Window& win = w->windows[round];
+  if (win.bytes != bytes)
+    return fail(CECOLL_INVALID_ARGUMENT, "cecoll_register: windows must be symmetric (same size on every rank)");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  CU_TRY(driver_api()->MemGetAddressRange(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)));
+  RegInfo mine;
+  std::memset(&mine, 0, sizeof(mine));
+  mine.rank = rank;
+  mine.offset = reinterpret_cast<uint64_t>(ptr) - base;
+  mine.bytes = bytes;
+  CUDA_TRY(cudaIpcGetMemHandle(&mine.handle, reinterpret_cast<void*>(base)));
+  const int procs = w->nranks / w->nlocal;
+  std::vector<RegInfo> all(procs);
+  if (fn(ctx, &mine, sizeof(RegInfo), all.data()) != 0) return fail(CECOLL_INTERNAL, "exchange failed");
+  for (const RegInfo& ri : all) {
+    if (ri.bytes != bytes)
+      return fail(CECOLL_INVALID_ARGUMENT, "cecoll_register: windows must be symmetric (same size on every rank)");
+    if (ri.rank < 0 || ri.rank >= w->nranks) return fail(CECOLL_INVALID_ARGUMENT, "bad rank in registration");
+    if (ri.rank == rank) {
+      win.rank_base[ri.rank] = static_cast<char*>(ptr);
+      continue;
+    }
+    void* opened = nullptr;
+    STATUS_TRY(open_ipc(w, ri.handle, &opened));
+    win.rank_base[ri.rank] = static_cast<char*>(opened) + ri.offset;
+  }
+  return {};
+}
+
+Status world_deregister(World* w, void* ptr) {
+  (void)ptr;
+  // Windows stay mapped until the communicator is destroyed (mappings are
+  // shared by every plan built on them).
+  return w->multiprocess ? Status{} : Status{};
+}
+
+void world_release(World* w) {
+  for (auto& p : w->plans) plan_destroy(w, p.get());
+  w->plans.clear();
+  // Armed explicit plans would keep their gate kernels waiting (and the
+  // device synchronisation below would never return): cancel them. Their
+  // cecoll_plan handles must not be used afterwards.
+  for (Plan* p : w->explicit_plans) plan_destroy(w, p);
+  w->explicit_plans.clear();
+  for (auto& rs : w->local) {
+    if (!rs) continue;
+    DeviceGuard g(rs->device);
+    cudaDeviceSynchronize();
+    for (auto s : rs->lanes) cudaStreamDestroy(s);
+    for (auto e : rs->lane_done) cudaEventDestroy(e);
+    if (rs->start) cudaEventDestroy(rs->start);
+    if (rs->flags && rs->owns_flags) cudaFree(rs->flags);
+  }
+  for (void* p : w->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (w->flag_block) cudaFree(w->flag_block);
+  delete w;
+}
+
+}  // namespace cecoll
