@@ -137,7 +137,17 @@ cecoll_status_t cecoll_comm_info(cecoll_comm_t comm, int* rank, int* nranks, int
  * windows are symmetric — same size on every rank — and a collective's
  * buffers must sit at the same offset inside every rank's window. */
 cecoll_status_t cecoll_register(cecoll_comm_t comm, void* ptr, size_t bytes);
+/* Multi-process: `ptr` must be a registered window base; the window stops
+ * translating and cached plans are dropped (IPC mappings stay open until
+ * cecoll_comm_destroy). Explicit plans on the window must be destroyed first. */
 cecoll_status_t cecoll_deregister(cecoll_comm_t comm, void* ptr);
+/* Library-owned buffers (SURVEY §8(b) cecoll_mem_alloc): device memory on the
+ * rank's B200, rounded up to whole 2 MiB pages and registered as a window
+ * (collective in multi-process mode, like cecoll_register). cecoll_mem_free
+ * deregisters and frees (waits for work still using it); buffers left
+ * allocated are freed by cecoll_comm_destroy of the last communicator. */
+cecoll_status_t cecoll_mem_alloc(cecoll_comm_t comm, size_t bytes, void** ptr);
+cecoll_status_t cecoll_mem_free(cecoll_comm_t comm, void* ptr);
 
 /* ---------------------------------------------------------------------
  * Collectives (the runtime the reference simulates, sim.cpp:470).
@@ -199,6 +209,17 @@ cecoll_status_t cecoll_plan_disarm(cecoll_plan_t plan);
 /* Destroy plans before their communicators; cecoll_comm_destroy cancels any
  * plan still armed (its handle must not be used afterwards). */
 cecoll_status_t cecoll_plan_destroy(cecoll_plan_t plan);
+
+/* Hardware timelines in the reference's trace-event format (sim.cpp:523-544,
+ * export_trace_json): between trace_begin and trace_end every collective of
+ * the communicator's world is recorded per command with CUDA events (copies
+ * are then submitted one call each). trace_end stops recording and returns
+ * the JSON array ({"name": "<phase>:<command>", "ph": "B"|"E", "ts" µs,
+ * "pid": rank or -1 for the host, "tid": lane, -1 for the caller stream}):
+ * call it with json == NULL (or too small a capacity) to get *length; the
+ * trace is kept until it has been copied out. */
+cecoll_status_t cecoll_trace_begin(cecoll_comm_t comm);
+cecoll_status_t cecoll_trace_end(cecoll_comm_t comm, char* json, size_t capacity, size_t* length);
 
 /* Counters since comm creation: [0] collectives, [1] copy commands issued
  * (CE memcpys), [2] flag writes, [3] flag waits, [4] kernel launches,

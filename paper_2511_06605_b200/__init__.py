@@ -115,6 +115,10 @@ def lib():
         "cecoll_comm_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
         "cecoll_register": ([vp, vp, sz], i32),
         "cecoll_deregister": ([vp, vp], i32),
+        "cecoll_mem_alloc": ([vp, sz, C.POINTER(vp)], i32),
+        "cecoll_mem_free": ([vp, vp], i32),
+        "cecoll_trace_begin": ([vp], i32),
+        "cecoll_trace_end": ([vp, C.c_char_p, sz, C.POINTER(sz)], i32),
         "cecoll_allgather": ([vp, vp, sz, i32, vp, vp], i32),
         "cecoll_alltoall": ([vp, vp, sz, i32, vp, vp], i32),
         "cecoll_group_start": ([], i32),
@@ -146,6 +150,7 @@ EXPORTED_SYMBOLS = [
     "cecoll_group_end", "cecoll_plan_create", "cecoll_plan_launch", "cecoll_plan_destroy", "cecoll_comm_counters",
     "cecoll_program_parse", "cecoll_plan_create_program", "cecoll_comm_init_ranks", "cecoll_exchange_check",
     "cecoll_collective_n", "cecoll_plan_disarm", "cecoll_reduce_scatter", "cecoll_reduce_scatter_n",
+    "cecoll_mem_alloc", "cecoll_mem_free", "cecoll_trace_begin", "cecoll_trace_end",
 ]
 DTYPES = {"f32": 0, "float32": 0, "bf16": 1, "bfloat16": 1, "f16": 2, "float16": 2}
 REDOPS = {"sum": 0, "max": 1, "min": 2}
@@ -308,6 +313,29 @@ class Comm:
             nbytes = buf.numel() * buf.element_size()
         _check(lib().cecoll_register(self._h, ptr, nbytes), "register")
 
+    def deregister(self, buf):
+        _check(lib().cecoll_deregister(self._h, _ptr(buf)), "deregister")
+
+    def mem_alloc(self, nbytes: int):
+        """Library-owned, registered device buffer of `nbytes` (rounded up to
+        2 MiB pages; collective in multi-process communicators). Returned as a
+        uint8 CUDA tensor that does not own the memory: release it with
+        mem_free."""
+        import torch
+
+        p = C.c_void_p()
+        _check(lib().cecoll_mem_alloc(self._h, nbytes, C.byref(p)), "mem_alloc")
+
+        class _View:  # __cuda_array_interface__ lets torch wrap the pointer without a copy
+            __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (p.value, False),
+                                        "version": 3, "strides": None}
+
+        with torch.cuda.device(self.device):
+            return torch.as_tensor(_View(), device=f"cuda:{self.device}")
+
+    def mem_free(self, buf):
+        _check(lib().cecoll_mem_free(self._h, _ptr(buf)), "mem_free")
+
     def counters(self) -> dict:
         out = (C.c_int64 * 8)()
         _check(lib().cecoll_comm_counters(self._h, out))
@@ -319,6 +347,42 @@ class Comm:
         if self._h is not None:
             _check(lib().cecoll_comm_destroy(self._h))
             self._h = None
+
+
+class Trace:
+    """Records the hardware timeline of every collective issued inside the
+    block, in the reference's trace-event format (sim.cpp:523-544): after the
+    block, `events` is the list of {"name", "ph", "ts", "pid", "tid"} dicts
+    (chrome://tracing / Perfetto load `save(path)` directly).
+
+        with cc.Trace(comms[0]) as t:
+            cc.all_to_all(comms, sends, recvs, s, impl="pcpy")
+        t.save("aa_pcpy.json")
+    """
+
+    def __init__(self, comm: Comm):
+        self._comm = comm
+        self.events: list[dict] = []
+
+    def __enter__(self):
+        _check(lib().cecoll_trace_begin(self._comm._h), "trace_begin")
+        return self
+
+    def __exit__(self, *exc):
+        n = C.c_size_t()
+        _check(lib().cecoll_trace_end(self._comm._h, None, 0, C.byref(n)), "trace_end")
+        buf = C.create_string_buffer(n.value + 1)
+        _check(lib().cecoll_trace_end(self._comm._h, buf, n.value + 1, C.byref(n)), "trace_end")
+        import json
+
+        self.events = json.loads(buf.value.decode())
+        return False
+
+    def save(self, path: str):
+        import json
+
+        with open(path, "w") as f:
+            json.dump(self.events, f, indent=1)
 
 
 def destroy_all(comms: Sequence[Comm]):

@@ -272,6 +272,17 @@ cecoll_status_t cecoll_deregister(cecoll_comm_t comm, void* ptr) {
   return st(world_deregister(comm->world, ptr));
 }
 
+cecoll_status_t cecoll_mem_alloc(cecoll_comm_t comm, size_t bytes, void** ptr) {
+  if (!comm || !ptr || !bytes) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  *ptr = nullptr;
+  return st(world_mem_alloc(comm->world, comm->rank, bytes, ptr));
+}
+
+cecoll_status_t cecoll_mem_free(cecoll_comm_t comm, void* ptr) {
+  if (!comm || !ptr) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  return st(world_mem_free(comm->world, ptr));
+}
+
 cecoll_status_t cecoll_allgather(const void* send, void* recv, size_t chunk_bytes, cecoll_impl_t impl,
                                  cecoll_comm_t comm, void* stream) {
   return enqueue(Kind::AllGather, send, recv, chunk_bytes, impl, comm, stream);
@@ -412,6 +423,27 @@ cecoll_status_t cecoll_plan_destroy(cecoll_plan_t plan) {
 cecoll_status_t cecoll_plan_disarm(cecoll_plan_t plan) {
   if (!plan) return err(CECOLL_INVALID_ARGUMENT, "null plan");
   return st(plan_disarm(plan->world, plan->plan));
+}
+
+cecoll_status_t cecoll_trace_begin(cecoll_comm_t comm) {
+  if (!comm) return err(CECOLL_INVALID_ARGUMENT, "null communicator");
+  return st(trace_begin(comm->world));
+}
+
+cecoll_status_t cecoll_trace_end(cecoll_comm_t comm, char* json, size_t capacity, size_t* length) {
+  if (!comm || !length) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  World* w = comm->world;
+  if (w->tracer) {
+    std::string out;
+    cecoll_status_t r = st(trace_end(w, &out));
+    w->trace_json = std::move(out);
+    if (r != CECOLL_SUCCESS) return r;
+  }
+  *length = w->trace_json.size();
+  if (!json || capacity < w->trace_json.size() + 1) return CECOLL_SUCCESS;  // size query: keep the trace
+  std::memcpy(json, w->trace_json.c_str(), w->trace_json.size() + 1);
+  w->trace_json.clear();
+  return CECOLL_SUCCESS;
 }
 
 cecoll_status_t cecoll_comm_counters(cecoll_comm_t comm, int64_t out8[8]) {

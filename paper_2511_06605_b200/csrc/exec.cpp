@@ -38,45 +38,80 @@ Status run_reduce_scatter(World* w, Impl impl, int64_t count, int dtype, int op,
 
 namespace {
 
+const char* table_name(const ItemTable& t) {
+  if (t.kinds & (1 << kItemSwap)) return "copy:swap";
+  if (t.kinds & ((1 << kItemBcst) | (1 << kItemFan))) return "copy:broadcast";
+  return "copy:copy";
+}
+
+// Traced copy submission: one call per copy, each bracketed by events.
+Status issue_copies_traced(World* w, const std::vector<Copy>& copies, cudaStream_t s, bool allow_batch, int device,
+                           int pid, int tid) {
+  if (!w->tracer) return issue_copies(w, copies, s, allow_batch);
+  for (const Copy& c : copies) {
+    cudaEvent_t b = trace_mark(w, device, s);
+    STATUS_TRY(issue_copies(w, {c}, s, false));
+    trace_span(w, "copy:copy", pid, tid, device, b, trace_mark(w, device, s));
+  }
+  return {};
+}
+
+// Stream memory operations (+ the signal kernel for other devices' flags)
+// bracketed as one traced span when tracing and the batch is not empty.
+Status submit_traced(World* w, cudaStream_t s, const MemOps& ops, uint64_t** remote_tab, size_t nremote,
+                     const char* name, int device, int pid, int tid) {
+  if (ops.empty() && nremote == 0) return {};
+  cudaEvent_t b = trace_mark(w, device, s);
+  STATUS_TRY(submit(w, s, ops));
+  STATUS_TRY(signal_remote(w, remote_tab, nremote, s));
+  trace_span(w, name, pid, tid, device, b, trace_mark(w, device, s));
+  return {};
+}
+
 Status run_ce(World* w, Plan* p) {
-  const DriverApi* d = driver_api();
-  (void)d;
   // Phase 1: every unit announces readiness (rdy), forks its lanes and places
   // its own chunk. Phase 2: lanes poll rdy, copy, signal done. Phase 3: units
   // poll done and join their lanes. Every poll is submitted after the signal
   // it waits for, so streams that share a hardware queue cannot deadlock.
   for (Unit& u : p->units) {
     DeviceGuard g(u.device);
-    STATUS_TRY(issue_copies(w, u.precopy, u.stream, true));
-    STATUS_TRY(submit(w, u.stream, u.start));
-    STATUS_TRY(signal_remote(w, u.start_remote_tab, u.start_remote.size(), u.stream));
+    const double h0 = trace_host_now(w);
+    const int pid = u.ranks[0];
+    STATUS_TRY(issue_copies_traced(w, u.precopy, u.stream, true, u.device, pid, -1));
+    STATUS_TRY(submit_traced(w, u.stream, u.start, u.start_remote_tab, u.start_remote.size(), "sync:signal",
+                             u.device, pid, -1));
     for (int r : u.ranks) {
       CUDA_TRY(cudaEventRecord(w->local[r]->start, u.stream));
       ++w->counters[6];
     }
-    STATUS_TRY(issue_copies(w, u.placement, u.stream, true));
+    STATUS_TRY(issue_copies_traced(w, u.placement, u.stream, true, u.device, pid, -1));
+    trace_host_span(w, "control", h0);
   }
   for (LaneExec& l : p->lanes) {
     RankState* rs = w->local[l.rank].get();
     DeviceGuard g(rs->device);
+    const double h0 = trace_host_now(w);
     cudaStream_t s = rs->lanes[l.lane];
     CUDA_TRY(cudaStreamWaitEvent(s, rs->start, 0));
     ++w->counters[6];
-    STATUS_TRY(submit(w, s, l.pre));
-    STATUS_TRY(issue_copies(w, l.copies, s, true));
+    STATUS_TRY(submit_traced(w, s, l.pre, nullptr, 0, "poll:poll", rs->device, l.rank, l.lane));
+    STATUS_TRY(issue_copies_traced(w, l.copies, s, true, rs->device, l.rank, l.lane));
     if (l.table.nitems) {
+      cudaEvent_t b = trace_mark(w, rs->device, s);
       CUDA_TRY(launch_items(l.table, mover_grid_for(l.table, p->sms), s));
       ++w->counters[4];
       ++w->counters[6];
+      trace_span(w, table_name(l.table), l.rank, l.lane, rs->device, b, trace_mark(w, rs->device, s));
     }
-    STATUS_TRY(submit(w, s, l.post));
-    STATUS_TRY(signal_remote(w, l.post_remote_tab, l.post_remote.size(), s));
+    STATUS_TRY(submit_traced(w, s, l.post, l.post_remote_tab, l.post_remote.size(), "sync:signal", rs->device,
+                             l.rank, l.lane));
     CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], s));
     ++w->counters[6];
+    trace_host_span(w, "control", h0);
   }
   for (Unit& u : p->units) {
     DeviceGuard g(u.device);
-    STATUS_TRY(submit(w, u.stream, u.finish));
+    STATUS_TRY(submit_traced(w, u.stream, u.finish, nullptr, 0, "poll:poll", u.device, u.ranks[0], -1));
     for (const LaneExec& l : p->lanes) {
       if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) == u.ranks.end()) continue;
       CUDA_TRY(cudaStreamWaitEvent(u.stream, w->local[l.rank]->lane_done[l.lane], 0));
@@ -89,28 +124,36 @@ Status run_ce(World* w, Plan* p) {
 Status run_sm(World* w, Plan* p) {
   for (Unit& u : p->units) {  // phase 1: readiness to sources in other units
     DeviceGuard g(u.device);
-    STATUS_TRY(submit(w, u.stream, u.start));
-    STATUS_TRY(signal_remote(w, u.start_remote_tab, u.start_remote.size(), u.stream));
+    STATUS_TRY(submit_traced(w, u.stream, u.start, u.start_remote_tab, u.start_remote.size(), "sync:signal",
+                             u.device, u.ranks[0], -1));
   }
   for (Unit& u : p->units) {  // phase 2: wait destinations, move, signal
     DeviceGuard g(u.device);
-    STATUS_TRY(submit(w, u.stream, u.sm_pre));
+    const double h0 = trace_host_now(w);
+    const int pid = u.ranks[0];
+    STATUS_TRY(submit_traced(w, u.stream, u.sm_pre, nullptr, 0, "poll:poll", u.device, pid, -1));
     if (u.table.nitems) {
+      cudaEvent_t b = trace_mark(w, u.device, u.stream);
       CUDA_TRY(launch_items(u.table, mover_grid_for(u.table, p->sms), u.stream));
       ++w->counters[4];
       ++w->counters[6];
+      trace_span(w, std::string("kernel:") + (table_name(u.table) + 5), pid, -1, u.device, b,
+                 trace_mark(w, u.device, u.stream));
     }
     if (u.red.nitems) {
+      cudaEvent_t b = trace_mark(w, u.device, u.stream);
       CUDA_TRY(launch_reduce(u.red, 4 * p->sms, u.stream));
       ++w->counters[4];
       ++w->counters[6];
+      trace_span(w, "kernel:reduce", pid, -1, u.device, b, trace_mark(w, u.device, u.stream));
     }
-    STATUS_TRY(submit(w, u.stream, u.sm_post));
-    STATUS_TRY(signal_remote(w, u.sm_post_remote_tab, u.sm_post_remote.size(), u.stream));
+    STATUS_TRY(submit_traced(w, u.stream, u.sm_post, u.sm_post_remote_tab, u.sm_post_remote.size(), "sync:signal",
+                             u.device, pid, -1));
+    trace_host_span(w, "control", h0);
   }
   for (Unit& u : p->units) {  // phase 3: incoming chunks
     DeviceGuard g(u.device);
-    STATUS_TRY(submit(w, u.stream, u.finish));
+    STATUS_TRY(submit_traced(w, u.stream, u.finish, nullptr, 0, "poll:poll", u.device, u.ranks[0], -1));
   }
   return {};
 }
@@ -137,20 +180,29 @@ Status arm_unit(World* w, Unit& u) {
 
 Status trigger_unit(World* w, Plan* p, Unit& u) {
   DeviceGuard g(u.device);
-  STATUS_TRY(issue_copies(w, u.precopy, u.stream, true));
+  const double h0 = trace_host_now(w);
+  const int pid = u.ranks[0];
+  STATUS_TRY(issue_copies_traced(w, u.precopy, u.stream, true, u.device, pid, -1));
   MemOps ops = u.start;
   ops.push_back(op_write(u.ready_flag, 1));
-  STATUS_TRY(submit(w, u.stream, ops));
-  STATUS_TRY(signal_remote(w, u.start_remote_tab, u.start_remote.size(), u.stream));
+  cudaEvent_t b = trace_mark(w, u.device, u.stream);
+  STATUS_TRY(submit_traced(w, u.stream, ops, u.start_remote_tab, u.start_remote.size(), "trigger:signal", u.device,
+                           pid, -1));
   STATUS_TRY(post_gate(u, 1));
   u.armed = false;
+  trace_host_span(w, "trigger", h0);
   if (u.nfin) {
+    cudaEvent_t pb = trace_mark(w, u.device, u.stream);
     CUDA_TRY(launch_poll(u.fin_tab, u.nfin, u.err, u.stream));
     ++w->counters[4];
     ++w->counters[6];
+    trace_span(w, "poll:poll", pid, -1, u.device, pb, trace_mark(w, u.device, u.stream));
   }
   CUDA_TRY(cudaStreamWaitEvent(u.stream, u.graph_done, 0));
   ++w->counters[6];
+  // The gated graph body (polls, copies, signals) runs on the arm stream; its
+  // span is taken from the trigger to its completion as seen by the caller.
+  trace_span(w, "copy:graph", pid, 0, u.device, b, trace_mark(w, u.device, u.stream));
   (void)p;
   return {};
 }
@@ -265,7 +317,9 @@ Status run_collective(World* w, Kind kind, Impl impl, int64_t s, const std::vect
       break;
     }
   if (!p) {
+    const double h0 = trace_host_now(w);
     STATUS_TRY(plan_create(w, kind, impl, s, args, &p));
+    trace_host_span(w, "control:compile", h0);
     w->plans.emplace_back(p);
     if (w->plans.size() > 64) {  // bounded cache: drop the oldest plan
       for (Unit& u : w->plans.front()->units) {

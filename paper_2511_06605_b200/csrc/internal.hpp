@@ -55,6 +55,12 @@ Status issue_copies(World* w, const std::vector<Copy>& copies, cudaStream_t s, b
 Status ensure_lanes(RankState* rs, int n);
 // Signal kernel for flags on other devices (see split_remote in lower.cpp).
 Status signal_remote(World* w, uint64_t** tab, size_t n, cudaStream_t s);
+// Tracing (trace.cpp); every call is a no-op unless the world traces.
+// trace_mark records a timing event on `s` (nullptr when not tracing).
+cudaEvent_t trace_mark(World* w, int device, cudaStream_t s);
+void trace_span(World* w, const std::string& name, int pid, int tid, int device, cudaEvent_t b, cudaEvent_t e);
+double trace_host_now(World* w);
+void trace_host_span(World* w, const std::string& name, double b_us);
 // Records a unit's prelaunch graph (lower.cpp).
 Status build_graph(World* w, Plan* p, Unit& u);
 

@@ -19,10 +19,14 @@ struct Addressing {
 };
 
 // Address of `mine` (a pointer of local rank `me`) in rank `target`'s
-// registered window at the same offset.
+// registered window at the same offset. The latest registration covering the
+// pointer wins (an older window over the same allocator block may still be
+// listed).
 char* translate(World* w, int me, int target, const void* mine, bool* ok) {
   const char* p = static_cast<const char*>(mine);
-  for (const Window& win : w->windows) {
+  for (auto it = w->windows.rbegin(); it != w->windows.rend(); ++it) {
+    const Window& win = *it;
+    if (!win.live) continue;
     const char* b = win.rank_base[me];
     if (b && p >= b && p < b + win.bytes && win.rank_base[target]) return win.rank_base[target] + (p - b);
   }

@@ -22,6 +22,7 @@
 #pragma once
 
 #include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -66,6 +67,7 @@ struct RankState {
 struct Window {  // a symmetric registered window: its base in every rank, as mapped here
   size_t bytes = 0;
   std::vector<char*> rank_base;
+  bool live = true;  // false once any local rank deregistered it
 };
 
 struct ProcInfoView {
@@ -74,6 +76,25 @@ struct ProcInfoView {
 };
 
 struct Plan;
+
+// Trace recording state (trace.cpp): CUDA event pairs per traced command and
+// host spans, turned into the reference's trace-event JSON at trace_end.
+struct Tracer {
+  struct Span {
+    std::string name;
+    int pid, tid, device;
+    cudaEvent_t b, e;
+  };
+  struct HostSpan {
+    std::string name;
+    double b_us, e_us;
+  };
+  std::vector<Span> spans;
+  std::vector<HostSpan> host;
+  std::vector<std::pair<cudaEvent_t, int>> events;  // every recorded event, for release
+  std::map<int, cudaEvent_t> base;                  // per device: time zero
+  std::chrono::steady_clock::time_point host0;
+};
 
 struct World {
   int nranks = 0;
@@ -88,12 +109,15 @@ struct World {
   std::vector<Window> windows;
   std::vector<int> reg_rounds;  // per local index
   std::vector<void*> ipc_opened;
+  std::vector<std::pair<void*, int>> allocs;  // cecoll_mem_alloc: pointer, device
   std::map<std::string, void*> ipc_by_handle;
   void* flag_block = nullptr;
   int first_local = 0, nlocal = 0;
   cecoll_exchange_fn exchange = nullptr;  // multi-process: kept for registration
   void* exchange_ctx = nullptr;
   int live_comms = 0;
+  std::unique_ptr<Tracer> tracer;  // non-null between cecoll_trace_begin and _end
+  std::string trace_json;          // last finished trace, until read through the C ABI
   World() {
     for (auto& c : counters) c = 0;
   }
@@ -185,6 +209,8 @@ Status gather_procs(int nranks, int first, int nlocal, int device, const cudaIpc
 void world_release(World* w);
 Status world_register(World* w, int rank, void* ptr, size_t bytes, cecoll_exchange_fn fn, void* ctx);
 Status world_deregister(World* w, void* ptr);
+Status world_mem_alloc(World* w, int rank, size_t bytes, void** out);
+Status world_mem_free(World* w, void* ptr);
 
 struct CallArgs {
   int rank;
@@ -210,6 +236,9 @@ Status plan_arm(World* w, Plan* p);
 Status plan_disarm(World* w, Plan* p);
 Status plan_launch(World* w, Plan* p, bool rearm);
 Status plan_destroy(World* w, Plan* p);
+
+Status trace_begin(World* w);
+Status trace_end(World* w, std::string* json);
 
 }  // namespace cecoll
 

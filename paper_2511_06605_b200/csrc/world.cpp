@@ -241,13 +241,63 @@ Status world_register(World* w, int rank, void* ptr, size_t bytes, cecoll_exchan
 }
 
 Status world_deregister(World* w, void* ptr) {
-  (void)ptr;
-  // Windows stay mapped until the communicator is destroyed (mappings are
-  // shared by every plan built on them).
-  return w->multiprocess ? Status{} : Status{};
+  if (!w->multiprocess) return {};  // nothing was mapped
+  // The window stops translating addresses, and cached plans (which hold the
+  // peers' mapped addresses) are dropped so a later registration at the same
+  // local address cannot reuse stale peer addresses. The IPC mappings
+  // themselves stay open until the communicator is destroyed. Explicit plans
+  // built on the window must be destroyed by the caller first.
+  bool found = false;
+  for (Window& win : w->windows) {
+    for (int k = 0; k < w->nlocal; ++k) {
+      if (win.rank_base[w->first_local + k] == ptr) {
+        win.live = false;  // symmetric: the window is gone for every rank
+        found = true;
+        break;
+      }
+    }
+  }
+  if (!found) return fail(CECOLL_NOT_REGISTERED, "cecoll_deregister: pointer is not a registered window base");
+  for (auto& p : w->plans) plan_destroy(w, p.get());
+  w->plans.clear();
+  return {};
+}
+
+Status world_mem_alloc(World* w, int rank, size_t bytes, void** out) {
+  RankState* rs = w->local[rank].get();
+  if (!rs) return fail(CECOLL_INVALID_ARGUMENT, "cecoll_mem_alloc: rank is not local");
+  DeviceGuard g(rs->device);
+  // Whole 2 MiB pages: the registered window then covers the allocation
+  // exactly (symmetric when every rank asks for the same size).
+  constexpr size_t kPage = size_t(2) << 20;
+  const size_t padded = (bytes + kPage - 1) / kPage * kPage;
+  void* p = nullptr;
+  CUDA_TRY(cudaMalloc(&p, padded));
+  Status s = world_register(w, rank, p, padded, w->exchange, w->exchange_ctx);
+  if (!s.ok()) {
+    cudaFree(p);
+    return s;
+  }
+  w->allocs.push_back({p, rs->device});
+  *out = p;
+  return {};
+}
+
+Status world_mem_free(World* w, void* ptr) {
+  auto it = std::find_if(w->allocs.begin(), w->allocs.end(), [&](const auto& a) { return a.first == ptr; });
+  if (it == w->allocs.end()) return fail(CECOLL_INVALID_ARGUMENT, "cecoll_mem_free: not a cecoll_mem_alloc pointer");
+  STATUS_TRY(world_deregister(w, ptr));
+  DeviceGuard g(it->second);
+  CUDA_TRY(cudaFree(ptr));  // synchronises with work still reading the buffer
+  w->allocs.erase(it);
+  return {};
 }
 
 void world_release(World* w) {
+  if (w->tracer) {
+    std::string discard;
+    trace_end(w, &discard);
+  }
   for (auto& p : w->plans) plan_destroy(w, p.get());
   w->plans.clear();
   // Armed explicit plans would keep their gate kernels waiting (and the
@@ -263,6 +313,10 @@ void world_release(World* w) {
     for (auto e : rs->lane_done) cudaEventDestroy(e);
     if (rs->start) cudaEventDestroy(rs->start);
     if (rs->flags && rs->owns_flags) cudaFree(rs->flags);
+  }
+  for (auto& a : w->allocs) {
+    DeviceGuard g(a.second);
+    cudaFree(a.first);
   }
   for (void* p : w->ipc_opened) cudaIpcCloseMemHandle(p);
   if (w->flag_block) cudaFree(w->flag_block);

@@ -285,3 +285,29 @@ def test_flag_protocol_under_random_delays(impl):
         torch.cuda.synchronize()
         res = [t.cpu().numpy() for t in recvs]
         assert O.check("alltoall", s, n, impl.endswith("swap"), host_in, res) == -1, it
+
+
+@pytest.mark.parametrize("kind,impl", [("allgather", "sm"), ("allgather", "bcst"), ("alltoall", "sm"),
+                                       ("alltoall", "prelaunch_pcpy")])
+def test_mem_alloc_buffers(kind, impl):
+    """cecoll_mem_alloc: library-owned registered buffers used as send/recv,
+    then freed; a second free is rejected."""
+    n, s = 8, 2 * 65536 + 80
+    cs = comms(n)
+    in_bytes = s if kind == "allgather" else n * s
+    sends = [c.mem_alloc(in_bytes) for c in cs]
+    recvs = [c.mem_alloc(n * s) for c in cs]
+    assert all(t.numel() == in_bytes for t in sends)
+    assert all(t.data_ptr() % (2 << 20) == 0 for t in sends + recvs)
+    try:
+        host_in, res, _, _ = run(kind, impl, s, n, 91, sends=sends, recvs=recvs)
+        want = [np.zeros(n * s, np.uint8) for _ in range(n)]
+        ora.Oracle().reference_result(kind, s, n, host_in, want)
+        assert all(np.array_equal(a, b) for a, b in zip(res, want))
+    finally:
+        torch.cuda.synchronize()
+        for c, a, b in zip(cs, sends, recvs):
+            c.mem_free(a)
+            c.mem_free(b)
+    with pytest.raises(cc.CecollError):
+        cs[0].mem_free(sends[0])

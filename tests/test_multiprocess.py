@@ -129,6 +129,79 @@ def _gpu_worker(rank, world, port, out):
         out.put((rank, traceback.format_exc()))
 
 
+def _alloc_worker(rank, world, port, out):
+    """Windows from cecoll_mem_alloc (auto-registered), freed and allocated
+    again between collectives."""
+    try:
+        dist = _init(rank, world, port)
+        import numpy as np
+        import torch
+
+        import paper_2511_06605_b200 as cc
+        from oracle import oracle as ora
+
+        nranks, nlocal = 4, 2
+        first = rank * nlocal
+        comms = cc.Comm.init_ranks(nranks, first, nlocal, 0, cc.torch_exchange())
+        O = ora.Oracle()
+        s = 3 * 65536 + 48
+        results = []
+        for cycle, impl in enumerate(["sm", "pcpy", "b2b", "sm"]):
+            wins = [c.mem_alloc(2 * nranks * s) for c in comms]
+            host_all = [ora.splitmix_pattern(nranks * s, r, 70 + cycle) for r in range(nranks)]
+            sends, recvs = [], []
+            for k, w in enumerate(wins):
+                w[: nranks * s].copy_(torch.from_numpy(host_all[first + k]))
+                w[nranks * s:].fill_(0xA5)
+                sends.append(w[: nranks * s])
+                recvs.append(w[nranks * s: 2 * nranks * s])
+            torch.cuda.synchronize()
+            dist.barrier()
+            cc.all_to_all(comms, sends, recvs, s, impl=impl, streams=torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            dist.barrier()
+            full = [np.zeros(nranks * s, np.uint8) for _ in range(nranks)]
+            O.reference_result("alltoall", s, nranks, host_all, full)
+            ok = all(np.array_equal(recvs[k].cpu().numpy(), full[first + k]) for k in range(nlocal))
+            results.append((cycle, impl, ok))
+            del sends, recvs
+            for c, w in zip(comms, wins):
+                c.mem_free(w)
+        # Freeing twice (or a foreign pointer) is an error, not a crash.
+        try:
+            comms[0].mem_free(wins[0])
+            results.append(("double free", "", False))
+        except cc.CecollError:
+            results.append(("double free", "", True))
+        out.put((rank, results))
+        for c in comms:
+            c.destroy()
+        dist.destroy_process_group()
+    except Exception:  # noqa: BLE001
+        out.put((rank, traceback.format_exc()))
+
+
+def _run2(target):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    return res
+
+
+@pytest.mark.gpu
+def test_two_processes_mem_alloc_windows():
+    for rank, results in _run2(_alloc_worker):
+        assert isinstance(results, list), results
+        assert len(results) == 5
+        assert all(r[2] for r in results), (rank, results)
+
+
 @pytest.mark.gpu
 def test_two_processes_share_one_gpu_through_ipc():
     ctx = mp.get_context("spawn")
