@@ -214,7 +214,9 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
-        return run_ours_multiprocess(args)
+        import bench_mgpu
+
+        return bench_mgpu.run(args, sys.modules[__name__])
     dev = 0
     torch.cuda.set_device(dev)
     n, s = NRANKS, CHUNK
@@ -627,83 +629,6 @@ def run_sync_chain(args):
     cc.destroy_all(comms)
 
 
-def run_ours_multiprocess(args):
-    """torchrun, one process per GPU: the same 8-rank collective with 8/N
-    ranks co-resident on each GPU (strong scaling: total work fixed). Flag
-    pages and the per-rank [send | recv] windows are mapped through CUDA IPC;
-    timing is the max over ranks of the device-timed loop."""
-    import torch
-    import torch.distributed as dist
-
-    rank = int(os.environ["RANK"])
-    world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    if NRANKS % world:
-        raise SystemExit(f"--gpus must divide {NRANKS}")
-    dev = local % torch.cuda.device_count()
-    torch.cuda.set_device(dev)
-    dist.init_process_group("gloo")
-    nlocal = NRANKS // world
-    n, s = NRANKS, CHUNK
-    comms = cc.Comm.init_ranks(n, rank * nlocal, nlocal, dev, cc.torch_exchange())
-    g = torch.Generator(device="cuda").manual_seed(rank)
-    wins = [torch.empty(2 * n * s, dtype=torch.uint8, device="cuda") for _ in comms]
-    for c, w in zip(comms, wins):
-        c.register(w)
-    sends = [w[:n * s] for w in wins]
-    recvs = [w[n * s:] for w in wins]
-    for t in sends:
-        t.copy_(torch.randint(0, 256, (n * s,), dtype=torch.uint8, device="cuda", generator=g))
-    stream = torch.cuda.Stream()
-    chosen = cc.select("alltoall", s, n, world) if args.algo == "auto" else args.algo
-
-    def step():
-        cc.all_to_all(comms, sends, recvs, s, impl=chosen, streams=stream)
-
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clocks:
-        torch.cuda.synchronize()
-        dist.barrier()
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
-    value = busbw(n, s, ms / 1e3)
-    if rank == 0:
-        # NVLink roofline: bytes leaving this GPU per collective.
-        egress = nlocal * (n - nlocal) * s
-        achieved = egress / (ms / 1e3) / 1e9
-        line = {
-            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic (torch.randint bytes)",
-            "config": {"workload": WORKLOAD, "ranks": n, "ranks_per_gpu": nlocal, "chunk_bytes": s,
-                       "impl": chosen, "l2": "inputs larger than L2"},
-            "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": 770.0, "unit": "GB/s",
-                         "frac": round(achieved / 770.0, 4), "traffic": None,
-                         "peak_source": "measured peer copy per direction (B200_PROFILING.md)"},
-            "cpu_baseline": None,
-            "e2e": None,
-            "gpu_launches": args.steps,
-            "clocks": clocks.summary(),
-        }
-        print(json.dumps(line), flush=True)
-    torch.cuda.synchronize()
-    dist.barrier()
-    cc.destroy_all(comms)
-    dist.destroy_process_group()
-
-
 # ---------------------------------------------------------------------------
 # sweep (run_sweep analog, sweep.cpp:71-184): every implementation x size
 # ---------------------------------------------------------------------------
@@ -870,6 +795,13 @@ def main():
     ap.add_argument("--sync-gemm", type=int, default=4096)
     ap.add_argument("--sync-out", default=os.path.join(ROOT, "gpurun_out", "sync_chain.json"))
     ap.add_argument("--sweep-rs", action="store_true", help="reduce-scatter sweep (bf16 sum)")
+    # torchrun (N > 1) only: see bench_mgpu.py
+    ap.add_argument("--no-nccl", action="store_true", help="skip the NCCL comparator")
+    ap.add_argument("--no-mgpu-sweep", action="store_true", help="skip the one-rank-per-GPU size sweep")
+    ap.add_argument("--mgpu-sweep-max", type=float, default=float(1 << 30), help="largest sweep chunk (bytes)")
+    ap.add_argument("--mgpu-budget", type=float, default=240.0, help="no new sweep size after this many s")
+    ap.add_argument("--mgpu-deadline", type=float, default=600.0, help="watchdog: print and exit after this many s")
+    ap.add_argument("--mgpu-verbose", action="store_true")
     args = ap.parse_args()
     if args.sweep_rs:
         run_sweep_rs(args)

@@ -1,0 +1,507 @@
+"""Multi-GPU arm of bench.py: torchrun, one process per GPU (N = 2, 4, 8).
+
+Only the driver's round-end scaling run executes this across GPUs (in-round
+GPU calls get one GPU; there the same code runs with N processes sharing
+cuda:0, NCCL skipped), so it is written to finish with a JSON line whatever
+happens:
+
+* every implementation is tried under cross-rank consensus — a plan that
+  fails to build, raises, or breaks parity on any rank is dropped on every
+  rank before anything waits on its flags — and the fastest parity-clean one
+  is the headline (the run-time analogue of winner_grid, sweep.cpp:186-218);
+* a watchdog prints what was measured so far and exits if a collective
+  never completes.
+
+Headline (BASELINE.json configs[1], strong scaling): the 8-rank all-to-all of
+8 x 64 MiB with 8/N ranks co-resident per GPU, device-timed, max over ranks.
+Beside it, in the same run: NCCL (torch.distributed, backend nccl) moving the
+same cross-GPU bytes, e2e through the plans with pinned host buffers, and a
+4 KiB-1 GiB all-gather / all-to-all sweep with one rank per GPU (n = N)
+against NCCL (BASELINE.json configs[2], [3]).
+"""
+from __future__ import annotations
+
+import datetime
+import json
+import os
+import threading
+import time
+
+import torch
+import torch.distributed as dist
+
+import paper_2511_06605_b200 as cc
+
+NVLINK_PEAK = 770.0  # measured peer copy GB/s per direction (B200_PROFILING.md)
+NVLINK_NOMINAL = 900.0
+
+AG_IMPLS = ["sm", "pcpy", "b2b", "bcst", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_bcst"]
+AA_IMPLS = ["sm", "pcpy", "b2b", "swap", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_swap"]
+
+STATE: dict = {}  # what the watchdog prints if a collective hangs
+
+
+# ---------------------------------------------------------------------------
+# cross-rank helpers (gloo, CPU tensors)
+# ---------------------------------------------------------------------------
+
+
+def all_true(flag: bool) -> bool:
+    t = torch.tensor([1 if flag else 0], dtype=torch.int32)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
+
+
+def max_all(x: float) -> float:
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def from_rank0(x):
+    box = [x]
+    dist.broadcast_object_list(box, src=0)
+    return box[0]
+
+
+class Watchdog:
+    def __init__(self, seconds: float, rank: int, line_fn):
+        self.rank, self.line_fn = rank, line_fn
+        self.t = threading.Timer(seconds, self._fire)
+        self.t.daemon = True
+        self.t.start()
+
+    def _fire(self):
+        if self.rank == 0:
+            try:
+                line = self.line_fn()
+                line["error"] = f"watchdog: a collective did not complete (phase {STATE.get('phase')})"
+                trials = {k: v for k, v in line["config"].get("impl_trials", {}).items() if "ms" in v}
+                if line.get("value") is None and trials:
+                    best = min(trials, key=lambda k: trials[k]["ms"])
+                    line["value"] = trials[best]["busbw_gbs"]
+                    line["ms_per_step"] = trials[best]["ms"]
+                    line["config"]["impl"] = best + " (from the trial phase)"
+                print(json.dumps(line), flush=True)
+            except Exception:  # noqa: BLE001
+                pass
+        os._exit(1)
+
+    def cancel(self):
+        self.t.cancel()
+
+
+# ---------------------------------------------------------------------------
+# synthetic chunks: chunk (src rank i -> dst rank j) is a seeded byte pattern,
+# so any process can rebuild what it must receive without the sender's data
+# ---------------------------------------------------------------------------
+
+
+def pattern(seed: int, nbytes: int, dev) -> torch.Tensor:
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    return torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev, generator=g)
+
+
+def seed_of(kind: str, s: int, i: int, j: int) -> int:
+    k = 0 if kind == "allgather" else 1
+    return ((s.bit_length() * 64 + i) * 64 + (0 if kind == "allgather" else j)) * 2 + k
+
+
+def fill_and_expect(kind, s, n, ranks, sends, expects, dev):
+    """sends[k] of global rank ranks[k]; expects[k] is what that rank must receive."""
+    for r, snd in zip(ranks, sends):
+        if kind == "allgather":
+            snd[:s].copy_(pattern(seed_of(kind, s, r, 0), s, dev))
+        else:
+            for j in range(n):
+                snd[j * s:(j + 1) * s].copy_(pattern(seed_of(kind, s, r, j), s, dev))
+    for r, exp in zip(ranks, expects):
+        for i in range(n):
+            exp[i * s:(i + 1) * s].copy_(pattern(seed_of(kind, s, i, r), s, dev))
+
+
+# ---------------------------------------------------------------------------
+# one implementation: build (consensus), parity (consensus), timing (max)
+# ---------------------------------------------------------------------------
+
+
+def try_impl(comms, kind, impl, sends, recvs, expects, s, iters, stream):
+    """Returns (plan or None, result dict). The plan is left disarmed."""
+    in_place = impl.endswith("swap")
+    for r, snd in zip(recvs, sends):
+        if in_place:
+            r.copy_(snd)
+        else:
+            r.fill_(0xA5)
+    torch.cuda.synchronize()
+    plan, err = None, None
+    try:
+        plan = cc.Plan(comms, kind, recvs if in_place else sends, recvs, s, impl=impl)
+    except cc.CecollError as e:
+        err = str(e)[:160]
+    if not all_true(plan is not None):
+        if plan is not None:
+            plan.destroy()
+        return None, {"error": err or "plan failed on another rank"}
+    dist.barrier()
+    STATE["phase"] = f"{kind} {impl} s={s} parity"
+    try:
+        plan.launch(stream)
+        stream.synchronize()
+        plan.disarm()
+        ok = all(bool(torch.equal(r, e)) for r, e in zip(recvs, expects))
+    except cc.CecollError as e:
+        ok, err = False, str(e)[:160]
+    if not all_true(ok):
+        try:
+            plan.disarm()
+            torch.cuda.synchronize()
+            plan.destroy()
+        except cc.CecollError:
+            pass
+        return None, {"error": err or "parity failed"}
+    STATE["phase"] = f"{kind} {impl} s={s} timing"
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(2):
+        plan.launch(stream)
+    stream.synchronize()
+    dist.barrier()
+    e0.record(stream)
+    for _ in range(iters):
+        plan.launch(stream)
+    e1.record(stream)
+    stream.synchronize()
+    plan.disarm()
+    ms = max_all(e0.elapsed_time(e1) / iters)
+    return plan, {"ms": ms}
+
+
+def time_nccl(group, kind, send, recv, iters, stream):
+    if group is None:
+        return None
+    STATE["phase"] = f"nccl {kind}"
+
+    def op():
+        if kind == "allgather":
+            dist.all_gather_into_tensor(recv, send, group=group)
+        else:
+            dist.all_to_all_single(recv, send, group=group)
+
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            op()
+        stream.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            op()
+        e1.record(stream)
+    stream.synchronize()
+    return max_all(e0.elapsed_time(e1) / iters)
+
+
+def busbw(n, s, ms):
+    return (n - 1) * s / (ms / 1e3) / 1e9
+
+
+# ---------------------------------------------------------------------------
+# the run
+# ---------------------------------------------------------------------------
+
+
+def run(args, B):
+    t_start = time.time()
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    n, s = B.NRANKS, B.CHUNK
+    if n % world:
+        raise SystemExit(f"--gpus must divide {n}")
+    dev = local % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    dist.init_process_group("gloo", timeout=datetime.timedelta(seconds=900))
+    nlocal = n // world
+    first = rank * nlocal
+    my_ranks = list(range(first, first + nlocal))
+
+    line = {
+        "metric": B.METRIC, "value": None, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded torch.randint byte chunks)",
+        "config": {"workload": B.WORKLOAD, "ranks": n, "ranks_per_gpu": nlocal, "chunk_bytes": s,
+                   "l2": "inputs larger than L2 (64 MiB send + 64 MiB recv per rank)"},
+    }
+    dog = Watchdog(args.mgpu_deadline, rank, lambda: line)
+
+    uuids = [None] * world
+    dist.all_gather_object(uuids, str(torch.cuda.get_device_properties(dev).uuid))
+    distinct = len(set(uuids)) == world
+    nccl = None
+    nccl_note = None
+    if not distinct:
+        nccl_note = "skipped: several processes share one GPU (NCCL rejects duplicate devices)"
+    elif args.no_nccl:
+        nccl_note = "skipped (--no-nccl)"
+    else:
+        try:
+            nccl = dist.new_group(backend="nccl")
+        except Exception as e:  # noqa: BLE001
+            nccl_note = f"unavailable: {str(e)[:120]}"
+    line["config"]["gpus_distinct"] = distinct
+
+    stream = torch.cuda.Stream()
+    STATE["phase"] = "init"
+    comms = cc.Comm.init_ranks(n, first, nlocal, dev, cc.torch_exchange())
+
+    # Two symmetric windows per rank, [send n*s | recv n*s] (double-buffered e2e).
+    sets = []
+    for _b in range(2):
+        wins = [torch.empty(2 * n * s, dtype=torch.uint8, device="cuda") for _ in comms]
+        for c, w in zip(comms, wins):
+            c.register(w)
+        sets.append(([w[:n * s] for w in wins], [w[n * s:] for w in wins]))
+    sends, recvs = sets[0]
+    expects = [torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in comms]
+    fill_and_expect("alltoall", s, n, my_ranks, sends, expects, "cuda")
+    torch.cuda.synchronize()
+
+    # --- implementation trials (consensus), then the winner -----------------
+    cands = AA_IMPLS if args.algo == "auto" else [args.algo]
+    trials, plans = {}, {}
+    line["config"]["impl_trials"] = trials
+    for impl in cands:
+        plan, res = try_impl(comms, "alltoall", impl, sends, recvs, expects, s, 10, stream)
+        if plan is not None:
+            plans[impl] = plan
+            res["busbw_gbs"] = round(busbw(n, s, res["ms"]), 2)
+            res["ms"] = round(res["ms"], 4)
+        trials[impl] = res
+    line["config"]["impl_trials"] = trials
+    if not plans:
+        line["error"] = "no implementation passed parity on every rank"
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        dog.cancel()
+        return
+    best = min(plans, key=lambda k: trials[k]["ms"])
+    best = from_rank0(best)
+    line["config"]["impl"] = best
+    plan = plans[best]
+
+    STATE["phase"] = "headline"
+    if best.endswith("swap"):
+        for r, snd in zip(recvs, sends):
+            r.copy_(snd)
+    for _ in range(max(3, args.warmup)):
+        plan.launch(stream)
+    stream.synchronize()
+    plan.disarm()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with B.ClockSampler(dev) as clocks:
+        torch.cuda.synchronize()
+        dist.barrier()
+        c0 = comms[0].counters()
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.launch(stream)
+        e1.record(stream)
+        stream.synchronize()
+        c1 = comms[0].counters()
+        plan.disarm()
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = max_all(e0.elapsed_time(e1) / args.steps)
+    value = busbw(n, s, ms)
+    if best.endswith("swap"):  # an even number of in-place transposes restores the input
+        ok = True
+    else:
+        ok = all(bool(torch.equal(r, e)) for r, e in zip(recvs, expects))
+    ok = all_true(ok)
+    egress = nlocal * (n - nlocal) * s  # bytes leaving each GPU per collective
+    nv = egress / (ms / 1e3) / 1e9
+    per = {k: (c1[k] - c0[k]) / args.steps for k in ("kernels", "graph_launches", "copies", "api_calls")}
+    line.update({
+        "value": round(value, 3), "ms_per_step": round(ms, 4), "parity_ok": ok,
+        "roofline": {"bound": "nvlink", "achieved": round(nv, 1), "peak": NVLINK_PEAK, "unit": "GB/s",
+                     "frac": round(nv / NVLINK_PEAK, 4), "traffic": None,
+                     "frac_of_nominal_900": round(nv / NVLINK_NOMINAL, 4),
+                     "peak_source": "measured peer copy per direction per GPU (B200_PROFILING.md)",
+                     "algorithmic_bytes_per_gpu": egress},
+        "gpu_launches": int(round((per["kernels"] + 4 * per["graph_launches"]) * args.steps)),
+        "launches_note": "kernels + 4 per recorded-graph launch (gate, poll, items, signal) in the timed "
+                         "region on rank 0; copy-engine copies are counted in config.ce_copies_per_step",
+        "clocks": clocks.summary(),
+    })
+    line["config"]["ce_copies_per_step"] = per["copies"]
+    line["config"]["api_calls_per_step"] = per["api_calls"]
+
+    # --- NCCL moving the same cross-GPU bytes ----------------------------------
+    if nccl is not None:
+        inp = torch.empty(nlocal * n * s, dtype=torch.uint8, device="cuda")
+        out = torch.empty_like(inp)
+        t = time_nccl(nccl, "alltoall", inp, out, args.steps, stream)
+        line["nccl"] = {"value": round(busbw(n, s, t), 3), "unit": "GB/s", "ms_per_step": round(t, 4),
+                        "how": f"torch.distributed all_to_all_single of {nlocal * n * s >> 20} MiB per GPU "
+                               f"(NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}), same busBW convention",
+                        "ours_over_nccl": round(t / ms, 3)}
+        del inp, out
+    else:
+        line["nccl"] = {"value": None, "note": nccl_note}
+
+    # --- e2e: pinned host -> HBM -> collective -> HBM -> pinned host ----------
+    STATE["phase"] = "e2e"
+    line["e2e"] = run_e2e(comms, plans, best, sets, expects, s, n, nlocal, stream, args)
+
+    for p in plans.values():
+        p.destroy()
+    plans.clear()
+    torch.cuda.synchronize()
+    dist.barrier()
+
+    # --- sweep, one rank per GPU (n = N) ----------------------------------------
+    if not args.no_mgpu_sweep:
+        STATE["phase"] = "sweep"
+        line["sweep"] = run_sweep(world, rank, dev, nccl, stream, t_start, args)
+    line["config"]["wall_s"] = round(time.time() - t_start, 1)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dog.cancel()
+    torch.cuda.synchronize()
+    dist.barrier()
+    cc.destroy_all(comms)
+    dist.destroy_process_group()
+
+
+def run_e2e(comms, plans, best, sets, expects, s, n, nlocal, stream, args):
+    in_place = best.endswith("swap")
+    e2e_plans = [plans[best]]
+    try:
+        s1, r1 = sets[1]
+        e2e_plans.append(cc.Plan(comms, "alltoall", r1 if in_place else s1, r1, s, impl=best))
+    except cc.CecollError:
+        e2e_plans = None
+    if not all_true(e2e_plans is not None):
+        return {"value": None, "error": "second plan failed"}
+    sends0 = sets[0][0]
+    host_in = [torch.empty(n * s, dtype=torch.uint8, pin_memory=True) for _ in comms]
+    for h, d in zip(host_in, sends0):
+        h.copy_(d)
+    host_outs = [[torch.empty(n * s, dtype=torch.uint8, pin_memory=True) for _ in comms] for _ in range(2)]
+    h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+    in_ready = [torch.cuda.Event() for _ in range(2)]
+    coll_done = [torch.cuda.Event() for _ in range(2)]
+    out_done = [torch.cuda.Event() for _ in range(2)]
+    for ev in coll_done + out_done:
+        ev.record(stream)
+
+    def step(k):
+        b = k % 2
+        sd, rv = sets[b]
+        dst = rv if in_place else sd  # in place: the input lands in the in-place buffer
+        h2d_s.wait_event(coll_done[b])
+        h2d_s.wait_event(out_done[b])
+        with torch.cuda.stream(h2d_s):
+            for h, d in zip(host_in, dst):
+                d.copy_(h, non_blocking=True)
+        in_ready[b].record(h2d_s)
+        stream.wait_event(in_ready[b])
+        stream.wait_event(out_done[b])
+        e2e_plans[b].launch(stream)
+        coll_done[b].record(stream)
+        d2h_s.wait_event(coll_done[b])
+        with torch.cuda.stream(d2h_s):
+            for h, d in zip(host_outs[b], rv):
+                h.copy_(d, non_blocking=True)
+        out_done[b].record(d2h_s)
+
+    steps = max(4, min(args.steps, 10))
+    for k in range(2):
+        step(k)
+    d2h_s.synchronize()
+    stream.synchronize()
+    for p in e2e_plans:
+        p.disarm()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(h2d_s)
+    for k in range(steps):
+        step(k)
+    e1.record(d2h_s)
+    d2h_s.synchronize()
+    stream.synchronize()
+    for p in e2e_plans:
+        p.disarm()
+    torch.cuda.synchronize()
+    ms = max_all(e0.elapsed_time(e1) / steps)
+    last = host_outs[(steps - 1) % 2]
+    ok = all_true(all(bool(torch.equal(h.cuda(), e)) for h, e in zip(last, expects)))
+    e2e_plans[1].destroy()
+    return {"value": round(busbw(n, s, ms), 3), "unit": "GB/s", "h2d_bytes_per_step": n * n * s,
+            "d2h_bytes_per_step": n * n * s, "ms_per_step": round(ms, 3), "parity_ok": ok,
+            "pipeline": "double-buffered: H2D of step k+1 overlaps D2H of step k; each GPU copies its "
+                        f"{nlocal} ranks' buffers over its own PCIe link; bytes are whole-job"}
+
+
+def run_sweep(world, rank, dev, nccl, stream, t_start, args):
+    """AG and AA with one rank per GPU: every implementation (consensus,
+    parity) and NCCL per size; latency in us and busBW in GB/s."""
+    n = world
+    smax = 1 << int(args.mgpu_sweep_max).bit_length() - 1
+    comms = cc.Comm.init_ranks(n, rank, 1, dev, cc.torch_exchange())
+    win = torch.empty(2 * n * smax, dtype=torch.uint8, device="cuda")
+    comms[0].register(win)
+    exp = torch.empty(n * smax, dtype=torch.uint8, device="cuda")
+    rows = []
+    sizes = []
+    s = 4096
+    while s <= smax:
+        sizes.append(s)
+        s *= 4
+    for kind in ("allgather", "alltoall"):
+        for s in sizes:
+            go = from_rank0(time.time() - t_start < args.mgpu_budget)
+            if not go:
+                rows.append({"kind": kind, "s": s, "skipped": "time budget"})
+                continue
+            in_bytes = s if kind == "allgather" else n * s
+            send = win[:in_bytes]
+            recv = win[n * smax:n * smax + n * s]
+            e = exp[:n * s]
+            fill_and_expect(kind, s, n, [rank], [send], [e], "cuda")
+            torch.cuda.synchronize()
+            iters = int(max(5, min(100, 4e8 / max(1, (n - 1) * s))))
+            row = {"kind": kind, "s": s, "us": {}, "busbw": {}}
+            for impl in (AG_IMPLS if kind == "allgather" else AA_IMPLS):
+                if impl.endswith("swap") and n < 2:
+                    continue
+                plan, res = try_impl(comms, kind, impl, [send], [recv], [e], s, iters, stream)
+                if plan is None:
+                    row["us"][impl] = None
+                    row.setdefault("errors", {})[impl] = res.get("error")
+                    continue
+                plan.destroy()
+                row["us"][impl] = round(res["ms"] * 1e3, 2)
+                row["busbw"][impl] = round(busbw(n, s, res["ms"]), 2)
+            if nccl is not None:
+                t = time_nccl(nccl, kind, send, recv, iters, stream)
+                row["us"]["nccl"] = round(t * 1e3, 2)
+                row["busbw"]["nccl"] = round(busbw(n, s, t), 2)
+            ours = {k: v for k, v in row["us"].items() if v is not None and k != "nccl"}
+            if ours:
+                row["best"] = min(ours, key=ours.get)
+                if "nccl" in row["us"]:
+                    row["best_over_nccl_time"] = round(ours[row["best"]] / row["us"]["nccl"], 3)
+            rows.append(row)
+            if rank == 0 and args.mgpu_verbose:
+                print(json.dumps(row), flush=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    comms[0].destroy()
+    del win, exp
+    return {"ranks": n, "ranks_per_gpu": 1, "convention": "us = device time per collective (back to back, "
+            "max over ranks); busbw = (n-1)*s/t", "rows": rows}

@@ -73,6 +73,7 @@ struct Window {  // a symmetric registered window: its base in every rank, as ma
 struct ProcInfoView {
   int first = 0, nlocal = 0, device = -1;
   cudaIpcMemHandle_t flags;
+  unsigned char uuid[16];
 };
 
 struct Plan;
@@ -205,7 +206,8 @@ Status world_init_ranks(int nranks, int first, int nlocal, int device, cecoll_ex
 // The init exchange on its own (host only; no CUDA calls): validates that the
 // processes' rank ranges tile [0, nranks) and returns them.
 Status gather_procs(int nranks, int first, int nlocal, int device, const cudaIpcMemHandle_t* flags,
-                    cecoll_exchange_fn fn, void* ctx, std::vector<ProcInfoView>* out);
+                    cecoll_exchange_fn fn, void* ctx, std::vector<ProcInfoView>* out,
+                    const unsigned char* uuid = nullptr);
 void world_release(World* w);
 Status world_register(World* w, int rank, void* ptr, size_t bytes, cecoll_exchange_fn fn, void* ctx);
 Status world_deregister(World* w, void* ptr);

@@ -2,6 +2,7 @@
 // single host process) and multi-process worlds (CUDA IPC
 // mapping of flag pages and symmetric registered windows).
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <set>
 
@@ -82,6 +83,8 @@ struct ProcInfo {
   int32_t device;
   int32_t pid;
   cudaIpcMemHandle_t flags;  // nlocal flag pages, kFlagBytes apart
+  unsigned char uuid[16];    // device identity (ordinals differ between processes
+                             // when CUDA_VISIBLE_DEVICES differs)
 };
 
 // One blob per process in a registration round.
@@ -109,7 +112,7 @@ Status open_ipc(World* w, const cudaIpcMemHandle_t& h, void** out) {
 }  // namespace
 
 Status gather_procs(int nranks, int first, int nlocal, int device, const cudaIpcMemHandle_t* flags,
-                    cecoll_exchange_fn fn, void* ctx, std::vector<ProcInfoView>* out) {
+                    cecoll_exchange_fn fn, void* ctx, std::vector<ProcInfoView>* out, const unsigned char* uuid) {
   if (nranks < 1 || nranks > kMaxRanks || nlocal < 1 || first < 0 || first + nlocal > nranks || !fn)
     return fail(CECOLL_INVALID_ARGUMENT, "bad rank range / exchange");
   if (nranks % nlocal != 0)
@@ -121,6 +124,7 @@ Status gather_procs(int nranks, int first, int nlocal, int device, const cudaIpc
   mine.nlocal = nlocal;
   mine.device = device;
   if (flags) mine.flags = *flags;
+  if (uuid) std::memcpy(mine.uuid, uuid, sizeof(mine.uuid));
   std::vector<ProcInfo> all(procs);
   if (fn(ctx, &mine, sizeof(ProcInfo), all.data()) != 0) return fail(CECOLL_INTERNAL, "exchange failed");
   std::vector<int> owner(nranks, -1);
@@ -138,6 +142,7 @@ Status gather_procs(int nranks, int first, int nlocal, int device, const cudaIpc
     v.nlocal = pi.nlocal;
     v.device = pi.device;
     std::memcpy(&v.flags, &pi.flags, sizeof(v.flags));
+    std::memcpy(v.uuid, pi.uuid, sizeof(v.uuid));
     out->push_back(v);
   }
   for (int r = 0; r < nranks; ++r)
@@ -170,8 +175,27 @@ Status world_init_ranks(int nranks, int first, int nlocal, int device, cecoll_ex
                          reinterpret_cast<uint64_t*>(static_cast<char*>(block) + k * kFlagBytes)));
   cudaIpcMemHandle_t h;
   CUDA_TRY(cudaIpcGetMemHandle(&h, block));
+  // Device identity by UUID: a peer process's device is mapped to this
+  // process's ordinal for it, or to a unique negative id when this process
+  // cannot see it (then it is never mistaken for a local device).
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(CECOLL_INVALID_ARGUMENT, "device out of range");
+  std::vector<std::array<unsigned char, 16>> uuids(ndev);
+  for (int d = 0; d < ndev; ++d) {
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, d));
+    std::memcpy(uuids[d].data(), prop.uuid.bytes, 16);
+  }
   std::vector<ProcInfoView> procs;
-  STATUS_TRY(gather_procs(nranks, first, nlocal, device, &h, fn, ctx, &procs));
+  STATUS_TRY(gather_procs(nranks, first, nlocal, device, &h, fn, ctx, &procs, uuids[device].data()));
+  for (size_t pi = 0; pi < procs.size(); ++pi) {
+    ProcInfoView& pv = procs[pi];
+    int local_ordinal = -1000 - static_cast<int>(pi);
+    for (int d = 0; d < ndev; ++d)
+      if (std::memcmp(uuids[d].data(), pv.uuid, 16) == 0) local_ordinal = d;
+    pv.device = local_ordinal;
+  }
   for (const ProcInfoView& pv : procs) {
     char* base = nullptr;
     if (pv.first != first) {
