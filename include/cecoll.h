@@ -190,6 +190,13 @@ cecoll_status_t cecoll_collective_n(cecoll_kind_t kind, const cecoll_comm_t* com
  * producer→collective sync chain, sim.cpp:475-499). A plan binds the ranks'
  * buffers once, records the command lists as CUDA graphs gated by trigger
  * polls, and keeps one instance armed ahead of the trigger.
+ * Plans of the other implementations (and the cached plans behind the eager
+ * calls) are recorded too: from their second launch on, each unit's whole
+ * submission — flag operations, lanes, copies, kernels — replays as one CUDA
+ * graph launched on the caller stream (one host call per collective). This
+ * applies when every unit of the plan has its own device and an explicit,
+ * non-capturing stream; otherwise, or with CECOLL_GRAPH=0, commands are
+ * submitted one by one on every launch.
  * ------------------------------------------------------------------- */
 cecoll_status_t cecoll_plan_create(const cecoll_comm_t* comms, int ncomms, cecoll_kind_t kind,
                                    const void* const* sends, void* const* recvs, size_t chunk_bytes,
@@ -223,7 +230,8 @@ cecoll_status_t cecoll_trace_end(cecoll_comm_t comm, char* json, size_t capacity
 
 /* Counters since comm creation: [0] collectives, [1] copy commands issued
  * (CE memcpys), [2] flag writes, [3] flag waits, [4] kernel launches,
- * [5] graph launches, [6] host API calls issued, [7] lanes (streams) used. */
+ * [5] prelaunch graph launches, [6] host API calls issued, [7] replays of a
+ * recorded command list (whose copies, flags and kernels count in [1]-[4]). */
 cecoll_status_t cecoll_comm_counters(cecoll_comm_t comm, int64_t out8[8]);
 
 #ifdef __cplusplus

@@ -339,8 +339,11 @@ class Comm:
     def counters(self) -> dict:
         out = (C.c_int64 * 8)()
         _check(lib().cecoll_comm_counters(self._h, out))
+        # graph_launches: prelaunch graphs (their kernels are not in `kernels`);
+        # recorded_launches: replays of a recorded command list (their kernels,
+        # copies and flag operations are counted in the other keys).
         keys = ["collectives", "copies", "flag_writes", "flag_waits", "kernels", "graph_launches", "api_calls",
-                "lanes"]
+                "recorded_launches"]
         return dict(zip(keys, list(out)))
 
     def destroy(self):

@@ -1,7 +1,9 @@
 // Executors: copy-engine lanes (pcpy / b2b / bcst / swap), the SM path,
 // prelaunch triggers, plan lifetime and the eager-call plan cache.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <set>
 
 #include "internal.hpp"
 
@@ -207,6 +209,96 @@ Status trigger_unit(World* w, Plan* p, Unit& u) {
   return {};
 }
 
+// Recorded command lists. A plan qualifies when every unit
+// has its own device (two units on one device keep the phase-ordered eager
+// submission, which never lets a poll block the queue of the signal it waits
+// for), its stream is an explicit, non-capturing stream, and nothing traces.
+bool graph_mode_wanted(World* w, Plan* p) {
+  static const bool off = [] {
+    const char* e = std::getenv("CECOLL_GRAPH");
+    return e && std::string(e) == "0";
+  }();
+  if (off || p->prelaunch || w->tracer) return false;
+  std::set<int> devs;
+  for (const Unit& u : p->units) {
+    if (!u.stream || u.stream == cudaStreamLegacy || u.stream == cudaStreamPerThread) return false;
+    if (!devs.insert(u.device).second) return false;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(u.stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+  }
+  return true;
+}
+
+void drop_recording(Plan* p) {
+  for (Unit& u : p->units) {
+    DeviceGuard g(u.device);
+    if (u.rec_exec) cudaGraphExecDestroy(u.rec_exec);
+    if (u.rec_graph) cudaGraphDestroy(u.rec_graph);
+    u.rec_exec = nullptr;
+    u.rec_graph = nullptr;
+  }
+  p->recorded = false;
+}
+
+// Captures the plan's eager submission (run_ce / run_sm) on every unit stream
+// at once — one graph per unit; lane streams join through the start / lane_done
+// events — and instantiates the graphs. Nothing executes while recording.
+Status record_plan(World* w, Plan* p) {
+  int64_t before[8];
+  for (int i = 0; i < 8; ++i) before[i] = w->counters[i];
+  size_t begun = 0;
+  Status st;
+  for (Unit& u : p->units) {
+    DeviceGuard g(u.device);
+    cudaError_t e = cudaStreamBeginCapture(u.stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+      st = cuda_fail(e, "cudaStreamBeginCapture", __FILE__, __LINE__);
+      break;
+    }
+    ++begun;
+  }
+  w->capturing = true;
+  if (st.ok()) st = p->sm ? run_sm(w, p) : run_ce(w, p);
+  w->capturing = false;
+  for (size_t i = 0; i < begun; ++i) {
+    Unit& u = p->units[i];
+    DeviceGuard g(u.device);
+    cudaGraph_t gph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(u.stream, &gph);
+    if (e != cudaSuccess && st.ok()) st = cuda_fail(e, "cudaStreamEndCapture", __FILE__, __LINE__);
+    u.rec_graph = gph;
+  }
+  for (Unit& u : p->units) {
+    if (!st.ok()) break;
+    DeviceGuard g(u.device);
+    const cudaError_t e = cudaGraphInstantiate(&u.rec_exec, u.rec_graph, 0);
+    if (e != cudaSuccess) st = cuda_fail(e, "cudaGraphInstantiate", __FILE__, __LINE__);
+  }
+  for (int i = 0; i < 8; ++i) {
+    p->rec_delta[i] = w->counters[i] - before[i];
+    w->counters[i] = before[i];  // recording submitted nothing
+  }
+  if (!st.ok()) {
+    drop_recording(p);
+    cudaGetLastError();
+    p->record_note = st.msg.empty() ? "recording failed" : st.msg;
+    return st;
+  }
+  p->recorded = true;
+  return {};
+}
+
+Status launch_recorded(World* w, Plan* p) {
+  for (Unit& u : p->units) {
+    DeviceGuard g(u.device);
+    CUDA_TRY(cudaGraphLaunch(u.rec_exec, u.stream));
+    ++w->counters[7];
+    ++w->counters[6];
+  }
+  for (int i : {1, 2, 3, 4}) w->counters[i] += p->rec_delta[i];
+  return {};
+}
+
 bool same_call(const Plan* p, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args) {
   if (p->kind != kind || p->chunk != s || p->key_rank.size() != args.size()) return false;
   if (p->impl != impl) return false;
@@ -254,8 +346,14 @@ Status plan_launch(World* w, Plan* p, bool rearm) {
     return {};
   }
   ++w->counters[0];
-  if (p->sm) return run_sm(w, p);
-  if (!p->prelaunch) return run_ce(w, p);
+  if (!p->prelaunch) {
+    // First launch eager; from the second on, one recorded graph per unit.
+    const bool want = graph_mode_wanted(w, p);
+    if (p->recorded && want) return launch_recorded(w, p);
+    if (!p->recorded && want && p->launches++ >= 1 && p->record_note.empty() && record_plan(w, p).ok())
+      return launch_recorded(w, p);
+    return p->sm ? run_sm(w, p) : run_ce(w, p);
+  }
   // prelaunch: make sure every unit is armed, trigger all, re-arm if asked.
   STATUS_TRY(plan_arm(w, p));
   for (Unit& u : p->units) STATUS_TRY(trigger_unit(w, p, u));
@@ -266,6 +364,7 @@ Status plan_launch(World* w, Plan* p, bool rearm) {
 Status plan_destroy(World* w, Plan* p) {
   Status result;
   if (p->inner) result = plan_destroy(w, p->inner.get());
+  drop_recording(p);
   for (Unit& u : p->units) {
     DeviceGuard g(u.device);
     if (u.armed) {

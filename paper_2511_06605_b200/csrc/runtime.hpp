@@ -117,6 +117,7 @@ struct World {
   cecoll_exchange_fn exchange = nullptr;  // multi-process: kept for registration
   void* exchange_ctx = nullptr;
   int live_comms = 0;
+  bool capturing = false;  // record_plan in progress: no batched memcpy (not capturable)
   std::unique_ptr<Tracer> tracer;  // non-null between cecoll_trace_begin and _end
   std::string trace_json;          // last finished trace, until read through the C ABI
   World() {
@@ -174,6 +175,10 @@ struct Unit {
   uint64_t* ready_flag = nullptr;  // device word the caller stream writes
   bool armed = false;
   uint64_t posts = 0;
+  // Recorded command list of a non-prelaunch plan (exec.cpp record_plan):
+  // the unit's whole submission (flags, lanes, copies, kernels) as one graph.
+  cudaGraph_t rec_graph = nullptr;
+  cudaGraphExec_t rec_exec = nullptr;
 };
 
 struct Plan {
@@ -195,6 +200,12 @@ struct Plan {
   int dtype = 0, op = 0;          // reduce-scatter element type / operator
   std::unique_ptr<Plan> inner;    // reduce-scatter over copy engines: the all-to-all into staging
   std::string graph_fallback;     // why a prelaunch plan runs without its graph (empty: it has one)
+  // Non-prelaunch plans are recorded into one CUDA graph per unit at their
+  // second launch and replayed afterwards (command scheduling paid once).
+  int launches = 0;
+  bool recorded = false;
+  std::string record_note;        // why recording failed (then the plan stays eager)
+  int64_t rec_delta[8] = {};      // counter increments of one recorded launch
 };
 
 void set_error(const std::string& msg);

@@ -82,7 +82,12 @@ Status issue_copies(World* w, const std::vector<Copy>& copies, cudaStream_t s, b
   const DriverApi* d = driver_api();
   // cuMemcpyBatchAsync rejects the legacy NULL stream.
   const bool legacy = s == nullptr || s == cudaStreamLegacy;
-  if (copies.size() > 1 && allow_batch && d->has_batch_memcpy && !legacy) {
+  // cuMemcpyBatchAsync cannot be captured: inside a recording (ours or the
+  // caller's stream capture) every copy becomes its own memcpy node.
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (!legacy && copies.size() > 1) cudaStreamIsCapturing(s, &cs);
+  const bool capturing = w->capturing || cs != cudaStreamCaptureStatusNone;
+  if (copies.size() > 1 && allow_batch && d->has_batch_memcpy && !legacy && !capturing) {
     std::vector<CUdeviceptr> dst, src;
     std::vector<size_t> sz;
     for (const Copy& c : copies) {

@@ -1,0 +1,130 @@
+"""Recorded command lists: non-prelaunch plans replay as one CUDA graph per
+unit from their second launch (include/cecoll.h). Every
+replay is checked against the oracle; the counters show that the replays
+happened. Also: a caller capturing an eager collective into its own CUDA
+graph (the library then submits into the capture)."""
+import numpy as np
+import pytest
+
+import paper_2511_06605_b200 as cc
+from oracle import oracle as ora
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+IMPLS = {"allgather": ["sm", "pcpy", "b2b", "bcst"], "alltoall": ["sm", "pcpy", "b2b", "swap"]}
+CASES = [(k, i) for k in IMPLS for i in IMPLS[k]]
+
+
+def _bufs(kind, n, s, impl):
+    in_bytes = s if kind == "allgather" else n * s
+    sends = [torch.empty(in_bytes, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    recvs = sends if impl.endswith("swap") else [torch.empty(n * s, dtype=torch.uint8, device="cuda")
+                                                 for _ in range(n)]
+    return in_bytes, sends, recvs
+
+
+def _load(sends, recvs, in_bytes, n, seed, in_place):
+    host = [ora.splitmix_pattern(in_bytes, r, seed) for r in range(n)]
+    for t, h in zip(sends, host):
+        t.copy_(torch.from_numpy(h))
+    if not in_place:
+        for t in recvs:
+            t.fill_(0xA5)
+    return host
+
+
+@pytest.mark.parametrize("n", [4, 8])
+@pytest.mark.parametrize("kind,impl", CASES)
+def test_eager_calls_replay_recorded_lists(kind, impl, n):
+    s = 8192 + 16
+    comms = cc.Comm.init_all([0] * n)
+    O = ora.Oracle()
+    st = torch.cuda.Stream()
+    in_place = impl.endswith("swap")
+    try:
+        in_bytes, sends, recvs = _bufs(kind, n, s, impl)
+        fn = cc.all_gather if kind == "allgather" else cc.all_to_all
+        c0 = comms[0].counters()
+        for it in range(5):
+            host = _load(sends, recvs, in_bytes, n, 300 + it, in_place)
+            torch.cuda.synchronize()
+            fn(comms, sends, recvs, s, impl=impl, streams=st)
+            st.synchronize()
+            res = [t.cpu().numpy() for t in recvs]
+            assert O.check(kind, s, n, in_place, host, res) == -1, (kind, impl, it)
+        c1 = comms[0].counters()
+        # first call eager, calls 2..5 replay one recorded graph (one unit)
+        assert c1["recorded_launches"] - c0["recorded_launches"] == 4
+        assert c1["collectives"] - c0["collectives"] == 5
+    finally:
+        torch.cuda.synchronize()
+        cc.destroy_all(comms)
+
+
+@pytest.mark.parametrize("kind,impl", [("alltoall", "pcpy"), ("alltoall", "sm"), ("allgather", "b2b")])
+def test_explicit_plan_replays_and_rebinds_streams(kind, impl):
+    n, s = 4, 65536 + 48
+    comms = cc.Comm.init_all([0] * n)
+    O = ora.Oracle()
+    try:
+        in_bytes, sends, recvs = _bufs(kind, n, s, impl)
+        plan = cc.Plan(comms, kind, sends, recvs, s, impl=impl)
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        for it in range(6):
+            host = _load(sends, recvs, in_bytes, n, 400 + it, False)
+            torch.cuda.synchronize()
+            st = streams[it % 2]  # a replay may run on another stream than the recording
+            plan.launch(st)
+            st.synchronize()
+            res = [t.cpu().numpy() for t in recvs]
+            assert O.check(kind, s, n, False, host, res) == -1, (kind, impl, it)
+        plan.destroy()
+    finally:
+        torch.cuda.synchronize()
+        cc.destroy_all(comms)
+
+
+def test_per_rank_streams_stay_eager():
+    # Several units on one device keep the phase-ordered submission.
+    n, s = 4, 4096
+    comms = cc.Comm.init_all([0] * n)
+    try:
+        sends = [torch.zeros(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+        recvs = [torch.zeros(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+        streams = [torch.cuda.Stream() for _ in range(n)]
+        c0 = comms[0].counters()
+        for _ in range(3):
+            cc.all_to_all(comms, sends, recvs, s, impl="pcpy", streams=streams)
+        torch.cuda.synchronize()
+        assert comms[0].counters()["recorded_launches"] == c0["recorded_launches"]
+    finally:
+        cc.destroy_all(comms)
+
+
+@pytest.mark.parametrize("impl", ["sm", "pcpy", "b2b"])
+def test_caller_captures_eager_collective(impl):
+    n, s = 4, 32768
+    comms = cc.Comm.init_all([0] * n)
+    O = ora.Oracle()
+    try:
+        in_bytes, sends, recvs = _bufs("alltoall", n, s, impl)
+        st = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        _load(sends, recvs, in_bytes, n, 1, False)
+        # warm-up outside the capture: the plan (device tables) is built here
+        cc.all_to_all(comms, sends, recvs, s, impl=impl, streams=st)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=st):
+            cc.all_to_all(comms, sends, recvs, s, impl=impl, streams=st)
+        for it in range(3):
+            host = _load(sends, recvs, in_bytes, n, 500 + it, False)
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            res = [t.cpu().numpy() for t in recvs]
+            assert O.check("alltoall", s, n, False, host, res) == -1, (impl, it)
+        del g
+    finally:
+        torch.cuda.synchronize()
+        cc.destroy_all(comms)
