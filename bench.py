@@ -271,7 +271,7 @@ def run_ours(args):
     host_out = [torch.empty(n * s, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
     for h, d in zip(host_in, sends):
         h.copy_(d)
-    e2e_steps = max(4, min(args.steps, 10))
+    e2e_steps = max(4, args.steps)
     # Two device buffer sets so that step k's device->host copy overlaps step
     # k+1's host->device copy (PCIe is full duplex); every step still copies
     # its inputs in and its results out inside the timed region.

@@ -202,6 +202,59 @@ def time_nccl(group, kind, send, recv, iters, stream):
     return max_all(e0.elapsed_time(e1) / iters)
 
 
+def topology(dev: int, world: int) -> dict:
+    """What the box offers beyond what one-GPU development boxes show: copy
+    engines, switch multicast (NVLS; a probe cuMulticastCreate for N devices),
+    peer access, active NVLink links. Reported for the next design round."""
+    import ctypes as C
+
+    out: dict = {"visible_gpus": torch.cuda.device_count()}
+    try:
+        cu = C.CDLL("libcuda.so.1")
+        cu.cuInit(0)
+        d = C.c_int()
+        cu.cuDeviceGet(C.byref(d), dev)
+        for name, attr in (("async_engine_count", 40), ("multicast_supported", 132)):
+            v = C.c_int(-1)
+            cu.cuDeviceGetAttribute(C.byref(v), attr, d)
+            out[name] = v.value
+
+        class McProp(C.Structure):
+            _fields_ = [("numDevices", C.c_uint), ("size", C.c_size_t), ("handleTypes", C.c_ulonglong),
+                        ("flags", C.c_ulonglong)]
+
+        for ht, label in ((1, "posix_fd"), (8, "fabric")):
+            prop = McProp(world, 2 << 20, ht, 0)
+            h = C.c_ulonglong()
+            r = cu.cuMulticastCreate(C.byref(h), C.byref(prop))
+            out[f"multicast_create_{label}_n{world}"] = int(r)
+            if r == 0:
+                cu.cuMemRelease(h)
+    except Exception as e:  # noqa: BLE001
+        out["cuda_probe_error"] = str(e)[:120]
+    try:
+        out["peer_access"] = all(torch.cuda.can_device_access_peer(dev, o)
+                                 for o in range(torch.cuda.device_count()) if o != dev)
+    except Exception:  # noqa: BLE001
+        pass
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+        active = 0
+        for link in range(18):
+            try:
+                active += int(pynvml.nvmlDeviceGetNvLinkState(h, link) == 1)
+            except Exception:  # noqa: BLE001
+                break
+        out["nvlink_active_links"] = active
+        out["driver"] = pynvml.nvmlSystemGetDriverVersion()
+    except Exception:  # noqa: BLE001
+        pass
+    return out
+
+
 def busbw(n, s, ms):
     return (n - 1) * s / (ms / 1e3) / 1e9
 
@@ -250,6 +303,8 @@ def run(args, B):
         except Exception as e:  # noqa: BLE001
             nccl_note = f"unavailable: {str(e)[:120]}"
     line["config"]["gpus_distinct"] = distinct
+    if rank == 0:
+        line["topology"] = topology(dev, world)
 
     stream = torch.cuda.Stream()
     STATE["phase"] = "init"
@@ -418,7 +473,7 @@ def run_e2e(comms, plans, best, sets, expects, s, n, nlocal, stream, args):
                 h.copy_(d, non_blocking=True)
         out_done[b].record(d2h_s)
 
-    steps = max(4, min(args.steps, 10))
+    steps = max(4, args.steps)
     for k in range(2):
         step(k)
     d2h_s.synchronize()
