@@ -133,10 +133,14 @@ Status run_sm(World* w, Plan* p) {
     DeviceGuard g(u.device);
     const double h0 = trace_host_now(w);
     const int pid = u.ranks[0];
-    STATUS_TRY(submit_traced(w, u.stream, u.sm_pre, nullptr, 0, "poll:poll", u.device, pid, -1));
+    if (!u.fused) STATUS_TRY(submit_traced(w, u.stream, u.sm_pre, nullptr, 0, "poll:poll", u.device, pid, -1));
     if (u.table.nitems) {
       cudaEvent_t b = trace_mark(w, u.device, u.stream);
-      CUDA_TRY(launch_items(u.table, mover_grid_for(u.table, p->sms), u.stream));
+      CUDA_TRY(launch_items(u.table, mover_grid_for(u.table, p->sms), u.stream, u.fused ? &u.sm_flags : nullptr));
+      if (u.fused) {
+        w->counters[2] += u.sm_flags.nsig;
+        w->counters[3] += u.sm_flags.npoll;
+      }
       ++w->counters[4];
       ++w->counters[6];
       trace_span(w, std::string("kernel:") + (table_name(u.table) + 5), pid, -1, u.device, b,
@@ -149,8 +153,9 @@ Status run_sm(World* w, Plan* p) {
       ++w->counters[6];
       trace_span(w, "kernel:reduce", pid, -1, u.device, b, trace_mark(w, u.device, u.stream));
     }
-    STATUS_TRY(submit_traced(w, u.stream, u.sm_post, u.sm_post_remote_tab, u.sm_post_remote.size(), "sync:signal",
-                             u.device, pid, -1));
+    if (!u.fused)
+      STATUS_TRY(submit_traced(w, u.stream, u.sm_post, u.sm_post_remote_tab, u.sm_post_remote.size(), "sync:signal",
+                               u.device, pid, -1));
     trace_host_span(w, "control", h0);
   }
   for (Unit& u : p->units) {  // phase 3: incoming chunks
@@ -180,19 +185,30 @@ Status arm_unit(World* w, Unit& u) {
   return {};
 }
 
-Status trigger_unit(World* w, Plan* p, Unit& u) {
+// Trigger phase 1 (signals): the unit's start / ready writes and the host
+// post that opens its armed graph.
+Status trigger_signal(World* w, Unit& u, cudaEvent_t* span_begin) {
   DeviceGuard g(u.device);
   const double h0 = trace_host_now(w);
   const int pid = u.ranks[0];
   STATUS_TRY(issue_copies_traced(w, u.precopy, u.stream, true, u.device, pid, -1));
   MemOps ops = u.start;
   ops.push_back(op_write(u.ready_flag, 1));
-  cudaEvent_t b = trace_mark(w, u.device, u.stream);
+  *span_begin = trace_mark(w, u.device, u.stream);
   STATUS_TRY(submit_traced(w, u.stream, ops, u.start_remote_tab, u.start_remote.size(), "trigger:signal", u.device,
                            pid, -1));
   STATUS_TRY(post_gate(u, 1));
   u.armed = false;
   trace_host_span(w, "trigger", h0);
+  return {};
+}
+
+// Trigger phase 2 (polls): incoming done flags and the graph's completion.
+// Submitted for every unit only after every unit's phase 1, so a poll never
+// sits ahead of a signal it waits for in a shared hardware queue (§3.2).
+Status trigger_wait(World* w, Unit& u, cudaEvent_t span_begin) {
+  DeviceGuard g(u.device);
+  const int pid = u.ranks[0];
   if (u.nfin) {
     cudaEvent_t pb = trace_mark(w, u.device, u.stream);
     CUDA_TRY(launch_poll(u.fin_tab, u.nfin, u.err, u.stream));
@@ -204,8 +220,7 @@ Status trigger_unit(World* w, Plan* p, Unit& u) {
   ++w->counters[6];
   // The gated graph body (polls, copies, signals) runs on the arm stream; its
   // span is taken from the trigger to its completion as seen by the caller.
-  trace_span(w, "copy:graph", pid, 0, u.device, b, trace_mark(w, u.device, u.stream));
-  (void)p;
+  trace_span(w, "copy:graph", pid, 0, u.device, span_begin, trace_mark(w, u.device, u.stream));
   return {};
 }
 
@@ -356,7 +371,9 @@ Status plan_launch(World* w, Plan* p, bool rearm) {
   }
   // prelaunch: make sure every unit is armed, trigger all, re-arm if asked.
   STATUS_TRY(plan_arm(w, p));
-  for (Unit& u : p->units) STATUS_TRY(trigger_unit(w, p, u));
+  std::vector<cudaEvent_t> spans(p->units.size(), nullptr);
+  for (size_t i = 0; i < p->units.size(); ++i) STATUS_TRY(trigger_signal(w, p->units[i], &spans[i]));
+  for (size_t i = 0; i < p->units.size(); ++i) STATUS_TRY(trigger_wait(w, p->units[i], spans[i]));
   if (rearm) STATUS_TRY(plan_arm(w, p));
   return {};
 }

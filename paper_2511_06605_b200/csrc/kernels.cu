@@ -16,6 +16,64 @@ namespace cecoll {
 namespace {
 
 // ---------------------------------------------------------------------------
+// Flags (kernel side of the flag protocol)
+// ---------------------------------------------------------------------------
+
+constexpr unsigned long long kPollTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Fused prologue (thread 0 of a CTA): wait for every incoming flag.
+__device__ __forceinline__ void fused_wait(const FlagSet& f) {
+  for (int i = 0; i < f.npoll; ++i) {
+    const uint64_t* p = f.polls[i];
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(p) < 1) {
+      if (globaltimer() - t0 > kPollTimeoutNs) {
+        atomicOr(reinterpret_cast<unsigned long long*>(f.err), 1ull);
+        break;
+      }
+      __nanosleep(32);
+    }
+  }
+}
+
+// Fused epilogue (thread 0 of a CTA, after the CTA's data writes are
+// complete: bar.sync for the register mover, bulk wait_group + proxy fence
+// for TMA). With outgoing signals the CTA's writes are published by one
+// system-scope release fence before its ticket; the last CTA's acq_rel
+// ticket then orders every CTA's writes (and its own resets) before the
+// st.release.sys signals — the barrier-then-one-thread-fence pattern, no
+// fence per thread. Without signals nothing outside this unit waits on the
+// data, and the kernel boundary publishes it: no system fence at all (they
+// cost several microseconds each when every CTA issues them).
+__device__ __forceinline__ void fused_finish(const FlagSet& f) {
+  if (f.nsig) asm volatile("fence.acq_rel.sys;" ::: "memory");
+  unsigned ticket;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(ticket) : "l"(f.ctr) : "memory");
+  if (ticket != gridDim.x - 1) return;
+  *f.ctr = 0;
+  // Every CTA passed its polls before taking its ticket: reset them for the
+  // next collective (its writers only write again after our signals).
+  for (int i = 0; i < f.npoll; ++i) *f.polls[i] = 0;
+  for (int i = 0; i < f.nsig; ++i) st_release_sys(f.sigs[i], 1);
+}
+
+// ---------------------------------------------------------------------------
 // Register mover
 // ---------------------------------------------------------------------------
 
@@ -158,9 +216,10 @@ __device__ __forceinline__ int find_item(const int* first, int nitems, int tile)
 
 template <int kKinds, int kMinBlocks>
 __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
-    reg_items_kernel(const Item* __restrict__ items, int nitems, int ntiles) {
+    reg_items_kernel(const Item* __restrict__ items, int nitems, int ntiles, FlagSet flags) {
   __shared__ int first[kMaxItemsSmem];
   for (int i = threadIdx.x; i < nitems; i += kRegThreads) first[i] = items[i].first_tile;
+  if (flags.npoll && threadIdx.x == 0) fused_wait(flags);
   __syncthreads();
   int cur = find_item(first, nitems, blockIdx.x);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -169,6 +228,10 @@ __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
     const int64_t off = static_cast<int64_t>(tile - it.first_tile) * kRegTile;
     const int64_t rem = it.bytes - off;
     move_tile<kKinds>(it, off, rem < kRegTile ? rem : kRegTile);
+  }
+  if (flags.ctr) {
+    __syncthreads();  // every thread's stores (peer stores over NVLink included) precede thread 0's fence
+    if (threadIdx.x == 0) fused_finish(flags);
   }
 }
 
@@ -185,13 +248,14 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 }
 
 __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict__ items, int nitems, int ntiles,
-                                                          int evict_first) {
+                                                          int evict_first, FlagSet flags) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ int first[kMaxItemsSmem];
   for (int i = threadIdx.x; i < nitems; i += 32) first[i] = items[i].first_tile;
   __syncwarp();
   if (threadIdx.x != 0) return;
+  if (flags.npoll) fused_wait(flags);
   for (int i = 0; i < kTmaStages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[i])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 
@@ -269,29 +333,17 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
     }
   }
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (flags.ctr) {
+    // The bulk stores are complete; order them (async proxy) before the
+    // generic-proxy fence and ticket that publish them.
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    fused_finish(flags);
+  }
 }
 
 // ---------------------------------------------------------------------------
 // Flag kernels
 // ---------------------------------------------------------------------------
-
-constexpr unsigned long long kPollTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 
 __global__ void poll_kernel(uint64_t* const* flags, int n, uint64_t* err) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -365,7 +417,8 @@ int mover_grid_for(const ItemTable& t, int sms) {
   return mover_grid(t.mover, sms);
 }
 
-cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream) {
+cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream, const FlagSet* fp) {
+  const FlagSet flags = fp ? *fp : FlagSet{};
   if (t.nitems <= 0 || t.ntiles <= 0) return cudaSuccess;
   if (t.nitems > kMaxItemsSmem) return cudaErrorInvalidValue;
   if (grid > t.ntiles) grid = t.ntiles;
@@ -382,14 +435,14 @@ cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream) {
       const char* e = std::getenv("CECOLL_TMA_EVICT_FIRST");
       return e ? std::atoi(e) : 0;
     }();
-    tma_items_kernel<<<grid, 32, kTmaSmem, stream>>>(t.items, t.nitems, t.ntiles, evict_first);
+    tma_items_kernel<<<grid, 32, kTmaSmem, stream>>>(t.items, t.nitems, t.ntiles, evict_first, flags);
   } else if (t.kinds == (1 << kItemCopy)) {
-    reg_items_kernel<(1 << kItemCopy), 2><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems, t.ntiles);
+    reg_items_kernel<(1 << kItemCopy), 2><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems, t.ntiles, flags);
   } else if (!(t.kinds & ((1 << kItemSwap) | (1 << kItemFan)))) {
     reg_items_kernel<(1 << kItemCopy) | (1 << kItemBcst), 2><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems,
-                                                                                              t.ntiles);
+                                                                                              t.ntiles, flags);
   } else {
-    reg_items_kernel<15, 1><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems, t.ntiles);
+    reg_items_kernel<15, 1><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems, t.ntiles, flags);
   }
   return cudaGetLastError();
 }

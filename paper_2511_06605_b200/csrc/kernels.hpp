@@ -58,7 +58,24 @@ int mover_grid(Mover m, int sms);
 // Grid for one table (honours CECOLL_SM_TILES_PER_CTA).
 int mover_grid_for(const ItemTable& t, int sms);
 
-cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream);
+// Flag work fused into an item kernel (one launch instead of poll kernel /
+// memops -> mover -> signal kernel / memops). Before moving, thread 0 of
+// every CTA waits for polls[i] >= 1 (ld.acquire.sys, 20 s bound: on timeout
+// *err |= 1 and it proceeds). After its tiles, every CTA fences (system
+// scope) and takes a ticket on *ctr; the last CTA resets *ctr and every
+// polls[i] to 0 (all CTAs have passed their polls by then), then writes
+// sigs[i] = 1 with st.release.sys. Tables and ctr live in device memory;
+// ctr starts at 0.
+struct FlagSet {
+  uint64_t* const* polls = nullptr;
+  int npoll = 0;
+  uint64_t* const* sigs = nullptr;
+  int nsig = 0;
+  unsigned* ctr = nullptr;
+  uint64_t* err = nullptr;
+};
+
+cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream, const FlagSet* flags = nullptr);
 
 // Reduce-scatter reduction: dst[e] = op over srcs[0..nsrc)
 // in source order of src[e], accumulated in fp32 and rounded once (RNE) to

@@ -184,6 +184,54 @@ Status split_remote(World* w, Plan* p) {
 }
 
 
+// Zeroed device words for a fused kernel: [0] err (u64), [1] ticket counter.
+Status alloc_fused_words(Plan* p, int device, uint64_t** err, unsigned** ctr) {
+  DeviceGuard g(device);
+  void* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, 64));
+  CUDA_TRY(cudaMemset(d, 0, 64));
+  p->dev_allocs.push_back(d);
+  p->dev_alloc_device.push_back(device);
+  *err = static_cast<uint64_t*>(d);
+  *ctr = reinterpret_cast<unsigned*>(static_cast<uint64_t*>(d) + 1);
+  return {};
+}
+
+bool fusion_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CECOLL_FUSED");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
+// SM path: the unit's rdy polls and done signals move into its item kernel.
+Status fuse_sm_flags(World* w, Plan* p) {
+  (void)w;
+  if (!fusion_enabled()) return {};
+  for (Unit& u : p->units) {
+    if (!u.table.nitems || u.red.nitems) continue;
+    std::vector<uint64_t*> polls, sigs;
+    for (const auto& op : u.sm_pre)
+      if (op.operation == CU_STREAM_MEM_OP_WAIT_VALUE_64) polls.push_back(reinterpret_cast<uint64_t*>(op.waitValue.address));
+    for (const auto& op : u.sm_post) sigs.push_back(reinterpret_cast<uint64_t*>(op.writeValue.address));
+    sigs.insert(sigs.end(), u.sm_post_remote.begin(), u.sm_post_remote.end());
+    if (polls.empty() && sigs.empty()) continue;  // nothing to fuse: plain kernel
+    uint64_t** pt = nullptr;
+    uint64_t** st = nullptr;
+    STATUS_TRY(upload_ptrs(p, u.device, polls, &pt));
+    STATUS_TRY(upload_ptrs(p, u.device, sigs, &st));
+    u.sm_flags.polls = pt;
+    u.sm_flags.npoll = static_cast<int>(polls.size());
+    u.sm_flags.sigs = st;
+    u.sm_flags.nsig = static_cast<int>(sigs.size());
+    STATUS_TRY(alloc_fused_words(p, u.device, &u.sm_flags.err, &u.sm_flags.ctr));
+    u.err = u.sm_flags.err;  // plan_destroy reports poll timeouts from here
+    u.fused = true;
+  }
+  return {};
+}
+
 }  // namespace
 
 
@@ -433,6 +481,7 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
       STATUS_TRY(upload_items(p, p->units[ui].device, unit_items[ui], &p->units[ui].table));
   }
   STATUS_TRY(split_remote(w, p));
+  if (p->sm) STATUS_TRY(fuse_sm_flags(w, p));
   if (p->prelaunch)
     for (Unit& u : p->units) {
       const Status gs = build_graph(w, p, u);
@@ -719,6 +768,12 @@ Status build_graph(World* w, Plan* p, Unit& u) {
   // Body: poll -> fork lanes -> join -> signal.
   CUDA_TRY(cudaStreamBeginCaptureToGraph(u.arm, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   Status st;
+  // The body's waits stay in one-CTA poll kernels: an armed instance runs
+  // ahead of the caller stream, and a full-grid mover spinning on its flags
+  // could hold every SM that the caller's own poll kernel (on which those
+  // flags transitively depend) needs — measured as a deadlock with eight
+  // units on one GPU. The SM path fuses its flags instead (fuse_sm_flags):
+  // there everything a kernel waits for precedes it in stream order.
   auto body_ops = [&]() -> Status {
     CUDA_TRY(launch_poll(u.poll_tab, u.npoll, u.err, u.arm));
     for (const Copy& c : u.placement) CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, u.arm));

@@ -156,6 +156,10 @@ struct Unit {
   std::vector<uint64_t*> start_remote, sm_post_remote;  // other-device flags (signal kernel)
   uint64_t** start_remote_tab = nullptr;
   uint64_t** sm_post_remote_tab = nullptr;
+  // SM path with the flag work fused into the item kernel (kernels.hpp
+  // FlagSet): device tables of the sm_pre poll and sm_post signal addresses.
+  bool fused = false;
+  FlagSet sm_flags;
   std::vector<Copy> placement;    // local-slot placement (verifier.cpp:40-44)
   std::vector<Copy> precopy;      // swap with send != recv: send -> recv first
   ItemTable table;                // SM path: every chunk of the unit's ranks

@@ -128,3 +128,30 @@ def test_caller_captures_eager_collective(impl):
     finally:
         torch.cuda.synchronize()
         cc.destroy_all(comms)
+
+
+@pytest.mark.timeout(180)
+@pytest.mark.parametrize("impl", ["sm", "prelaunch_b2b", "prelaunch_pcpy"])
+@pytest.mark.parametrize("s", [256 << 10, 1 << 20])
+def test_many_units_back_to_back(impl, s):
+    """Eight units on one GPU (one stream per rank: flags between all of
+    them), many collectives in flight. Regression for a resource deadlock: a
+    full-grid mover spinning on flags inside an armed prelaunch graph could
+    hold every SM that a caller-stream poll kernel needed (DESIGN.md §3.4);
+    the SM path's fused kernel is safe by stream order (§3.5)."""
+    n = 8
+    comms = cc.Comm.init_all([0] * n)
+    O = ora.Oracle()
+    try:
+        in_bytes, sends, recvs = _bufs("allgather", n, s, impl)
+        host = _load(sends, recvs, in_bytes, n, 600, False)
+        streams = [torch.cuda.Stream() for _ in range(n)]
+        torch.cuda.synchronize()
+        for _ in range(30):
+            cc.all_gather(comms, sends, recvs, s, impl=impl, streams=streams)
+        torch.cuda.synchronize()
+        res = [t.cpu().numpy() for t in recvs]
+        assert O.check("allgather", s, n, False, host, res) == -1
+    finally:
+        torch.cuda.synchronize()
+        cc.destroy_all(comms)

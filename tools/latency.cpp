@@ -1,7 +1,9 @@
 // Small-message latency of every implementation through the C ABI, from C++
 // (no Python in the loop): the library's own control cost per collective.
 //
-//   tools/latency [nranks] [iters]      (GPU box; ranks co-resident on GPU 0)
+//   tools/latency [nranks] [iters] [per_rank_streams] [impl-filter]
+//     (GPU box; ranks co-resident on GPU 0; per_rank_streams=1 gives every
+//      rank its own stream: one unit per rank, flags between all of them)
 //
 // Prints CSV: api,impl,collective,size_bytes,device_us_b2b,device_us_isolated,host_us
 #include <cuda_runtime.h>
@@ -34,8 +36,13 @@
   } while (0)
 
 int main(int argc, char** argv) {
+  // As the Python package does: give the driver its maximum number of
+  // hardware queues before the context exists.
+  setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
   const int n = argc > 1 ? std::atoi(argv[1]) : 8;
   const int iters = argc > 2 ? std::atoi(argv[2]) : 500;
+  const bool per_rank = argc > 3 && std::atoi(argv[3]) != 0;
+  const std::string only = argc > 4 ? argv[4] : "";
   CK(cudaSetDevice(0));
   std::vector<int> devs(n, 0);
   std::vector<cecoll_comm_t> comms(n);
@@ -43,6 +50,33 @@ int main(int argc, char** argv) {
   cudaStream_t stream;
   CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   std::vector<void*> streams(n, stream);
+  std::vector<cudaEvent_t> joins(n);
+  for (int r = 0; r < n; ++r) {
+    CK(cudaEventCreateWithFlags(&joins[r], cudaEventDisableTiming));
+    if (per_rank && r > 0) {
+      cudaStream_t sr;
+      CK(cudaStreamCreateWithFlags(&sr, cudaStreamNonBlocking));
+      streams[r] = sr;
+    }
+  }
+  // Fork the rank streams off `stream` after e0 / join them before e1.
+  auto fork = [&]() {
+    if (!per_rank) return;
+    CK(cudaEventRecord(joins[0], stream));
+    for (int r = 1; r < n; ++r) CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(streams[r]), joins[0], 0));
+  };
+  // Not cudaDeviceSynchronize: an armed prelaunch plan keeps its gate kernel
+  // waiting on the device until the next launch.
+  auto sync_all = [&]() {
+    for (int r = 0; r < n; ++r) CK(cudaStreamSynchronize(static_cast<cudaStream_t>(streams[r])));
+  };
+  auto join = [&]() {
+    if (!per_rank) return;
+    for (int r = 1; r < n; ++r) {
+      CK(cudaEventRecord(joins[r], static_cast<cudaStream_t>(streams[r])));
+      CK(cudaStreamWaitEvent(stream, joins[r], 0));
+    }
+  };
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -59,6 +93,7 @@ int main(int argc, char** argv) {
   for (int kind = 0; kind < 2; ++kind) {
     for (size_t s = 4096; s <= max_s; s *= 4) {
       for (const char* name : names) {
+        if (!only.empty() && only != name) continue;
         const cecoll_impl_t impl = cecoll_parse_impl(name);
         if (!cecoll_impl_valid_for(impl, static_cast<cecoll_kind_t>(kind))) continue;
         const bool in_place = std::string(name).find("swap") != std::string::npos;
@@ -77,10 +112,12 @@ int main(int argc, char** argv) {
             CC(cecoll_plan_create(comms.data(), n, static_cast<cecoll_kind_t>(kind), send.data(), rv.data(), s, impl,
                                   &plan));
           for (int i = 0; i < 10; ++i) call();
-          CK(cudaStreamSynchronize(stream));
+          sync_all();
           auto h0 = std::chrono::steady_clock::now();
           CK(cudaEventRecord(e0, stream));
+          fork();
           for (int i = 0; i < iters; ++i) call();
+          join();
           CK(cudaEventRecord(e1, stream));
           auto h1 = std::chrono::steady_clock::now();
           CK(cudaStreamSynchronize(stream));
@@ -88,9 +125,11 @@ int main(int argc, char** argv) {
           CK(cudaEventElapsedTime(&ms_b2b, e0, e1));
           std::vector<float> iso;
           for (int i = 0; i < 20; ++i) {
-            CK(cudaStreamSynchronize(stream));
+            sync_all();
             CK(cudaEventRecord(e0, stream));
+            fork();
             call();
+            join();
             CK(cudaEventRecord(e1, stream));
             CK(cudaStreamSynchronize(stream));
             float ms = 0;
@@ -104,7 +143,7 @@ int main(int argc, char** argv) {
                       host_us);
           std::fflush(stdout);
           if (plan) CC(cecoll_plan_destroy(plan));
-          CK(cudaStreamSynchronize(stream));
+          sync_all();
         }
       }
     }
