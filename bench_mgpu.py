@@ -72,10 +72,15 @@ class Watchdog:
         self.t.start()
 
     def _fire(self):
+        phase = str(STATE.get("phase"))
+        in_experiments = phase.startswith("experiment")
         if self.rank == 0:
             try:
                 line = self.line_fn()
-                line["error"] = f"watchdog: a collective did not complete (phase {STATE.get('phase')})"
+                if in_experiments:  # the main measurement is complete
+                    line.setdefault("experiments", {})["hung"] = phase
+                else:
+                    line["error"] = f"watchdog: a collective did not complete (phase {phase})"
                 trials = {k: v for k, v in line["config"].get("impl_trials", {}).items() if "ms" in v}
                 if line.get("value") is None and trials:
                     best = min(trials, key=lambda k: trials[k]["ms"])
@@ -85,7 +90,7 @@ class Watchdog:
                 print(json.dumps(line), flush=True)
             except Exception:  # noqa: BLE001
                 pass
-        os._exit(1)
+        os._exit(0 if in_experiments else 1)
 
     def cancel(self):
         self.t.cancel()
@@ -420,7 +425,12 @@ def run(args, B):
     # --- sweep, one rank per GPU (n = N) ----------------------------------------
     if not args.no_mgpu_sweep:
         STATE["phase"] = "sweep"
-        line["sweep"] = run_sweep(world, rank, dev, nccl, stream, t_start, args)
+        line["sweep"] = {"rows": []}
+        line["sweep"] = run_sweep(world, rank, dev, nccl, stream, t_start, args, line["sweep"]["rows"])
+    if not args.no_mgpu_experiments:
+        STATE["phase"] = "experiments"
+        line["experiments"] = {}
+        run_experiments(comms, sets, n, s, my_ranks, stream, line["experiments"])
     line["config"]["wall_s"] = round(time.time() - t_start, 1)
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -502,7 +512,7 @@ def run_e2e(comms, plans, best, sets, expects, s, n, nlocal, stream, args):
                         f"{nlocal} ranks' buffers over its own PCIe link; bytes are whole-job"}
 
 
-def run_sweep(world, rank, dev, nccl, stream, t_start, args):
+def run_sweep(world, rank, dev, nccl, stream, t_start, args, rows):
     """AG and AA with one rank per GPU: every implementation (consensus,
     parity) and NCCL per size; latency in us and busBW in GB/s."""
     n = world
@@ -511,7 +521,6 @@ def run_sweep(world, rank, dev, nccl, stream, t_start, args):
     win = torch.empty(2 * n * smax, dtype=torch.uint8, device="cuda")
     comms[0].register(win)
     exp = torch.empty(n * smax, dtype=torch.uint8, device="cuda")
-    rows = []
     sizes = []
     s = 4096
     while s <= smax:
@@ -560,3 +569,88 @@ def run_sweep(world, rank, dev, nccl, stream, t_start, args):
     del win, exp
     return {"ranks": n, "ranks_per_gpu": 1, "convention": "us = device time per collective (back to back, "
             "max over ranks); busbw = (n-1)*s/t", "rows": rows}
+
+
+# ---------------------------------------------------------------------------
+# experiments: design questions only a multi-GPU node can answer, run after
+# every main result is in the line (a hang here prints the line and exits 0)
+# ---------------------------------------------------------------------------
+
+EXPERIMENTS = [
+    # (name, kind, impl, environment read at plan creation)
+    ("sm_peer_tma", "alltoall", "sm", {"CECOLL_PEER_TMA": "1"}),
+    ("sm_peer_tma", "allgather", "sm", {"CECOLL_PEER_TMA": "1"}),
+    ("pcpy_memop_signals", "alltoall", "pcpy", {"CECOLL_REMOTE_SIGNAL": "memop"}),
+    ("b2b_memop_signals", "alltoall", "b2b", {"CECOLL_REMOTE_SIGNAL": "memop"}),
+    ("pcpy_memop_signals", "allgather", "pcpy", {"CECOLL_REMOTE_SIGNAL": "memop"}),
+]
+
+
+def guarded_trial(comms, kind, impl, sends, recvs, expects, s, iters, stream):
+    """try_impl's protocol with every local failure caught, so every rank runs
+    the same sequence of gloo collectives whatever happens on one of them."""
+    plan, ok, err, ms = None, True, None, float("inf")
+    try:
+        for r in recvs:
+            r.fill_(0xA5)
+        torch.cuda.synchronize()
+        plan = cc.Plan(comms, kind, sends, recvs, s, impl=impl)
+    except Exception as e:  # noqa: BLE001
+        ok, err = False, str(e)[:160]
+    ok = all_true(ok)
+    if ok:
+        try:
+            plan.launch(stream)
+            stream.synchronize()
+            ok = all(bool(torch.equal(r, e)) for r, e in zip(recvs, expects))
+            err = None if ok else "parity failed"
+        except Exception as e:  # noqa: BLE001
+            ok, err = False, str(e)[:160]
+    ok = all_true(ok)
+    if ok:
+        try:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for _ in range(2):
+                plan.launch(stream)
+            stream.synchronize()
+            e0.record(stream)
+            for _ in range(iters):
+                plan.launch(stream)
+            e1.record(stream)
+            stream.synchronize()
+            ms = e0.elapsed_time(e1) / iters
+        except Exception as e:  # noqa: BLE001
+            ok, err = False, str(e)[:160]
+    ok = all_true(ok)
+    ms = max_all(ms)
+    try:
+        if plan is not None:
+            plan.destroy()
+    except Exception:  # noqa: BLE001
+        pass
+    return ({"ms": round(ms, 4), "busbw_gbs": round(busbw(comms[0].nranks, s, ms), 2)}
+            if ok else {"error": err or "failed on another rank"})
+
+
+def run_experiments(comms, sets, n, s, my_ranks, stream, out):
+    sends, recvs = sets[0]
+    expects = [torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in comms]
+    filled = None
+    for name, kind, impl, env in EXPERIMENTS:
+        STATE["phase"] = f"experiments {name} {kind}"
+        if filled != kind:
+            fill_and_expect(kind, s, n, my_ranks, sends, expects, "cuda")
+            torch.cuda.synchronize()
+            filled = kind
+        snd = [t[:s] for t in sends] if kind == "allgather" else sends
+        saved = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            res = guarded_trial(comms, kind, impl, snd, recvs, expects, s, 10, stream)
+        finally:
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        out[f"{name}/{kind}"] = res

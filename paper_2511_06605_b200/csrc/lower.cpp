@@ -65,6 +65,10 @@ Status upload_items(Plan* p, int device, std::vector<HostItem>& host, ItemTable*
     return fail(CECOLL_INVALID_ARGUMENT, "too many chunk transfers for one launch");
   DeviceGuard g(device);
   bool tma = true;
+  // CECOLL_PEER_TMA=1 (read per plan): TMA bulk stores into peer-device
+  // memory too (measured only on a multi-GPU node; default: register mover).
+  const char* pt = std::getenv("CECOLL_PEER_TMA");
+  const bool peer_tma = pt && std::string(pt) == "1";
   int kinds = 0;
   size_t nfan = 0;
   for (const HostItem& h : host) {
@@ -72,7 +76,8 @@ Status upload_items(Plan* p, int device, std::vector<HostItem>& host, ItemTable*
     kinds |= 1 << it.kind;
     uintptr_t a = reinterpret_cast<uintptr_t>(it.src) | reinterpret_cast<uintptr_t>(it.dst);
     for (char* f : h.fan) a |= reinterpret_cast<uintptr_t>(f);
-    tma &= (it.kind == kItemCopy || it.kind == kItemFan) && (a & 15) == 0 && (it.bytes & 15) == 0 && !h.remote;
+    tma &= (it.kind == kItemCopy || it.kind == kItemFan) && (a & 15) == 0 && (it.bytes & 15) == 0 &&
+           (!h.remote || peer_tma);
     nfan += h.fan.size();
   }
   const char* env = std::getenv("CECOLL_MOVER");
@@ -169,6 +174,11 @@ void split_writes(World* w, int device, MemOps& ops, std::vector<uint64_t*>& rem
 }
 
 Status split_remote(World* w, Plan* p) {
+  // CECOLL_REMOTE_SIGNAL=memop (read per plan): peer-device flags are written
+  // by stream memory operations too, so the copy-engine path launches no
+  // kernel at all (measured only on a multi-GPU node; default: signal kernel).
+  const char* rs = std::getenv("CECOLL_REMOTE_SIGNAL");
+  if (rs && std::string(rs) == "memop") return {};
   for (Unit& u : p->units) {
     split_writes(w, u.device, u.start, u.start_remote);
     split_writes(w, u.device, u.sm_post, u.sm_post_remote);
