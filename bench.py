@@ -803,6 +803,7 @@ def main():
     ap.add_argument("--mgpu-deadline", type=float, default=600.0, help="watchdog: print and exit after this many s")
     ap.add_argument("--mgpu-verbose", action="store_true")
     ap.add_argument("--no-mgpu-experiments", action="store_true", help="skip the multi-GPU design experiments")
+    ap.add_argument("--no-mgpu-interference", action="store_true", help="skip the multi-GPU GEMM interference phase")
     args = ap.parse_args()
     if args.sweep_rs:
         run_sweep_rs(args)

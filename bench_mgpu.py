@@ -427,6 +427,10 @@ def run(args, B):
         STATE["phase"] = "sweep"
         line["sweep"] = {"rows": []}
         line["sweep"] = run_sweep(world, rank, dev, nccl, stream, t_start, args, line["sweep"]["rows"])
+    if not args.no_mgpu_interference and from_rank0(time.time() - t_start < args.mgpu_budget + 120):
+        STATE["phase"] = "interference"
+        line["interference"] = {}
+        run_interference(world, rank, dev, nccl, stream, args, line["interference"])
     if not args.no_mgpu_experiments:
         STATE["phase"] = "experiments"
         line["experiments"] = {}
@@ -569,6 +573,118 @@ def run_sweep(world, rank, dev, nccl, stream, t_start, args, rows):
     del win, exp
     return {"ranks": n, "ranks_per_gpu": 1, "convention": "us = device time per collective (back to back, "
             "max over ranks); busbw = (n-1)*s/t", "rows": rows}
+
+
+# ---------------------------------------------------------------------------
+# interference (BASELINE.json configs[4]): FSDP-style all-gather of bf16
+# shards beside back-to-back cuBLAS bf16 GEMMs, one rank per GPU
+# ---------------------------------------------------------------------------
+
+
+def run_interference(world, rank, dev, nccl, stream, args, out):
+    n = world
+    s = int(args.interference_chunk)
+    N = 8192
+    iters = 40
+    comms = cc.Comm.init_ranks(n, rank, 1, dev, cc.torch_exchange())
+    win = torch.empty((n + 1) * s, dtype=torch.uint8, device="cuda")
+    comms[0].register(win)
+    send, recv = win[:s], win[s:(n + 1) * s]
+    exp = torch.empty(n * s, dtype=torch.uint8, device="cuda")
+    fill_and_expect("allgather", s, n, [rank], [send], [exp], "cuda")
+    a = torch.randn(N, N, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(N, N, device="cuda", dtype=torch.bfloat16)
+    c = torch.empty(N, N, device="cuda", dtype=torch.bfloat16)
+    gs = torch.cuda.Stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def gemms(k):
+        with torch.cuda.stream(gs):
+            for _ in range(k):
+                torch.matmul(a, b, out=c)
+
+    gemms(5)
+    gs.synchronize()
+    g0, g1 = ev(), ev()
+    g0.record(gs)
+    gemms(iters)
+    g1.record(gs)
+    gs.synchronize()
+    gemm_alone = max_all(g0.elapsed_time(g1) / iters)
+    out.update({"workload": f"all-gather of {s >> 20} MiB bf16 shards x {n} GPUs beside cuBLAS bf16 {N}^3 "
+                            f"GEMMs (one rank per GPU)", "gemm_alone_ms": round(gemm_alone, 4),
+                "gemm_alone_tflops": round(2 * N ** 3 / gemm_alone / 1e9, 1), "impls": {}})
+    cands = ["pcpy", "b2b", "sm", "prelaunch_pcpy"] + (["nccl"] if nccl is not None else [])
+    for impl in cands:
+        STATE["phase"] = f"interference {impl}"
+        plan, ok, err = None, True, None
+        if impl != "nccl":
+            try:
+                recv.fill_(0xA5)
+                torch.cuda.synchronize()
+                plan = cc.Plan(comms, "allgather", [send], [recv], s, impl=impl)
+            except cc.CecollError as e:
+                ok, err = False, str(e)[:160]
+        if not all_true(ok):
+            out["impls"][impl] = {"error": err or "failed on another rank"}
+            continue
+
+        def coll():
+            if plan is None:
+                dist.all_gather_into_tensor(recv, send, group=nccl)
+            else:
+                plan.launch(stream)
+
+        with torch.cuda.stream(stream):
+            coll()
+        stream.synchronize()
+        if plan is not None:
+            plan.disarm()
+        ok = all_true(bool(torch.equal(recv, exp)))
+        if not ok:
+            out["impls"][impl] = {"error": "parity failed"}
+            if plan is not None:
+                plan.destroy()
+            continue
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                coll()
+            stream.synchronize()
+            dist.barrier()
+            c0, c1 = ev(), ev()
+            c0.record(stream)
+            for _ in range(5):
+                coll()
+            c1.record(stream)
+        stream.synchronize()
+        alone = max_all(c0.elapsed_time(c1) / 5)
+        k = int(max(4, min(400, round(iters * gemm_alone / alone))))
+        dist.barrier()
+        g0, g1, c0, c1 = ev(), ev(), ev(), ev()
+        g0.record(gs)
+        gemms(iters)
+        g1.record(gs)
+        with torch.cuda.stream(stream):
+            c0.record(stream)
+            for _ in range(k):
+                coll()
+            c1.record(stream)
+        gs.synchronize()
+        stream.synchronize()
+        if plan is not None:
+            plan.disarm()
+            torch.cuda.synchronize()
+            plan.destroy()
+        gemm_with = max_all(g0.elapsed_time(g1) / iters)
+        coll_with = max_all(c0.elapsed_time(c1) / k)
+        out["impls"][impl] = {
+            "collective_alone_ms": round(alone, 4), "collective_with_gemm_ms": round(coll_with, 4),
+            "collective_busbw_alone_gbs": round(busbw(n, s, alone), 1), "collectives": k,
+            "gemm_with_collective_ms": round(gemm_with, 4), "gemm_slowdown": round(gemm_with / gemm_alone, 3),
+            "collective_slowdown": round(coll_with / alone, 3)}
+    torch.cuda.synchronize()
+    dist.barrier()
+    comms[0].destroy()
 
 
 # ---------------------------------------------------------------------------
