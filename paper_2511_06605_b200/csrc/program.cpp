@@ -540,8 +540,12 @@ Impl reference_select(Kind kind, int64_t size) {
 // all-gather size (fan items read each source once) and all-to-all up to
 // 16 MiB chunks; above that the driver's batched copies (b2b) are ~5%
 // faster. Several devices: not measured in round 1 — the SM path for
-// latency-bound chunks, prelaunched per-peer copies (copy engines over
-// NVLink) above. CECOLL_SM_MAX_BYTES overrides the SM cutoff.
+// latency-bound chunks, per-peer copies (copy engines over NVLink, one lane
+// per peer) above; their plans replay as recorded graphs (exec.cpp), which
+// beat the gated prelaunch graphs at every measured size on one GPU
+// (profiles/sweep_r01_plan_n8_recorded.csv). CECOLL_SM_MAX_BYTES overrides
+// the SM cutoff. (bench_mgpu.py measures every implementation per size on
+// the multi-GPU node and reports the winner grid.)
 Impl select(Kind kind, int64_t size, int nranks, int ndevices) {
   (void)nranks;
   int64_t sm_max;
@@ -549,7 +553,7 @@ Impl select(Kind kind, int64_t size, int nranks, int ndevices) {
   else sm_max = int64_t{1} << 20;
   if (const char* env = std::getenv("CECOLL_SM_MAX_BYTES")) sm_max = std::atoll(env);
   if (size <= sm_max) return Impl::Sm;
-  return ndevices <= 1 ? Impl::B2b : Impl::PrelaunchPcpy;
+  return ndevices <= 1 ? Impl::B2b : Impl::Pcpy;
 }
 
 }  // namespace cecoll
