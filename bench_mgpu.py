@@ -567,12 +567,97 @@ def run_sweep(world, rank, dev, nccl, stream, t_start, args, rows):
             rows.append(row)
             if rank == 0 and args.mgpu_verbose:
                 print(json.dumps(row), flush=True)
+    # reduce-scatter, bf16 sum: the SM path (every rank reads
+    # its chunk from every peer over NVLink) against NCCL reduce_scatter.
+    for s in [x for x in (65536, 1 << 20, 16 << 20, 256 << 20) if x <= smax]:
+        if not from_rank0(time.time() - t_start < args.mgpu_budget):
+            rows.append({"kind": "reduce_scatter_bf16_sum", "s": s, "skipped": "time budget"})
+            continue
+        row = {"kind": "reduce_scatter_bf16_sum", "s": s, "us": {}, "busbw": {}}
+        rows.append(row)
+        count = s // 2
+        send, recv = win[:n * s], win[n * smax:n * smax + s]
+        row.update(rs_trial(comms, nccl, send, recv, count, n, rank, stream))
+        if rank == 0 and args.mgpu_verbose:
+            print(json.dumps(row), flush=True)
     torch.cuda.synchronize()
     dist.barrier()
     comms[0].destroy()
     del win, exp
     return {"ranks": n, "ranks_per_gpu": 1, "convention": "us = device time per collective (back to back, "
             "max over ranks); busbw = (n-1)*s/t", "rows": rows}
+
+
+def bf16_chunk(i: int, j: int, count: int) -> torch.Tensor:
+    g = torch.Generator(device="cuda")
+    g.manual_seed(((count.bit_length() * 64 + i) * 64 + j) * 2 + 7)
+    return torch.randn(count, generator=g, device="cuda").to(torch.bfloat16)
+
+
+def rs_trial(comms, nccl, send, recv, count, n, rank, stream):
+    """Reduce-scatter, bf16 sum: chunk (i -> j) is seeded, so every rank
+    rebuilds its expected result — the fp32 fold over ranks in rank order,
+    rounded once (the oracle's definition, bit-exact)."""
+    s = count * 2
+    sb, rb = send.view(torch.bfloat16), recv.view(torch.bfloat16)
+    for j in range(n):
+        sb[j * count:(j + 1) * count].copy_(bf16_chunk(rank, j, count))
+    acc = None
+    for i in range(n):
+        x = bf16_chunk(i, rank, count).float()
+        acc = x if acc is None else acc + x
+    exp = acc.to(torch.bfloat16)
+    out = {"us": {}, "busbw": {}}
+    iters = int(max(5, min(100, 4e8 / max(1, (n - 1) * s))))
+
+    def ours():
+        cc.reduce_scatter(comms, [send], [recv], count, dtype="bf16", op="sum", impl="sm", streams=stream)
+
+    ok, err = True, None
+    try:
+        recv.fill_(0)
+        torch.cuda.synchronize()
+        ours()
+        stream.synchronize()
+        ok = bool(torch.equal(rb, exp))
+        err = None if ok else "parity failed"
+    except Exception as e:  # noqa: BLE001
+        ok, err = False, str(e)[:160]
+    if all_true(ok):
+        for _ in range(2):
+            ours()
+        stream.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            ours()
+        e1.record(stream)
+        stream.synchronize()
+        ms = max_all(e0.elapsed_time(e1) / iters)
+        out["us"]["sm"] = round(ms * 1e3, 2)
+        out["busbw"]["sm"] = round(busbw(n, s, ms), 2)
+    else:
+        out["errors"] = {"sm": err or "failed on another rank"}
+    if nccl is not None:
+        STATE["phase"] = "nccl reduce_scatter"
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                dist.reduce_scatter_tensor(rb, sb, op=dist.ReduceOp.SUM, group=nccl)
+            stream.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(iters):
+                dist.reduce_scatter_tensor(rb, sb, op=dist.ReduceOp.SUM, group=nccl)
+            e1.record(stream)
+        stream.synchronize()
+        t = max_all(e0.elapsed_time(e1) / iters)
+        out["us"]["nccl"] = round(t * 1e3, 2)
+        out["busbw"]["nccl"] = round(busbw(n, s, t), 2)
+        if "sm" in out["us"]:
+            out["best_over_nccl_time"] = round(out["us"]["sm"] / out["us"]["nccl"], 3)
+    return out
 
 
 # ---------------------------------------------------------------------------
