@@ -217,6 +217,7 @@ __device__ __forceinline__ int find_item(const int* first, int nitems, int tile)
 template <int kKinds, int kMinBlocks>
 __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
     reg_items_kernel(const Item* __restrict__ items, int nitems, int ntiles, FlagSet flags) {
+  if (flags.skip && *reinterpret_cast<const volatile uint64_t*>(flags.skip)) return;
   __shared__ int first[kMaxItemsSmem];
   for (int i = threadIdx.x; i < nitems; i += kRegThreads) first[i] = items[i].first_tile;
   if (flags.npoll && threadIdx.x == 0) fused_wait(flags);
@@ -249,6 +250,7 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 
 __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict__ items, int nitems, int ntiles,
                                                           int evict_first, FlagSet flags) {
+  if (flags.skip && *reinterpret_cast<const volatile uint64_t*>(flags.skip)) return;
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ int first[kMaxItemsSmem];
@@ -384,6 +386,33 @@ __global__ void gate_kernel(volatile uint64_t* posted, uint64_t* consumed, cudaG
   cudaGraphSetConditional(handle, kind == 1 ? 1u : 0u);
 }
 
+__global__ void gate_poll_kernel(volatile uint64_t* posted, uint64_t* consumed, uint64_t* const* flags, int n,
+                                 uint64_t* skip, uint64_t* err) {
+  if (threadIdx.x != 0) return;
+  const uint64_t c = *consumed;
+  while (posted[0] <= c) __nanosleep(256);
+  const uint64_t kind = posted[1 + (c % 64)];
+  *consumed = c + 1;
+  if (kind != 1 && kind != 2) atomicOr(reinterpret_cast<unsigned long long*>(err), 2ull);
+  if (kind != 1) {
+    *skip = 1;
+    return;
+  }
+  for (int i = 0; i < n; ++i) {
+    uint64_t* f = flags[i];
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(f) < 1) {
+      if (globaltimer() - t0 > kPollTimeoutNs) {
+        atomicOr(reinterpret_cast<unsigned long long*>(err), 1ull);
+        break;
+      }
+      __nanosleep(32);
+    }
+    *f = 0;
+  }
+  *skip = 0;
+}
+
 }  // namespace
 
 int64_t mover_tile_bytes(Mover m) { return m == Mover::Tma ? kTmaTile : kRegTile; }
@@ -456,6 +485,12 @@ cudaError_t launch_poll(uint64_t* const* flags, int n, uint64_t* err, cudaStream
 cudaError_t launch_signal(uint64_t* const* flags, int n, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   signal_kernel<<<(n + 127) / 128, 128, 0, stream>>>(flags, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gate_poll(volatile uint64_t* posted, uint64_t* consumed, uint64_t* const* flags, int n,
+                             uint64_t* skip, uint64_t* err, cudaStream_t stream) {
+  gate_poll_kernel<<<1, 32, 0, stream>>>(posted, consumed, flags, n, skip, err);
   return cudaGetLastError();
 }
 

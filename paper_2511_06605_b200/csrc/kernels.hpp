@@ -73,6 +73,9 @@ struct FlagSet {
   int nsig = 0;
   unsigned* ctr = nullptr;
   uint64_t* err = nullptr;
+  // Non-null: the kernel does nothing when *skip != 0 (a cancelled
+  // prelaunch instance; written by the gate kernel before it).
+  const uint64_t* skip = nullptr;
 };
 
 cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream, const FlagSet* flags = nullptr);
@@ -117,5 +120,11 @@ cudaError_t launch_poll(uint64_t* const* flags, int n, uint64_t* err, cudaStream
 cudaError_t launch_signal(uint64_t* const* flags, int n, cudaStream_t stream);
 cudaError_t launch_gate(volatile uint64_t* posted, uint64_t* consumed, cudaGraphConditionalHandle handle,
                         uint64_t* err, cudaStream_t stream);
+//  gate_poll: the gate of a kernel-only prelaunch body (no conditional node):
+//          waits for the next host post; on "go" polls flags[0..n) (>= 1,
+//          reset to 0, as poll) and writes *skip = 0; on "cancel" writes
+//          *skip = 1 so the mover after it returns at once.
+cudaError_t launch_gate_poll(volatile uint64_t* posted, uint64_t* consumed, uint64_t* const* flags, int n,
+                             uint64_t* skip, uint64_t* err, cudaStream_t stream);
 
 }  // namespace cecoll

@@ -744,11 +744,43 @@ Status build_graph(World* w, Plan* p, Unit& u) {
   STATUS_TRY(upload_ptrs(p, u.device, sigs, &u.sig_tab));
   STATUS_TRY(upload_ptrs(p, u.device, fins, &u.fin_tab));
 
+  uint64_t* posted_dev = nullptr;
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&posted_dev), u.posted, 0));
+
+  // Kernel-only body (every chunk of the unit in its item kernel: no
+  // copy-engine lanes, no placement copies): no conditional node. A one-CTA
+  // gate_poll kernel waits for the host post and the flags (or, on cancel,
+  // sets the skip word), then the mover runs with the done signals fused in
+  // (it never spins, so it cannot hold SMs while waiting). Saves the
+  // conditional body launch and two kernel boundaries per collective.
+  // CECOLL_PRELAUNCH_COND=1 keeps the conditional form for comparison.
+  bool lanes_idle = u.placement.empty();
+  for (const LaneExec& l : p->lanes)
+    if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) != u.ranks.end() && (!l.copies.empty() || l.table.nitems))
+      lanes_idle = false;
+  const char* pc = std::getenv("CECOLL_PRELAUNCH_COND");
+  if (lanes_idle && u.table.nitems > 0 && fusion_enabled() && !(pc && std::string(pc) == "1")) {
+    FlagSet f;
+    f.sigs = u.sig_tab;
+    f.nsig = u.nsig;
+    f.err = u.err;
+    f.ctr = u.nsig ? reinterpret_cast<unsigned*>(static_cast<uint64_t*>(d) + 2) : nullptr;
+    uint64_t* skip = static_cast<uint64_t*>(d) + 3;
+    f.skip = skip;
+    CUDA_TRY(cudaStreamBeginCapture(u.arm, cudaStreamCaptureModeRelaxed));
+    cudaError_t e1 = launch_gate_poll(posted_dev, u.consumed, u.poll_tab, u.npoll, skip, u.err, u.arm);
+    cudaError_t e2 = e1 == cudaSuccess ? launch_items(u.table, mover_grid_for(u.table, p->sms), u.arm, &f) : e1;
+    const cudaError_t ec = cudaStreamEndCapture(u.arm, &u.graph);
+    CUDA_TRY(e1);
+    CUDA_TRY(e2);
+    CUDA_TRY(ec);
+    CUDA_TRY(cudaGraphInstantiate(&u.exec, u.graph, 0));
+    return {};
+  }
+
   CUDA_TRY(cudaGraphCreate(&u.graph, 0));
   cudaGraphConditionalHandle handle;
   CUDA_TRY(cudaGraphConditionalHandleCreate(&handle, u.graph, 0, cudaGraphCondAssignDefault));
-  uint64_t* posted_dev = nullptr;
-  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&posted_dev), u.posted, 0));
 
   // Root: the gate kernel.
   CUDA_TRY(cudaStreamBeginCaptureToGraph(u.arm, u.graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
