@@ -182,6 +182,47 @@ def try_impl(comms, kind, impl, sends, recvs, expects, s, iters, stream):
     return plan, {"ms": ms}
 
 
+def energy_loop(step, stream, dev, n, s, plan, seconds=1.5):
+    """J/GB over a loop of `step` on every GPU: the collective count is rank
+    0's (all ranks run the same count), energy is summed over ranks."""
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+    except Exception as e:  # noqa: BLE001
+        all_true(False)
+        return {"error": f"nvml: {str(e)[:80]}"}
+    if not all_true(True):
+        return {"error": "nvml unavailable on a rank"}
+    step()
+    stream.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(20):
+        step()
+    stream.synchronize()
+    per = max(1e-6, (time.perf_counter() - t0) / 20)
+    count = int(from_rank0(int(max(40, seconds / per))))
+    dist.barrier()
+    e0 = pynvml.nvmlDeviceGetTotalEnergyConsumption(h)
+    t0 = time.perf_counter()
+    for k in range(count):
+        step()
+        if k % 50 == 49:
+            stream.synchronize()  # bounded queue
+    stream.synchronize()
+    dt = time.perf_counter() - t0
+    e1 = pynvml.nvmlDeviceGetTotalEnergyConsumption(h)
+    if plan is not None:
+        plan.disarm()
+    t = torch.tensor([(e1 - e0) / 1e3, dt], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    joules, secs = float(t[0]), float(t[1]) / dist.get_world_size()
+    gb = n * (n - 1) * s * count / 1e9
+    return {"j_per_gb": round(joules / gb, 5), "joules": round(joules, 2), "seconds": round(secs, 3),
+            "collectives": count, "avg_power_w_per_gpu": round(joules / secs / dist.get_world_size(), 1)}
+
+
 def time_nccl(group, kind, send, recv, iters, stream):
     if group is None:
         return None
@@ -411,6 +452,22 @@ def run(args, B):
         del inp, out
     else:
         line["nccl"] = {"value": None, "note": nccl_note}
+
+    # --- NVML energy per link-equivalent GB, summed over the GPUs --------------
+    STATE["phase"] = "energy"
+    line["energy"] = {"ours": energy_loop(lambda: plan.launch(stream), stream, dev, n, s, plan)}
+    if nccl is not None:
+        inp = torch.empty(nlocal * n * s, dtype=torch.uint8, device="cuda")
+        out = torch.empty_like(inp)
+
+        def nccl_step():
+            with torch.cuda.stream(stream):
+                dist.all_to_all_single(out, inp, group=nccl)
+
+        line["energy"]["nccl"] = energy_loop(nccl_step, stream, dev, n, s, None)
+        del inp, out
+    line["energy"]["note"] = ("NVML total energy of every GPU over a >= 1.5 s loop (rank 0 decides the "
+                              "count), summed / link-equivalent bytes n(n-1)s per collective")
 
     # --- e2e: pinned host -> HBM -> collective -> HBM -> pinned host ----------
     STATE["phase"] = "e2e"
