@@ -35,8 +35,10 @@ import paper_2511_06605_b200 as cc
 NVLINK_PEAK = 770.0  # measured peer copy GB/s per direction (B200_PROFILING.md)
 NVLINK_NOMINAL = 900.0
 
-AG_IMPLS = ["sm", "pcpy", "b2b", "bcst", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_bcst"]
-AA_IMPLS = ["sm", "pcpy", "b2b", "swap", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_swap"]
+AG_IMPLS = ["sm", "pcpy", "b2b", "bcst", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_bcst", "hybrid"]
+AA_IMPLS = ["sm", "pcpy", "b2b", "swap", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_swap", "hybrid"]
+# headline trials also scan the hybrid's SM share ("impl@pct": CECOLL_HYBRID_SM_PCT at plan creation)
+HEADLINE_EXTRA = ["hybrid@25", "hybrid@75"]
 
 STATE: dict = {}  # what the watchdog prints if a collective hangs
 
@@ -141,10 +143,20 @@ def try_impl(comms, kind, impl, sends, recvs, expects, s, iters, stream):
             r.fill_(0xA5)
     torch.cuda.synchronize()
     plan, err = None, None
+    name, _, pct = impl.partition("@")
+    saved = os.environ.get("CECOLL_HYBRID_SM_PCT")
+    if pct:
+        os.environ["CECOLL_HYBRID_SM_PCT"] = pct
     try:
-        plan = cc.Plan(comms, kind, recvs if in_place else sends, recvs, s, impl=impl)
+        plan = cc.Plan(comms, kind, recvs if in_place else sends, recvs, s, impl=name)
     except cc.CecollError as e:
         err = str(e)[:160]
+    finally:
+        if pct:
+            if saved is None:
+                os.environ.pop("CECOLL_HYBRID_SM_PCT", None)
+            else:
+                os.environ["CECOLL_HYBRID_SM_PCT"] = saved
     if not all_true(plan is not None):
         if plan is not None:
             plan.destroy()
@@ -369,7 +381,7 @@ def run(args, B):
     torch.cuda.synchronize()
 
     # --- implementation trials (consensus), then the winner -----------------
-    cands = AA_IMPLS if args.algo == "auto" else [args.algo]
+    cands = AA_IMPLS + HEADLINE_EXTRA if args.algo == "auto" else [args.algo]
     trials, plans = {}, {}
     line["config"]["impl_trials"] = trials
     for impl in cands:

@@ -39,6 +39,7 @@ IMPLS = {
     "prelaunch_swap": 6,
     "prelaunch_b2b": 7,
     "sm": 8,
+    "hybrid": 9,
 }
 IMPL_NAMES = {v: k for k, v in IMPLS.items() if k != "baseline"}
 # implementations_for (compiler.cpp:77-85) + the SM path

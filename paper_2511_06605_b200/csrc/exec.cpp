@@ -134,6 +134,24 @@ Status run_sm(World* w, Plan* p) {
     const double h0 = trace_host_now(w);
     const int pid = u.ranks[0];
     if (!u.fused) STATUS_TRY(submit_traced(w, u.stream, u.sm_pre, nullptr, 0, "poll:poll", u.device, pid, -1));
+    // Hybrid: the copy-engine shares fork after the rdy polls and join
+    // before the done signals.
+    std::vector<const LaneExec*> forked;
+    if (p->hybrid) {
+      cudaEvent_t fork = w->local[u.ranks[0]]->start;
+      CUDA_TRY(cudaEventRecord(fork, u.stream));
+      ++w->counters[6];
+      for (const LaneExec& l : p->lanes) {
+        if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) == u.ranks.end()) continue;
+        RankState* rs = w->local[l.rank].get();
+        cudaStream_t ls = rs->lanes[l.lane];
+        CUDA_TRY(cudaStreamWaitEvent(ls, fork, 0));
+        STATUS_TRY(issue_copies_traced(w, l.copies, ls, false, rs->device, l.rank, l.lane));
+        CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], ls));
+        w->counters[6] += 2;
+        forked.push_back(&l);
+      }
+    }
     if (u.table.nitems) {
       cudaEvent_t b = trace_mark(w, u.device, u.stream);
       CUDA_TRY(launch_items(u.table, mover_grid_for(u.table, p->sms), u.stream, u.fused ? &u.sm_flags : nullptr));
@@ -152,6 +170,10 @@ Status run_sm(World* w, Plan* p) {
       ++w->counters[4];
       ++w->counters[6];
       trace_span(w, "kernel:reduce", pid, -1, u.device, b, trace_mark(w, u.device, u.stream));
+    }
+    for (const LaneExec* l : forked) {
+      CUDA_TRY(cudaStreamWaitEvent(u.stream, w->local[l->rank]->lane_done[l->lane], 0));
+      ++w->counters[6];
     }
     if (!u.fused)
       STATUS_TRY(submit_traced(w, u.stream, u.sm_post, u.sm_post_remote_tab, u.sm_post_remote.size(), "sync:signal",

@@ -218,7 +218,7 @@ bool fusion_enabled() {
 // SM path: the unit's rdy polls and done signals move into its item kernel.
 Status fuse_sm_flags(World* w, Plan* p) {
   (void)w;
-  if (!fusion_enabled()) return {};
+  if (!fusion_enabled() || p->hybrid) return {};  // hybrid: lanes need the rdy polls too
   for (Unit& u : p->units) {
     if (!u.table.nitems || u.red.nitems) continue;
     std::vector<uint64_t*> polls, sigs;
@@ -272,13 +272,20 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
     for (const CallArgs& a : args) in_place &= a.send == a.recv;
     impl = in_place ? Impl::Swap : select(kind, s, n, w->ndevices);
   }
-  if (impl != Impl::Sm && !valid_for(impl, kind))
+  if (impl != Impl::Sm && impl != Impl::Hybrid && !valid_for(impl, kind))
     return fail(CECOLL_UNSUPPORTED, std::string(impl_name(impl)) + " does not apply to " +
                                          (kind == Kind::AllGather ? "allgather" : "alltoall"));
   const bool in_place_impl = base_of(impl) == Impl::Swap;
   p->impl = impl;
-  p->sm = impl == Impl::Sm;
+  p->sm = impl == Impl::Sm || impl == Impl::Hybrid;
+  p->hybrid = impl == Impl::Hybrid;
   p->prelaunch = is_prelaunched(impl);
+  if (p->hybrid) {
+    const char* e = std::getenv("CECOLL_HYBRID_SM_PCT");
+    int pct = e ? std::atoi(e) : 50;
+    pct = std::max(0, std::min(100, pct));
+    p->hybrid_sm_bytes = (s * pct / 100) & ~int64_t{15};
+  }
 
   // Addresses of every rank's buffers as usable from this process.
   Addressing ad;
@@ -394,7 +401,52 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
       if (src != dst) u.placement.push_back({dst, src, s});
     }
 
-  if (p->sm) {
+  if (p->hybrid) {
+    // Each chunk: bytes [0, ce) by a copy-engine lane (lane d-1 of rank r
+    // carries the chunk to (r+d)%n, the pcpy rotation of compiler.cpp:150),
+    // bytes [ce, s) by the unit's SM mover; the local slot entirely by the
+    // mover. Flags are the SM path's (unit-level rdy polls before the lanes
+    // fork, done signals after they join).
+    const int64_t sm_b = p->hybrid_sm_bytes, ce = s - sm_b;
+    for (Unit& u : p->units) {
+      std::vector<HostItem> items;
+      for (int r : u.ranks) {
+        const char* src_ag = ad.send[r];
+        for (const Copy& c : u.placement)
+          if (c.dst == ad.recv[r] + r * s) items.push_back({make_item(kItemCopy, c.src, c.dst, nullptr, c.bytes), {}});
+        if (kind == Kind::AllGather && sm_b > 0) {
+          HostItem h{make_item(kItemFan, src_ag + ce, nullptr, nullptr, sm_b), {}};
+          for (int d = 1; d < n; ++d) {
+            const int j = (r + d) % n;
+            h.fan.push_back(ad.recv[j] + r * s + ce);
+            h.remote |= w->device[j] != u.device;
+          }
+          if (h.fan.size() == 1) h.item = make_item(kItemCopy, src_ag + ce, h.fan[0], nullptr, sm_b), h.fan.clear();
+          items.push_back(h);
+        }
+        for (int d = 1; d < n; ++d) {
+          const int j = (r + d) % n;
+          const char* src = kind == Kind::AllGather ? src_ag : ad.send[r] + j * s;
+          char* dst = ad.recv[j] + r * s;
+          if (kind == Kind::AllToAll && sm_b > 0)
+            items.push_back({make_item(kItemCopy, src + ce, dst + ce, nullptr, sm_b), {}, w->device[j] != u.device});
+          if (ce > 0) {
+            LaneExec le;
+            le.rank = r;
+            le.lane = d - 1;
+            le.copies.push_back({dst, src, ce});
+            STATUS_TRY(ensure_lanes(w->local[r].get(), d));
+            p->lanes.push_back(std::move(le));
+          }
+        }
+      }
+      u.placement.clear();
+      STATUS_TRY(upload_items(p, u.device, items, &u.table));
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->units[0].device);
+    p->sms = sms;
+  } else if (p->sm) {
     for (Unit& u : p->units) {
       std::vector<HostItem> items;
       for (int r : u.ranks) {

@@ -28,6 +28,10 @@ enum class Impl : int {
   PrelaunchSwap = 6,
   PrelaunchB2b = 7,
   Sm = 8,
+  // B200 hybrid: each chunk is split between a copy-engine lane (the pcpy
+  // rotation, compiler.cpp:150) and the SM mover (SURVEY §7 "hybrid CE + SM
+  // lanes" fallback when copy engines alone cannot fill NVLink).
+  Hybrid = 9,
 };
 
 const char* impl_name(Impl impl);

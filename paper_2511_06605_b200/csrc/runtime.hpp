@@ -198,7 +198,9 @@ struct Plan {
   std::vector<void*> dev_allocs;
   std::vector<int> dev_alloc_device;
   Program program;
-  bool sm = false;
+  bool sm = false;       // SM path flag structure (sm, hybrid)
+  bool hybrid = false;   // + copy-engine lanes for each chunk's CE share
+  int64_t hybrid_sm_bytes = 0;  // SM share of every chunk (16-byte multiple)
   bool prelaunch = false;
   int sms = 148;
   int dtype = 0, op = 0;          // reduce-scatter element type / operator

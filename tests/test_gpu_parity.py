@@ -86,12 +86,12 @@ def test_sm_path_matches_reference_digest(d, stream_mode):
 
 
 @pytest.mark.parametrize("impl", ["pcpy", "b2b", "bcst", "swap", "prelaunch_pcpy", "prelaunch_b2b",
-                                  "prelaunch_bcst", "prelaunch_swap", "sm"])
+                                  "prelaunch_bcst", "prelaunch_swap", "sm", "hybrid"])
 @pytest.mark.parametrize("stream_mode", ["shared", "per_rank"])
 def test_repeated_calls_reuse_plans_and_flags(impl, stream_mode):
     n, s = 4, 8192 + 16
     kind = "allgather" if impl.endswith("bcst") else "alltoall"
-    if impl in ("pcpy", "b2b", "prelaunch_pcpy", "prelaunch_b2b", "sm"):
+    if impl in ("pcpy", "b2b", "prelaunch_pcpy", "prelaunch_b2b", "sm", "hybrid"):
         kinds = ["allgather", "alltoall"]
     else:
         kinds = [kind]
@@ -110,6 +110,8 @@ def test_repeated_calls_reuse_plans_and_flags(impl, stream_mode):
     ("alltoall", "b2b", 8 << 20),
     ("alltoall", "prelaunch_pcpy", 8 << 20),
     ("alltoall", "swap", 8 << 20),
+    ("alltoall", "hybrid", 8 << 20),
+    ("allgather", "hybrid", 16 << 20),
     ("allgather", "sm", 64 << 20),
     ("allgather", "bcst", 16 << 20),
     ("allgather", "prelaunch_pcpy", 16 << 20),

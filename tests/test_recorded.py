@@ -12,7 +12,7 @@ from oracle import oracle as ora
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-IMPLS = {"allgather": ["sm", "pcpy", "b2b", "bcst"], "alltoall": ["sm", "pcpy", "b2b", "swap"]}
+IMPLS = {"allgather": ["sm", "pcpy", "b2b", "bcst", "hybrid"], "alltoall": ["sm", "pcpy", "b2b", "swap", "hybrid"]}
 CASES = [(k, i) for k in IMPLS for i in IMPLS[k]]
 
 
@@ -152,6 +152,34 @@ def test_many_units_back_to_back(impl, s):
         torch.cuda.synchronize()
         res = [t.cpu().numpy() for t in recvs]
         assert O.check("allgather", s, n, False, host, res) == -1
+    finally:
+        torch.cuda.synchronize()
+        cc.destroy_all(comms)
+
+
+@pytest.mark.parametrize("pct", [0, 25, 50, 100])
+@pytest.mark.parametrize("kind", ["allgather", "alltoall"])
+@pytest.mark.parametrize("stream_mode", ["shared", "per_rank"])
+def test_hybrid_split_against_oracle(kind, pct, stream_mode, monkeypatch):
+    """Every chunk split between a copy-engine lane and the SM mover at the
+    given SM share (odd chunk size: misaligned split points), explicit plans
+    launched repeatedly, with one stream or one stream per rank (flags)."""
+    monkeypatch.setenv("CECOLL_HYBRID_SM_PCT", str(pct))
+    n, s = 4, 3 * 65536 + 40
+    comms = cc.Comm.init_all([0] * n)
+    O = ora.Oracle()
+    try:
+        in_bytes, sends, recvs = _bufs(kind, n, s, "hybrid")
+        plan = cc.Plan(comms, kind, sends, recvs, s, impl="hybrid")
+        streams = torch.cuda.Stream() if stream_mode == "shared" else [torch.cuda.Stream() for _ in range(n)]
+        for it in range(3):
+            host = _load(sends, recvs, in_bytes, n, 700 + it, False)
+            torch.cuda.synchronize()
+            plan.launch(streams)
+            torch.cuda.synchronize()
+            res = [t.cpu().numpy() for t in recvs]
+            assert O.check(kind, s, n, False, host, res) == -1, (kind, pct, it)
+        plan.destroy()
     finally:
         torch.cuda.synchronize()
         cc.destroy_all(comms)
