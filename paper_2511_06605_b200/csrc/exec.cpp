@@ -166,7 +166,11 @@ Status run_sm(World* w, Plan* p) {
     }
     if (u.red.nitems) {
       cudaEvent_t b = trace_mark(w, u.device, u.stream);
-      CUDA_TRY(launch_reduce(u.red, 4 * p->sms, u.stream));
+      CUDA_TRY(launch_reduce(u.red, 4 * p->sms, u.stream, u.fused ? &u.sm_flags : nullptr));
+      if (u.fused) {
+        w->counters[2] += u.sm_flags.nsig;
+        w->counters[3] += u.sm_flags.npoll;
+      }
       ++w->counters[4];
       ++w->counters[6];
       trace_span(w, "kernel:reduce", pid, -1, u.device, b, trace_mark(w, u.device, u.stream));

@@ -15,63 +15,7 @@ namespace cecoll {
 
 namespace {
 
-// ---------------------------------------------------------------------------
-// Flags (kernel side of the flag protocol)
-// ---------------------------------------------------------------------------
-
-constexpr unsigned long long kPollTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// Fused prologue (thread 0 of a CTA): wait for every incoming flag.
-__device__ __forceinline__ void fused_wait(const FlagSet& f) {
-  for (int i = 0; i < f.npoll; ++i) {
-    const uint64_t* p = f.polls[i];
-    const unsigned long long t0 = globaltimer();
-    while (ld_acquire_sys(p) < 1) {
-      if (globaltimer() - t0 > kPollTimeoutNs) {
-        atomicOr(reinterpret_cast<unsigned long long*>(f.err), 1ull);
-        break;
-      }
-      __nanosleep(32);
-    }
-  }
-}
-
-// Fused epilogue (thread 0 of a CTA, after the CTA's data writes are
-// complete: bar.sync for the register mover, bulk wait_group + proxy fence
-// for TMA). With outgoing signals the CTA's writes are published by one
-// system-scope release fence before its ticket; the last CTA's acq_rel
-// ticket then orders every CTA's writes (and its own resets) before the
-// st.release.sys signals — the barrier-then-one-thread-fence pattern, no
-// fence per thread. Without signals nothing outside this unit waits on the
-// data, and the kernel boundary publishes it: no system fence at all (they
-// cost several microseconds each when every CTA issues them).
-__device__ __forceinline__ void fused_finish(const FlagSet& f) {
-  if (f.nsig) asm volatile("fence.acq_rel.sys;" ::: "memory");
-  unsigned ticket;
-  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(ticket) : "l"(f.ctr) : "memory");
-  if (ticket != gridDim.x - 1) return;
-  *f.ctr = 0;
-  // Every CTA passed its polls before taking its ticket: reset them for the
-  // next collective (its writers only write again after our signals).
-  for (int i = 0; i < f.npoll; ++i) *f.polls[i] = 0;
-  for (int i = 0; i < f.nsig; ++i) st_release_sys(f.sigs[i], 1);
-}
+#include "flags.cuh"
 
 // ---------------------------------------------------------------------------
 // Register mover

@@ -107,7 +107,7 @@ struct RedTable {
 };
 
 constexpr int64_t kRedTileElems = 4096;
-cudaError_t launch_reduce(const RedTable& t, int grid, cudaStream_t stream);
+cudaError_t launch_reduce(const RedTable& t, int grid, cudaStream_t stream, const FlagSet* flags = nullptr);
 
 // Flag kernels used inside recorded (prelaunch) graphs, where stream memory
 // operations are not allowed in conditional bodies.

@@ -220,7 +220,7 @@ Status fuse_sm_flags(World* w, Plan* p) {
   (void)w;
   if (!fusion_enabled() || p->hybrid) return {};  // hybrid: lanes need the rdy polls too
   for (Unit& u : p->units) {
-    if (!u.table.nitems || u.red.nitems) continue;
+    if (!u.table.nitems && !u.red.nitems) continue;  // the mover or the reduction carries them
     std::vector<uint64_t*> polls, sigs;
     for (const auto& op : u.sm_pre)
       if (op.operation == CU_STREAM_MEM_OP_WAIT_VALUE_64) polls.push_back(reinterpret_cast<uint64_t*>(op.waitValue.address));
@@ -754,6 +754,7 @@ Status plan_create_rs(World* w, Impl impl, int64_t count, int dtype, int op, con
     STATUS_TRY(upload_red(p, u.device, items, srcs, dtype, op, &u.red));
   }
   STATUS_TRY(split_remote(w, p));
+  STATUS_TRY(fuse_sm_flags(w, p));
   *out = plan.release();
   return {};
 }

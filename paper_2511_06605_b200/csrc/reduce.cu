@@ -19,6 +19,8 @@ namespace cecoll {
 
 namespace {
 
+#include "flags.cuh"
+
 constexpr int kRedThreads = 256;
 constexpr int kElemsPerThread = static_cast<int>(kRedTileElems / kRedThreads);  // 16
 
@@ -52,13 +54,15 @@ __device__ __forceinline__ float fold(float acc, float x) {
 
 template <int kDtype, int kOp>
 __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const RedItem* __restrict__ items, int nitems,
-                                                              int ntiles) {
+                                                              int ntiles, FlagSet flags) {
   using E = Elem<kDtype>;
   using T = typename E::T;
   constexpr int kVecElems = 16 / static_cast<int>(sizeof(T));            // elements per 16-byte vector
   constexpr int kVecs = kElemsPerThread / kVecElems;                       // vectors per thread
   __shared__ int first[kMaxItemsSmem];
   for (int i = threadIdx.x; i < nitems; i += kRedThreads) first[i] = items[i].first_tile;
+  // Fused flags (kernels.hpp FlagSet): every source rank's send is ready.
+  if (flags.npoll && threadIdx.x == 0) fused_wait(flags);
   __syncthreads();
   int cur = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -107,14 +111,18 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const RedItem* __re
       for (int e = 0; e < m; ++e) q[e] = E::from_f(acc[e]);
     }
   }
+  if (flags.ctr) {  // every source read: tell the source ranks (last CTA)
+    __syncthreads();
+    if (threadIdx.x == 0) fused_finish(flags);
+  }
 }
 
 template <int kDtype>
-cudaError_t launch_dtype(const RedTable& t, int grid, cudaStream_t stream) {
+cudaError_t launch_dtype(const RedTable& t, int grid, cudaStream_t stream, const FlagSet& f) {
   switch (t.op) {
-    case kSum: reduce_kernel<kDtype, kSum><<<grid, kRedThreads, 0, stream>>>(t.items, t.nitems, t.ntiles); break;
-    case kMax: reduce_kernel<kDtype, kMax><<<grid, kRedThreads, 0, stream>>>(t.items, t.nitems, t.ntiles); break;
-    case kMin: reduce_kernel<kDtype, kMin><<<grid, kRedThreads, 0, stream>>>(t.items, t.nitems, t.ntiles); break;
+    case kSum: reduce_kernel<kDtype, kSum><<<grid, kRedThreads, 0, stream>>>(t.items, t.nitems, t.ntiles, f); break;
+    case kMax: reduce_kernel<kDtype, kMax><<<grid, kRedThreads, 0, stream>>>(t.items, t.nitems, t.ntiles, f); break;
+    case kMin: reduce_kernel<kDtype, kMin><<<grid, kRedThreads, 0, stream>>>(t.items, t.nitems, t.ntiles, f); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -122,14 +130,15 @@ cudaError_t launch_dtype(const RedTable& t, int grid, cudaStream_t stream) {
 
 }  // namespace
 
-cudaError_t launch_reduce(const RedTable& t, int grid, cudaStream_t stream) {
+cudaError_t launch_reduce(const RedTable& t, int grid, cudaStream_t stream, const FlagSet* fp) {
+  const FlagSet f = fp ? *fp : FlagSet{};
   if (t.nitems <= 0 || t.ntiles <= 0) return cudaSuccess;
   if (t.nitems > kMaxItemsSmem) return cudaErrorInvalidValue;
   if (grid > t.ntiles) grid = t.ntiles;
   switch (t.dtype) {
-    case kF32: return launch_dtype<kF32>(t, grid, stream);
-    case kBF16: return launch_dtype<kBF16>(t, grid, stream);
-    case kF16: return launch_dtype<kF16>(t, grid, stream);
+    case kF32: return launch_dtype<kF32>(t, grid, stream, f);
+    case kBF16: return launch_dtype<kBF16>(t, grid, stream, f);
+    case kF16: return launch_dtype<kF16>(t, grid, stream, f);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -120,6 +120,28 @@ def _gpu_worker(rank, world, port, out):
                 O.reference_result(kind, s, nranks, host_all, full)
                 ok = all(np.array_equal(mine[k], full[first + k]) for k in range(nlocal))
                 results.append((kind, impl, ok))
+        # reduce-scatter (SM path: every rank reads its chunk from every peer's
+        # registered send window), bf16 sum, against the oracle's rank-order fold
+        count = 4096 + 8
+        ins = [ora.splitmix_pattern(nranks * count * 2, r, 90) for r in range(nranks)]
+        for b in ins:  # finite bf16 values: clear the exponent MSB
+            b.view(np.uint16)[:] &= np.uint16(0xBFFF)
+        want = O.reduce_scatter(1, 0, count, ins)
+        wins = [torch.empty(nranks * count * 2, dtype=torch.uint8, device="cuda") for _ in comms]
+        for c, w in zip(comms, wins):
+            c.register(w)
+        for k, w in enumerate(wins):
+            w.copy_(torch.from_numpy(ins[first + k]))
+        recvs = [torch.full((count * 2,), 0xA5, dtype=torch.uint8, device="cuda") for _ in comms]
+        torch.cuda.synchronize()
+        dist.barrier()
+        for _ in range(2):
+            cc.reduce_scatter(comms, wins, recvs, count, dtype="bf16", op="sum", impl="sm",
+                              streams=torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        dist.barrier()
+        results.append(("reduce_scatter", "sm",
+                        all(np.array_equal(recvs[k].cpu().numpy(), want[first + k]) for k in range(nlocal))))
         out.put((rank, results))
         torch.cuda.synchronize()
         for c in comms:
@@ -217,4 +239,4 @@ def test_two_processes_share_one_gpu_through_ipc():
         assert isinstance(results, list), results
         bad = [r for r in results if not r[2]]
         assert not bad, (rank, bad)
-        assert len(results) == 9
+        assert len(results) == 10

@@ -71,7 +71,8 @@ def test_oracle_matches_numpy(dtype, op, n, count):
 @pytest.mark.parametrize("impl", ["sm", "pcpy", "b2b", "prelaunch_pcpy", "prelaunch_b2b"])
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
 @pytest.mark.parametrize("op", ["sum", "max"])
-@pytest.mark.parametrize("n,count,streams", [(2, 4096, "shared"), (4, 1000, "per_rank"), (8, 65536 + 24, "shared")])
+@pytest.mark.parametrize("n,count,streams", [(2, 4096, "shared"), (4, 1000, "per_rank"), (8, 65536 + 24, "shared"),
+                                             (8, 262144 + 8, "per_rank")])
 def test_gpu_matches_oracle(impl, dtype, op, n, count, streams):
     torch = pytest.importorskip("torch")
     import paper_2511_06605_b200 as cc
