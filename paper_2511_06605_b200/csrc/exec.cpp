@@ -105,20 +105,23 @@ Status run_ce(World* w, Plan* p) {
       ++w->counters[6];
       trace_span(w, table_name(l.table), l.rank, l.lane, rs->device, b, trace_mark(w, rs->device, s));
     }
-    STATUS_TRY(submit_traced(w, s, l.post, l.post_remote_tab, l.post_remote.size(), "sync:signal", rs->device,
-                             l.rank, l.lane));
+    STATUS_TRY(submit_traced(w, s, l.post, nullptr, 0, "sync:signal", rs->device, l.rank, l.lane));
     CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], s));
     ++w->counters[6];
     trace_host_span(w, "control", h0);
   }
   for (Unit& u : p->units) {
+    // Join the lanes, signal other-device destinations (one kernel), then
+    // wait for the incoming chunks.
     DeviceGuard g(u.device);
-    STATUS_TRY(submit_traced(w, u.stream, u.finish, nullptr, 0, "poll:poll", u.device, u.ranks[0], -1));
     for (const LaneExec& l : p->lanes) {
       if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) == u.ranks.end()) continue;
       CUDA_TRY(cudaStreamWaitEvent(u.stream, w->local[l.rank]->lane_done[l.lane], 0));
       ++w->counters[6];
     }
+    STATUS_TRY(submit_traced(w, u.stream, {}, u.lanes_remote_tab, u.lanes_remote.size(), "sync:signal", u.device,
+                             u.ranks[0], -1));
+    STATUS_TRY(submit_traced(w, u.stream, u.finish, nullptr, 0, "poll:poll", u.device, u.ranks[0], -1));
   }
   return {};
 }

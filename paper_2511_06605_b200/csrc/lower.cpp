@@ -157,13 +157,13 @@ int flag_device(World* w, const uint64_t* addr) {
 // peer-mapped page) rather than a stream memory operation, the portable way
 // to signal across NVLink. Same-device pages (also across processes) keep
 // the memop.
-void split_writes(World* w, int device, MemOps& ops, std::vector<uint64_t*>& remote) {
+void split_writes(World* w, int device, MemOps& ops, std::vector<uint64_t*>& remote, bool force) {
   MemOps keep;
   for (const auto& op : ops) {
     if (op.operation == CU_STREAM_MEM_OP_WRITE_VALUE_64) {
       uint64_t* a = reinterpret_cast<uint64_t*>(op.writeValue.address);
       const int d = flag_device(w, a);
-      if (d >= 0 && d != device) {
+      if (force || (d >= 0 && d != device)) {
         remote.push_back(a);
         continue;
       }
@@ -179,17 +179,25 @@ Status split_remote(World* w, Plan* p) {
   // kernel at all (measured only on a multi-GPU node; default: signal kernel).
   const char* rs = std::getenv("CECOLL_REMOTE_SIGNAL");
   if (rs && std::string(rs) == "memop") return {};
+  // CECOLL_FORCE_REMOTE_SIGNALS=1 (read per plan; tests): every cross-unit
+  // signal takes the other-device path, so one GPU exercises it.
+  const char* fr = std::getenv("CECOLL_FORCE_REMOTE_SIGNALS");
+  const bool force = fr && std::string(fr) == "1";
   for (Unit& u : p->units) {
-    split_writes(w, u.device, u.start, u.start_remote);
-    split_writes(w, u.device, u.sm_post, u.sm_post_remote);
+    split_writes(w, u.device, u.start, u.start_remote, force);
+    split_writes(w, u.device, u.sm_post, u.sm_post_remote, force);
     STATUS_TRY(upload_ptrs(p, u.device, u.start_remote, &u.start_remote_tab));
     STATUS_TRY(upload_ptrs(p, u.device, u.sm_post_remote, &u.sm_post_remote_tab));
   }
   for (LaneExec& l : p->lanes) {
     const int dev = w->device[l.rank];
-    split_writes(w, dev, l.post, l.post_remote);
-    STATUS_TRY(upload_ptrs(p, dev, l.post_remote, &l.post_remote_tab));
+    std::vector<uint64_t*> remote;
+    split_writes(w, dev, l.post, remote, force);
+    for (Unit& u : p->units)
+      if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) != u.ranks.end())
+        u.lanes_remote.insert(u.lanes_remote.end(), remote.begin(), remote.end());
   }
+  for (Unit& u : p->units) STATUS_TRY(upload_ptrs(p, u.device, u.lanes_remote, &u.lanes_remote_tab));
   return {};
 }
 
@@ -786,8 +794,8 @@ Status build_graph(World* w, Plan* p, Unit& u) {
     for (const auto& op : le.pre)
       if (op.operation == CU_STREAM_MEM_OP_WAIT_VALUE_64) polls.push_back(reinterpret_cast<uint64_t*>(op.waitValue.address));
     for (const auto& op : le.post) sigs.push_back(reinterpret_cast<uint64_t*>(op.writeValue.address));
-    sigs.insert(sigs.end(), le.post_remote.begin(), le.post_remote.end());
   }
+  sigs.insert(sigs.end(), u.lanes_remote.begin(), u.lanes_remote.end());
   for (const auto& op : u.finish)
     if (op.operation == CU_STREAM_MEM_OP_WAIT_VALUE_64) fins.push_back(reinterpret_cast<uint64_t*>(op.waitValue.address));
   u.npoll = static_cast<int>(polls.size());

@@ -139,11 +139,9 @@ struct LaneExec {
   MemOps pre;                 // rdy polls (+ resets) for destinations in other units
   std::vector<Copy> copies;   // copy commands
   ItemTable table;            // Broadcast / Swap commands (no copy-engine form)
-  MemOps post;                // done signals to destinations in other units
-  // Signals whose flag page lives on another device are written by a signal
-  // kernel (st.release.sys over NVLink) instead of a stream memory operation.
-  std::vector<uint64_t*> post_remote;
-  uint64_t** post_remote_tab = nullptr;
+  MemOps post;                // done signals to destinations in other units (same device)
+  // (signals whose flag page lives on another device are the unit's
+  // lanes_remote: one signal kernel after the lanes join)
 };
 
 struct Unit {
@@ -156,6 +154,11 @@ struct Unit {
   std::vector<uint64_t*> start_remote, sm_post_remote;  // other-device flags (signal kernel)
   uint64_t** start_remote_tab = nullptr;
   uint64_t** sm_post_remote_tab = nullptr;
+  // The lanes' done signals to other-device flags, written by one signal
+  // kernel on the unit stream after the lanes join (one kernel per unit
+  // instead of one per lane; a destination waits for all its sources anyway).
+  std::vector<uint64_t*> lanes_remote;
+  uint64_t** lanes_remote_tab = nullptr;
   // SM path with the flag work fused into the item kernel (kernels.hpp
   // FlagSet): device tables of the sm_pre poll and sm_post signal addresses.
   bool fused = false;

@@ -183,3 +183,34 @@ def test_hybrid_split_against_oracle(kind, pct, stream_mode, monkeypatch):
     finally:
         torch.cuda.synchronize()
         cc.destroy_all(comms)
+
+
+@pytest.mark.parametrize("impl", ["pcpy", "b2b", "bcst", "swap", "sm", "hybrid", "prelaunch_pcpy",
+                                  "prelaunch_b2b", "prelaunch_swap"])
+def test_other_device_signal_path_on_one_gpu(impl, monkeypatch):
+    """CECOLL_FORCE_REMOTE_SIGNALS=1 sends every cross-unit signal down the
+    other-device path (signal kernels with st.release.sys; the lanes' done
+    signals as one kernel per unit after the join) — the path a multi-GPU
+    node takes — with one stream per rank so every transfer is flagged."""
+    monkeypatch.setenv("CECOLL_FORCE_REMOTE_SIGNALS", "1")
+    n, s = 4, 65536 + 32
+    kinds = ["allgather"] if impl.endswith("bcst") else ["alltoall"] if impl.endswith("swap") else \
+        ["allgather", "alltoall"]
+    comms = cc.Comm.init_all([0] * n)
+    O = ora.Oracle()
+    try:
+        for kind in kinds:
+            in_place = impl.endswith("swap")
+            in_bytes, sends, recvs = _bufs(kind, n, s, impl)
+            streams = [torch.cuda.Stream() for _ in range(n)]
+            fn = cc.all_gather if kind == "allgather" else cc.all_to_all
+            for it in range(4):
+                host = _load(sends, recvs, in_bytes, n, 800 + it, in_place)
+                torch.cuda.synchronize()
+                fn(comms, sends, recvs, s, impl=impl, streams=streams)
+                torch.cuda.synchronize()
+                res = [t.cpu().numpy() for t in recvs]
+                assert O.check(kind, s, n, in_place, host, res) == -1, (kind, impl, it)
+    finally:
+        torch.cuda.synchronize()
+        cc.destroy_all(comms)
