@@ -77,8 +77,10 @@ def test_exchange_over_gloo_world2():
         assert uneven == "rejected"
 
 
-def _gpu_worker(rank, world, port, out):
+def _gpu_worker(rank, world, port, out, force_remote=False):
     try:
+        if force_remote:  # every cross-process signal down the other-device path (signal kernels)
+            os.environ["CECOLL_FORCE_REMOTE_SIGNALS"] = "1"
         dist = _init(rank, world, port)
         import numpy as np
         import torch
@@ -225,11 +227,12 @@ def test_two_processes_mem_alloc_windows():
 
 
 @pytest.mark.gpu
-def test_two_processes_share_one_gpu_through_ipc():
+@pytest.mark.parametrize("force_remote", [False, True])
+def test_two_processes_share_one_gpu_through_ipc(force_remote):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q, force_remote)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
