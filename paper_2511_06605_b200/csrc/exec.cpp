@@ -128,6 +128,10 @@ Status run_ce(World* w, Plan* p) {
 
 Status run_sm(World* w, Plan* p) {
   for (Unit& u : p->units) {  // phase 1: readiness to sources in other units
+    if (u.start_folded) {     // written by the fused kernel itself
+      w->counters[2] += u.sm_flags.npre;
+      continue;
+    }
     DeviceGuard g(u.device);
     STATUS_TRY(submit_traced(w, u.stream, u.start, u.start_remote_tab, u.start_remote.size(), "sync:signal",
                              u.device, u.ranks[0], -1));

@@ -21,8 +21,11 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Fused prologue (thread 0 of a CTA): wait for every incoming flag.
+// Fused prologue (thread 0 of a CTA): CTA 0 first writes the folded start
+// signals, then every CTA waits for every incoming flag.
 __device__ __forceinline__ void fused_wait(const FlagSet& f) {
+  if (blockIdx.x == 0)
+    for (int i = 0; i < f.npre; ++i) st_release_sys(f.pre[i], 1);
   for (int i = 0; i < f.npoll; ++i) {
     const uint64_t* p = f.polls[i];
     const unsigned long long t0 = globaltimer();

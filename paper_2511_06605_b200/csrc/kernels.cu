@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
   if (flags.skip && *reinterpret_cast<const volatile uint64_t*>(flags.skip)) return;
   __shared__ int first[kMaxItemsSmem];
   for (int i = threadIdx.x; i < nitems; i += kRegThreads) first[i] = items[i].first_tile;
-  if (flags.npoll && threadIdx.x == 0) fused_wait(flags);
+  if ((flags.npoll || flags.npre) && threadIdx.x == 0) fused_wait(flags);
   __syncthreads();
   int cur = find_item(first, nitems, blockIdx.x);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
   for (int i = threadIdx.x; i < nitems; i += 32) first[i] = items[i].first_tile;
   __syncwarp();
   if (threadIdx.x != 0) return;
-  if (flags.npoll) fused_wait(flags);
+  if (flags.npoll || flags.npre) fused_wait(flags);
   for (int i = 0; i < kTmaStages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[i])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 

@@ -67,6 +67,10 @@ int mover_grid_for(const ItemTable& t, int sms);
 // sigs[i] = 1 with st.release.sys. Tables and ctr live in device memory;
 // ctr starts at 0.
 struct FlagSet {
+  // Written (= 1, st.release.sys) by thread 0 of CTA 0 before anything else:
+  // the unit's start signals ("my buffers may be used"), when folded in.
+  uint64_t* const* pre = nullptr;
+  int npre = 0;
   uint64_t* const* polls = nullptr;
   int npoll = 0;
   uint64_t* const* sigs = nullptr;

@@ -227,6 +227,13 @@ bool fusion_enabled() {
 Status fuse_sm_flags(World* w, Plan* p) {
   (void)w;
   if (!fusion_enabled() || p->hybrid) return {};  // hybrid: lanes need the rdy polls too
+  // With every unit on its own device (one process per GPU) the start
+  // signals fold into the kernel too: no other unit's kernel on this device
+  // can be starved by the spinning grid, so writing them at kernel start is
+  // as good as a separate submission ahead of it.
+  std::set<int> devs;
+  bool distinct = true;
+  for (const Unit& u : p->units) distinct &= devs.insert(u.device).second;
   for (Unit& u : p->units) {
     if (!u.table.nitems && !u.red.nitems) continue;  // the mover or the reduction carries them
     std::vector<uint64_t*> polls, sigs;
@@ -235,10 +242,20 @@ Status fuse_sm_flags(World* w, Plan* p) {
     for (const auto& op : u.sm_post) sigs.push_back(reinterpret_cast<uint64_t*>(op.writeValue.address));
     sigs.insert(sigs.end(), u.sm_post_remote.begin(), u.sm_post_remote.end());
     if (polls.empty() && sigs.empty()) continue;  // nothing to fuse: plain kernel
+    std::vector<uint64_t*> pre;
+    if (distinct) {
+      for (const auto& op : u.start) pre.push_back(reinterpret_cast<uint64_t*>(op.writeValue.address));
+      pre.insert(pre.end(), u.start_remote.begin(), u.start_remote.end());
+    }
     uint64_t** pt = nullptr;
     uint64_t** st = nullptr;
+    uint64_t** prt = nullptr;
     STATUS_TRY(upload_ptrs(p, u.device, polls, &pt));
     STATUS_TRY(upload_ptrs(p, u.device, sigs, &st));
+    STATUS_TRY(upload_ptrs(p, u.device, pre, &prt));
+    u.sm_flags.pre = prt;
+    u.sm_flags.npre = static_cast<int>(pre.size());
+    u.start_folded = !pre.empty();
     u.sm_flags.polls = pt;
     u.sm_flags.npoll = static_cast<int>(polls.size());
     u.sm_flags.sigs = st;

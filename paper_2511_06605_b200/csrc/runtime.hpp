@@ -162,6 +162,7 @@ struct Unit {
   // SM path with the flag work fused into the item kernel (kernels.hpp
   // FlagSet): device tables of the sm_pre poll and sm_post signal addresses.
   bool fused = false;
+  bool start_folded = false;  // the start signals are the fused kernel's `pre` writes
   FlagSet sm_flags;
   std::vector<Copy> placement;    // local-slot placement (verifier.cpp:40-44)
   std::vector<Copy> precopy;      // swap with send != recv: send -> recv first
