@@ -448,7 +448,7 @@ cecoll_status_t cecoll_trace_end(cecoll_comm_t comm, char* json, size_t capacity
 
 cecoll_status_t cecoll_comm_counters(cecoll_comm_t comm, int64_t out8[8]) {
   if (!comm || !out8) return err(CECOLL_INVALID_ARGUMENT, "null argument");
-  for (int i = 0; i < 8; ++i) out8[i] = comm->world->counters[i].load();
+  for (int i = 0; i < kNumCounters; ++i) out8[i] = comm->world->counters[i].load();
   return CECOLL_SUCCESS;
 }
 

@@ -84,7 +84,7 @@ Status run_ce(World* w, Plan* p) {
                              u.device, pid, -1));
     for (int r : u.ranks) {
       CUDA_TRY(cudaEventRecord(w->local[r]->start, u.stream));
-      ++w->counters[6];
+      ++w->counters[kCtrApiCalls];
     }
     STATUS_TRY(issue_copies_traced(w, u.placement, u.stream, true, u.device, pid, -1));
     trace_host_span(w, "control", h0);
@@ -95,19 +95,19 @@ Status run_ce(World* w, Plan* p) {
     const double h0 = trace_host_now(w);
     cudaStream_t s = rs->lanes[l.lane];
     CUDA_TRY(cudaStreamWaitEvent(s, rs->start, 0));
-    ++w->counters[6];
+    ++w->counters[kCtrApiCalls];
     STATUS_TRY(submit_traced(w, s, l.pre, nullptr, 0, "poll:poll", rs->device, l.rank, l.lane));
     STATUS_TRY(issue_copies_traced(w, l.copies, s, true, rs->device, l.rank, l.lane));
     if (l.table.nitems) {
       cudaEvent_t b = trace_mark(w, rs->device, s);
       CUDA_TRY(launch_items(l.table, mover_grid_for(l.table, p->sms), s));
-      ++w->counters[4];
-      ++w->counters[6];
+      ++w->counters[kCtrKernels];
+      ++w->counters[kCtrApiCalls];
       trace_span(w, table_name(l.table), l.rank, l.lane, rs->device, b, trace_mark(w, rs->device, s));
     }
     STATUS_TRY(submit_traced(w, s, l.post, nullptr, 0, "sync:signal", rs->device, l.rank, l.lane));
     CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], s));
-    ++w->counters[6];
+    ++w->counters[kCtrApiCalls];
     trace_host_span(w, "control", h0);
   }
   for (Unit& u : p->units) {
@@ -117,7 +117,7 @@ Status run_ce(World* w, Plan* p) {
     for (const LaneExec& l : p->lanes) {
       if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) == u.ranks.end()) continue;
       CUDA_TRY(cudaStreamWaitEvent(u.stream, w->local[l.rank]->lane_done[l.lane], 0));
-      ++w->counters[6];
+      ++w->counters[kCtrApiCalls];
     }
     STATUS_TRY(submit_traced(w, u.stream, {}, u.lanes_remote_tab, u.lanes_remote.size(), "sync:signal", u.device,
                              u.ranks[0], -1));
@@ -129,7 +129,7 @@ Status run_ce(World* w, Plan* p) {
 Status run_sm(World* w, Plan* p) {
   for (Unit& u : p->units) {  // phase 1: readiness to sources in other units
     if (u.start_folded) {     // written by the fused kernel itself
-      w->counters[2] += u.sm_flags.npre;
+      w->counters[kCtrFlagWrites] += u.sm_flags.npre;
       continue;
     }
     DeviceGuard g(u.device);
@@ -147,7 +147,7 @@ Status run_sm(World* w, Plan* p) {
     if (p->hybrid) {
       cudaEvent_t fork = w->local[u.ranks[0]]->start;
       CUDA_TRY(cudaEventRecord(fork, u.stream));
-      ++w->counters[6];
+      ++w->counters[kCtrApiCalls];
       for (const LaneExec& l : p->lanes) {
         if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) == u.ranks.end()) continue;
         RankState* rs = w->local[l.rank].get();
@@ -155,7 +155,7 @@ Status run_sm(World* w, Plan* p) {
         CUDA_TRY(cudaStreamWaitEvent(ls, fork, 0));
         STATUS_TRY(issue_copies_traced(w, l.copies, ls, false, rs->device, l.rank, l.lane));
         CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], ls));
-        w->counters[6] += 2;
+        w->counters[kCtrApiCalls] += 2;
         forked.push_back(&l);
       }
     }
@@ -163,11 +163,11 @@ Status run_sm(World* w, Plan* p) {
       cudaEvent_t b = trace_mark(w, u.device, u.stream);
       CUDA_TRY(launch_items(u.table, mover_grid_for(u.table, p->sms), u.stream, u.fused ? &u.sm_flags : nullptr));
       if (u.fused) {
-        w->counters[2] += u.sm_flags.nsig;
-        w->counters[3] += u.sm_flags.npoll;
+        w->counters[kCtrFlagWrites] += u.sm_flags.nsig;
+        w->counters[kCtrFlagWaits] += u.sm_flags.npoll;
       }
-      ++w->counters[4];
-      ++w->counters[6];
+      ++w->counters[kCtrKernels];
+      ++w->counters[kCtrApiCalls];
       trace_span(w, std::string("kernel:") + (table_name(u.table) + 5), pid, -1, u.device, b,
                  trace_mark(w, u.device, u.stream));
     }
@@ -175,16 +175,16 @@ Status run_sm(World* w, Plan* p) {
       cudaEvent_t b = trace_mark(w, u.device, u.stream);
       CUDA_TRY(launch_reduce(u.red, 4 * p->sms, u.stream, u.fused ? &u.sm_flags : nullptr));
       if (u.fused) {
-        w->counters[2] += u.sm_flags.nsig;
-        w->counters[3] += u.sm_flags.npoll;
+        w->counters[kCtrFlagWrites] += u.sm_flags.nsig;
+        w->counters[kCtrFlagWaits] += u.sm_flags.npoll;
       }
-      ++w->counters[4];
-      ++w->counters[6];
+      ++w->counters[kCtrKernels];
+      ++w->counters[kCtrApiCalls];
       trace_span(w, "kernel:reduce", pid, -1, u.device, b, trace_mark(w, u.device, u.stream));
     }
     for (const LaneExec* l : forked) {
       CUDA_TRY(cudaStreamWaitEvent(u.stream, w->local[l->rank]->lane_done[l->lane], 0));
-      ++w->counters[6];
+      ++w->counters[kCtrApiCalls];
     }
     if (!u.fused)
       STATUS_TRY(submit_traced(w, u.stream, u.sm_post, u.sm_post_remote_tab, u.sm_post_remote.size(), "sync:signal",
@@ -212,8 +212,8 @@ Status arm_unit(World* w, Unit& u) {
   DeviceGuard g(u.device);
   CUDA_TRY(cudaGraphLaunch(u.exec, u.arm));
   CUDA_TRY(cudaEventRecord(u.graph_done, u.arm));
-  ++w->counters[5];
-  w->counters[6] += 2;
+  ++w->counters[kCtrGraphLaunches];
+  w->counters[kCtrApiCalls] += 2;
   u.armed = true;
   return {};
 }
@@ -245,12 +245,12 @@ Status trigger_wait(World* w, Unit& u, cudaEvent_t span_begin) {
   if (u.nfin) {
     cudaEvent_t pb = trace_mark(w, u.device, u.stream);
     CUDA_TRY(launch_poll(u.fin_tab, u.nfin, u.err, u.stream));
-    ++w->counters[4];
-    ++w->counters[6];
+    ++w->counters[kCtrKernels];
+    ++w->counters[kCtrApiCalls];
     trace_span(w, "poll:poll", pid, -1, u.device, pb, trace_mark(w, u.device, u.stream));
   }
   CUDA_TRY(cudaStreamWaitEvent(u.stream, u.graph_done, 0));
-  ++w->counters[6];
+  ++w->counters[kCtrApiCalls];
   // The gated graph body (polls, copies, signals) runs on the arm stream; its
   // span is taken from the trigger to its completion as seen by the caller.
   trace_span(w, "copy:graph", pid, 0, u.device, span_begin, trace_mark(w, u.device, u.stream));
@@ -292,8 +292,8 @@ void drop_recording(Plan* p) {
 // at once — one graph per unit; lane streams join through the start / lane_done
 // events — and instantiates the graphs. Nothing executes while recording.
 Status record_plan(World* w, Plan* p) {
-  int64_t before[8];
-  for (int i = 0; i < 8; ++i) before[i] = w->counters[i];
+  int64_t before[kNumCounters];
+  for (int i = 0; i < kNumCounters; ++i) before[i] = w->counters[i];
   size_t begun = 0;
   Status st;
   for (Unit& u : p->units) {
@@ -322,7 +322,7 @@ Status record_plan(World* w, Plan* p) {
     const cudaError_t e = cudaGraphInstantiate(&u.rec_exec, u.rec_graph, 0);
     if (e != cudaSuccess) st = cuda_fail(e, "cudaGraphInstantiate", __FILE__, __LINE__);
   }
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < kNumCounters; ++i) {
     p->rec_delta[i] = w->counters[i] - before[i];
     w->counters[i] = before[i];  // recording submitted nothing
   }
@@ -340,10 +340,10 @@ Status launch_recorded(World* w, Plan* p) {
   for (Unit& u : p->units) {
     DeviceGuard g(u.device);
     CUDA_TRY(cudaGraphLaunch(u.rec_exec, u.stream));
-    ++w->counters[7];
-    ++w->counters[6];
+    ++w->counters[kCtrRecordedLaunches];
+    ++w->counters[kCtrApiCalls];
   }
-  for (int i : {1, 2, 3, 4}) w->counters[i] += p->rec_delta[i];
+  for (int i : {kCtrCopies, kCtrFlagWrites, kCtrFlagWaits, kCtrKernels}) w->counters[i] += p->rec_delta[i];
   return {};
 }
 
@@ -388,12 +388,12 @@ Status plan_launch(World* w, Plan* p, bool rearm) {
     for (Unit& u : p->units) {
       DeviceGuard g(u.device);
       CUDA_TRY(launch_reduce(u.red, 4 * p->sms, u.stream));
-      ++w->counters[4];
-      ++w->counters[6];
+      ++w->counters[kCtrKernels];
+      ++w->counters[kCtrApiCalls];
     }
     return {};
   }
-  ++w->counters[0];
+  ++w->counters[kCtrCollectives];
   if (!p->prelaunch) {
     // First launch eager; from the second on, one recorded graph per unit.
     const bool want = graph_mode_wanted(w, p);

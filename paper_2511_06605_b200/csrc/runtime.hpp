@@ -48,6 +48,19 @@ constexpr int kSlotDone = kMaxRanks;    // done[i]
 constexpr int kSlotReady = 2 * kMaxRanks;  // unit-ready word of a prelaunch graph
 constexpr size_t kFlagBytes = 4096;
 
+// World::counters (exported by cecoll_comm_counters in this order).
+enum Counter : int {
+  kCtrCollectives = 0,
+  kCtrCopies = 1,            // copy commands issued (CE memcpys)
+  kCtrFlagWrites = 2,
+  kCtrFlagWaits = 3,
+  kCtrKernels = 4,
+  kCtrGraphLaunches = 5,     // prelaunch graphs
+  kCtrApiCalls = 6,          // host CUDA calls issued by the executors
+  kCtrRecordedLaunches = 7,  // replays of a recorded command list
+  kNumCounters = 8,
+};
+
 struct Status {
   int code = 0;
   std::string msg;
@@ -104,7 +117,7 @@ struct World {
   std::vector<int> device;           // per rank
   std::vector<uint64_t*> flag_page;  // per rank, usable from this process
   std::vector<std::unique_ptr<RankState>> local;  // by rank; null if remote
-  std::atomic<int64_t> counters[8];
+  std::atomic<int64_t> counters[kNumCounters];
   std::vector<std::unique_ptr<Plan>> plans;  // eager-call plan cache
   std::vector<Plan*> explicit_plans;         // cecoll_plan_create; cancelled at release
   std::vector<Window> windows;
@@ -215,7 +228,7 @@ struct Plan {
   int launches = 0;
   bool recorded = false;
   std::string record_note;        // why recording failed (then the plan stays eager)
-  int64_t rec_delta[8] = {};      // counter increments of one recorded launch
+  int64_t rec_delta[kNumCounters] = {};      // counter increments of one recorded launch
 };
 
 void set_error(const std::string& msg);

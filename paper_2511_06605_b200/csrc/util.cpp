@@ -69,10 +69,10 @@ Status submit(World* w, cudaStream_t s, const MemOps& ops) {
     CU_TRY(d->StreamBatchMemOp(reinterpret_cast<CUstream>(s), count,
                                const_cast<CUstreamBatchMemOpParams*>(ops.data() + i), 0));
     for (unsigned k = 0; k < count; ++k) {
-      if (ops[i + k].operation == CU_STREAM_MEM_OP_WRITE_VALUE_64) ++w->counters[2];
-      else ++w->counters[3];
+      if (ops[i + k].operation == CU_STREAM_MEM_OP_WRITE_VALUE_64) ++w->counters[kCtrFlagWrites];
+      else ++w->counters[kCtrFlagWaits];
     }
-    ++w->counters[6];
+    ++w->counters[kCtrApiCalls];
     i += count;
   }
   return {};
@@ -102,14 +102,14 @@ Status issue_copies(World* w, const std::vector<Copy>& copies, cudaStream_t s, b
     size_t idx = 0, fail_idx = 0;
     CU_TRY(d->MemcpyBatchAsync(dst.data(), src.data(), sz.data(), copies.size(), &attr, &idx, 1, &fail_idx,
                                reinterpret_cast<CUstream>(s)));
-    w->counters[1] += static_cast<int64_t>(copies.size());
-    ++w->counters[6];
+    w->counters[kCtrCopies] += static_cast<int64_t>(copies.size());
+    ++w->counters[kCtrApiCalls];
     return {};
   }
   for (const Copy& c : copies) {
     CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, static_cast<size_t>(c.bytes), cudaMemcpyDefault, s));
-    ++w->counters[1];
-    ++w->counters[6];
+    ++w->counters[kCtrCopies];
+    ++w->counters[kCtrApiCalls];
   }
   return {};
 }
@@ -131,9 +131,9 @@ Status ensure_lanes(RankState* rs, int n) {
 Status signal_remote(World* w, uint64_t** tab, size_t n, cudaStream_t s) {
   if (!n) return {};
   CUDA_TRY(launch_signal(tab, static_cast<int>(n), s));
-  ++w->counters[4];
-  ++w->counters[6];
-  w->counters[2] += static_cast<int64_t>(n);
+  ++w->counters[kCtrKernels];
+  ++w->counters[kCtrApiCalls];
+  w->counters[kCtrFlagWrites] += static_cast<int64_t>(n);
   return {};
 }
 
