@@ -44,24 +44,31 @@ cecoll_status_t err(cecoll_status_t code, const std::string& msg) {
 bool impl_ok(cecoll_impl_t impl) { return impl >= CECOLL_IMPL_AUTO && impl <= CECOLL_IMPL_HYBRID; }
 
 cecoll_status_t flush_group(std::vector<PendingCall>& calls) {
-  cecoll_status_t result = CECOLL_SUCCESS;
+  // Group the calls per world and validate every group before anything is
+  // submitted: a rejected group must not leave other worlds' collectives
+  // half issued (their peers would wait on flags forever).
+  std::vector<std::vector<size_t>> groups;
   std::vector<bool> done(calls.size(), false);
   for (size_t i = 0; i < calls.size(); ++i) {
     if (done[i]) continue;
     World* w = calls[i].comm->world;
-    std::vector<CallArgs> args;
+    groups.emplace_back();
     for (size_t j = i; j < calls.size(); ++j) {
       if (done[j] || calls[j].comm->world != w) continue;
       if (calls[j].kind != calls[i].kind || calls[j].chunk != calls[i].chunk || calls[j].impl != calls[i].impl ||
-          calls[j].dtype != calls[i].dtype || calls[j].op != calls[i].op) {
+          calls[j].dtype != calls[i].dtype || calls[j].op != calls[i].op)
         return err(CECOLL_INVALID_ARGUMENT, "group: one collective per communicator set (kind, size and impl must match)");
-      }
-      args.push_back({calls[j].comm->rank, calls[j].send, calls[j].recv, calls[j].stream});
+      groups.back().push_back(j);
       done[j] = true;
     }
-    Status s = calls[i].kind == Kind::ReduceScatter
-                   ? run_reduce_scatter(w, calls[i].impl, calls[i].chunk, calls[i].dtype, calls[i].op, args)
-                   : run_collective(w, calls[i].kind, calls[i].impl, calls[i].chunk, args);
+  }
+  cecoll_status_t result = CECOLL_SUCCESS;
+  for (const auto& g : groups) {
+    const PendingCall& c = calls[g[0]];
+    std::vector<CallArgs> args;
+    for (size_t j : g) args.push_back({calls[j].comm->rank, calls[j].send, calls[j].recv, calls[j].stream});
+    Status s = c.kind == Kind::ReduceScatter ? run_reduce_scatter(c.comm->world, c.impl, c.chunk, c.dtype, c.op, args)
+                                             : run_collective(c.comm->world, c.kind, c.impl, c.chunk, args);
     if (!s.ok() && result == CECOLL_SUCCESS) result = st(s);
   }
   return result;
@@ -71,7 +78,8 @@ cecoll_status_t enqueue(Kind kind, const void* send, void* recv, size_t chunk, c
                         void* stream, int dtype = 0, int op = 0) {
   if (!comm || !comm->world) return err(CECOLL_INVALID_ARGUMENT, "null communicator");
   if (!impl_ok(impl)) return err(CECOLL_INVALID_ARGUMENT, "unknown implementation");
-  if (chunk == 0 || !send || !recv) return err(CECOLL_INVALID_ARGUMENT, "collective: chunk size must be positive");
+  if (!send || !recv) return err(CECOLL_INVALID_ARGUMENT, "collective: null send or recv buffer");
+  if (chunk == 0) return err(CECOLL_INVALID_ARGUMENT, "collective: chunk size must be positive");
   PendingCall c{comm,   kind, send, recv, static_cast<int64_t>(chunk), static_cast<Impl>(impl),
                 static_cast<cudaStream_t>(stream), dtype, op};
   if (g_group_depth > 0) {
