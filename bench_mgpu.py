@@ -504,6 +504,8 @@ def run(args, B):
         STATE["phase"] = "experiments"
         line["experiments"] = {}
         run_experiments(comms, sets, n, s, my_ranks, stream, line["experiments"])
+        STATE["phase"] = "experiments multicast"
+        run_mc_experiment(world, rank, dev, stream, line["experiments"])
     line["config"]["wall_s"] = round(time.time() - t_start, 1)
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -924,3 +926,62 @@ def run_experiments(comms, sets, n, s, my_ranks, stream, out):
                 else:
                     os.environ[k] = v
         out[f"{name}/{kind}"] = res
+
+
+def run_mc_experiment(world, rank, dev, stream, out):
+    """NVLS multicast all-gather (include/cecoll.h cecoll_mc_*):
+    one rank per GPU, window creation and every collective under consensus,
+    parity against the seeded expectation, then timing. Last experiment: the
+    least tested path in the library (never executed on a box that accepts
+    multicast objects)."""
+    n = world
+    cap = 64 << 20
+    res = {}
+    out["nvls_allgather"] = res
+    comms = cc.Comm.init_ranks(n, rank, 1, dev, cc.torch_exchange())
+    win, ok, err = None, True, None
+    try:
+        win = cc.McWindow(comms[0], cap)
+        res["handle_type"] = win.handle_type
+    except Exception as e:  # noqa: BLE001
+        ok, err = False, str(e)[:200]
+    if not all_true(ok):
+        res["error"] = err or "window creation failed on another rank"
+        comms[0].destroy()
+        return
+    send = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    exp = torch.empty(n * cap, dtype=torch.uint8, device="cuda")
+    for s in (1 << 20, 16 << 20, 64 << 20):
+        fill_and_expect("allgather", s, n, [rank], [send], [exp], "cuda")
+        torch.cuda.synchronize()
+        ok, err = True, None
+        try:
+            win.allgather(send, s, stream)
+            stream.synchronize()
+            ok = bool(torch.equal(win.recv[:n * s], exp[:n * s]))
+            err = None if ok else "parity failed"
+        except Exception as e:  # noqa: BLE001
+            ok, err = False, str(e)[:160]
+        if not all_true(ok):
+            res[str(s)] = {"error": err or "failed on another rank"}
+            break
+        iters = int(max(5, min(100, 4e8 / max(1, (n - 1) * s))))
+        for _ in range(2):
+            win.allgather(send, s, stream)
+        stream.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            win.allgather(send, s, stream)
+        e1.record(stream)
+        stream.synchronize()
+        ms = max_all(e0.elapsed_time(e1) / iters)
+        res[str(s)] = {"us": round(ms * 1e3, 2), "busbw_gbs": round(busbw(n, s, ms), 2)}
+    torch.cuda.synchronize()
+    dist.barrier()
+    try:
+        win.destroy()
+    except Exception:  # noqa: BLE001
+        pass
+    comms[0].destroy()

@@ -236,6 +236,26 @@ cecoll_status_t cecoll_trace_end(cecoll_comm_t comm, char* json, size_t capacity
  * recorded command list (whose copies, flags and kernels count in [1]-[4]). */
 cecoll_status_t cecoll_comm_counters(cecoll_comm_t comm, int64_t out8[8]);
 
+/* ---------------------------------------------------------------------
+ * EXPERIMENTAL: NVLS (switch multicast) all-gather, SURVEY §8(f)2 — the
+ * multicast analogue of the reference's broadcast command
+ * (compiler.cpp:166-205): each rank's chunk is read once and stored once to
+ * a multicast address; the NVSwitch writes it into every GPU's window.
+ * One process per GPU (cecoll_comm_init_rank). window_create is collective
+ * over the processes (it uses the communicator's exchange callback) and
+ * returns, in *recv, this rank's window: after cecoll_mc_allgather with
+ * chunk s (<= chunk_capacity, 16-byte multiple) it holds rank i's chunk at
+ * [i*s, (i+1)*s) (compiler.cpp:115-122), ordered on `stream`. Returns
+ * CECOLL_UNSUPPORTED wherever the node offers no multicast objects (e.g. the
+ * one-GPU development boxes). Not yet executed on hardware that accepts
+ * multicast objects.
+ * ------------------------------------------------------------------- */
+typedef struct cecoll_mc* cecoll_mc_t;
+cecoll_status_t cecoll_mc_window_create(cecoll_comm_t comm, size_t chunk_capacity, cecoll_mc_t* out, void** recv);
+cecoll_status_t cecoll_mc_allgather(cecoll_mc_t mc, const void* send, size_t chunk_bytes, void* stream);
+const char* cecoll_mc_handle_type(cecoll_mc_t mc); /* "fabric" or "posix_fd" */
+cecoll_status_t cecoll_mc_window_destroy(cecoll_mc_t mc);
+
 #ifdef __cplusplus
 }
 #endif

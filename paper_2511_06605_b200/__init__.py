@@ -133,6 +133,10 @@ def lib():
         "cecoll_plan_destroy": ([vp], i32),
         "cecoll_plan_disarm": ([vp], i32),
         "cecoll_comm_counters": ([vp, C.POINTER(i64)], i32),
+        "cecoll_mc_window_create": ([vp, sz, C.POINTER(vp), C.POINTER(vp)], i32),
+        "cecoll_mc_allgather": ([vp, vp, sz, vp], i32),
+        "cecoll_mc_handle_type": ([vp], C.c_char_p),
+        "cecoll_mc_window_destroy": ([vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -152,6 +156,7 @@ EXPORTED_SYMBOLS = [
     "cecoll_program_parse", "cecoll_plan_create_program", "cecoll_comm_init_ranks", "cecoll_exchange_check",
     "cecoll_collective_n", "cecoll_plan_disarm", "cecoll_reduce_scatter", "cecoll_reduce_scatter_n",
     "cecoll_mem_alloc", "cecoll_mem_free", "cecoll_trace_begin", "cecoll_trace_end",
+    "cecoll_mc_window_create", "cecoll_mc_allgather", "cecoll_mc_handle_type", "cecoll_mc_window_destroy",
 ]
 DTYPES = {"f32": 0, "float32": 0, "bf16": 1, "bfloat16": 1, "f16": 2, "float16": 2}
 REDOPS = {"sum": 0, "max": 1, "min": 2}
@@ -350,6 +355,39 @@ class Comm:
     def destroy(self):
         if self._h is not None:
             _check(lib().cecoll_comm_destroy(self._h))
+            self._h = None
+
+
+class McWindow:
+    """EXPERIMENTAL NVLS (switch multicast) all-gather window (include/cecoll.h,
+    csrc/mcast.cpp). Collective to create (one process per GPU); `recv` is this
+    rank's window: after allgather(send, s) it holds rank i's chunk at
+    [i*s, (i+1)*s). Raises CecollError (unsupported) where the node offers no
+    multicast objects."""
+
+    def __init__(self, comm: "Comm", chunk_capacity: int):
+        import torch
+
+        h, p = C.c_void_p(), C.c_void_p()
+        _check(lib().cecoll_mc_window_create(comm._h, chunk_capacity, C.byref(h), C.byref(p)), "mc_window_create")
+        self._h = h
+        self.capacity = chunk_capacity
+        self.handle_type = lib().cecoll_mc_handle_type(h).decode()
+        nbytes = comm.nranks * chunk_capacity
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (p.value, False),
+                                        "version": 3, "strides": None}
+
+        with torch.cuda.device(comm.device):
+            self.recv = torch.as_tensor(_View(), device=f"cuda:{comm.device}")
+
+    def allgather(self, send, chunk_bytes: int, stream=None):
+        _check(lib().cecoll_mc_allgather(self._h, _ptr(send), chunk_bytes, _stream(stream)), "mc_allgather")
+
+    def destroy(self):
+        if self._h is not None:
+            _check(lib().cecoll_mc_window_destroy(self._h), "mc_window_destroy")
             self._h = None
 
 

@@ -460,4 +460,29 @@ cecoll_status_t cecoll_comm_counters(cecoll_comm_t comm, int64_t out8[8]) {
   return CECOLL_SUCCESS;
 }
 
+cecoll_status_t cecoll_mc_window_create(cecoll_comm_t comm, size_t chunk_capacity, cecoll_mc_t* out, void** recv) {
+  if (!comm || !out) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  McWindow* m = nullptr;
+  Status s = mc_create(comm->world, comm->rank, static_cast<int64_t>(chunk_capacity), &m);
+  if (!s.ok()) return st(s);
+  *out = new cecoll_mc{m};
+  if (recv) *recv = mc_recv(m);
+  return CECOLL_SUCCESS;
+}
+
+cecoll_status_t cecoll_mc_allgather(cecoll_mc_t mc, const void* send, size_t chunk_bytes, void* stream) {
+  if (!mc || !send) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  return st(mc_allgather(mc->m, send, static_cast<int64_t>(chunk_bytes), static_cast<cudaStream_t>(stream)));
+}
+
+const char* cecoll_mc_handle_type(cecoll_mc_t mc) { return mc ? mc_how(mc->m) : ""; }
+
+cecoll_status_t cecoll_mc_window_destroy(cecoll_mc_t mc) {
+  if (!mc) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  mc_release(mc->m);
+  delete mc;
+  return CECOLL_SUCCESS;
+}
+
 }  // extern "C"

@@ -39,7 +39,23 @@ const DriverApi* driver_api() {
     ok &= load("cuDeviceGetAttribute", api.DeviceGetAttribute);
     ok &= load("cuGetErrorString", api.GetErrorString);
     api.has_batch_memcpy = load("cuMemcpyBatchAsync", api.MemcpyBatchAsync);
-    load("cuMulticastCreate", api.MulticastCreate);
+    bool mc = load("cuMulticastCreate", api.MulticastCreate);
+    mc &= load("cuMulticastGetGranularity", api.MulticastGetGranularity);
+    mc &= load("cuMulticastAddDevice", api.MulticastAddDevice);
+    mc &= load("cuMulticastBindMem", api.MulticastBindMem);
+    mc &= load("cuMulticastUnbind", api.MulticastUnbind);
+    mc &= load("cuMemCreate", api.MemCreate);
+    mc &= load("cuMemRelease", api.MemRelease);
+    mc &= load("cuMemExportToShareableHandle", api.MemExportToShareableHandle);
+    mc &= load("cuMemImportFromShareableHandle", api.MemImportFromShareableHandle);
+    mc &= load("cuMemAddressReserve", api.MemAddressReserve);
+    mc &= load("cuMemAddressFree", api.MemAddressFree);
+    mc &= load("cuMemMap", api.MemMap);
+    mc &= load("cuMemUnmap", api.MemUnmap);
+    mc &= load("cuMemSetAccess", api.MemSetAccess);
+    mc &= load("cuMemGetAllocationGranularity", api.MemGetAllocationGranularity);
+    mc &= load("cuDeviceGet", api.DeviceGet);
+    api.has_multicast = mc;
     ok &= load("cuMemGetAddressRange", api.MemGetAddressRange);
     api.loaded = ok;
   });

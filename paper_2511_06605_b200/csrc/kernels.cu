@@ -357,6 +357,27 @@ __global__ void gate_poll_kernel(volatile uint64_t* posted, uint64_t* consumed, 
   *skip = 0;
 }
 
+__global__ void __launch_bounds__(kRegThreads) mc_store_kernel(const int4* __restrict__ src, char* mc_dst,
+                                                                int64_t nvec, uint64_t* mc_flag, uint64_t epoch,
+                                                                unsigned* ctr) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kRegThreads;
+  for (int64_t v = static_cast<int64_t>(blockIdx.x) * kRegThreads + threadIdx.x; v < nvec; v += stride) {
+    const int4 x = ld_stream(src + v);
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc_dst + v * 16),
+                 "f"(__int_as_float(x.x)), "f"(__int_as_float(x.y)), "f"(__int_as_float(x.z)),
+                 "f"(__int_as_float(x.w))
+                 : "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  unsigned ticket;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(ticket) : "l"(ctr) : "memory");
+  if (ticket != gridDim.x - 1) return;
+  *ctr = 0;
+  asm volatile("multimem.st.release.sys.global.u64 [%0], %1;" ::"l"(mc_flag), "l"(epoch) : "memory");
+}
+
 }  // namespace
 
 int64_t mover_tile_bytes(Mover m) { return m == Mover::Tma ? kTmaTile : kRegTile; }
@@ -417,6 +438,16 @@ cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream, cons
   } else {
     reg_items_kernel<15, 1><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems, t.ntiles, flags);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mc_store(const char* src, char* mc_dst, int64_t bytes, uint64_t* mc_flag, uint64_t epoch,
+                            unsigned* ctr, int grid, cudaStream_t stream) {
+  const int64_t nvec = bytes / 16;
+  const int64_t need = (nvec + kRegThreads - 1) / kRegThreads;
+  if (grid > need) grid = static_cast<int>(need > 0 ? need : 1);
+  mc_store_kernel<<<grid, kRegThreads, 0, stream>>>(reinterpret_cast<const int4*>(src), mc_dst, nvec, mc_flag, epoch,
+                                                     ctr);
   return cudaGetLastError();
 }
 

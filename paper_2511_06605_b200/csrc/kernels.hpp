@@ -131,4 +131,12 @@ cudaError_t launch_gate(volatile uint64_t* posted, uint64_t* consumed, cudaGraph
 cudaError_t launch_gate_poll(volatile uint64_t* posted, uint64_t* consumed, uint64_t* const* flags, int n,
                              uint64_t* skip, uint64_t* err, cudaStream_t stream);
 
+// NVLS multicast all-gather store (mcast.cpp, experimental): src (bytes, a
+// multiple of 16, 16-byte aligned) -> mc_dst with multimem.st (the switch
+// writes every GPU of the multicast group); after every CTA's stores, the
+// last CTA publishes *mc_flag = epoch with multimem.st.release.sys. ctr is a
+// zeroed device word (restored to 0).
+cudaError_t launch_mc_store(const char* src, char* mc_dst, int64_t bytes, uint64_t* mc_flag, uint64_t epoch,
+                            unsigned* ctr, int grid, cudaStream_t stream);
+
 }  // namespace cecoll

@@ -273,6 +273,14 @@ Status plan_disarm(World* w, Plan* p);
 Status plan_launch(World* w, Plan* p, bool rearm);
 Status plan_destroy(World* w, Plan* p);
 
+// NVLS multicast all-gather windows (mcast.cpp, experimental).
+struct McWindow;
+Status mc_create(World* w, int rank, int64_t chunk_capacity, McWindow** out);
+Status mc_allgather(McWindow* m, const void* send, int64_t chunk, cudaStream_t stream);
+void mc_release(McWindow* m);
+void* mc_recv(McWindow* m);
+const char* mc_how(McWindow* m);
+
 Status trace_begin(World* w);
 Status trace_end(World* w, std::string* json);
 
@@ -281,6 +289,10 @@ Status trace_end(World* w, std::string* json);
 struct cecoll_comm {
   cecoll::World* world;
   int rank;
+};
+
+struct cecoll_mc {
+  cecoll::McWindow* m;
 };
 
 struct cecoll_plan {
