@@ -54,20 +54,32 @@ def main():
         for r in csv.DictReader(open(lat)):
             if r.get("api") == "eager":
                 meas[(r["collective"], r["impl"], int(r["size_bytes"]))] = float(r["device_us_b2b"])
+    now = {}
+    lin = os.path.join(ROOT, "profiles", "latency_r01_n8_prelaunch_linear.csv")
+    if os.path.exists(lin):  # explicit plans after recorded command lists / linear prelaunch bodies
+        for r in csv.DictReader(open(lin)):
+            if r.get("api") == "plan":
+                now[(r["collective"], r["impl"], int(r["size_bytes"]))] = float(r["device_us_b2b"])
     n = 8
     print("# Reference simulator with B200-measured phase latencies vs measured\n")
     print(f"Cost model: `profiles/b200_cost_model.conf` (tools/phase_probe.cu); link {LINK / 1e9:.1f} GB/s "
           "per directed pair; n = 8. Measured: eager calls from C++ (tools/latency.cpp), 8 co-resident ranks.\n")
-    print("| collective | impl | s | simulated MI300X-default µs | simulated B200-params µs | measured µs |")
-    print("|---|---|---|---|---|---|")
+    print("The last column is the same program after the command-overhead work of round 1: plans replay one "
+          "recorded CUDA graph per collective (DESIGN.md §3.7) and prelaunch bodies are two kernels (§3.4) "
+          "(profiles/latency_r01_n8_prelaunch_linear.csv, explicit plans). The reference's model charges host "
+          "control per command; recording removes exactly that term.\n")
+    print("| collective | impl | s | simulated MI300X-default µs | simulated B200-params µs | measured eager µs "
+          "| measured recorded / linear µs |")
+    print("|---|---|---|---|---|---|---|")
     for kind in ("allgather", "alltoall"):
         for impl in IMPLS[kind]:
             for s in (4096, 65536):
                 base = simulate(L, kind, impl, s, n, None, 64e9)[0] / 1e3
                 b200 = simulate(L, kind, impl, s, n, cost)[0] / 1e3
                 m = meas.get((kind, impl, s))
+                r = now.get((kind, impl, s))
                 print(f"| {kind} | {impl} | {s >> 10} KiB | {base:.1f} | {b200:.1f} | "
-                      f"{'' if m is None else f'{m:.1f}'} |")
+                      f"{'' if m is None else f'{m:.1f}'} | {'' if r is None else f'{r:.1f}'} |")
     print("\n## Selection under B200 parameters (simulated winner per size, n = 8)\n")
     print("| s | allgather | alltoall |")
     print("|---|---|---|")
