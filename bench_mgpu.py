@@ -35,8 +35,8 @@ import paper_2511_06605_b200 as cc
 NVLINK_PEAK = 770.0  # measured peer copy GB/s per direction (B200_PROFILING.md)
 NVLINK_NOMINAL = 900.0
 
-AG_IMPLS = ["sm", "pcpy", "b2b", "bcst", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_bcst", "hybrid"]
-AA_IMPLS = ["sm", "pcpy", "b2b", "swap", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_swap", "hybrid"]
+AG_IMPLS = ["sm", "pcpy", "b2b", "bcst", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_bcst", "hybrid", "pull"]
+AA_IMPLS = ["sm", "pcpy", "b2b", "swap", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_swap", "hybrid", "pull"]
 # headline trials also scan the hybrid's SM share ("impl@pct": CECOLL_HYBRID_SM_PCT at plan creation)
 HEADLINE_EXTRA = ["hybrid@25", "hybrid@75"]
 

@@ -55,7 +55,8 @@ typedef enum {
   CECOLL_IMPL_PRELAUNCH_B2B = 7,
   CECOLL_IMPL_SM = 8, /* one-shot sm_100a push kernel (latency regime) */
   CECOLL_IMPL_HYBRID = 9 /* each chunk split: copy-engine lane (pcpy rotation) + sm_100a mover;
-                            SM share CECOLL_HYBRID_SM_PCT percent (default 50), read per plan */
+                            SM share CECOLL_HYBRID_SM_PCT percent (default 50), read per plan */,
+  CECOLL_IMPL_PULL = 10 /* destination-issued copy-engine reads, one lane per source (pcpy rotation) */
 } cecoll_impl_t;
 
 typedef struct cecoll_comm* cecoll_comm_t;

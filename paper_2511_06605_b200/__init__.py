@@ -40,6 +40,7 @@ IMPLS = {
     "prelaunch_b2b": 7,
     "sm": 8,
     "hybrid": 9,
+    "pull": 10,
 }
 IMPL_NAMES = {v: k for k, v in IMPLS.items() if k != "baseline"}
 # implementations_for (compiler.cpp:77-85) + the SM path

@@ -41,7 +41,7 @@ cecoll_status_t err(cecoll_status_t code, const std::string& msg) {
   return code;
 }
 
-bool impl_ok(cecoll_impl_t impl) { return impl >= CECOLL_IMPL_AUTO && impl <= CECOLL_IMPL_HYBRID; }
+bool impl_ok(cecoll_impl_t impl) { return impl >= CECOLL_IMPL_AUTO && impl <= CECOLL_IMPL_PULL; }
 
 cecoll_status_t flush_group(std::vector<PendingCall>& calls) {
   // Group the calls per world and validate every group before anything is
@@ -121,7 +121,8 @@ cecoll_impl_t cecoll_parse_impl(const char* name) {
 }
 
 int cecoll_impl_valid_for(cecoll_impl_t impl, cecoll_kind_t kind) {
-  if (impl == CECOLL_IMPL_SM || impl == CECOLL_IMPL_HYBRID || impl == CECOLL_IMPL_AUTO) return 1;
+  if (impl == CECOLL_IMPL_SM || impl == CECOLL_IMPL_HYBRID || impl == CECOLL_IMPL_PULL || impl == CECOLL_IMPL_AUTO)
+    return 1;
   if (!impl_ok(impl)) return 0;
   return valid_for(static_cast<Impl>(impl), static_cast<Kind>(kind)) ? 1 : 0;
 }

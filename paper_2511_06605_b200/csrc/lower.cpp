@@ -297,19 +297,25 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
     for (const CallArgs& a : args) in_place &= a.send == a.recv;
     impl = in_place ? Impl::Swap : select(kind, s, n, w->ndevices);
   }
-  if (impl != Impl::Sm && impl != Impl::Hybrid && !valid_for(impl, kind))
+  if (impl != Impl::Sm && impl != Impl::Hybrid && impl != Impl::Pull && !valid_for(impl, kind))
     return fail(CECOLL_UNSUPPORTED, std::string(impl_name(impl)) + " does not apply to " +
                                          (kind == Kind::AllGather ? "allgather" : "alltoall"));
   const bool in_place_impl = base_of(impl) == Impl::Swap;
   p->impl = impl;
-  p->sm = impl == Impl::Sm || impl == Impl::Hybrid;
-  p->hybrid = impl == Impl::Hybrid;
+  // Pull runs on the hybrid executor with no SM share: the SM path's flag
+  // edges (r, (r+d)%n) read as "reader r, source (r+d)%n" — the source's rdy
+  // means "my send is ready", the reader's done "I have read it", exactly the
+  // reduce-scatter's reader-side protocol; the reader's own recv is free by
+  // its stream order.
+  p->sm = impl == Impl::Sm || impl == Impl::Hybrid || impl == Impl::Pull;
+  p->hybrid = impl == Impl::Hybrid || impl == Impl::Pull;
+  p->pull = impl == Impl::Pull;
   p->prelaunch = is_prelaunched(impl);
   if (p->hybrid) {
     const char* e = std::getenv("CECOLL_HYBRID_SM_PCT");
     int pct = e ? std::atoi(e) : 50;
     pct = std::max(0, std::min(100, pct));
-    p->hybrid_sm_bytes = (s * pct / 100) & ~int64_t{15};
+    p->hybrid_sm_bytes = p->pull ? 0 : (s * pct / 100) & ~int64_t{15};
   }
 
   // Addresses of every rank's buffers as usable from this process.
@@ -451,8 +457,10 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
         }
         for (int d = 1; d < n; ++d) {
           const int j = (r + d) % n;
-          const char* src = kind == Kind::AllGather ? src_ag : ad.send[r] + j * s;
-          char* dst = ad.recv[j] + r * s;
+          // push: r's chunk to j; pull: j's chunk read into r (lane d-1 of r either way)
+          const char* src = p->pull ? (kind == Kind::AllGather ? ad.send[j] : ad.send[j] + r * s)
+                                    : (kind == Kind::AllGather ? src_ag : ad.send[r] + j * s);
+          char* dst = p->pull ? ad.recv[r] + j * s : ad.recv[j] + r * s;
           if (kind == Kind::AllToAll && sm_b > 0)
             items.push_back({make_item(kItemCopy, src + ce, dst + ce, nullptr, sm_b), {}, w->device[j] != u.device});
           if (ce > 0) {

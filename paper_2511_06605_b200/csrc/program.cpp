@@ -22,13 +22,13 @@ constexpr int kTriggerBase = 100000;  // apply_prelaunch slot base (compiler.cpp
 
 const char* const kNames[] = {"pcpy",           "bcst",           "swap",           "b2b",
                               "prelaunch_pcpy", "prelaunch_bcst", "prelaunch_swap", "prelaunch_b2b",
-                              "sm",             "hybrid"};
+                              "sm",             "hybrid",         "pull"};
 }  // namespace
 
 const char* impl_name(Impl impl) {
   int i = static_cast<int>(impl);
   if (impl == Impl::Auto) return "auto";
-  return (i >= 0 && i <= 9) ? kNames[i] : "?";
+  return (i >= 0 && i <= 10) ? kNames[i] : "?";
 }
 
 bool parse_impl(const std::string& name, Impl* out) {
@@ -40,7 +40,7 @@ bool parse_impl(const std::string& name, Impl* out) {
     *out = Impl::Auto;
     return true;
   }
-  for (int i = 0; i <= 9; ++i)
+  for (int i = 0; i <= 10; ++i)
     if (name == kNames[i]) {
       *out = static_cast<Impl>(i);
       return true;

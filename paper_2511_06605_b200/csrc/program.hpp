@@ -32,6 +32,9 @@ enum class Impl : int {
   // rotation, compiler.cpp:150) and the SM mover (SURVEY §7 "hybrid CE + SM
   // lanes" fallback when copy engines alone cannot fill NVLink).
   Hybrid = 9,
+  // B200 pull: the destination's copy-engine lanes read every source's chunk
+  // (lane d-1 of rank r reads from (r+d)%n), SURVEY §7's push-vs-pull question.
+  Pull = 10,
 };
 
 const char* impl_name(Impl impl);

@@ -217,6 +217,7 @@ struct Plan {
   Program program;
   bool sm = false;       // SM path flag structure (sm, hybrid)
   bool hybrid = false;   // + copy-engine lanes for each chunk's CE share
+  bool pull = false;     // lanes belong to the destination and read the sources
   int64_t hybrid_sm_bytes = 0;  // SM share of every chunk (16-byte multiple)
   bool prelaunch = false;
   int sms = 148;

@@ -86,12 +86,12 @@ def test_sm_path_matches_reference_digest(d, stream_mode):
 
 
 @pytest.mark.parametrize("impl", ["pcpy", "b2b", "bcst", "swap", "prelaunch_pcpy", "prelaunch_b2b",
-                                  "prelaunch_bcst", "prelaunch_swap", "sm", "hybrid"])
+                                  "prelaunch_bcst", "prelaunch_swap", "sm", "hybrid", "pull"])
 @pytest.mark.parametrize("stream_mode", ["shared", "per_rank"])
 def test_repeated_calls_reuse_plans_and_flags(impl, stream_mode):
     n, s = 4, 8192 + 16
     kind = "allgather" if impl.endswith("bcst") else "alltoall"
-    if impl in ("pcpy", "b2b", "prelaunch_pcpy", "prelaunch_b2b", "sm", "hybrid"):
+    if impl in ("pcpy", "b2b", "prelaunch_pcpy", "prelaunch_b2b", "sm", "hybrid", "pull"):
         kinds = ["allgather", "alltoall"]
     else:
         kinds = [kind]
@@ -112,6 +112,8 @@ def test_repeated_calls_reuse_plans_and_flags(impl, stream_mode):
     ("alltoall", "swap", 8 << 20),
     ("alltoall", "hybrid", 8 << 20),
     ("allgather", "hybrid", 16 << 20),
+    ("alltoall", "pull", 8 << 20),
+    ("allgather", "pull", 16 << 20),
     ("allgather", "sm", 64 << 20),
     ("allgather", "bcst", 16 << 20),
     ("allgather", "prelaunch_pcpy", 16 << 20),

@@ -94,8 +94,8 @@ def _gpu_worker(rank, world, port, out, force_remote=False):
         O = ora.Oracle()
         s = 65536 + 64
         results = []
-        for kind, impls in (("alltoall", ["sm", "pcpy", "b2b", "prelaunch_pcpy", "swap"]),
-                            ("allgather", ["sm", "pcpy", "bcst", "prelaunch_b2b"])):
+        for kind, impls in (("alltoall", ["sm", "pcpy", "b2b", "prelaunch_pcpy", "swap", "hybrid", "pull"]),
+                            ("allgather", ["sm", "pcpy", "bcst", "prelaunch_b2b", "pull"])):
             in_bytes = s if kind == "allgather" else nranks * s
             # One symmetric window per rank: [send | recv].
             wins = [torch.full((in_bytes + nranks * s,), 0xA5, dtype=torch.uint8, device="cuda") for _ in comms]
@@ -242,4 +242,4 @@ def test_two_processes_share_one_gpu_through_ipc(force_remote):
         assert isinstance(results, list), results
         bad = [r for r in results if not r[2]]
         assert not bad, (rank, bad)
-        assert len(results) == 10
+        assert len(results) == 13

@@ -12,7 +12,8 @@ from oracle import oracle as ora
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-IMPLS = {"allgather": ["sm", "pcpy", "b2b", "bcst", "hybrid"], "alltoall": ["sm", "pcpy", "b2b", "swap", "hybrid"]}
+IMPLS = {"allgather": ["sm", "pcpy", "b2b", "bcst", "hybrid", "pull"],
+         "alltoall": ["sm", "pcpy", "b2b", "swap", "hybrid", "pull"]}
 CASES = [(k, i) for k in IMPLS for i in IMPLS[k]]
 
 
@@ -185,7 +186,7 @@ def test_hybrid_split_against_oracle(kind, pct, stream_mode, monkeypatch):
         cc.destroy_all(comms)
 
 
-@pytest.mark.parametrize("impl", ["pcpy", "b2b", "bcst", "swap", "sm", "hybrid", "prelaunch_pcpy",
+@pytest.mark.parametrize("impl", ["pcpy", "b2b", "bcst", "swap", "sm", "hybrid", "pull", "prelaunch_pcpy",
                                   "prelaunch_b2b", "prelaunch_swap"])
 def test_other_device_signal_path_on_one_gpu(impl, monkeypatch):
     """CECOLL_FORCE_REMOTE_SIGNALS=1 sends every cross-unit signal down the

@@ -89,7 +89,7 @@ int main(int argc, char** argv) {
   }
   std::printf("api,impl,collective,size_bytes,device_us_b2b,device_us_isolated,host_us\n");
   const char* names[] = {"sm", "pcpy", "b2b", "bcst", "swap", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_bcst",
-                         "prelaunch_swap", "hybrid"};
+                         "prelaunch_swap", "hybrid", "pull"};
   for (int kind = 0; kind < 2; ++kind) {
     for (size_t s = 4096; s <= max_s; s *= 4) {
       for (const char* name : names) {
