@@ -633,8 +633,11 @@ def run_sweep(world, rank, dev, nccl, stream, t_start, args, rows):
             ours = {k: v for k, v in row["us"].items() if v is not None and k != "nccl"}
             if ours:
                 row["best"] = min(ours, key=ours.get)
+                # fraction of the NVLink roofline (measured 770 GB/s per direction; busBW is per-GPU egress)
+                row["best_frac_nvlink"] = round(row["busbw"][row["best"]] / NVLINK_PEAK, 4)
                 if "nccl" in row["us"]:
                     row["best_over_nccl_time"] = round(ours[row["best"]] / row["us"]["nccl"], 3)
+                    row["nccl_frac_nvlink"] = round(row["busbw"]["nccl"] / NVLINK_PEAK, 4)
             rows.append(row)
             if rank == 0 and args.mgpu_verbose:
                 print(json.dumps(row), flush=True)
