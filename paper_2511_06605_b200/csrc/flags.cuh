@@ -21,22 +21,28 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Fused prologue (thread 0 of a CTA): CTA 0 first writes the folded start
-// signals, then every CTA waits for every incoming flag.
-__device__ __forceinline__ void fused_wait(const FlagSet& f) {
-  if (blockIdx.x == 0)
-    for (int i = 0; i < f.npre; ++i) st_release_sys(f.pre[i], 1);
-  for (int i = 0; i < f.npoll; ++i) {
-    const uint64_t* p = f.polls[i];
-    const unsigned long long t0 = globaltimer();
-    while (ld_acquire_sys(p) < 1) {
-      if (globaltimer() - t0 > kPollTimeoutNs) {
-        atomicOr(reinterpret_cast<unsigned long long*>(f.err), 1ull);
-        break;
-      }
-      __nanosleep(32);
+// One flag: spin (ld.acquire.sys, 20 s bound) until *p >= 1.
+__device__ __forceinline__ void wait_flag(const uint64_t* p, uint64_t* err) {
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_sys(p) < 1) {
+    if (globaltimer() - t0 > kPollTimeoutNs) {
+      atomicOr(reinterpret_cast<unsigned long long*>(err), 1ull);
+      return;
     }
+    __nanosleep(32);
   }
+}
+
+// Fused prologue, one full warp of a CTA (warp-level polling): CTA 0 first
+// writes the folded start signals, then lane i waits for flags i, i+32, ...
+// The closing __syncwarp orders every lane's acquire before the warp's (and,
+// after the caller's __syncthreads, the CTA's) data accesses.
+__device__ __forceinline__ void fused_wait(const FlagSet& f) {
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0)
+    for (int i = lane; i < f.npre; i += 32) st_release_sys(f.pre[i], 1);
+  for (int i = lane; i < f.npoll; i += 32) wait_flag(f.polls[i], f.err);
+  __syncwarp();
 }
 
 // Fused epilogue (thread 0 of a CTA, after the CTA's data writes are

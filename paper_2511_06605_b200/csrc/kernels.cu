@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
   if (flags.skip && *reinterpret_cast<const volatile uint64_t*>(flags.skip)) return;
   __shared__ int first[kMaxItemsSmem];
   for (int i = threadIdx.x; i < nitems; i += kRegThreads) first[i] = items[i].first_tile;
-  if ((flags.npoll || flags.npre) && threadIdx.x == 0) fused_wait(flags);
+  if ((flags.npoll || flags.npre) && threadIdx.x < 32) fused_wait(flags);
   __syncthreads();
   int cur = find_item(first, nitems, blockIdx.x);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -200,8 +200,8 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
   __shared__ int first[kMaxItemsSmem];
   for (int i = threadIdx.x; i < nitems; i += 32) first[i] = items[i].first_tile;
   __syncwarp();
+  if (flags.npoll || flags.npre) fused_wait(flags);  // the CTA is one warp
   if (threadIdx.x != 0) return;
-  if (flags.npoll || flags.npre) fused_wait(flags);
   for (int i = 0; i < kTmaStages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[i])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 
@@ -332,29 +332,27 @@ __global__ void gate_kernel(volatile uint64_t* posted, uint64_t* consumed, cudaG
 
 __global__ void gate_poll_kernel(volatile uint64_t* posted, uint64_t* consumed, uint64_t* const* flags, int n,
                                  uint64_t* skip, uint64_t* err) {
-  if (threadIdx.x != 0) return;
-  const uint64_t c = *consumed;
-  while (posted[0] <= c) __nanosleep(256);
-  const uint64_t kind = posted[1 + (c % 64)];
-  *consumed = c + 1;
-  if (kind != 1 && kind != 2) atomicOr(reinterpret_cast<unsigned long long*>(err), 2ull);
+  // Lane 0 takes the host post; on "go" the warp polls the flags in
+  // parallel (lane i: flags i, i+32, ...) and resets them.
+  __shared__ uint64_t kind;
+  if (threadIdx.x == 0) {
+    const uint64_t c = *consumed;
+    while (posted[0] <= c) __nanosleep(256);
+    kind = posted[1 + (c % 64)];
+    *consumed = c + 1;
+    if (kind != 1 && kind != 2) atomicOr(reinterpret_cast<unsigned long long*>(err), 2ull);
+  }
+  __syncwarp();
   if (kind != 1) {
-    *skip = 1;
+    if (threadIdx.x == 0) *skip = 1;
     return;
   }
-  for (int i = 0; i < n; ++i) {
-    uint64_t* f = flags[i];
-    const unsigned long long t0 = globaltimer();
-    while (ld_acquire_sys(f) < 1) {
-      if (globaltimer() - t0 > kPollTimeoutNs) {
-        atomicOr(reinterpret_cast<unsigned long long*>(err), 1ull);
-        break;
-      }
-      __nanosleep(32);
-    }
-    *f = 0;
+  for (int i = threadIdx.x; i < n; i += 32) {
+    wait_flag(flags[i], err);
+    *flags[i] = 0;
   }
-  *skip = 0;
+  __syncwarp();
+  if (threadIdx.x == 0) *skip = 0;
 }
 
 __global__ void __launch_bounds__(kRegThreads) mc_store_kernel(const int4* __restrict__ src, char* mc_dst,

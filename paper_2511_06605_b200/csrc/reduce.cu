@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const RedItem* __re
   __shared__ int first[kMaxItemsSmem];
   for (int i = threadIdx.x; i < nitems; i += kRedThreads) first[i] = items[i].first_tile;
   // Fused flags (kernels.hpp FlagSet): every source rank's send is ready.
-  if ((flags.npoll || flags.npre) && threadIdx.x == 0) fused_wait(flags);
+  if ((flags.npoll || flags.npre) && threadIdx.x < 32) fused_wait(flags);
   __syncthreads();
   int cur = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
