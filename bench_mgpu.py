@@ -76,6 +76,10 @@ class Watchdog:
     def _fire(self):
         phase = str(STATE.get("phase"))
         in_experiments = phase.startswith("experiment")
+        try:  # every rank holds the same line (value set on all ranks)
+            headline_done = self.line_fn().get("value") is not None
+        except Exception:  # noqa: BLE001
+            headline_done = False
         if self.rank == 0:
             try:
                 line = self.line_fn()
@@ -92,7 +96,9 @@ class Watchdog:
                 print(json.dumps(line), flush=True)
             except Exception:  # noqa: BLE001
                 pass
-        os._exit(0 if in_experiments else 1)
+        # The headline (value) was measured before the hang: the run stands,
+        # with the hung phase named in the line.
+        os._exit(0 if in_experiments or headline_done else 1)
 
     def cancel(self):
         self.t.cancel()

@@ -92,13 +92,15 @@ def test_consensus_helpers_over_gloo_world2():
         assert r["from0"] == {"impl": "from-0"}  # every rank runs rank 0's choice
 
 
-@pytest.mark.parametrize("phase,code", [("alltoall sm s=8 timing", 1), ("experiments sm_peer_tma alltoall", 0)])
-def test_watchdog_prints_the_line_and_exits(phase, code):
+@pytest.mark.parametrize("phase,code,value", [("alltoall sm s=8 timing", 1, None),
+                                              ("experiments sm_peer_tma alltoall", 0, None),
+                                              ("nccl alltoall", 0, 700.0)])
+def test_watchdog_prints_the_line_and_exits(phase, code, value):
     prog = textwrap.dedent(f"""
         import sys, time
         sys.path.insert(0, {ROOT!r})
         import bench_mgpu as bm
-        line = {{"metric": "m", "value": None, "config": {{"impl_trials": {{
+        line = {{"metric": "m", "value": {value!r}, "config": {{"impl_trials": {{
             "sm": {{"ms": 0.2, "busbw_gbs": 300.0}}, "pcpy": {{"error": "x"}}, "b2b": {{"ms": 0.1, "busbw_gbs": 600.0}}}}}}}}
         bm.STATE["phase"] = {phase!r}
         bm.Watchdog(0.2, 0, lambda: line)
@@ -107,8 +109,10 @@ def test_watchdog_prints_the_line_and_exits(phase, code):
     r = subprocess.run([sys.executable, "-c", prog], capture_output=True, text=True, timeout=60)
     assert r.returncode == code, r.stderr
     out = json.loads(r.stdout.strip().splitlines()[-1])
-    if code == 1:  # hung in the main measurement: best trial so far, flagged
+    if code == 1:  # hung before the headline: best trial so far, flagged
         assert out["value"] == 600.0 and out["config"]["impl"].startswith("b2b")
         assert "watchdog" in out["error"]
+    elif value is not None:  # hung after the headline: it stands, the phase is named
+        assert out["value"] == value and "nccl" in out["error"]
     else:  # hung in an experiment: the main line stands
         assert out["experiments"]["hung"] == phase and "error" not in out
