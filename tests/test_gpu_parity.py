@@ -315,3 +315,55 @@ def test_mem_alloc_buffers(kind, impl):
             c.mem_free(b)
     with pytest.raises(cc.CecollError):
         cs[0].mem_free(sends[0])
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("impl", ["sm", "pcpy", "b2b", "hybrid", "pull", "swap", "prelaunch_pcpy", "prelaunch_b2b"])
+def test_back_to_back_collectives_without_host_sync(impl, fresh=False):
+    """Flag reuse across collectives in flight: one stream
+    per rank; per iteration each rank's stream loads a fresh input, runs the
+    collective and copies its result out, with random spin delays — no host
+    synchronisation until the end. A destination overwritten before it
+    copied out the previous result (rdy), or a send buffer reloaded before
+    every peer finished reading it (done), changes some iteration's result."""
+    import random
+
+    n, s, iters = 4, 12288 + 16, 12
+    cs = cc.Comm.init_all([0] * n) if fresh else comms(n)
+    O = ora.Oracle()
+    rng = random.Random("b2b-" + impl)
+    in_place = impl.endswith("swap")
+    streams = [torch.cuda.Stream() for _ in range(n)]
+    hosts = [[ora.splitmix_pattern(n * s, r, 5000 + it) for r in range(n)] for it in range(iters)]
+    inputs = [[torch.from_numpy(hosts[it][r]).cuda() for r in range(n)] for it in range(iters)]
+    sends = [torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    recvs = sends if in_place else [torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    outs = [[torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)] for _ in range(iters)]
+    torch.cuda.synchronize()
+    for it in range(iters):
+        for r, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                if rng.random() < 0.5:
+                    torch.cuda._sleep(rng.randint(1000, 100000))
+                sends[r].copy_(inputs[it][r])
+        cc.all_to_all(cs, sends, recvs, s, impl=impl, streams=streams)
+        for r, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                if rng.random() < 0.5:
+                    torch.cuda._sleep(rng.randint(1000, 100000))
+                outs[it][r].copy_(recvs[r])
+    torch.cuda.synchronize()
+    for it in range(iters):
+        res = [t.cpu().numpy() for t in outs[it]]
+        assert O.check("alltoall", s, n, in_place, hosts[it], res) == -1, (impl, it)
+    if fresh:
+        cc.destroy_all(cs)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("impl", ["sm", "pcpy", "pull", "prelaunch_b2b"])
+def test_back_to_back_through_the_other_device_signal_path(impl, monkeypatch):
+    """The same, with every cross-unit signal on the other-device path
+    (signal kernels, folded start signals are not used: several units)."""
+    monkeypatch.setenv("CECOLL_FORCE_REMOTE_SIGNALS", "1")
+    test_back_to_back_collectives_without_host_sync(impl, fresh=True)
