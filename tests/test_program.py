@@ -188,3 +188,30 @@ def test_b200_selector_is_total_and_valid():
                 assert impl == "sm" or impl in cc.IMPLS_FOR[kind]
     assert cc.select("allgather", 1 << 30, 8, 1) == "sm"
     assert cc.select("alltoall", 4096, 8, 8) == "sm"
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/cecoll.h is the drop-in boundary for C callers (and cgo / JNI /
+    ctypes bindings): a C99 program compiles against it with -pedantic and
+    links against libcecoll.so; the program API runs without a GPU."""
+    import shutil
+    import subprocess
+
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no C compiler")
+    src = tmp_path / "t.c"
+    src.write_text(
+        '#include "cecoll.h"\n#include <stdio.h>\n'
+        "int main(void) {\n"
+        "  cecoll_program_t p = 0; int64_t m[5];\n"
+        "  if (cecoll_program_compile(CECOLL_ALLGATHER, CECOLL_IMPL_PCPY, 4096, 8, 16, &p) != CECOLL_SUCCESS) return 1;\n"
+        "  if (cecoll_program_metrics(p, m) != CECOLL_SUCCESS) return 2;\n"
+        '  printf("%lld %s\\n", (long long)m[0], cecoll_impl_name(CECOLL_IMPL_PULL));\n'
+        "  cecoll_program_free(p);\n  return 0;\n}\n")
+    libdir = os.path.dirname(cc.LIB_PATH)
+    exe = tmp_path / "t"
+    subprocess.run([gcc, "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", f"-I{os.path.join(ROOT, 'include')}",
+                    str(src), f"-L{libdir}", "-lcecoll", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
+    assert out == ["56", "pull"]  # n(n-1) copies (test_program.cpp:29-43)
