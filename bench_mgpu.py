@@ -442,6 +442,10 @@ def run(args, B):
     ok = all_true(ok)
     egress = nlocal * (n - nlocal) * s  # bytes leaving each GPU per collective
     nv = egress / (ms / 1e3) / 1e9
+    # the bound for this N: NVLink egress, or the GPU's own HBM traffic
+    # (every chunk of its ranks read once, every chunk for its ranks written once)
+    hbm_peak = B.load_peaks()[0]
+    bound_s = max(egress / (NVLINK_PEAK * 1e9), 2 * nlocal * n * s / (hbm_peak * 1e9))
     per = {k: (c1[k] - c0[k]) / args.steps for k in ("kernels", "graph_launches", "copies", "api_calls")}
     line.update({
         "value": round(value, 3), "ms_per_step": round(ms, 4), "parity_ok": ok,
@@ -449,7 +453,9 @@ def run(args, B):
                      "frac": round(nv / NVLINK_PEAK, 4), "traffic": None,
                      "frac_of_nominal_900": round(nv / NVLINK_NOMINAL, 4),
                      "peak_source": "measured peer copy per direction per GPU (B200_PROFILING.md)",
-                     "algorithmic_bytes_per_gpu": egress},
+                     "algorithmic_bytes_per_gpu": egress,
+                     "busbw_bound_gbs": round(busbw(n, s, bound_s * 1e3), 1),
+                     "bound_note": "max(NVLink egress / 770 GB/s, local HBM traffic / measured copy peak)"},
         "gpu_launches": int(round((per["kernels"] + 4 * per["graph_launches"]) * args.steps)),
         "launches_note": "kernels + 4 per recorded-graph launch (gate, poll, items, signal) in the timed "
                          "region on rank 0; copy-engine copies are counted in config.ce_copies_per_step",
