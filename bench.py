@@ -354,6 +354,7 @@ def run_ours(args):
             "traffic": load_traffic(),
             "peak_source": peak_kind + " hbm_gbs (copy, read+write)",
             "algorithmic_bytes_per_launch": alg_bytes,
+            "busbw_bound_gbs": round(busbw(n, s, alg_bytes / (peak * 1e9)), 1),
         },
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": n * n * s,
