@@ -270,6 +270,255 @@ Status fuse_sm_flags(World* w, Plan* p) {
 }  // namespace
 
 
+namespace {
+
+void set_key(Plan* p, const std::vector<CallArgs>& args) {
+  for (const CallArgs& a : args) {
+    p->key_rank.push_back(a.rank);
+    p->key_send.push_back(a.send);
+    p->key_recv.push_back(a.recv);
+    p->key_stream.push_back(a.stream);
+  }
+}
+
+// Every rank's send (and recv) as usable from this process: the call's own
+// pointers for local ranks, the peers' through the registered windows.
+Status resolve_addresses(World* w, const std::vector<CallArgs>& args, bool with_recv, Addressing* ad) {
+  const int n = w->nranks;
+  ad->send.assign(n, nullptr);
+  ad->recv.assign(n, nullptr);
+  std::vector<bool> have(n, false);
+  for (const CallArgs& a : args) {
+    if (a.rank < 0 || a.rank >= n || !w->local[a.rank]) return fail(CECOLL_INVALID_ARGUMENT, "rank not local");
+    if (have[a.rank]) return fail(CECOLL_INVALID_ARGUMENT, "rank appears twice in one group");
+    have[a.rank] = true;
+    ad->send[a.rank] = static_cast<const char*>(a.send);
+    ad->recv[a.rank] = static_cast<char*>(a.recv);
+  }
+  if (!w->multiprocess) {
+    for (int r = 0; r < n; ++r)
+      if (!have[r])
+        return fail(CECOLL_INVALID_ARGUMENT,
+                    "single-process communicator: every rank must take part (use cecoll_group_start/end)");
+    return {};
+  }
+  if (static_cast<int>(args.size()) != w->nlocal)
+    return fail(CECOLL_INVALID_ARGUMENT, "multi-process: every local rank must take part (group calls)");
+  const CallArgs& a = args[0];
+  for (int r = 0; r < n; ++r) {
+    if (have[r]) continue;
+    bool ok = true;
+    ad->send[r] = translate(w, a.rank, r, a.send, &ok);
+    if (with_recv) ad->recv[r] = translate(w, a.rank, r, a.recv, &ok);
+    if (!ok)
+      return fail(CECOLL_NOT_REGISTERED, with_recv ? "send/recv must lie in a window registered with cecoll_register"
+                                                   : "send must lie in a window registered with cecoll_register");
+  }
+  return {};
+}
+
+// Units: the local ranks sharing (device, stream). Returns unit_of[rank]
+// (-1 for ranks of other processes).
+std::vector<int> form_units(World* w, Plan* p, const std::vector<CallArgs>& args) {
+  std::vector<int> unit_of(w->nranks, -1);
+  for (const CallArgs& a : args) {
+    int found = -1;
+    for (size_t u = 0; u < p->units.size(); ++u)
+      if (p->units[u].device == w->device[a.rank] && p->units[u].stream == a.stream) found = static_cast<int>(u);
+    if (found < 0) {
+      Unit u;
+      u.device = w->device[a.rank];
+      u.stream = a.stream;
+      p->units.push_back(u);
+      found = static_cast<int>(p->units.size()) - 1;
+    }
+    p->units[found].ranks.push_back(a.rank);
+    unit_of[a.rank] = found;
+  }
+  for (Unit& u : p->units) std::sort(u.ranks.begin(), u.ranks.end());
+  return unit_of;
+}
+
+// Flag operations of the edges (r, j) between units: j
+// announces (rdy[j] in r's page) and waits for done[r]; with `unit_level`
+// (SM, hybrid, pull, reduce-scatter) r's unit polls rdy[j] and signals
+// done[r] itself — otherwise r's lanes do (lower_program).
+void add_edges(World* w, Plan* p, const std::vector<std::pair<int, int>>& edges, const std::vector<int>& unit_of,
+               bool unit_level) {
+  for (auto [r, j] : edges) {
+    if (unit_of[r] >= 0 && unit_of[r] == unit_of[j]) continue;  // stream order suffices
+    if (unit_of[j] >= 0) {
+      Unit& u = p->units[unit_of[j]];
+      u.start.push_back(op_write(slot(w, r, kSlotRdy + j), 1));
+      add_poll(u.finish, slot(w, j, kSlotDone + r));
+    }
+    if (unit_of[r] >= 0 && unit_level) {
+      Unit& u = p->units[unit_of[r]];
+      add_poll(u.sm_pre, slot(w, r, kSlotRdy + j));
+      u.sm_post.push_back(op_write(slot(w, j, kSlotDone + r), 1));
+    }
+  }
+}
+
+int device_sms(int device) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return sms;
+}
+
+// Hybrid and pull. Each chunk: bytes [0, ce) by a
+// copy-engine lane (lane d-1 of rank r carries the chunk to (r+d)%n, the
+// pcpy rotation of compiler.cpp:150 — or, pulling, reads it from there),
+// bytes [ce, s) by the unit's SM mover; the local slot entirely by the mover.
+Status lower_hybrid(World* w, Plan* p, Kind kind, int64_t s, const Addressing& ad) {
+  const int n = w->nranks;
+  const int64_t sm_b = p->hybrid_sm_bytes, ce = s - sm_b;
+  for (Unit& u : p->units) {
+    std::vector<HostItem> items;
+    for (int r : u.ranks) {
+      const char* src_ag = ad.send[r];
+      for (const Copy& c : u.placement)
+        if (c.dst == ad.recv[r] + r * s) items.push_back({make_item(kItemCopy, c.src, c.dst, nullptr, c.bytes), {}});
+      if (kind == Kind::AllGather && sm_b > 0) {
+        HostItem h{make_item(kItemFan, src_ag + ce, nullptr, nullptr, sm_b), {}};
+        for (int d = 1; d < n; ++d) {
+          const int j = (r + d) % n;
+          h.fan.push_back(ad.recv[j] + r * s + ce);
+          h.remote |= w->device[j] != u.device;
+        }
+        if (h.fan.size() == 1) h.item = make_item(kItemCopy, src_ag + ce, h.fan[0], nullptr, sm_b), h.fan.clear();
+        items.push_back(h);
+      }
+      for (int d = 1; d < n; ++d) {
+        const int j = (r + d) % n;
+        // push: r's chunk to j; pull: j's chunk read into r (lane d-1 of r either way)
+        const char* src = p->pull ? (kind == Kind::AllGather ? ad.send[j] : ad.send[j] + r * s)
+                                  : (kind == Kind::AllGather ? src_ag : ad.send[r] + j * s);
+        char* dst = p->pull ? ad.recv[r] + j * s : ad.recv[j] + r * s;
+        if (kind == Kind::AllToAll && sm_b > 0)
+          items.push_back({make_item(kItemCopy, src + ce, dst + ce, nullptr, sm_b), {}, w->device[j] != u.device});
+        if (ce > 0) {
+          LaneExec le;
+          le.rank = r;
+          le.lane = d - 1;
+          le.copies.push_back({dst, src, ce});
+          STATUS_TRY(ensure_lanes(w->local[r].get(), d));
+          p->lanes.push_back(std::move(le));
+        }
+      }
+    }
+    u.placement.clear();
+    STATUS_TRY(upload_items(p, u.device, items, &u.table));
+  }
+  return {};
+}
+
+// The SM path: one item table per unit holding every chunk
+// of its ranks, the local placement included.
+Status lower_sm(World* w, Plan* p, Kind kind, int64_t s, const Addressing& ad) {
+  const int n = w->nranks;
+  for (Unit& u : p->units) {
+    std::vector<HostItem> items;
+    for (int r : u.ranks) {
+      if (kind == Kind::AllGather) {
+        // One read of the source chunk, one write per rank's slot r (local
+        // slot first, then the pcpy rotation): n*s + n*n*s bytes instead of
+        // 2*n*n*s for n separate copies.
+        HostItem h{make_item(kItemFan, ad.send[r], nullptr, nullptr, s), {}};
+        for (int d = 0; d < n; ++d) {
+          char* dst = ad.recv[(r + d) % n] + r * s;
+          if (dst != ad.send[r]) h.fan.push_back(dst);
+          h.remote |= w->device[(r + d) % n] != u.device;
+        }
+        if (h.fan.size() == 1) h.item = make_item(kItemCopy, ad.send[r], h.fan[0], nullptr, s), h.fan.clear();
+        if (!h.fan.empty() || h.item.kind == kItemCopy) items.push_back(h);
+        continue;
+      }
+      for (const Copy& c : u.placement)
+        if (c.dst == ad.recv[r] + r * s) items.push_back({make_item(kItemCopy, c.src, c.dst, nullptr, c.bytes), {}});
+      for (int d = 1; d < n; ++d) {
+        const int j = (r + d) % n;
+        items.push_back({make_item(kItemCopy, ad.send[r] + j * s, ad.recv[j] + r * s, nullptr, s), {},
+                         w->device[j] != u.device});
+      }
+    }
+    u.placement.clear();
+    STATUS_TRY(upload_items(p, u.device, items, &u.table));
+  }
+  return {};
+}
+
+// A command program's lanes: copies stay copy-engine
+// commands; broadcast / swap become item kernels. A recorded (prelaunch)
+// graph moves its same-device chunks with one item kernel per unit instead
+// of one memcpy node per copy: the driver runs same-device memcpy on SMs
+// anyway (profiles/ce_probe2_r01.txt) and every graph node costs launch
+// latency. Cross-device copies stay memcpy nodes (copy engines over NVLink).
+// CECOLL_GRAPH_MEMCPY=1 keeps every copy a memcpy node.
+Status lower_program(World* w, Plan* p, const Addressing& ad, const std::vector<int>& unit_of, bool in_place_impl) {
+  auto base = [&](int rank, Buf b) -> char* {  // in place (swap): Input is `recv` (compiler.cpp:119-122)
+    if (in_place_impl || b == Buf::Output) return ad.recv[rank];
+    return const_cast<char*>(ad.send[rank]);
+  };
+  auto addr = [&](const Region& r) { return base(r.rank, r.buf) + r.off; };
+  auto same_unit = [&](int a, int b) { return unit_of[a] >= 0 && unit_of[a] == unit_of[b]; };
+  const char* gm = std::getenv("CECOLL_GRAPH_MEMCPY");
+  const bool merge = p->prelaunch && !(gm && std::string(gm) == "1");
+  std::vector<std::vector<HostItem>> unit_items(p->units.size());
+  if (merge)
+    for (size_t ui = 0; ui < p->units.size(); ++ui) {
+      for (const Copy& c : p->units[ui].placement)
+        unit_items[ui].push_back({make_item(kItemCopy, c.src, c.dst, nullptr, c.bytes), {}});
+      p->units[ui].placement.clear();
+    }
+  for (const Lane& l : p->program.lanes) {  // lanes owned by local ranks
+    if (unit_of[l.rank] < 0) continue;
+    LaneExec le;
+    le.rank = l.rank;
+    le.lane = l.index;
+    std::set<int> dests;
+    std::vector<HostItem> items;
+    const int dev = w->device[l.rank];
+    for (const Command& c : l.cmds) {
+      const bool local_cmd = w->device[c.src.rank] == dev && w->device[c.dst.rank] == dev &&
+                             (c.op != Op::Broadcast || w->device[c.dst2.rank] == dev) &&
+                             (c.op != Op::Swap || w->device[c.peer.rank] == dev);
+      std::vector<HostItem>& sink = merge && local_cmd ? unit_items[unit_of[l.rank]] : items;
+      switch (c.op) {
+        case Op::Copy:
+          if (merge && local_cmd) sink.push_back({make_item(kItemCopy, addr(c.src), addr(c.dst), nullptr, c.size), {}});
+          else le.copies.push_back({addr(c.dst), addr(c.src), c.size});
+          dests.insert(c.dst.rank);
+          break;
+        case Op::Broadcast:
+          sink.push_back({make_item(kItemBcst, addr(c.src), addr(c.dst), addr(c.dst2), c.size), {}, !local_cmd});
+          dests.insert(c.dst.rank);
+          dests.insert(c.dst2.rank);
+          break;
+        case Op::Swap:
+          sink.push_back({make_item(kItemSwap, addr(c.peer), addr(c.src), nullptr, c.size), {}, !local_cmd});
+          dests.insert(c.peer.rank);
+          break;
+        default: break;  // Signal / Poll: realised by the flag operations below
+      }
+    }
+    dests.erase(l.rank);
+    for (int j : dests) {
+      if (same_unit(l.rank, j)) continue;
+      add_poll(le.pre, slot(w, l.rank, kSlotRdy + j));
+      le.post.push_back(op_write(slot(w, j, kSlotDone + l.rank), 1));
+    }
+    STATUS_TRY(upload_items(p, w->device[l.rank], items, &le.table));
+    STATUS_TRY(ensure_lanes(w->local[l.rank].get(), l.index + 1));
+    p->lanes.push_back(std::move(le));
+  }
+  for (size_t ui = 0; ui < p->units.size(); ++ui)
+    STATUS_TRY(upload_items(p, p->units[ui].device, unit_items[ui], &p->units[ui].table));
+  return {};
+}
+
+}  // namespace
+
 Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args, Plan** out,
                    const Program* given) {
   const int n = w->nranks;
@@ -279,12 +528,7 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
   Plan* p = plan.get();
   p->kind = kind;
   p->chunk = s;
-  for (const CallArgs& a : args) {
-    p->key_rank.push_back(a.rank);
-    p->key_send.push_back(a.send);
-    p->key_recv.push_back(a.recv);
-    p->key_stream.push_back(a.stream);
-  }
+  set_key(p, args);
   if (given) {
     if (given->spec.kind != kind || given->spec.chunk != s || given->spec.nranks != n)
       return fail(CECOLL_INVALID_ARGUMENT, "program spec does not match the communicator / call");
@@ -318,69 +562,15 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
     p->hybrid_sm_bytes = p->pull ? 0 : (s * pct / 100) & ~int64_t{15};
   }
 
-  // Addresses of every rank's buffers as usable from this process.
   Addressing ad;
-  ad.send.assign(n, nullptr);
-  ad.recv.assign(n, nullptr);
-  std::vector<bool> have(n, false);
-  for (const CallArgs& a : args) {
-    if (a.rank < 0 || a.rank >= n || !w->local[a.rank]) return fail(CECOLL_INVALID_ARGUMENT, "rank not local");
-    if (have[a.rank]) return fail(CECOLL_INVALID_ARGUMENT, "rank appears twice in one group");
-    have[a.rank] = true;
-    ad.send[a.rank] = static_cast<const char*>(a.send);
-    ad.recv[a.rank] = static_cast<char*>(a.recv);
-  }
-  if (!w->multiprocess) {
-    for (int r = 0; r < n; ++r)
-      if (!have[r])
-        return fail(CECOLL_INVALID_ARGUMENT,
-                    "single-process communicator: every rank must take part (use cecoll_group_start/end)");
-  } else {
-    if (static_cast<int>(args.size()) != w->nlocal)
-      return fail(CECOLL_INVALID_ARGUMENT, "multi-process: every local rank must take part (group calls)");
-    const CallArgs& a = args[0];
-    for (int r = 0; r < n; ++r) {
-      if (have[r]) continue;
-      bool ok = true;
-      ad.send[r] = translate(w, a.rank, r, a.send, &ok);
-      ad.recv[r] = translate(w, a.rank, r, a.recv, &ok);
-      if (!ok) return fail(CECOLL_NOT_REGISTERED, "send/recv must lie in a window registered with cecoll_register");
-    }
-  }
-  for (const CallArgs& a : args) {
-    const bool aliased = a.send == a.recv;
-    if (kind == Kind::AllToAll && aliased && !in_place_impl)
+  STATUS_TRY(resolve_addresses(w, args, true, &ad));
+  for (const CallArgs& a : args)
+    if (kind == Kind::AllToAll && a.send == a.recv && !in_place_impl)
       return fail(CECOLL_INVALID_ARGUMENT, "alltoall in place requires the swap implementation");
-  }
+  const std::vector<int> unit_of = form_units(w, p, args);
 
-  // Units: local ranks sharing (device, stream).
-  std::vector<int> unit_of(n, -1);
-  for (const CallArgs& a : args) {
-    int found = -1;
-    for (size_t u = 0; u < p->units.size(); ++u)
-      if (p->units[u].device == w->device[a.rank] && p->units[u].stream == a.stream) found = static_cast<int>(u);
-    if (found < 0) {
-      Unit u;
-      u.device = w->device[a.rank];
-      u.stream = a.stream;
-      p->units.push_back(u);
-      found = static_cast<int>(p->units.size()) - 1;
-    }
-    p->units[found].ranks.push_back(a.rank);
-    unit_of[a.rank] = found;
-  }
-  for (Unit& u : p->units) std::sort(u.ranks.begin(), u.ranks.end());
-  auto same_unit = [&](int a, int b) { return unit_of[a] >= 0 && unit_of[a] == unit_of[b]; };
-
-  // Buffer of a program region. In-place programs (swap) address the
-  // in-place buffer as Input (compiler.cpp:119-122); it is `recv`.
-  auto base = [&](int rank, Buf b) -> char* {
-    if (in_place_impl || b == Buf::Output) return ad.recv[rank];
-    return const_cast<char*>(ad.send[rank]);
-  };
-  auto addr = [&](const Region& r) { return base(r.rank, r.buf) + r.off; };
-
-  // Edges writer -> destination and the flag operations they imply.
+  // Edges writer -> destination (SM / hybrid: every pair; pull: reader ->
+  // source) and the flag operations they imply.
   std::vector<std::pair<int, int>> edges;
   if (p->sm) {
     for (int r = 0; r < n; ++r)
@@ -405,26 +595,13 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
           if (d && d->rank != l.rank) edges.push_back({l.rank, d->rank});
       }
   }
-  for (auto [r, j] : edges) {
-    if (same_unit(r, j)) continue;
-    if (unit_of[j] >= 0) {  // j is local: it announces readiness and waits for r's data
-      Unit& u = p->units[unit_of[j]];
-      u.start.push_back(op_write(slot(w, r, kSlotRdy + j), 1));
-      add_poll(u.finish, slot(w, j, kSlotDone + r));
-    }
-    if (unit_of[r] >= 0 && p->sm) {  // r is local: wait for j, then signal it
-      Unit& u = p->units[unit_of[r]];
-      add_poll(u.sm_pre, slot(w, r, kSlotRdy + j));
-      u.sm_post.push_back(op_write(slot(w, j, kSlotDone + r), 1));
-    }
-  }
+  add_edges(w, p, edges, unit_of, p->sm);
 
   // Local-slot placement (verifier.cpp:40-44) and the swap pre-copy.
   for (Unit& u : p->units)
     for (int r : u.ranks) {
       if (in_place_impl) {
-        if (ad.send[r] != ad.recv[r])
-          u.precopy.push_back({ad.recv[r], ad.send[r], s * n});
+        if (ad.send[r] != ad.recv[r]) u.precopy.push_back({ad.recv[r], ad.send[r], s * n});
         continue;
       }
       const char* src = ad.send[r] + (kind == Kind::AllGather ? 0 : r * s);
@@ -432,149 +609,10 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
       if (src != dst) u.placement.push_back({dst, src, s});
     }
 
-  if (p->hybrid) {
-    // Each chunk: bytes [0, ce) by a copy-engine lane (lane d-1 of rank r
-    // carries the chunk to (r+d)%n, the pcpy rotation of compiler.cpp:150),
-    // bytes [ce, s) by the unit's SM mover; the local slot entirely by the
-    // mover. Flags are the SM path's (unit-level rdy polls before the lanes
-    // fork, done signals after they join).
-    const int64_t sm_b = p->hybrid_sm_bytes, ce = s - sm_b;
-    for (Unit& u : p->units) {
-      std::vector<HostItem> items;
-      for (int r : u.ranks) {
-        const char* src_ag = ad.send[r];
-        for (const Copy& c : u.placement)
-          if (c.dst == ad.recv[r] + r * s) items.push_back({make_item(kItemCopy, c.src, c.dst, nullptr, c.bytes), {}});
-        if (kind == Kind::AllGather && sm_b > 0) {
-          HostItem h{make_item(kItemFan, src_ag + ce, nullptr, nullptr, sm_b), {}};
-          for (int d = 1; d < n; ++d) {
-            const int j = (r + d) % n;
-            h.fan.push_back(ad.recv[j] + r * s + ce);
-            h.remote |= w->device[j] != u.device;
-          }
-          if (h.fan.size() == 1) h.item = make_item(kItemCopy, src_ag + ce, h.fan[0], nullptr, sm_b), h.fan.clear();
-          items.push_back(h);
-        }
-        for (int d = 1; d < n; ++d) {
-          const int j = (r + d) % n;
-          // push: r's chunk to j; pull: j's chunk read into r (lane d-1 of r either way)
-          const char* src = p->pull ? (kind == Kind::AllGather ? ad.send[j] : ad.send[j] + r * s)
-                                    : (kind == Kind::AllGather ? src_ag : ad.send[r] + j * s);
-          char* dst = p->pull ? ad.recv[r] + j * s : ad.recv[j] + r * s;
-          if (kind == Kind::AllToAll && sm_b > 0)
-            items.push_back({make_item(kItemCopy, src + ce, dst + ce, nullptr, sm_b), {}, w->device[j] != u.device});
-          if (ce > 0) {
-            LaneExec le;
-            le.rank = r;
-            le.lane = d - 1;
-            le.copies.push_back({dst, src, ce});
-            STATUS_TRY(ensure_lanes(w->local[r].get(), d));
-            p->lanes.push_back(std::move(le));
-          }
-        }
-      }
-      u.placement.clear();
-      STATUS_TRY(upload_items(p, u.device, items, &u.table));
-    }
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->units[0].device);
-    p->sms = sms;
-  } else if (p->sm) {
-    for (Unit& u : p->units) {
-      std::vector<HostItem> items;
-      for (int r : u.ranks) {
-        if (kind == Kind::AllGather) {
-          // One read of the source chunk, one write per rank's slot r (local
-          // slot first, then the pcpy rotation): n*s + n*n*s bytes instead
-          // of 2*n*n*s for n separate copies.
-          HostItem h{make_item(kItemFan, ad.send[r], nullptr, nullptr, s), {}};
-          for (int d = 0; d < n; ++d) {
-            char* dst = ad.recv[(r + d) % n] + r * s;
-            if (dst != ad.send[r]) h.fan.push_back(dst);
-            h.remote |= w->device[(r + d) % n] != u.device;
-          }
-          if (h.fan.size() == 1) h.item = make_item(kItemCopy, ad.send[r], h.fan[0], nullptr, s), h.fan.clear();
-          if (!h.fan.empty() || h.item.kind == kItemCopy) items.push_back(h);
-          continue;
-        }
-        for (const Copy& c : u.placement)
-          if (c.dst == ad.recv[r] + r * s) items.push_back({make_item(kItemCopy, c.src, c.dst, nullptr, c.bytes), {}});
-        for (int d = 1; d < n; ++d) {
-          const int j = (r + d) % n;
-          items.push_back({make_item(kItemCopy, ad.send[r] + j * s, ad.recv[j] + r * s, nullptr, s), {},
-                           w->device[j] != u.device});
-        }
-      }
-      u.placement.clear();
-      STATUS_TRY(upload_items(p, u.device, items, &u.table));
-    }
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->units[0].device);
-    p->sms = sms;
-  } else {
-    // A recorded (prelaunch) graph moves its same-device chunks with one item
-    // kernel per unit instead of one memcpy node per copy: the driver runs
-    // same-device memcpy on SMs anyway (profiles/ce_probe2_r01.txt) and every
-    // graph node costs launch latency. Cross-device copies stay memcpy nodes
-    // (copy engines over NVLink). CECOLL_GRAPH_MEMCPY=1 keeps every copy a
-    // memcpy node.
-    const char* gm = std::getenv("CECOLL_GRAPH_MEMCPY");
-    const bool merge = p->prelaunch && !(gm && std::string(gm) == "1");
-    std::vector<std::vector<HostItem>> unit_items(p->units.size());
-    if (merge)
-      for (size_t ui = 0; ui < p->units.size(); ++ui) {
-        for (const Copy& c : p->units[ui].placement)
-          unit_items[ui].push_back({make_item(kItemCopy, c.src, c.dst, nullptr, c.bytes), {}});
-        p->units[ui].placement.clear();
-      }
-    // Lanes of the command program owned by local ranks.
-    for (const Lane& l : p->program.lanes) {
-      if (unit_of[l.rank] < 0) continue;
-      LaneExec le;
-      le.rank = l.rank;
-      le.lane = l.index;
-      std::set<int> dests;
-      std::vector<HostItem> items;
-      const int dev = w->device[l.rank];
-      for (const Command& c : l.cmds) {
-        const bool local_cmd = w->device[c.src.rank] == dev && w->device[c.dst.rank] == dev &&
-                               (c.op != Op::Broadcast || w->device[c.dst2.rank] == dev) &&
-                               (c.op != Op::Swap || w->device[c.peer.rank] == dev);
-        std::vector<HostItem>& sink = merge && local_cmd ? unit_items[unit_of[l.rank]] : items;
-        switch (c.op) {
-          case Op::Copy:
-            if (merge && local_cmd) sink.push_back({make_item(kItemCopy, addr(c.src), addr(c.dst), nullptr, c.size), {}});
-            else le.copies.push_back({addr(c.dst), addr(c.src), c.size});
-            dests.insert(c.dst.rank);
-            break;
-          case Op::Broadcast:
-            sink.push_back({make_item(kItemBcst, addr(c.src), addr(c.dst), addr(c.dst2), c.size), {}, !local_cmd});
-            dests.insert(c.dst.rank);
-            dests.insert(c.dst2.rank);
-            break;
-          case Op::Swap:
-            sink.push_back({make_item(kItemSwap, addr(c.peer), addr(c.src), nullptr, c.size), {}, !local_cmd});
-            dests.insert(c.peer.rank);
-            break;
-          default: break;  // Signal / Poll: realised by the flag operations below
-        }
-      }
-      dests.erase(l.rank);
-      for (int j : dests) {
-        if (same_unit(l.rank, j)) continue;
-        add_poll(le.pre, slot(w, l.rank, kSlotRdy + j));
-        le.post.push_back(op_write(slot(w, j, kSlotDone + l.rank), 1));
-      }
-      STATUS_TRY(upload_items(p, w->device[l.rank], items, &le.table));
-      STATUS_TRY(ensure_lanes(w->local[l.rank].get(), l.index + 1));
-      p->lanes.push_back(std::move(le));
-    }
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->units[0].device);
-    p->sms = sms;
-    for (size_t ui = 0; ui < p->units.size(); ++ui)
-      STATUS_TRY(upload_items(p, p->units[ui].device, unit_items[ui], &p->units[ui].table));
-  }
+  if (p->hybrid) STATUS_TRY(lower_hybrid(w, p, kind, s, ad));
+  else if (p->sm) STATUS_TRY(lower_sm(w, p, kind, s, ad));
+  else STATUS_TRY(lower_program(w, p, ad, unit_of, in_place_impl));
+  p->sms = device_sms(p->units[0].device);
   STATUS_TRY(split_remote(w, p));
   if (p->sm) STATUS_TRY(fuse_sm_flags(w, p));
   if (p->prelaunch)
@@ -670,41 +708,14 @@ Status plan_create_rs(World* w, Impl impl, int64_t count, int dtype, int op, con
   p->dtype = dtype;
   p->op = op;
   p->sm = impl == Impl::Sm;
-  for (const CallArgs& a : args) {
-    p->key_rank.push_back(a.rank);
-    p->key_send.push_back(a.send);
-    p->key_recv.push_back(a.recv);
-    p->key_stream.push_back(a.stream);
-  }
-  std::vector<const char*> send(n, nullptr);
-  std::vector<char*> recv(n, nullptr);
-  std::vector<bool> have(n, false);
-  for (const CallArgs& a : args) {
-    if (a.rank < 0 || a.rank >= n || !w->local[a.rank]) return fail(CECOLL_INVALID_ARGUMENT, "rank not local");
-    if (have[a.rank]) return fail(CECOLL_INVALID_ARGUMENT, "rank appears twice in one group");
-    have[a.rank] = true;
-    send[a.rank] = static_cast<const char*>(a.send);
-    recv[a.rank] = static_cast<char*>(a.recv);
-  }
-  if (!w->multiprocess) {
-    for (int r = 0; r < n; ++r)
-      if (!have[r])
-        return fail(CECOLL_INVALID_ARGUMENT,
-                    "single-process communicator: every rank must take part (use cecoll_group_start/end)");
-  } else {
-    if (static_cast<int>(args.size()) != w->nlocal)
-      return fail(CECOLL_INVALID_ARGUMENT, "multi-process: every local rank must take part (group calls)");
-    if (!p->sm) return fail(CECOLL_UNSUPPORTED, "reduce-scatter over copy engines needs a single-process communicator");
-    for (int r = 0; r < n; ++r) {
-      if (have[r]) continue;
-      bool ok = true;
-      send[r] = translate(w, args[0].rank, r, args[0].send, &ok);
-      if (!ok) return fail(CECOLL_NOT_REGISTERED, "send must lie in a window registered with cecoll_register");
-    }
-  }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, w->device[args[0].rank]);
-  p->sms = sms;
+  set_key(p, args);
+  if (w->multiprocess && !p->sm)
+    return fail(CECOLL_UNSUPPORTED, "reduce-scatter over copy engines needs a single-process communicator");
+  Addressing ad;  // the readers need every rank's send; recv stays local
+  STATUS_TRY(resolve_addresses(w, args, false, &ad));
+  const std::vector<const char*>& send = ad.send;
+  const std::vector<char*>& recv = ad.recv;
+  p->sms = device_sms(w->device[args[0].rank]);
 
   if (!p->sm) {
     // Copy-engine gather: chunk j of every rank lands in rank j's staging
@@ -743,38 +754,12 @@ Status plan_create_rs(World* w, Impl impl, int64_t count, int dtype, int op, con
     return {};
   }
 
-  // SM path: units, flags (rank j reads every rank i's send), reductions.
-  std::vector<int> unit_of(n, -1);
-  for (const CallArgs& a : args) {
-    int found = -1;
-    for (size_t u = 0; u < p->units.size(); ++u)
-      if (p->units[u].device == w->device[a.rank] && p->units[u].stream == a.stream) found = static_cast<int>(u);
-    if (found < 0) {
-      Unit u;
-      u.device = w->device[a.rank];
-      u.stream = a.stream;
-      p->units.push_back(u);
-      found = static_cast<int>(p->units.size()) - 1;
-    }
-    p->units[found].ranks.push_back(a.rank);
-    unit_of[a.rank] = found;
-  }
-  for (Unit& u : p->units) std::sort(u.ranks.begin(), u.ranks.end());
+  // SM path: units, flags (edge (r, j): rank r reads rank j's send), reductions.
+  const std::vector<int> unit_of = form_units(w, p, args);
+  std::vector<std::pair<int, int>> edges;
   for (int r = 0; r < n; ++r)
-    for (int d = 1; d < n; ++d) {
-      const int j = (r + d) % n;  // r reads j's send
-      if (unit_of[r] >= 0 && unit_of[r] == unit_of[j]) continue;
-      if (unit_of[j] >= 0) {
-        Unit& u = p->units[unit_of[j]];
-        u.start.push_back(op_write(slot(w, r, kSlotRdy + j), 1));
-        add_poll(u.finish, slot(w, j, kSlotDone + r));
-      }
-      if (unit_of[r] >= 0) {
-        Unit& u = p->units[unit_of[r]];
-        add_poll(u.sm_pre, slot(w, r, kSlotRdy + j));
-        u.sm_post.push_back(op_write(slot(w, j, kSlotDone + r), 1));
-      }
-    }
+    for (int d = 1; d < n; ++d) edges.push_back({r, (r + d) % n});
+  add_edges(w, p, edges, unit_of, true);
   for (Unit& u : p->units) {
     std::vector<RedItem> items;
     std::vector<std::vector<const char*>> srcs;
