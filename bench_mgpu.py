@@ -35,10 +35,14 @@ import paper_2511_06605_b200 as cc
 NVLINK_PEAK = 770.0  # measured peer copy GB/s per direction (B200_PROFILING.md)
 NVLINK_NOMINAL = 900.0
 
-AG_IMPLS = ["sm", "pcpy", "b2b", "bcst", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_bcst", "hybrid", "pull"]
-AA_IMPLS = ["sm", "pcpy", "b2b", "swap", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_swap", "hybrid", "pull"]
-# headline trials also scan the hybrid's SM share ("impl@pct": CECOLL_HYBRID_SM_PCT at plan creation)
-HEADLINE_EXTRA = ["hybrid@25", "hybrid@75"]
+# Per sweep size, the prelaunch forms last: their cross-device bodies are
+# conditional graphs with copy-engine nodes, the least exercised form.
+AG_IMPLS = ["sm", "pcpy", "b2b", "bcst", "hybrid", "pull", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_bcst"]
+AA_IMPLS = ["sm", "pcpy", "b2b", "swap", "hybrid", "pull", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_swap"]
+# Headline trials: every non-prelaunch form plus the hybrid's SM-share scan
+# ("impl@pct": CECOLL_HYBRID_SM_PCT at plan creation). The prelaunch forms
+# are measured in the sweep, after the headline is in the line.
+HEADLINE_IMPLS = ["sm", "pcpy", "b2b", "swap", "hybrid", "pull", "hybrid@25", "hybrid@75"]
 
 STATE: dict = {}  # what the watchdog prints if a collective hangs
 
@@ -387,7 +391,7 @@ def run(args, B):
     torch.cuda.synchronize()
 
     # --- implementation trials (consensus), then the winner -----------------
-    cands = AA_IMPLS + HEADLINE_EXTRA if args.algo == "auto" else [args.algo]
+    cands = HEADLINE_IMPLS if args.algo == "auto" else [args.algo]
     trials, plans = {}, {}
     line["config"]["impl_trials"] = trials
     for impl in cands:
