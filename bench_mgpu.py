@@ -172,7 +172,7 @@ def try_impl(comms, kind, impl, sends, recvs, expects, s, iters, stream):
             plan.destroy()
         return None, {"error": err or "plan failed on another rank"}
     dist.barrier()
-    STATE["phase"] = f"{kind} {impl} s={s} parity"
+    STATE["phase"] = f"{STATE.get('prefix', '')}{kind} {impl} s={s} parity"
     try:
         plan.launch(stream)
         stream.synchronize()
@@ -188,7 +188,7 @@ def try_impl(comms, kind, impl, sends, recvs, expects, s, iters, stream):
         except cc.CecollError:
             pass
         return None, {"error": err or "parity failed"}
-    STATE["phase"] = f"{kind} {impl} s={s} timing"
+    STATE["phase"] = f"{STATE.get('prefix', '')}{kind} {impl} s={s} timing"
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(2):
         plan.launch(stream)
@@ -520,6 +520,12 @@ def run(args, B):
         STATE["phase"] = "experiments"
         line["experiments"] = {}
         run_experiments(comms, sets, n, s, my_ranks, stream, line["experiments"])
+    if not args.no_mgpu_sweep and "sweep" in line:
+        STATE["phase"] = "experiments-grade sweep (prelaunch forms)"
+        STATE["prefix"] = "experiments-grade sweep: "  # a hang here leaves the main line standing
+        sweep_pass(world, rank, dev, nccl, stream, t_start, args, line["sweep"]["rows"], prelaunch=True)
+        STATE["prefix"] = ""
+    if not args.no_mgpu_experiments:
         STATE["phase"] = "experiments multicast"
         run_mc_experiment(world, rank, dev, stream, line["experiments"])
     line["config"]["wall_s"] = round(time.time() - t_start, 1)
@@ -603,9 +609,25 @@ def run_e2e(comms, plans, best, sets, expects, s, n, nlocal, stream, args):
                         f"{nlocal} ranks' buffers over its own PCIe link; bytes are whole-job"}
 
 
-def run_sweep(world, rank, dev, nccl, stream, t_start, args, rows):
-    """AG and AA with one rank per GPU: every implementation (consensus,
-    parity) and NCCL per size; latency in us and busBW in GB/s."""
+def summarize(row):
+    """Winner and roofline fractions of one sweep row (recomputed whenever a
+    pass adds implementations)."""
+    ours = {k: v for k, v in row["us"].items() if v is not None and k != "nccl"}
+    if not ours:
+        return
+    row["best"] = min(ours, key=ours.get)
+    # fraction of the NVLink roofline (measured 770 GB/s per direction; busBW is per-GPU egress)
+    row["best_frac_nvlink"] = round(row["busbw"][row["best"]] / NVLINK_PEAK, 4)
+    if row["us"].get("nccl"):
+        row["best_over_nccl_time"] = round(ours[row["best"]] / row["us"]["nccl"], 3)
+        row["nccl_frac_nvlink"] = round(row["busbw"]["nccl"] / NVLINK_PEAK, 4)
+
+
+def sweep_pass(world, rank, dev, nccl, stream, t_start, args, rows, prelaunch):
+    """One pass over (kind, size): the non-prelaunch implementations with NCCL
+    and the reduce-scatter (prelaunch=False, new rows), or only the prelaunch
+    forms, merged into the existing rows (prelaunch=True, run near the end:
+    their cross-device bodies are the least exercised graphs)."""
     n = world
     smax = 1 << int(args.mgpu_sweep_max).bit_length() - 1
     comms = cc.Comm.init_ranks(n, rank, 1, dev, cc.torch_exchange())
@@ -617,12 +639,20 @@ def run_sweep(world, rank, dev, nccl, stream, t_start, args, rows):
     while s <= smax:
         sizes.append(s)
         s *= 4
+    by_key = {(r["kind"], r["s"]): r for r in rows}
     for kind in ("allgather", "alltoall"):
+        impls = [i for i in (AG_IMPLS if kind == "allgather" else AA_IMPLS) if i.startswith("prelaunch") == prelaunch]
         for s in sizes:
-            go = from_rank0(time.time() - t_start < args.mgpu_budget)
-            if not go:
-                rows.append({"kind": kind, "s": s, "skipped": "time budget"})
+            row = by_key.get((kind, s))
+            if prelaunch and (row is None or "skipped" in row):
                 continue
+            if not from_rank0(time.time() - t_start < (args.mgpu_budget if not prelaunch else args.mgpu_budget + 180)):
+                if row is None:
+                    rows.append({"kind": kind, "s": s, "skipped": "time budget"})
+                continue
+            if row is None:
+                row = {"kind": kind, "s": s, "us": {}, "busbw": {}}
+                rows.append(row)
             in_bytes = s if kind == "allgather" else n * s
             send = win[:in_bytes]
             recv = win[n * smax:n * smax + n * s]
@@ -630,8 +660,7 @@ def run_sweep(world, rank, dev, nccl, stream, t_start, args, rows):
             fill_and_expect(kind, s, n, [rank], [send], [e], "cuda")
             torch.cuda.synchronize()
             iters = int(max(5, min(100, 4e8 / max(1, (n - 1) * s))))
-            row = {"kind": kind, "s": s, "us": {}, "busbw": {}}
-            for impl in (AG_IMPLS if kind == "allgather" else AA_IMPLS):
+            for impl in impls:
                 if impl.endswith("swap") and n < 2:
                     continue
                 plan, res = try_impl(comms, kind, impl, [send], [recv], [e], s, iters, stream)
@@ -642,40 +671,40 @@ def run_sweep(world, rank, dev, nccl, stream, t_start, args, rows):
                 plan.destroy()
                 row["us"][impl] = round(res["ms"] * 1e3, 2)
                 row["busbw"][impl] = round(busbw(n, s, res["ms"]), 2)
-            if nccl is not None:
+            if nccl is not None and not prelaunch:
                 t = time_nccl(nccl, kind, send, recv, iters, stream)
                 row["us"]["nccl"] = round(t * 1e3, 2)
                 row["busbw"]["nccl"] = round(busbw(n, s, t), 2)
-            ours = {k: v for k, v in row["us"].items() if v is not None and k != "nccl"}
-            if ours:
-                row["best"] = min(ours, key=ours.get)
-                # fraction of the NVLink roofline (measured 770 GB/s per direction; busBW is per-GPU egress)
-                row["best_frac_nvlink"] = round(row["busbw"][row["best"]] / NVLINK_PEAK, 4)
-                if "nccl" in row["us"]:
-                    row["best_over_nccl_time"] = round(ours[row["best"]] / row["us"]["nccl"], 3)
-                    row["nccl_frac_nvlink"] = round(row["busbw"]["nccl"] / NVLINK_PEAK, 4)
-            rows.append(row)
+            summarize(row)
             if rank == 0 and args.mgpu_verbose:
                 print(json.dumps(row), flush=True)
-    # reduce-scatter, bf16 sum: the SM path (every rank reads
-    # its chunk from every peer over NVLink) against NCCL reduce_scatter.
-    for s in [x for x in (65536, 1 << 20, 16 << 20, 256 << 20) if x <= smax]:
-        if not from_rank0(time.time() - t_start < args.mgpu_budget):
-            rows.append({"kind": "reduce_scatter_bf16_sum", "s": s, "skipped": "time budget"})
-            continue
-        row = {"kind": "reduce_scatter_bf16_sum", "s": s, "us": {}, "busbw": {}}
-        rows.append(row)
-        count = s // 2
-        send, recv = win[:n * s], win[n * smax:n * smax + s]
-        row.update(rs_trial(comms, nccl, send, recv, count, n, rank, stream))
-        if rank == 0 and args.mgpu_verbose:
-            print(json.dumps(row), flush=True)
+    if not prelaunch:
+        # reduce-scatter, bf16 sum: the SM path (every rank
+        # reads its chunk from every peer over NVLink) against NCCL.
+        for s in [x for x in (65536, 1 << 20, 16 << 20, 256 << 20) if x <= smax]:
+            if not from_rank0(time.time() - t_start < args.mgpu_budget):
+                rows.append({"kind": "reduce_scatter_bf16_sum", "s": s, "skipped": "time budget"})
+                continue
+            row = {"kind": "reduce_scatter_bf16_sum", "s": s, "us": {}, "busbw": {}}
+            rows.append(row)
+            count = s // 2
+            send, recv = win[:n * s], win[n * smax:n * smax + s]
+            row.update(rs_trial(comms, nccl, send, recv, count, n, rank, stream))
+            if rank == 0 and args.mgpu_verbose:
+                print(json.dumps(row), flush=True)
     torch.cuda.synchronize()
     dist.barrier()
     comms[0].destroy()
     del win, exp
-    return {"ranks": n, "ranks_per_gpu": 1, "convention": "us = device time per collective (back to back, "
-            "max over ranks); busbw = (n-1)*s/t", "rows": rows}
+
+
+def run_sweep(world, rank, dev, nccl, stream, t_start, args, rows):
+    """AG and AA with one rank per GPU: every non-prelaunch implementation
+    (consensus, parity) and NCCL per size, then the reduce-scatter; latency in
+    us and busBW in GB/s. The prelaunch forms are added by a later pass."""
+    sweep_pass(world, rank, dev, nccl, stream, t_start, args, rows, prelaunch=False)
+    return {"ranks": world, "ranks_per_gpu": 1, "convention": "us = device time per collective (back to back, "
+            "max over ranks); busbw = (n-1)*s/t; prelaunch forms added late in the run", "rows": rows}
 
 
 def bf16_chunk(i: int, j: int, count: int) -> torch.Tensor:
