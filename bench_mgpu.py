@@ -818,7 +818,8 @@ def run_interference(world, rank, dev, nccl, stream, args, out):
     out.update({"workload": f"all-gather of {s >> 20} MiB bf16 shards x {n} GPUs beside cuBLAS bf16 {N}^3 "
                             f"GEMMs (one rank per GPU)", "gemm_alone_ms": round(gemm_alone, 4),
                 "gemm_alone_tflops": round(2 * N ** 3 / gemm_alone / 1e9, 1), "impls": {}})
-    cands = ["pcpy", "b2b", "sm", "prelaunch_pcpy"] + (["nccl"] if nccl is not None else [])
+    # prelaunch last (cross-device conditional graphs: the least exercised form)
+    cands = ["pcpy", "b2b", "hybrid", "sm"] + (["nccl"] if nccl is not None else []) + ["prelaunch_pcpy"]
     for impl in cands:
         STATE["phase"] = f"interference {impl}"
         plan, ok, err = None, True, None
