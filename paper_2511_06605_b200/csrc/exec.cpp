@@ -87,6 +87,13 @@ Status run_ce(World* w, Plan* p) {
       ++w->counters[kCtrApiCalls];
     }
     STATUS_TRY(issue_copies_traced(w, u.placement, u.stream, true, u.device, pid, -1));
+    if (u.table.nitems) {  // the lanes' merged item-kernel commands (lower.cpp lower_program)
+      cudaEvent_t b = trace_mark(w, u.device, u.stream);
+      CUDA_TRY(launch_items(u.table, mover_grid_for(u.table, p->sms), u.stream));
+      ++w->counters[kCtrKernels];
+      ++w->counters[kCtrApiCalls];
+      trace_span(w, table_name(u.table), pid, -1, u.device, b, trace_mark(w, u.device, u.stream));
+    }
     trace_host_span(w, "control", h0);
   }
   for (LaneExec& l : p->lanes) {

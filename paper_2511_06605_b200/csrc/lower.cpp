@@ -471,6 +471,24 @@ Status lower_program(World* w, Plan* p, const Addressing& ad, const std::vector<
         unit_items[ui].push_back({make_item(kItemCopy, c.src, c.dst, nullptr, c.bytes), {}});
       p->units[ui].placement.clear();
     }
+  // Outside recorded prelaunch graphs, the broadcast / swap commands (item
+  // kernels: no copy-engine form) of lanes that exchange no flags — every
+  // destination in the same unit — also merge into the unit's one item
+  // kernel, launched beside the lanes (exec.cpp run_ce): one kernel instead
+  // of one per lane. Copies stay copy-engine commands. CECOLL_MERGE_KERNELS=0
+  // keeps one kernel per lane.
+  const char* mk = std::getenv("CECOLL_MERGE_KERNELS");
+  const bool merge_kernels = !p->prelaunch && !(mk && std::string(mk) == "0");
+  auto lane_dests = [&](const Lane& l) {
+    std::set<int> d;
+    for (const Command& c : l.cmds) {
+      if (!c.moves_data()) continue;
+      d.insert(c.op == Op::Swap ? c.peer.rank : c.dst.rank);
+      if (c.op == Op::Broadcast) d.insert(c.dst2.rank);
+    }
+    d.erase(l.rank);
+    return d;
+  };
   for (const Lane& l : p->program.lanes) {  // lanes owned by local ranks
     if (unit_of[l.rank] < 0) continue;
     LaneExec le;
@@ -479,11 +497,14 @@ Status lower_program(World* w, Plan* p, const Addressing& ad, const std::vector<
     std::set<int> dests;
     std::vector<HostItem> items;
     const int dev = w->device[l.rank];
+    bool flagless = true;
+    for (int j : lane_dests(l)) flagless &= same_unit(l.rank, j);
     for (const Command& c : l.cmds) {
       const bool local_cmd = w->device[c.src.rank] == dev && w->device[c.dst.rank] == dev &&
                              (c.op != Op::Broadcast || w->device[c.dst2.rank] == dev) &&
                              (c.op != Op::Swap || w->device[c.peer.rank] == dev);
-      std::vector<HostItem>& sink = merge && local_cmd ? unit_items[unit_of[l.rank]] : items;
+      const bool to_unit = local_cmd && (merge || (merge_kernels && flagless && c.op != Op::Copy));
+      std::vector<HostItem>& sink = to_unit ? unit_items[unit_of[l.rank]] : items;
       switch (c.op) {
         case Op::Copy:
           if (merge && local_cmd) sink.push_back({make_item(kItemCopy, addr(c.src), addr(c.dst), nullptr, c.size), {}});
