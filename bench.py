@@ -641,6 +641,13 @@ def alg_hbm_bytes(kind, impl, s, n):
     all-gather reads each source once (fan item)."""
     if impl == "sm":
         return (n * s + n * n * s) if kind == "allgather" else 2 * n * n * s
+    if impl == "pull":  # n(n-1) chunk copies + the local placement
+        return 2 * n * n * s
+    if impl == "hybrid":  # CE share: n(n-1) copies; SM share as the SM path; placement
+        sm_b = (s * 50 // 100) & ~15
+        ce = s - sm_b
+        sm_part = (n * sm_b + n * (n - 1) * sm_b) if kind == "allgather" else 2 * n * (n - 1) * sm_b
+        return 2 * n * (n - 1) * ce + sm_part + 2 * n * s
     t = cc.Program(kind, impl, s, n).traffic()
     extra = 0 if impl.endswith("swap") else 2 * n * s
     return t["read"] + t["write"] + extra
@@ -672,7 +679,7 @@ def run_sweep(args):
     out_path = args.sweep_out
     O = ora.Oracle()
     for kind in ("allgather", "alltoall"):
-        impls = ["sm"] + cc.IMPLS_FOR[kind]
+        impls = ["sm", "hybrid", "pull"] + cc.IMPLS_FOR[kind]
         for s in sizes:
             in_bytes = s if kind == "allgather" else n * s
             if n * (in_bytes + n * s) > args.max_bytes:

@@ -475,10 +475,15 @@ Status lower_program(World* w, Plan* p, const Addressing& ad, const std::vector<
   // kernels: no copy-engine form) of lanes that exchange no flags — every
   // destination in the same unit — also merge into the unit's one item
   // kernel, launched beside the lanes (exec.cpp run_ce): one kernel instead
-  // of one per lane. Copies stay copy-engine commands. CECOLL_MERGE_KERNELS=0
-  // keeps one kernel per lane.
+  // of one per lane. Copies stay copy-engine commands. Below 4 MiB chunks
+  // only: above, the lanes' concurrent kernels move broadcast / swap traffic
+  // 7-10% faster (profiles/sweep_r01_plan_n8_merged.csv vs
+  // sweep_r01_plan_n8_recorded.csv). CECOLL_MERGE_KERNELS=0 keeps one kernel
+  // per lane; CECOLL_MERGE_KERNELS_MAX=<bytes> moves the cutoff.
   const char* mk = std::getenv("CECOLL_MERGE_KERNELS");
-  const bool merge_kernels = !p->prelaunch && !(mk && std::string(mk) == "0");
+  const char* mkx = std::getenv("CECOLL_MERGE_KERNELS_MAX");
+  const int64_t merge_max = mkx ? std::atoll(mkx) : (int64_t{4} << 20);
+  const bool merge_kernels = !p->prelaunch && !(mk && std::string(mk) == "0") && p->chunk < merge_max;
   auto lane_dests = [&](const Lane& l) {
     std::set<int> d;
     for (const Command& c : l.cmds) {
