@@ -143,6 +143,23 @@ def fill_and_expect(kind, s, n, ranks, sends, expects, dev):
 # ---------------------------------------------------------------------------
 
 
+def make_plan(comms, kind, sends, recvs, s, impl):
+    """cc.Plan for an implementation name, or "name@pct" for the hybrid's SM
+    share (CECOLL_HYBRID_SM_PCT, read at plan creation)."""
+    name, _, pct = impl.partition("@")
+    saved = os.environ.get("CECOLL_HYBRID_SM_PCT")
+    if pct:
+        os.environ["CECOLL_HYBRID_SM_PCT"] = pct
+    try:
+        return cc.Plan(comms, kind, sends, recvs, s, impl=name)
+    finally:
+        if pct:
+            if saved is None:
+                os.environ.pop("CECOLL_HYBRID_SM_PCT", None)
+            else:
+                os.environ["CECOLL_HYBRID_SM_PCT"] = saved
+
+
 def try_impl(comms, kind, impl, sends, recvs, expects, s, iters, stream):
     """Returns (plan or None, result dict). The plan is left disarmed."""
     in_place = impl.endswith("swap")
@@ -153,20 +170,10 @@ def try_impl(comms, kind, impl, sends, recvs, expects, s, iters, stream):
             r.fill_(0xA5)
     torch.cuda.synchronize()
     plan, err = None, None
-    name, _, pct = impl.partition("@")
-    saved = os.environ.get("CECOLL_HYBRID_SM_PCT")
-    if pct:
-        os.environ["CECOLL_HYBRID_SM_PCT"] = pct
     try:
-        plan = cc.Plan(comms, kind, recvs if in_place else sends, recvs, s, impl=name)
+        plan = make_plan(comms, kind, recvs if in_place else sends, recvs, s, impl)
     except cc.CecollError as e:
         err = str(e)[:160]
-    finally:
-        if pct:
-            if saved is None:
-                os.environ.pop("CECOLL_HYBRID_SM_PCT", None)
-            else:
-                os.environ["CECOLL_HYBRID_SM_PCT"] = saved
     if not all_true(plan is not None):
         if plan is not None:
             plan.destroy()
@@ -543,7 +550,7 @@ def run_e2e(comms, plans, best, sets, expects, s, n, nlocal, stream, args):
     e2e_plans = [plans[best]]
     try:
         s1, r1 = sets[1]
-        e2e_plans.append(cc.Plan(comms, "alltoall", r1 if in_place else s1, r1, s, impl=best))
+        e2e_plans.append(make_plan(comms, "alltoall", r1 if in_place else s1, r1, s, best))
     except cc.CecollError:
         e2e_plans = None
     if not all_true(e2e_plans is not None):
