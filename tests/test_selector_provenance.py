@@ -1,10 +1,12 @@
 """The B200 selector against the measured winner grid (winner_grid,
-sweep.cpp:186-218): at every size of the committed one-GPU sweeps
-(profiles/sweep_r01_plan_n{8,2}_recorded.csv, explicit plans) the
-implementation cecoll_select picks for an out-of-place collective is within
-10% of the fastest out-of-place implementation measured at that size — the
-analogue of the reference's own check that its table matches the simulated
-winners within tolerance (acceptance.cpp:85-87). CPU only: reads the CSVs."""
+sweep.cpp:186-218): at every measured size the implementation
+cecoll_select picks for an out-of-place collective is within 10% (plus one
+~2 µs device-time step) of the fastest out-of-place implementation — the analogue of the reference's own
+check that its table matches the simulated winners (acceptance.cpp:85-87).
+Latency regime (chunks <= 1 MiB): device time per collective from C++
+(tools/latency.cpp, profiles/latency_r01_n{8,2}_final.csv) — the Python
+sweep is host-bound there. Bandwidth regime: the plan sweep
+(profiles/sweep_r01_plan_n{8,2}_final.csv). CPU only: reads the files."""
 import csv
 import os
 
@@ -14,32 +16,37 @@ import paper_2511_06605_b200 as cc
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 TOL = 1.10
+# Back-to-back device times of small collectives come in steps of ~2.05 µs
+# (profiles/latency_r01_n*_final.csv: 4.11, 6.15, 8.20 ...): one step of slack.
+SLACK_US = 2.1
 
 
 def _grid(n):
-    path = os.path.join(ROOT, "profiles", f"sweep_r01_plan_n{n}_recorded.csv")
     t = {}
-    with open(path) as f:
+    with open(os.path.join(ROOT, "profiles", f"latency_r01_n{n}_final.csv")) as f:
         for r in csv.DictReader(f):
-            if r.get("api") != "plan" or r["parity"] != "True" or r["impl"].endswith("swap"):
-                continue  # in-place programs answer a different call
-            t.setdefault((r["collective"], int(r["size_bytes"])), {})[r["impl"]] = int(r["total_ns"])
+            if r["api"] == "plan" and not r["impl"].endswith("swap"):
+                t.setdefault((r["collective"], int(r["size_bytes"])), {})[r["impl"]] = float(r["device_us_b2b"])
+    with open(os.path.join(ROOT, "profiles", f"sweep_r01_plan_n{n}_final.csv")) as f:
+        for r in csv.DictReader(f):
+            s = int(r["size_bytes"])
+            if r.get("api") != "plan" or r["parity"] != "True" or r["impl"].endswith("swap") or s <= 1 << 20:
+                continue  # in-place programs answer a different call; small sizes come from C++
+            if s >= 1 << 30:
+                continue  # 64 GiB per collective: bimodal between runs
+            t.setdefault((r["collective"], s), {})[r["impl"]] = int(r["total_ns"]) / 1e3
     return t
 
 
 @pytest.mark.parametrize("n", [8, 2])
 def test_selector_within_tolerance_of_measured_winner(n):
     grid = _grid(n)
-    assert len(grid) >= 18
-    worst = []
+    assert len(grid) >= 16
     for (kind, s), times in sorted(grid.items()):
-        if s >= 1 << 30:
-            continue  # 64 GiB per collective: bimodal between runs
         pick = cc.select(kind, s, n, 1)
         assert pick in times, (kind, s, pick)
         best = min(times.values())
-        worst.append((times[pick] / best, kind, s, pick, min(times, key=times.get)))
-        assert times[pick] <= TOL * best, (kind, s, pick, times)
+        assert times[pick] <= TOL * best + SLACK_US, (kind, s, pick, times)
     # the table in words: the SM path everywhere for all-gather, up to 32 MiB
     # for all-to-all, the driver's copies above
     assert cc.select("allgather", 1 << 28, n, 1) == "sm"
