@@ -538,10 +538,17 @@ class Plan:
         self._h = h
 
     def launch(self, streams=None):
-        if streams is None or not isinstance(streams, (list, tuple)):
-            streams = [streams] * self._n
-        arr = (C.c_void_p * self._n)(*[_stream(s) for s in streams])
-        _check(lib().cecoll_plan_launch(self._h, arr), "plan_launch")
+        # The marshalled stream array is cached per streams argument: a plan is
+        # relaunched with the same streams in latency-bound loops.
+        key = tuple(streams) if isinstance(streams, (list, tuple)) else streams
+        cache = self.__dict__.setdefault("_arrs", {})
+        arr = cache.get(key)
+        if arr is None:
+            seq = list(streams) if isinstance(streams, (list, tuple)) else [streams] * self._n
+            arr = cache[key] = (C.c_void_p * self._n)(*[_stream(s) for s in seq])
+        st = _lib.cecoll_plan_launch(self._h, arr)
+        if st:
+            _check(st, "plan_launch")
 
     def disarm(self):
         """Cancel the armed instance (needed before torch.cuda.synchronize())."""
