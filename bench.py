@@ -361,7 +361,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": n * n * s, "ms_per_step": round(e2e_ms, 3), "parity_ok": bool(e2e_ok),
                 "pipeline": "double-buffered: H2D of step k+1 overlaps D2H of step k",
                 "bound_note": "PCIe-bound: 512 MiB host->device and 512 MiB device->host per step over one "
-                              "x16 link; both directions at once take 10.9-11.1 ms on these boxes "
+                              "x16 link; both directions at once take 10.9-11.7 ms on these boxes "
                               "(profiles/pcie_probe2_r01.txt, ce_both), so ~5.0 GB/s busBW is the floor "
                               "for host-resident buffers on one GPU"},
         "gpu_launches": int(round((kernels_per_step + 4 * graphs_per_step) * args.steps)),

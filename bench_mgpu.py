@@ -383,15 +383,30 @@ def run(args, B):
 
     stream = torch.cuda.Stream()
     STATE["phase"] = "init"
-    comms = cc.Comm.init_ranks(n, first, nlocal, dev, cc.torch_exchange())
-
-    # Two symmetric windows per rank, [send n*s | recv n*s] (double-buffered e2e).
-    sets = []
-    for _b in range(2):
-        wins = [torch.empty(2 * n * s, dtype=torch.uint8, device="cuda") for _ in comms]
-        for c, w in zip(comms, wins):
-            c.register(w)
-        sets.append(([w[:n * s] for w in wins], [w[n * s:] for w in wins]))
+    # Communicator and two symmetric windows per rank, [send n*s | recv n*s]
+    # (double-buffered e2e). Both are collective (exchange over gloo), so a
+    # failure on one rank surfaces as an exchange failure on the others;
+    # either way every rank reports and the line still carries NCCL.
+    comms, sets, init_err = None, [], None
+    try:
+        comms = cc.Comm.init_ranks(n, first, nlocal, dev, cc.torch_exchange())
+        for _b in range(2):
+            wins = [torch.empty(2 * n * s, dtype=torch.uint8, device="cuda") for _ in comms]
+            for c, w in zip(comms, wins):
+                c.register(w)
+            sets.append(([w[:n * s] for w in wins], [w[n * s:] for w in wins]))
+    except Exception as e:  # noqa: BLE001
+        init_err = str(e)[:200]
+    if not all_true(init_err is None):
+        line["error"] = f"communicator / window setup failed: {init_err or 'on another rank'}"
+        if nccl is not None:
+            inp = torch.empty(nlocal * n * s, dtype=torch.uint8, device="cuda")
+            t = time_nccl(nccl, "alltoall", inp, torch.empty_like(inp), args.steps, stream)
+            line["nccl"] = {"value": round(busbw(n, s, t), 3), "unit": "GB/s", "ms_per_step": round(t, 4)}
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        dog.cancel()
+        return
     sends, recvs = sets[0]
     expects = [torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in comms]
     fill_and_expect("alltoall", s, n, my_ranks, sends, expects, "cuda")
