@@ -242,7 +242,7 @@ Status world_init_ranks(int nranks, int first, int nlocal, int device, cecoll_ex
 // processes' rank ranges tile [0, nranks) and returns them.
 Status gather_procs(int nranks, int first, int nlocal, int device, const cudaIpcMemHandle_t* flags,
                     cecoll_exchange_fn fn, void* ctx, std::vector<ProcInfoView>* out,
-                    const unsigned char* uuid = nullptr);
+                    const unsigned char* uuid = nullptr, int32_t local_status = 0);
 void world_release(World* w);
 Status world_register(World* w, int rank, void* ptr, size_t bytes, cecoll_exchange_fn fn, void* ctx);
 Status world_deregister(World* w, void* ptr);

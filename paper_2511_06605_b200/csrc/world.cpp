@@ -81,7 +81,7 @@ struct ProcInfo {
   int32_t first;   // first global rank owned by the process
   int32_t nlocal;  // ranks owned (consecutive)
   int32_t device;
-  int32_t pid;
+  int32_t status;  // the process's local steps before the exchange (0: ok)
   cudaIpcMemHandle_t flags;  // nlocal flag pages, kFlagBytes apart
   unsigned char uuid[16];    // device identity (ordinals differ between processes
                              // when CUDA_VISIBLE_DEVICES differs)
@@ -90,11 +90,25 @@ struct ProcInfo {
 // One blob per process in a registration round.
 struct RegInfo {
   int32_t rank;
-  int32_t pad;
+  int32_t pad;      // status of the process's local steps (0: ok)
   uint64_t offset;  // of the window inside its allocation
   uint64_t bytes;
   cudaIpcMemHandle_t handle;  // of the allocation
 };
+
+// Collective calls fail collectively: every process exchanges its status
+// after its local steps, so a failure on one process (e.g. opening a peer's
+// IPC handle) fails the call on all of them instead of leaving the others to
+// wait in the next exchange.
+Status agree_all(cecoll_exchange_fn fn, void* ctx, int procs, const Status& local, const char* what) {
+  int32_t mine = local.code;
+  std::vector<int32_t> all(procs);
+  if (fn(ctx, &mine, sizeof(mine), all.data()) != 0) return fail(CECOLL_INTERNAL, std::string(what) + ": exchange failed");
+  if (!local.ok()) return local;
+  for (int32_t c : all)
+    if (c != 0) return fail(c, std::string(what) + ": failed on another process");
+  return {};
+}
 
 Status open_ipc(World* w, const cudaIpcMemHandle_t& h, void** out) {
   std::string key(reinterpret_cast<const char*>(&h), sizeof(h));
@@ -112,7 +126,8 @@ Status open_ipc(World* w, const cudaIpcMemHandle_t& h, void** out) {
 }  // namespace
 
 Status gather_procs(int nranks, int first, int nlocal, int device, const cudaIpcMemHandle_t* flags,
-                    cecoll_exchange_fn fn, void* ctx, std::vector<ProcInfoView>* out, const unsigned char* uuid) {
+                    cecoll_exchange_fn fn, void* ctx, std::vector<ProcInfoView>* out, const unsigned char* uuid,
+                    int32_t local_status) {
   if (nranks < 1 || nranks > kMaxRanks || nlocal < 1 || first < 0 || first + nlocal > nranks || !fn)
     return fail(CECOLL_INVALID_ARGUMENT, "bad rank range / exchange");
   if (nranks % nlocal != 0)
@@ -125,8 +140,12 @@ Status gather_procs(int nranks, int first, int nlocal, int device, const cudaIpc
   mine.device = device;
   if (flags) mine.flags = *flags;
   if (uuid) std::memcpy(mine.uuid, uuid, sizeof(mine.uuid));
+  mine.status = local_status;
   std::vector<ProcInfo> all(procs);
   if (fn(ctx, &mine, sizeof(ProcInfo), all.data()) != 0) return fail(CECOLL_INTERNAL, "exchange failed");
+  if (local_status != 0) return fail(local_status, last_error());  // keep this process's own message
+  for (const ProcInfo& pi : all)
+    if (pi.status != 0) return fail(pi.status, "comm_init: failed on another process");
   std::vector<int> owner(nranks, -1);
   out->clear();
   for (int p = 0; p < procs; ++p) {
@@ -164,43 +183,54 @@ Status world_init_ranks(int nranks, int first, int nlocal, int device, cecoll_ex
   w->device.assign(nranks, -1);
   w->flag_page.assign(nranks, nullptr);
   w->local.resize(nranks);
-  // One allocation holds the flag pages of every local rank (one IPC handle).
-  void* block = nullptr;
-  CUDA_TRY(cudaMalloc(&block, kFlagBytes * nlocal));
-  CUDA_TRY(cudaMemset(block, 0, kFlagBytes * nlocal));
-  CUDA_TRY(cudaDeviceSynchronize());
-  w->flag_block = block;
-  for (int k = 0; k < nlocal; ++k)
-    STATUS_TRY(make_rank(w.get(), first + k, device,
-                         reinterpret_cast<uint64_t*>(static_cast<char*>(block) + k * kFlagBytes)));
+  // Local steps before the exchange report their status through it (a
+  // process that fails here must not leave the others waiting in it).
   cudaIpcMemHandle_t h;
-  CUDA_TRY(cudaIpcGetMemHandle(&h, block));
-  // Device identity by UUID: a peer process's device is mapped to this
-  // process's ordinal for it, or to a unique negative id when this process
-  // cannot see it (then it is never mistaken for a local device).
-  int ndev = 0;
-  CUDA_TRY(cudaGetDeviceCount(&ndev));
-  if (device < 0 || device >= ndev) return fail(CECOLL_INVALID_ARGUMENT, "device out of range");
-  std::vector<std::array<unsigned char, 16>> uuids(ndev);
-  for (int d = 0; d < ndev; ++d) {
-    cudaDeviceProp prop;
-    CUDA_TRY(cudaGetDeviceProperties(&prop, d));
-    std::memcpy(uuids[d].data(), prop.uuid.bytes, 16);
-  }
+  std::memset(&h, 0, sizeof(h));
+  std::vector<std::array<unsigned char, 16>> uuids(1);
+  auto local_steps = [&]() -> Status {
+    // One allocation holds the flag pages of every local rank (one IPC handle).
+    void* block = nullptr;
+    CUDA_TRY(cudaMalloc(&block, kFlagBytes * nlocal));
+    w->flag_block = block;
+    CUDA_TRY(cudaMemset(block, 0, kFlagBytes * nlocal));
+    CUDA_TRY(cudaDeviceSynchronize());
+    for (int k = 0; k < nlocal; ++k)
+      STATUS_TRY(make_rank(w.get(), first + k, device,
+                           reinterpret_cast<uint64_t*>(static_cast<char*>(block) + k * kFlagBytes)));
+    CUDA_TRY(cudaIpcGetMemHandle(&h, block));
+    // Device identity by UUID: a peer process's device is mapped to this
+    // process's ordinal for it, or to a unique negative id when this process
+    // cannot see it (then it is never mistaken for a local device).
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(CECOLL_INVALID_ARGUMENT, "device out of range");
+    uuids.assign(ndev, {});
+    for (int d = 0; d < ndev; ++d) {
+      cudaDeviceProp prop;
+      CUDA_TRY(cudaGetDeviceProperties(&prop, d));
+      std::memcpy(uuids[d].data(), prop.uuid.bytes, 16);
+    }
+    return {};
+  };
+  const Status pre = local_steps();
+  const int dev_index = pre.ok() ? device : 0;
   std::vector<ProcInfoView> procs;
-  STATUS_TRY(gather_procs(nranks, first, nlocal, device, &h, fn, ctx, &procs, uuids[device].data()));
+  STATUS_TRY(gather_procs(nranks, first, nlocal, device, &h, fn, ctx, &procs, uuids[dev_index].data(), pre.code));
   for (size_t pi = 0; pi < procs.size(); ++pi) {
     ProcInfoView& pv = procs[pi];
     int local_ordinal = -1000 - static_cast<int>(pi);
-    for (int d = 0; d < ndev; ++d)
-      if (std::memcmp(uuids[d].data(), pv.uuid, 16) == 0) local_ordinal = d;
+    for (size_t d = 0; d < uuids.size(); ++d)
+      if (std::memcmp(uuids[d].data(), pv.uuid, 16) == 0) local_ordinal = static_cast<int>(d);
     pv.device = local_ordinal;
   }
+  Status opened_all;
   for (const ProcInfoView& pv : procs) {
     char* base = nullptr;
     if (pv.first != first) {
       void* opened = nullptr;
-      STATUS_TRY(open_ipc(w.get(), pv.flags, &opened));
+      opened_all = open_ipc(w.get(), pv.flags, &opened);
+      if (!opened_all.ok()) break;
       base = static_cast<char*>(opened);
     }
     for (int k = 0; k < pv.nlocal; ++k) {
@@ -209,6 +239,7 @@ Status world_init_ranks(int nranks, int first, int nlocal, int device, cecoll_ex
       if (pv.first != first) w->flag_page[r] = reinterpret_cast<uint64_t*>(base + k * kFlagBytes);
     }
   }
+  STATUS_TRY(agree_all(fn, ctx, nranks / nlocal, opened_all, "comm_init_ranks"));
   w->ndevices = count_devices(w->device);
   w->live_comms = nlocal;
   w->reg_rounds.assign(nlocal, 0);
@@ -235,33 +266,55 @@ Status world_register(World* w, int rank, void* ptr, size_t bytes, cecoll_exchan
     w->windows.push_back(win);
   }
   Window& win = w->windows[round];
-  if (win.bytes != bytes)
-    return fail(CECOLL_INVALID_ARGUMENT, "cecoll_register: windows must be symmetric (same size on every rank)");
-  CUdeviceptr base = 0;
-  size_t size = 0;
-  CU_TRY(driver_api()->MemGetAddressRange(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)));
+  // Local steps report through the exchange (pad = status) rather than
+  // returning early: the other processes are about to wait in it.
   RegInfo mine;
   std::memset(&mine, 0, sizeof(mine));
   mine.rank = rank;
-  mine.offset = reinterpret_cast<uint64_t>(ptr) - base;
   mine.bytes = bytes;
-  CUDA_TRY(cudaIpcGetMemHandle(&mine.handle, reinterpret_cast<void*>(base)));
+  Status local;
+  if (win.bytes != bytes) {
+    local = fail(CECOLL_INVALID_ARGUMENT, "cecoll_register: windows must be symmetric (same size on every rank)");
+  } else {
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    const CUresult r = driver_api()->MemGetAddressRange(&base, &size, reinterpret_cast<CUdeviceptr>(ptr));
+    if (r != CUDA_SUCCESS) {
+      local = cu_fail(r, "cuMemGetAddressRange", __FILE__, __LINE__);
+    } else {
+      mine.offset = reinterpret_cast<uint64_t>(ptr) - base;
+      const cudaError_t e = cudaIpcGetMemHandle(&mine.handle, reinterpret_cast<void*>(base));
+      if (e != cudaSuccess) local = cuda_fail(e, "cudaIpcGetMemHandle", __FILE__, __LINE__);
+    }
+  }
+  mine.pad = local.code;
   const int procs = w->nranks / w->nlocal;
   std::vector<RegInfo> all(procs);
   if (fn(ctx, &mine, sizeof(RegInfo), all.data()) != 0) return fail(CECOLL_INTERNAL, "exchange failed");
+  if (!local.ok()) return agree_all(fn, ctx, procs, local, "cecoll_register");
+  for (const RegInfo& ri : all)
+    if (ri.pad != 0) return agree_all(fn, ctx, procs, fail(ri.pad, "cecoll_register: failed on another process"),
+                                      "cecoll_register");
+  Status st;
   for (const RegInfo& ri : all) {
-    if (ri.bytes != bytes)
-      return fail(CECOLL_INVALID_ARGUMENT, "cecoll_register: windows must be symmetric (same size on every rank)");
-    if (ri.rank < 0 || ri.rank >= w->nranks) return fail(CECOLL_INVALID_ARGUMENT, "bad rank in registration");
+    if (ri.bytes != bytes) {
+      st = fail(CECOLL_INVALID_ARGUMENT, "cecoll_register: windows must be symmetric (same size on every rank)");
+      break;
+    }
+    if (ri.rank < 0 || ri.rank >= w->nranks) {
+      st = fail(CECOLL_INVALID_ARGUMENT, "bad rank in registration");
+      break;
+    }
     if (ri.rank == rank) {
       win.rank_base[ri.rank] = static_cast<char*>(ptr);
       continue;
     }
     void* opened = nullptr;
-    STATUS_TRY(open_ipc(w, ri.handle, &opened));
+    st = open_ipc(w, ri.handle, &opened);
+    if (!st.ok()) break;
     win.rank_base[ri.rank] = static_cast<char*>(opened) + ri.offset;
   }
-  return {};
+  return agree_all(fn, ctx, procs, st, "cecoll_register");
 }
 
 Status world_deregister(World* w, void* ptr) {

@@ -243,3 +243,40 @@ def test_two_processes_share_one_gpu_through_ipc(force_remote):
         bad = [r for r in results if not r[2]]
         assert not bad, (rank, bad)
         assert len(results) == 13
+
+
+def _asymmetric_failure_worker(rank, world, port, out):
+    """Rank 0 registers a host pointer (its local step fails before the
+    exchange); rank 1 a valid device window. Collective calls fail
+    collectively: both must raise, neither may hang in the exchange."""
+    try:
+        dist = _init(rank, world, port)
+        import torch
+
+        import paper_2511_06605_b200 as cc
+
+        comms = cc.Comm.init_ranks(2, rank, 1, 0, cc.torch_exchange())
+        buf = torch.empty(1 << 20, dtype=torch.uint8) if rank == 0 else \
+            torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+        try:
+            comms[0].register(buf)
+            res = "registered"
+        except cc.CecollError as e:
+            res = "error: " + str(e)[:80]
+        # the communicator stays usable for a good registration afterwards
+        good = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+        comms[0].register(good)
+        out.put((rank, res))
+        torch.cuda.synchronize()
+        comms[0].destroy()
+        dist.destroy_process_group()
+    except Exception:  # noqa: BLE001
+        out.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(240)
+def test_registration_fails_on_every_process_together():
+    res = dict(_run2(_asymmetric_failure_worker))
+    assert res[0].startswith("error"), res
+    assert res[1].startswith("error") and "another process" in res[1], res
