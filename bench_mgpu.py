@@ -538,6 +538,10 @@ def run(args, B):
         STATE["phase"] = "interference"
         line["interference"] = {}
         run_interference(world, rank, dev, nccl, stream, args, line["interference"])
+    if not args.no_mgpu_interference and from_rank0(time.time() - t_start < args.mgpu_budget + 150):
+        STATE["phase"] = "sync chain"
+        line["sync_chain"] = {}
+        run_sync_chain(world, rank, dev, stream, line["sync_chain"])
     if not args.no_mgpu_experiments:
         STATE["phase"] = "experiments"
         line["experiments"] = {}
@@ -909,6 +913,75 @@ def run_interference(world, rank, dev, nccl, stream, args, out):
             "collective_busbw_alone_gbs": round(busbw(n, s, alone), 1), "collectives": k,
             "gemm_with_collective_ms": round(gemm_with, 4), "gemm_slowdown": round(gemm_with / gemm_alone, 3),
             "collective_slowdown": round(coll_with / alone, 3)}
+    torch.cuda.synchronize()
+    dist.barrier()
+    comms[0].destroy()
+
+
+def run_sync_chain(world, rank, dev, stream, out):
+    """Producer -> collective (simulate_sync_chain, sim.cpp:475-499):
+    a bf16 4096^3 GEMM, then an all-gather on the same stream, one rank per
+    GPU. overhead = T(chain) - T(GEMM) - T(collective), device time, max over
+    ranks: stream-ordered plans (the collective enqueued behind the producer,
+    no host in between) against the CPU-forwarded chain (the host waits for
+    the GEMM, then issues — the paper's baseline)."""
+    n = world
+    N = 4096
+    a = torch.randn(N, N, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(N, N, device="cuda", dtype=torch.bfloat16)
+    c = torch.empty(N, N, device="cuda", dtype=torch.bfloat16)
+    comms = cc.Comm.init_ranks(n, rank, 1, dev, cc.torch_exchange())
+    smax = 16 << 20
+    win = torch.empty((n + 1) * smax, dtype=torch.uint8, device="cuda")
+    comms[0].register(win)
+
+    def timed(fn, iters=10):
+        ts = []
+        for _ in range(iters + 2):
+            stream.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            stream.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ts = sorted(ts[2:])
+        return max_all(ts[len(ts) // 2])
+
+    def gemm():
+        with torch.cuda.stream(stream):
+            torch.matmul(a, b, out=c)
+
+    t_gemm = timed(gemm)
+    out.update({"gemm": f"bf16 {N}^3", "gemm_ms": round(t_gemm, 4), "cases": []})
+    for s in (1 << 20, smax):
+        send, recv = win[:s], win[s:(n + 1) * s]
+        for mode, impl in (("stream", "sm"), ("stream", "pcpy"), ("host", "sm")):
+            ok, err, plan = True, None, None
+            try:
+                plan = cc.Plan(comms, "allgather", [send], [recv], s, impl=impl)
+            except cc.CecollError as e:
+                ok, err = False, str(e)[:120]
+            if not all_true(ok):
+                out["cases"].append({"s": s, "mode": mode, "impl": impl, "error": err or "another rank"})
+                continue
+
+            def coll():
+                plan.launch(stream)
+
+            def chain():
+                gemm()
+                if mode == "host":
+                    stream.synchronize()  # the CPU observes the GEMM, then issues
+                coll()
+
+            t_coll = timed(coll)
+            t_chain = timed(chain)
+            plan.destroy()
+            out["cases"].append({"s": s, "mode": mode, "impl": impl, "collective_ms": round(t_coll, 4),
+                                 "chain_ms": round(t_chain, 4),
+                                 "overhead_us": round((t_chain - t_gemm - t_coll) * 1e3, 2)})
     torch.cuda.synchronize()
     dist.barrier()
     comms[0].destroy()
