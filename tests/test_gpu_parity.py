@@ -85,6 +85,16 @@ def test_sm_path_matches_reference_digest(d, stream_mode):
     assert [sha(r) for r in res] == d["sha256"]
 
 
+@pytest.mark.parametrize("impl", ["hybrid", "pull"])
+@pytest.mark.parametrize("stream_mode", ["shared", "per_rank"])
+@pytest.mark.parametrize("d", SM_CASES, ids=lambda d: f"{d['kind']}-n{d['n']}-s{d['s']}-seed{d['seed']}")
+def test_b200_executors_match_reference_digest(d, stream_mode, impl):
+    # The hybrid (copy-engine lane + SM share per chunk) and pull (destination-
+    # issued reads) executors against the same reference digests.
+    _, res, _, _ = run(d["kind"], impl, d["s"], d["n"], d["seed"], stream_mode)
+    assert [sha(r) for r in res] == d["sha256"]
+
+
 @pytest.mark.parametrize("impl", ["pcpy", "b2b", "bcst", "swap", "prelaunch_pcpy", "prelaunch_b2b",
                                   "prelaunch_bcst", "prelaunch_swap", "sm", "hybrid", "pull"])
 @pytest.mark.parametrize("stream_mode", ["shared", "per_rank"])
