@@ -215,3 +215,32 @@ def test_other_device_signal_path_on_one_gpu(impl, monkeypatch):
     finally:
         torch.cuda.synchronize()
         cc.destroy_all(comms)
+
+
+@pytest.mark.timeout(300)
+def test_plan_cache_eviction_with_recorded_graphs():
+    """More distinct calls than the eager-call plan cache holds (64): every
+    plan is recorded (second call) and the oldest are evicted with their
+    graphs; results stay exact, including for sizes evicted and re-created."""
+    n = 4
+    comms = cc.Comm.init_all([0] * n)
+    O = ora.Oracle()
+    st = torch.cuda.Stream()
+    try:
+        sizes = [4096 + 16 * k for k in range(70)] + [4096, 4096 + 16]  # the last two were evicted
+        sends = [torch.empty(n * sizes[-3], dtype=torch.uint8, device="cuda") for _ in range(n)]
+        recvs = [torch.empty(n * sizes[-3], dtype=torch.uint8, device="cuda") for _ in range(n)]
+        for i, s in enumerate(sizes):
+            snd = [t[:n * s] for t in sends]
+            rcv = [t[:n * s] for t in recvs]
+            host = _load(snd, rcv, n * s, n, 900 + i, False)
+            torch.cuda.synchronize()
+            for _ in range(2):  # eager, then recorded replay
+                cc.all_to_all(comms, snd, rcv, s, impl="pcpy", streams=st)
+            st.synchronize()
+            if i % 7 == 0 or i >= len(sizes) - 3:
+                res = [t.cpu().numpy() for t in rcv]
+                assert O.check("alltoall", s, n, False, host, res) == -1, (i, s)
+    finally:
+        torch.cuda.synchronize()
+        cc.destroy_all(comms)
