@@ -377,3 +377,35 @@ def test_back_to_back_through_the_other_device_signal_path(impl, monkeypatch):
     (signal kernels, folded start signals are not used: several units)."""
     monkeypatch.setenv("CECOLL_FORCE_REMOTE_SIGNALS", "1")
     test_back_to_back_collectives_without_host_sync(impl, fresh=True)
+
+
+def test_misrouted_program_fails_parity_on_the_gpu():
+    """Negative control for every parity test here (test_verifier.cpp:35-49
+    on hardware): the reference's own program text with one copy misrouted
+    (rank 0's chunk for rank 1 written to slot 2 instead of slot 0) executes
+    fine — and the byte check must catch it, exactly at the bytes it broke."""
+    kind, n, s = "allgather", 4, 4096
+    with open(os.path.join(GOLDEN, "programs.json")) as f:
+        text = next(e["dump"] for e in json.load(f)["programs"]
+                    if (e["kind"], e["impl"], e["s"], e["n"]) == (kind, "pcpy", s, n) and "dump" in e)
+    lines = [line.split("\t") for line in text.splitlines()]
+    hits = 0
+    for f in lines:
+        if f[2] == "copy" and f[3].startswith("g0.in") and f[4] == f"g1.out[0+{s}]":
+            f[4] = f"g1.out[{2 * s}+{s}]"  # slot 2 instead of slot 0
+            hits += 1
+    assert hits == 1
+    bad = "\n".join("\t".join(f) for f in lines) + "\n"
+    host_in = [ora.splitmix_pattern(s, r, 21) for r in range(n)]
+    O = ora.Oracle()
+    for txt, want_ok in ((text, True), (bad, False)):
+        sends = [torch.from_numpy(h).cuda() for h in host_in]
+        recvs = [torch.full((n * s,), 0xA5, dtype=torch.uint8, device="cuda") for _ in range(n)]
+        plan = cc.Plan(comms(n), kind, sends, recvs, program=cc.Program.parse(txt, kind, s, n))
+        plan.launch([torch.cuda.current_stream()] * n)
+        torch.cuda.current_stream().synchronize()
+        res = [t.cpu().numpy() for t in recvs]
+        plan.destroy()
+        torch.cuda.synchronize()
+        bad_at = O.check(kind, s, n, False, host_in, res)
+        assert (bad_at == -1) == want_ok, (want_ok, bad_at)
