@@ -1,0 +1,67 @@
+"""cecoll_program_parse reads program text from outside (the reference's
+dump_program output, or hand-written programs): random mutations of the
+golden dumps must parse or be rejected with InvalidArgument — never crash —
+and whatever parses must go through validate / metrics / dump (CPU only)."""
+import json
+import os
+import random
+
+import paper_2511_06605_b200 as cc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _dumps():
+    with open(os.path.join(ROOT, "tests", "golden", "programs.json")) as f:
+        return [e for e in json.load(f)["programs"] if "dump" in e and e["n"] <= 8]
+
+
+def _mutate(rng, text):
+    lines = text.splitlines()
+    op = rng.randrange(7)
+    i = rng.randrange(len(lines))
+    if op == 0:  # drop a line
+        del lines[i]
+    elif op == 1:  # duplicate a line
+        lines.insert(i, lines[i])
+    elif op == 2:  # swap two lines
+        j = rng.randrange(len(lines))
+        lines[i], lines[j] = lines[j], lines[i]
+    elif op == 3:  # corrupt one field
+        f = lines[i].split("\t")
+        k = rng.randrange(len(f))
+        f[k] = rng.choice(["", "-", "x", "-1", "999999999999999999999", "g9.in[0+1]", "g0.out[-5+3]",
+                           "q0(g0e0)", "copy", "swap", "poll", "signal", "broadcast", "1e9", "\x00"])
+        lines[i] = "\t".join(f)
+    elif op == 4:  # truncate a line
+        lines[i] = lines[i][: rng.randrange(len(lines[i]) + 1)]
+    elif op == 5:  # random bytes
+        lines[i] = "".join(chr(rng.randrange(32, 127)) for _ in range(rng.randrange(40)))
+    else:  # change a number somewhere
+        f = lines[i].split("\t")
+        k = rng.randrange(len(f))
+        f[k] = "".join(ch if not ch.isdigit() else str(rng.randrange(10)) for ch in f[k])
+        lines[i] = "\t".join(f)
+    return "\n".join(lines) + ("\n" if rng.random() < 0.9 else "")
+
+
+def test_parse_survives_mutated_reference_text():
+    rng = random.Random(2511)
+    dumps = _dumps()
+    parsed = rejected = 0
+    for _ in range(3000):
+        e = rng.choice(dumps)
+        text = e["dump"]
+        for _ in range(rng.randrange(1, 4)):
+            text = _mutate(rng, text)
+        try:
+            p = cc.Program.parse(text, e["kind"], e["s"], e["n"])
+        except cc.InvalidArgument:
+            rejected += 1
+            continue
+        parsed += 1
+        p.validate()  # None or the first violation; must not crash
+        p.metrics()
+        p.traffic()
+        p.dump()
+    assert parsed > 100 and rejected > 100, (parsed, rejected)
