@@ -299,8 +299,16 @@ Traffic traffic(const Program& p) {  // account_traffic, verifier.cpp:281-327
   const int n = p.spec.nranks;
   t.rank_read.assign(n, 0);
   t.rank_write.assign(n, 0);
-  auto rd = [&](int r, int64_t b) { t.read += b; t.rank_read[r] += b; };
-  auto wr = [&](int r, int64_t b) { t.write += b; t.rank_write[r] += b; };
+  // Parsed programs may reference gpus outside [0, n) (validate() reports
+  // them); their bytes count in the totals only.
+  auto rd = [&](int r, int64_t b) {
+    t.read += b;
+    if (r >= 0 && r < n) t.rank_read[r] += b;
+  };
+  auto wr = [&](int r, int64_t b) {
+    t.write += b;
+    if (r >= 0 && r < n) t.rank_write[r] += b;
+  };
   for (const Lane& l : p.lanes)
     for (const Command& c : l.cmds) {
       switch (c.op) {
@@ -449,6 +457,8 @@ std::vector<std::string> split(const std::string& s, char sep) {
 }  // namespace
 
 Program parse_dump(const std::string& text, Kind kind, int64_t chunk, int nranks) {
+  if (nranks < 1 || nranks > 1024) throw std::invalid_argument("parse_dump: gpu_count out of range");
+  if (kind != Kind::AllGather && kind != Kind::AllToAll) throw std::invalid_argument("parse_dump: unknown collective");
   Program p;
   p.spec.kind = kind;
   p.spec.chunk = chunk;

@@ -65,3 +65,13 @@ def test_parse_survives_mutated_reference_text():
         p.traffic()
         p.dump()
     assert parsed > 100 and rejected > 100, (parsed, rejected)
+
+
+def test_parse_rejects_bad_parameters():
+    e = _dumps()[0]
+    for n in (0, -3, 5000):
+        try:
+            cc.Program.parse(e["dump"], e["kind"], e["s"], n)
+            raise AssertionError(f"accepted gpu_count {n}")
+        except cc.InvalidArgument:
+            pass
