@@ -75,3 +75,34 @@ def test_parse_rejects_bad_parameters():
             raise AssertionError(f"accepted gpu_count {n}")
         except cc.InvalidArgument:
             pass
+
+
+def test_program_api_survives_random_arguments():
+    """compile / select / metrics / traffic / validate / dump through the C
+    ABI with hostile arguments: errors, never crashes or runaway work."""
+    import ctypes as C
+
+    L = cc.lib()
+    rng = random.Random(606)
+    ok = 0
+    for _ in range(3000):
+        kind = rng.choice([0, 1, 2, -1, 7])
+        impl = rng.choice(list(range(-3, 13)))
+        s = rng.choice([0, -1, 1, 15, 4096, 1 << 40, -(1 << 62)])
+        n = rng.choice([0, 1, 2, 3, 8, 16, 33, 1025, -5])
+        lanes = rng.choice([0, 1, 2, 16, 64, -1])
+        h = C.c_void_p()
+        st = L.cecoll_program_compile(kind, impl, s, n, lanes, C.byref(h))
+        L.cecoll_select(kind, s, n, rng.choice([0, 1, 8]))
+        L.cecoll_reference_select(kind, s)
+        if st != 0:
+            assert not h.value
+            continue
+        ok += 1
+        p = cc.Program({0: "allgather", 1: "alltoall"}[kind], None, s, n, _handle=h)
+        p.metrics()
+        p.traffic()
+        p.validate(max(1, lanes))
+        if n <= 16:
+            p.dump()
+    assert ok > 50, ok
