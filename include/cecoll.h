@@ -113,6 +113,12 @@ cecoll_impl_t cecoll_select(cecoll_kind_t kind, int64_t chunk_bytes, int nranks,
  * (SPEC.md:61); cecoll_comm_init_all is that model (like
  * ncclCommInitAll). devlist may repeat a device: several ranks then share
  * one B200 ("co-resident ranks") and their transfers are intra-HBM.
+ *
+ * Threads: the communicators of one cecoll_comm_init_all / init_ranks call
+ * (one "world"), and the plans built on them, are driven by one host thread
+ * at a time, as with an NCCL communicator. Different worlds may be used from
+ * different threads concurrently. cecoll_last_error and the group state
+ * (cecoll_group_start/end) are per thread.
  * ------------------------------------------------------------------- */
 cecoll_status_t cecoll_comm_init_all(cecoll_comm_t* comms, int nranks, const int* devlist);
 /* Multi-process: one process per GPU owning one rank. `exchange` must

@@ -6,6 +6,7 @@
 // (1 read + 1 write), bcst 3*bytes (1 read + 2 writes), swap 4*bytes.
 // Variant choice (tile shape, occupancy, TMA vs registers) was measured with
 // tools/copy_bench.cu on the bench workload (profiles/copy_bench_r01.txt).
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 
@@ -415,13 +416,15 @@ cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream, cons
   if (t.nitems > kMaxItemsSmem) return cudaErrorInvalidValue;
   if (grid > t.ntiles) grid = t.ntiles;
   if (t.mover == Mover::Tma) {
-    static bool configured[64] = {false};
+    // The attribute is per device; set it once per device (any thread may
+    // launch, so the flags are atomic; devices beyond 64 set it every time).
+    static std::atomic<bool> configured[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 64 && !configured[dev]) {
+    if (dev >= 64 || !configured[dev].load(std::memory_order_acquire)) {
       cudaError_t e = cudaFuncSetAttribute(tma_items_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
       if (e != cudaSuccess) return e;
-      configured[dev] = true;
+      if (dev < 64) configured[dev].store(true, std::memory_order_release);
     }
     static const int evict_first = [] {
       const char* e = std::getenv("CECOLL_TMA_EVICT_FIRST");
