@@ -137,7 +137,18 @@ cecoll_status_t cecoll_comm_init_ranks(cecoll_comm_t* comms, int nranks, int fir
  * processes' rank ranges tile [0, nranks) and writes every rank's device. */
 cecoll_status_t cecoll_exchange_check(int nranks, int first_rank, int nlocal, int device, cecoll_exchange_fn exchange,
                                       void* ctx, int32_t* out_devices);
+/* Returns the world's async error when the last communicator of a world is
+ * destroyed (see cecoll_comm_get_async_error); everything is released anyway. */
 cecoll_status_t cecoll_comm_destroy(cecoll_comm_t comm);
+/* Like ncclCommGetAsyncError. Device-side flag polls give up after 20 s (the
+ * reference's untriggered-poll deadlock, sim.cpp:227-242) and record it in
+ * the plan's error word; collectives are asynchronous, so the failure is
+ * reported here: *async_error = CECOLL_TIMEOUT (message in
+ * cecoll_last_error) once any plan of the communicator's world has timed
+ * out, else CECOLL_SUCCESS. Sticky: a world that timed out has flags out of
+ * phase and must be destroyed. Reads the error words on a private stream, so
+ * it never waits for armed plans or running collectives. */
+cecoll_status_t cecoll_comm_get_async_error(cecoll_comm_t comm, cecoll_status_t* async_error);
 cecoll_status_t cecoll_comm_info(cecoll_comm_t comm, int* rank, int* nranks, int* device);
 
 /* Buffer registration (≙ BufferId::Input/Output being addressable on every
@@ -218,6 +229,15 @@ cecoll_status_t cecoll_plan_create_program(const cecoll_comm_t* comms, int ncomm
  * comms[i]; NULL entries = host trigger) and make each stream wait for
  * completion; re-arms the next instance off the critical path. */
 cecoll_status_t cecoll_plan_launch(cecoll_plan_t plan, void* const* streams);
+/* The two halves of cecoll_plan_launch, for callers that schedule the arming
+ * themselves (SURVEY §8(b) plan_arm / plan_trigger). cecoll_plan_arm launches
+ * the gated instance of every unit now (no-op for plans that are not
+ * prelaunch_* and for units already armed); cecoll_plan_trigger opens the
+ * armed instance exactly as cecoll_plan_launch does (arming first if needed)
+ * but leaves nothing armed behind, so device-wide synchronisation returns
+ * once the collective completes. */
+cecoll_status_t cecoll_plan_arm(cecoll_plan_t plan);
+cecoll_status_t cecoll_plan_trigger(cecoll_plan_t plan, void* const* streams);
 /* Cancels the armed instance (the next launch re-arms). While a plan is
  * armed its gate kernel waits on the device, so device-wide synchronisation
  * (cudaDeviceSynchronize) only returns after disarm, destroy or a launch. */

@@ -133,6 +133,9 @@ def lib():
         "cecoll_plan_launch": ([vp, C.POINTER(vp)], i32),
         "cecoll_plan_destroy": ([vp], i32),
         "cecoll_plan_disarm": ([vp], i32),
+        "cecoll_plan_arm": ([vp], i32),
+        "cecoll_comm_get_async_error": ([vp, C.POINTER(i32)], i32),
+        "cecoll_plan_trigger": ([vp, C.POINTER(vp)], i32),
         "cecoll_comm_counters": ([vp, C.POINTER(i64)], i32),
         "cecoll_mc_window_create": ([vp, sz, C.POINTER(vp), C.POINTER(vp)], i32),
         "cecoll_mc_allgather": ([vp, vp, sz, vp], i32),
@@ -155,7 +158,8 @@ EXPORTED_SYMBOLS = [
     "cecoll_register", "cecoll_deregister", "cecoll_allgather", "cecoll_alltoall", "cecoll_group_start",
     "cecoll_group_end", "cecoll_plan_create", "cecoll_plan_launch", "cecoll_plan_destroy", "cecoll_comm_counters",
     "cecoll_program_parse", "cecoll_plan_create_program", "cecoll_comm_init_ranks", "cecoll_exchange_check",
-    "cecoll_collective_n", "cecoll_plan_disarm", "cecoll_reduce_scatter", "cecoll_reduce_scatter_n",
+    "cecoll_collective_n", "cecoll_plan_disarm", "cecoll_plan_arm", "cecoll_plan_trigger",
+    "cecoll_comm_get_async_error", "cecoll_reduce_scatter", "cecoll_reduce_scatter_n",
     "cecoll_mem_alloc", "cecoll_mem_free", "cecoll_trace_begin", "cecoll_trace_end",
     "cecoll_mc_window_create", "cecoll_mc_allgather", "cecoll_mc_handle_type", "cecoll_mc_window_destroy",
 ]
@@ -353,10 +357,19 @@ class Comm:
                 "recorded_launches"]
         return dict(zip(keys, list(out)))
 
+    def async_error(self):
+        """None, or the CecollError a device-side poll of this world recorded
+        (CECOLL_TIMEOUT after 20 s without the peer's signal)."""
+        code = C.c_int32(0)
+        _check(lib().cecoll_comm_get_async_error(self._h, C.byref(code)), "comm_get_async_error")
+        if code.value == 0:
+            return None
+        return CecollError(code.value, lib().cecoll_last_error().decode(errors="replace"))
+
     def destroy(self):
         if self._h is not None:
-            _check(lib().cecoll_comm_destroy(self._h))
-            self._h = None
+            h, self._h = self._h, None
+            _check(lib().cecoll_comm_destroy(h), "comm_destroy")
 
 
 class McWindow:
@@ -537,7 +550,7 @@ class Plan:
                    "plan_create")
         self._h = h
 
-    def launch(self, streams=None):
+    def _streams(self, streams):
         # The marshalled stream array is cached per streams argument: a plan is
         # relaunched with the same streams in latency-bound loops.
         key = tuple(streams) if isinstance(streams, (list, tuple)) else streams
@@ -546,9 +559,20 @@ class Plan:
         if arr is None:
             seq = list(streams) if isinstance(streams, (list, tuple)) else [streams] * self._n
             arr = cache[key] = (C.c_void_p * self._n)(*[_stream(s) for s in seq])
-        st = _lib.cecoll_plan_launch(self._h, arr)
+        return arr
+
+    def launch(self, streams=None):
+        st = _lib.cecoll_plan_launch(self._h, self._streams(streams))
         if st:
             _check(st, "plan_launch")
+
+    def arm(self):
+        """Launch the gated instance now (prelaunch_* plans; no-op otherwise)."""
+        _check(lib().cecoll_plan_arm(self._h), "plan_arm")
+
+    def trigger(self, streams=None):
+        """Open the armed instance (arming first if needed) without re-arming."""
+        _check(lib().cecoll_plan_trigger(self._h, self._streams(streams)), "plan_trigger")
 
     def disarm(self):
         """Cancel the armed instance (needed before torch.cuda.synchronize())."""

@@ -258,7 +258,18 @@ cecoll_status_t cecoll_comm_destroy(cecoll_comm_t comm) {
   if (!comm) return err(CECOLL_INVALID_ARGUMENT, "null communicator");
   World* w = comm->world;
   delete comm;
-  if (--w->live_comms == 0) world_release(w);
+  if (--w->live_comms == 0) {
+    const Status s = world_release(w);
+    if (!s.ok()) return err(st(s), s.msg);
+  }
+  return CECOLL_SUCCESS;
+}
+
+cecoll_status_t cecoll_comm_get_async_error(cecoll_comm_t comm, cecoll_status_t* async_error) {
+  if (!comm || !async_error) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  const Status s = world_async_error(comm->world);
+  *async_error = st(s);
+  if (!s.ok()) set_error(s.msg);
   return CECOLL_SUCCESS;
 }
 
@@ -405,18 +416,34 @@ cecoll_status_t cecoll_plan_create_program(const cecoll_comm_t* comms, int ncomm
   return CECOLL_SUCCESS;
 }
 
-cecoll_status_t cecoll_plan_launch(cecoll_plan_t plan, void* const* streams) {
-  if (!plan) return err(CECOLL_INVALID_ARGUMENT, "null plan");
-  Plan* p = plan->plan;
-  // Units were formed per device (streams are bound at launch): each unit
-  // runs on the stream given for its lowest rank.
+namespace {
+// Units were formed per device (streams are bound at launch): each unit runs
+// on the stream given for its lowest rank.
+void bind_streams(Plan* p, void* const* streams) {
   for (Unit& u : p->units) {
     cudaStream_t s = nullptr;
     for (size_t i = 0; i < p->key_rank.size(); ++i)
       if (p->key_rank[i] == u.ranks[0] && streams) s = static_cast<cudaStream_t>(streams[i]);
     u.stream = s;
   }
-  return st(plan_launch(plan->world, p, true));
+}
+}  // namespace
+
+cecoll_status_t cecoll_plan_launch(cecoll_plan_t plan, void* const* streams) {
+  if (!plan) return err(CECOLL_INVALID_ARGUMENT, "null plan");
+  bind_streams(plan->plan, streams);
+  return st(plan_launch(plan->world, plan->plan, true));
+}
+
+cecoll_status_t cecoll_plan_arm(cecoll_plan_t plan) {
+  if (!plan) return err(CECOLL_INVALID_ARGUMENT, "null plan");
+  return st(plan_arm(plan->world, plan->plan));
+}
+
+cecoll_status_t cecoll_plan_trigger(cecoll_plan_t plan, void* const* streams) {
+  if (!plan) return err(CECOLL_INVALID_ARGUMENT, "null plan");
+  bind_streams(plan->plan, streams);
+  return st(plan_launch(plan->world, plan->plan, false));
 }
 
 cecoll_status_t cecoll_plan_destroy(cecoll_plan_t plan) {

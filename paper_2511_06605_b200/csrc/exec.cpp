@@ -418,6 +418,41 @@ Status plan_launch(World* w, Plan* p, bool rearm) {
   return {};
 }
 
+namespace {
+Status err_status(uint64_t err) {
+  return fail(CECOLL_TIMEOUT, (err & 1) ? "a flag poll timed out (20 s): a peer never signalled"
+                                        : "gate received an unknown post");
+}
+}  // namespace
+
+Status plan_poll_errors(Plan* p) {
+  if (p->inner) STATUS_TRY(plan_poll_errors(p->inner.get()));
+  for (Unit& u : p->units) {
+    if (!u.err) continue;
+    DeviceGuard g(u.device);
+    cudaStream_t s = nullptr;
+    CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    uint64_t err = 0;
+    cudaError_t e = cudaMemcpyAsync(&err, u.err, sizeof(err), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    CUDA_TRY(e);
+    if (err) return err_status(err);
+  }
+  return {};
+}
+
+void note_async(World* w, const Status& s) {
+  if (!s.ok() && w->async_error.ok()) w->async_error = s;
+}
+
+Status world_async_error(World* w) {
+  if (!w->async_error.ok()) return w->async_error;
+  for (auto& p : w->plans) note_async(w, plan_poll_errors(p.get()));
+  for (Plan* p : w->explicit_plans) note_async(w, plan_poll_errors(p));
+  return w->async_error;
+}
+
 Status plan_destroy(World* w, Plan* p) {
   Status result;
   if (p->inner) result = plan_destroy(w, p->inner.get());
@@ -433,8 +468,7 @@ Status plan_destroy(World* w, Plan* p) {
       if (u.arm) cudaStreamSynchronize(u.arm);
       uint64_t err = 0;
       if (cudaMemcpy(&err, u.err, sizeof(err), cudaMemcpyDeviceToHost) == cudaSuccess && err && result.ok())
-        result = fail(CECOLL_TIMEOUT, (err & 1) ? "a flag poll timed out (20 s): a peer never signalled"
-                                                : "gate received an unknown post");
+        result = err_status(err);
     }
     // Idempotent: every handle is cleared once released.
     if (u.exec) cudaGraphExecDestroy(u.exec);
@@ -482,7 +516,7 @@ Status run_collective(World* w, Kind kind, Impl impl, int64_t s, const std::vect
         DeviceGuard g(u.device);
         cudaStreamSynchronize(u.stream);
       }
-      plan_destroy(w, w->plans.front().get());
+      note_async(w, plan_destroy(w, w->plans.front().get()));
       w->plans.erase(w->plans.begin());
     }
   }

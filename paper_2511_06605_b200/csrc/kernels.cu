@@ -476,4 +476,32 @@ cudaError_t launch_gate(volatile uint64_t* posted, uint64_t* consumed, cudaGraph
   return cudaGetLastError();
 }
 
+// Loads every kernel of this file on the current device (and sets the TMA
+// mover's shared-memory attribute). With CUDA's lazy module loading (the
+// default) a kernel's first launch loads its module, and that load can wait
+// behind kernels already running on the device: an armed prelaunch gate
+// spinning on a trigger that this host thread has yet to post. Measured on
+// B200: the first eager collective with signal kernels stalled until a 20 s
+// flag poll timed out (tools/b2b_stress.py). Called for every device of a
+// world at init, so no launch of ours ever loads a module.
+cudaError_t preload_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {
+      reinterpret_cast<const void*>(reg_items_kernel<(1 << kItemCopy), 2>),
+      reinterpret_cast<const void*>(reg_items_kernel<(1 << kItemCopy) | (1 << kItemBcst), 2>),
+      reinterpret_cast<const void*>(reg_items_kernel<15, 1>),
+      reinterpret_cast<const void*>(tma_items_kernel),
+      reinterpret_cast<const void*>(poll_kernel),
+      reinterpret_cast<const void*>(signal_kernel),
+      reinterpret_cast<const void*>(gate_kernel),
+      reinterpret_cast<const void*>(gate_poll_kernel),
+      reinterpret_cast<const void*>(mc_store_kernel),
+  };
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaFuncSetAttribute(tma_items_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+}
+
 }  // namespace cecoll

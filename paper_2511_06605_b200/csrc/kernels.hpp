@@ -120,6 +120,10 @@ cudaError_t launch_reduce(const RedTable& t, int grid, cudaStream_t stream, cons
 //  signal: flags[i] = 1 with st.release.sys after a system-scope fence.
 //  gate:   wait for the next host post (pinned memory, see kernels.cu); a
 //          "go" post opens the conditional body, a "cancel" post skips it.
+// Load every kernel of the library on the current device (called at world
+// init for each device; see kernels.cu).
+cudaError_t preload_kernels();
+cudaError_t preload_reduce_kernels();
 cudaError_t launch_poll(uint64_t* const* flags, int n, uint64_t* err, cudaStream_t stream);
 cudaError_t launch_signal(uint64_t* const* flags, int n, cudaStream_t stream);
 cudaError_t launch_gate(volatile uint64_t* posted, uint64_t* consumed, cudaGraphConditionalHandle handle,

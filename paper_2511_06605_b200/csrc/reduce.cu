@@ -143,4 +143,22 @@ cudaError_t launch_reduce(const RedTable& t, int grid, cudaStream_t stream, cons
   }
 }
 
+// Loads every reduction kernel on the current device (see preload_kernels,
+// kernels.cu: a lazy module load can wait behind a spinning armed gate).
+cudaError_t preload_reduce_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {
+      reinterpret_cast<const void*>(reduce_kernel<kF32, kSum>),  reinterpret_cast<const void*>(reduce_kernel<kF32, kMax>),
+      reinterpret_cast<const void*>(reduce_kernel<kF32, kMin>),  reinterpret_cast<const void*>(reduce_kernel<kBF16, kSum>),
+      reinterpret_cast<const void*>(reduce_kernel<kBF16, kMax>), reinterpret_cast<const void*>(reduce_kernel<kBF16, kMin>),
+      reinterpret_cast<const void*>(reduce_kernel<kF16, kSum>),  reinterpret_cast<const void*>(reduce_kernel<kF16, kMax>),
+      reinterpret_cast<const void*>(reduce_kernel<kF16, kMin>),
+  };
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace cecoll

@@ -130,6 +130,10 @@ struct World {
   cecoll_exchange_fn exchange = nullptr;  // multi-process: kept for registration
   void* exchange_ctx = nullptr;
   int live_comms = 0;
+  // First failure of a cached plan found at its release or by
+  // cecoll_comm_get_async_error (a device-side flag poll timed out); sticky,
+  // returned by the communicator's destroy.
+  Status async_error;
   bool capturing = false;  // record_plan in progress: no batched memcpy (not capturable)
   std::unique_ptr<Tracer> tracer;  // non-null between cecoll_trace_begin and _end
   std::string trace_json;          // last finished trace, until read through the C ABI
@@ -243,7 +247,11 @@ Status world_init_ranks(int nranks, int first, int nlocal, int device, cecoll_ex
 Status gather_procs(int nranks, int first, int nlocal, int device, const cudaIpcMemHandle_t* flags,
                     cecoll_exchange_fn fn, void* ctx, std::vector<ProcInfoView>* out,
                     const unsigned char* uuid = nullptr, int32_t local_status = 0);
-void world_release(World* w);
+Status world_release(World* w);  // the world's async error, if any
+// Sticky async error of the world, refreshed from every live plan's device
+// error words (read on a private stream: never waits for armed graphs).
+Status world_async_error(World* w);
+void note_async(World* w, const Status& s);
 Status world_register(World* w, int rank, void* ptr, size_t bytes, cecoll_exchange_fn fn, void* ctx);
 Status world_deregister(World* w, void* ptr);
 Status world_mem_alloc(World* w, int rank, size_t bytes, void** out);
@@ -273,6 +281,7 @@ Status plan_arm(World* w, Plan* p);
 Status plan_disarm(World* w, Plan* p);
 Status plan_launch(World* w, Plan* p, bool rearm);
 Status plan_destroy(World* w, Plan* p);
+Status plan_poll_errors(Plan* p);  // CECOLL_TIMEOUT if a kernel-side poll of the plan timed out
 
 // NVLS multicast all-gather windows (mcast.cpp, experimental).
 struct McWindow;

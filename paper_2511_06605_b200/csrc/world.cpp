@@ -14,6 +14,9 @@ namespace {
 
 Status make_rank(World* w, int rank, int device, uint64_t* page = nullptr) {
   DeviceGuard g(device);
+  // Every kernel loaded now, never lazily behind an armed gate (kernels.cu).
+  CUDA_TRY(preload_kernels());
+  CUDA_TRY(preload_reduce_kernels());
   auto rs = std::make_unique<RankState>();
   rs->rank = rank;
   rs->device = device;
@@ -335,7 +338,7 @@ Status world_deregister(World* w, void* ptr) {
     }
   }
   if (!found) return fail(CECOLL_NOT_REGISTERED, "cecoll_deregister: pointer is not a registered window base");
-  for (auto& p : w->plans) plan_destroy(w, p.get());
+  for (auto& p : w->plans) note_async(w, plan_destroy(w, p.get()));
   w->plans.clear();
   return {};
 }
@@ -370,17 +373,17 @@ Status world_mem_free(World* w, void* ptr) {
   return {};
 }
 
-void world_release(World* w) {
+Status world_release(World* w) {
   if (w->tracer) {
     std::string discard;
     trace_end(w, &discard);
   }
-  for (auto& p : w->plans) plan_destroy(w, p.get());
+  for (auto& p : w->plans) note_async(w, plan_destroy(w, p.get()));
   w->plans.clear();
   // Armed explicit plans would keep their gate kernels waiting (and the
   // device synchronisation below would never return): cancel them. Their
   // cecoll_plan handles must not be used afterwards.
-  for (Plan* p : w->explicit_plans) plan_destroy(w, p);
+  for (Plan* p : w->explicit_plans) note_async(w, plan_destroy(w, p));
   w->explicit_plans.clear();
   for (auto& rs : w->local) {
     if (!rs) continue;
@@ -397,7 +400,9 @@ void world_release(World* w) {
   }
   for (void* p : w->ipc_opened) cudaIpcCloseMemHandle(p);
   if (w->flag_block) cudaFree(w->flag_block);
+  const Status result = w->async_error;
   delete w;
+  return result;
 }
 
 }  // namespace cecoll

@@ -409,3 +409,37 @@ def test_misrouted_program_fails_parity_on_the_gpu():
         torch.cuda.synchronize()
         bad_at = O.check(kind, s, n, False, host_in, res)
         assert (bad_at == -1) == want_ok, (want_ok, bad_at)
+
+
+@pytest.mark.parametrize("kind,impl", [("alltoall", "prelaunch_pcpy"), ("alltoall", "prelaunch_b2b"),
+                                       ("allgather", "prelaunch_bcst"), ("alltoall", "prelaunch_swap"),
+                                       ("allgather", "pcpy"), ("alltoall", "sm")])
+def test_plan_arm_and_trigger(kind, impl):
+    """SURVEY §8(b) plan_arm / plan_trigger: arm ahead (idempotent), trigger
+    without re-arming — after which device-wide synchronisation returns —,
+    disarm then trigger (re-arms inside), and every result byte-checked."""
+    n, s = 4, 12288
+    O = ora.Oracle()
+    in_place = impl.endswith("swap")
+    in_bytes = s if kind == "allgather" else n * s
+    sends = [torch.empty(in_bytes, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    recvs = sends if in_place else [torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    plan = cc.Plan(comms(n), kind, sends, recvs, s, impl=impl)
+    stream = torch.cuda.current_stream()
+    for it, steps in enumerate((["arm", "arm", "trigger"], ["trigger"], ["arm", "disarm", "trigger"])):
+        host_in = [ora.splitmix_pattern(in_bytes, r, 300 + it) for r in range(n)]
+        if not in_place:
+            for t in recvs:
+                t.fill_(0xA5)
+        for t, h in zip(sends, host_in):
+            t.copy_(torch.from_numpy(h))
+        torch.cuda.synchronize()
+        for step in steps:
+            if step == "trigger":
+                plan.trigger([stream] * n)
+            else:
+                getattr(plan, step)()
+        torch.cuda.synchronize()  # nothing is left armed after a trigger
+        res = [t.cpu().numpy() for t in recvs]
+        assert O.check(kind, s, n, in_place, host_in, res) == -1, (impl, steps)
+    plan.destroy()
