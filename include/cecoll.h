@@ -240,7 +240,14 @@ cecoll_status_t cecoll_plan_arm(cecoll_plan_t plan);
 cecoll_status_t cecoll_plan_trigger(cecoll_plan_t plan, void* const* streams);
 /* Cancels the armed instance (the next launch re-arms). While a plan is
  * armed its gate kernel waits on the device, so device-wide synchronisation
- * (cudaDeviceSynchronize) only returns after disarm, destroy or a launch. */
+ * (cudaDeviceSynchronize) only returns after disarm, destroy or a launch —
+ * and so does anything that synchronises the device implicitly or loads
+ * code: cudaFree, library plan creation (a cuFFT plan, measured), and under
+ * CUDA's default lazy module loading the first launch of any kernel not yet
+ * loaded in the process (tools/lazy_probe.py: a first torch kernel launched
+ * behind an armed plan never returned; CUDA_MODULE_LOADING=EAGER cures the
+ * kernel case, not the cuFFT one). Run such work before arming, disarm
+ * around it, or use cecoll_plan_trigger, which leaves nothing armed. */
 cecoll_status_t cecoll_plan_disarm(cecoll_plan_t plan);
 /* Destroy plans before their communicators; cecoll_comm_destroy cancels any
  * plan still armed (its handle must not be used afterwards). */
