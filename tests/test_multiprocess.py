@@ -280,3 +280,93 @@ def test_registration_fails_on_every_process_together():
     res = dict(_run2(_asymmetric_failure_worker))
     assert res[0].startswith("error"), res
     assert res[1].startswith("error") and "another process" in res[1], res
+
+
+def _stress_worker(rank, world, port, out, force_remote):
+    """Back-to-back collectives across two processes without host
+    synchronisation (DESIGN.md §3.2 across CUDA IPC): per local rank its own
+    stream; per iteration a random spin, the input reload, the collective, a
+    random spin and the copy-out; the processes meet only at the start."""
+    try:
+        if force_remote:
+            os.environ["CECOLL_FORCE_REMOTE_SIGNALS"] = "1"
+        dist = _init(rank, world, port)
+        import random
+
+        import numpy as np
+        import torch
+
+        import paper_2511_06605_b200 as cc
+        from oracle import oracle as ora
+
+        nranks, nlocal, iters = 4, 2, 10
+        first = rank * nlocal
+        comms = cc.Comm.init_ranks(nranks, first, nlocal, 0, cc.torch_exchange())
+        s = 24576 + 32
+        streams = [torch.cuda.Stream() for _ in range(nlocal)]
+        wins = [torch.zeros(2 * nranks * s, dtype=torch.uint8, device="cuda") for _ in comms]
+        for c, w in zip(comms, wins):
+            c.register(w)
+        results = []
+        for impl in ["sm", "pcpy", "b2b", "swap", "pull", "hybrid", "prelaunch_pcpy", "prelaunch_b2b"]:
+            rng = random.Random(f"{impl}-{rank}")
+            in_place = impl.endswith("swap")
+            hosts = [[ora.splitmix_pattern(nranks * s, r, 7000 + it) for r in range(nranks)] for it in range(iters)]
+            inputs = [[torch.from_numpy(hosts[it][first + k]).cuda() for k in range(nlocal)] for it in range(iters)]
+            outs = [[torch.empty(nranks * s, dtype=torch.uint8, device="cuda") for _ in range(nlocal)]
+                    for _ in range(iters)]
+            sends = [w[:nranks * s] for w in wins]
+            recvs = sends if in_place else [w[nranks * s:] for w in wins]
+            torch.cuda.synchronize()
+            dist.barrier()
+            for it in range(iters):
+                for k, st in enumerate(streams):
+                    with torch.cuda.stream(st):
+                        if rng.random() < 0.5:
+                            torch.cuda._sleep(rng.randint(1000, 100000))
+                        sends[k].copy_(inputs[it][k])
+                cc.all_to_all(comms, sends, recvs, s, impl=impl, streams=streams)
+                for k, st in enumerate(streams):
+                    with torch.cuda.stream(st):
+                        if rng.random() < 0.5:
+                            torch.cuda._sleep(rng.randint(1000, 100000))
+                        outs[it][k].copy_(recvs[k])
+            torch.cuda.synchronize()
+            bad = []
+            for it in range(iters):
+                for k in range(nlocal):
+                    r = first + k
+                    want = np.concatenate([hosts[it][j][r * s:(r + 1) * s] for j in range(nranks)])
+                    if not np.array_equal(outs[it][k].cpu().numpy(), want):
+                        bad.append((it, r))
+            results.append((impl, bad))
+            dist.barrier()
+        err = comms[0].async_error()
+        results.append(("async_error", [] if err is None else [str(err)]))
+        out.put((rank, results))
+        torch.cuda.synchronize()
+        for c in comms:
+            c.destroy()
+        dist.destroy_process_group()
+    except Exception:  # noqa: BLE001
+        out.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(400)
+@pytest.mark.parametrize("force_remote", [False, True])
+def test_two_processes_back_to_back_without_host_sync(force_remote):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stress_worker, args=(r, 2, port, q, force_remote)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=360) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, results in res:
+        assert isinstance(results, list), results
+        assert len(results) == 9
+        bad = [(impl, b) for impl, b in results if b]
+        assert not bad, (rank, bad)
