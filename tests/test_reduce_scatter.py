@@ -101,3 +101,54 @@ def _comms(n):
     if n not in _C:
         _C[n] = cc.Comm.init_all([0] * n)
     return _C[n]
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("impl,force_remote", [("sm", False), ("sm", True), ("pcpy", False), ("pcpy", True),
+                                               ("b2b", False), ("prelaunch_pcpy", False), ("prelaunch_pcpy", True)])
+def test_back_to_back_without_host_sync(impl, force_remote, monkeypatch):
+    """The reader-side protocol of reduce-scatter (a reader waits for the
+    owner's rdy and signals done back) under reuse: one stream per rank, per
+    iteration a random spin, the input reload, the collective, a random spin
+    and the copy-out, no host synchronisation. A send reloaded while a peer
+    still reads it, or a result read before every chunk was folded, changes
+    some iteration's bytes."""
+    import random
+
+    torch = pytest.importorskip("torch")
+    import paper_2511_06605_b200 as cc
+
+    if force_remote:
+        monkeypatch.setenv("CECOLL_FORCE_REMOTE_SIGNALS", "1")
+    n, count, iters = 4, 6144 + 8, 10
+    comms = cc.Comm.init_all([0] * n)
+    O = ora.Oracle()
+    rng = random.Random(f"rs-{impl}-{force_remote}")
+    ins = [_inputs("bf16", n, count, seed=500 + it) for it in range(iters)]
+    wants = [O.reduce_scatter(DT["bf16"], OPS["sum"], count, ins[it]) for it in range(iters)]
+    inputs = [[torch.from_numpy(b).cuda() for b in ins[it]] for it in range(iters)]
+    sends = [torch.empty(n * count * 2, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    recvs = [torch.empty(count * 2, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    outs = [[torch.empty(count * 2, dtype=torch.uint8, device="cuda") for _ in range(n)] for _ in range(iters)]
+    streams = [torch.cuda.Stream() for _ in range(n)]
+    torch.cuda.synchronize()
+    for it in range(iters):
+        for r, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                if rng.random() < 0.5:
+                    torch.cuda._sleep(rng.randint(1000, 100000))
+                sends[r].copy_(inputs[it][r])
+        cc.reduce_scatter(comms, sends, recvs, count, dtype="bf16", op="sum", impl=impl, streams=streams)
+        for r, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                if rng.random() < 0.5:
+                    torch.cuda._sleep(rng.randint(1000, 100000))
+                outs[it][r].copy_(recvs[r])
+    torch.cuda.synchronize()
+    bad = [(it, r) for it in range(iters) for r in range(n)
+           if not np.array_equal(outs[it][r].cpu().numpy(), wants[it][r])]
+    assert comms[0].async_error() is None
+    cc.destroy_all(comms)
+    assert not bad, bad
+
