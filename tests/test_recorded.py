@@ -244,3 +244,61 @@ def test_plan_cache_eviction_with_recorded_graphs():
     finally:
         torch.cuda.synchronize()
         cc.destroy_all(comms)
+
+
+@pytest.mark.timeout(180)
+@pytest.mark.parametrize("impl", ["sm", "pcpy", "b2b", "swap", "pull", "hybrid"])
+def test_caller_graph_with_many_collectives_on_rank_streams(impl):
+    """A caller's own CUDA graph holding K collectives on per-rank streams
+    (forked once from the capture stream, joined once): input reload,
+    collective, copy-out per iteration, flags between the four units inside
+    the graph; replayed twice back to back, three times (tools/caller_graph_probe.py)."""
+    n, s, K = 4, 16384 + 16, 4
+    comms = cc.Comm.init_all([0] * n)
+    try:
+        in_place = impl.endswith("swap")
+        hosts = [[ora.splitmix_pattern(n * s, r, 900 + it) for r in range(n)] for it in range(K)]
+        inputs = [[torch.from_numpy(hosts[it][r]).cuda() for r in range(n)] for it in range(K)]
+        sends = [torch.zeros(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+        recvs = sends if in_place else [torch.zeros(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+        outs = [[torch.zeros(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)] for _ in range(K)]
+        main = torch.cuda.Stream()
+        rs = [torch.cuda.Stream() for _ in range(n)]
+
+        def body():
+            for r in range(n):
+                rs[r].wait_stream(main)
+            for it in range(K):
+                for r in range(n):
+                    with torch.cuda.stream(rs[r]):
+                        sends[r].copy_(inputs[it][r])
+                cc.all_to_all(comms, sends, recvs, s, impl=impl, streams=rs)
+                for r in range(n):
+                    with torch.cuda.stream(rs[r]):
+                        outs[it][r].copy_(recvs[r])
+            for r in range(n):
+                main.wait_stream(rs[r])
+
+        with torch.cuda.stream(main):
+            body()  # eager warm-up: the plan is built outside the capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=main):
+            body()
+        for rep in range(3):
+            for it in range(K):
+                for t in outs[it]:
+                    t.zero_()
+            torch.cuda.synchronize()
+            g.replay()
+            g.replay()
+            torch.cuda.synchronize()
+            for it in range(K):
+                for r in range(n):
+                    want = np.concatenate([hosts[it][j][r * s:(r + 1) * s] for j in range(n)])
+                    assert np.array_equal(outs[it][r].cpu().numpy(), want), (impl, rep, it, r)
+        assert comms[0].async_error() is None
+        del g
+    finally:
+        torch.cuda.synchronize()
+        cc.destroy_all(comms)
