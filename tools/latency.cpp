@@ -148,6 +148,50 @@ int main(int argc, char** argv) {
       }
     }
   }
+  // Reduce-scatter (bf16 sum, eager collective call): chunk s bytes per rank.
+  const char* rs_names[] = {"sm", "pcpy", "b2b", "prelaunch_pcpy"};
+  for (size_t s = 4096; s <= max_s; s *= 4) {
+    for (const char* name : rs_names) {
+      if (!only.empty() && only != name) continue;
+      const cecoll_impl_t impl = cecoll_parse_impl(name);
+      const size_t count = s / 2;
+      auto call = [&]() {
+        CC(cecoll_reduce_scatter_n(comms.data(), n, send.data(), recv.data(), count, CECOLL_BF16, CECOLL_SUM, impl,
+                                   streams.data()));
+      };
+      for (int i = 0; i < 10; ++i) call();
+      sync_all();
+      auto h0 = std::chrono::steady_clock::now();
+      CK(cudaEventRecord(e0, stream));
+      fork();
+      for (int i = 0; i < iters; ++i) call();
+      join();
+      CK(cudaEventRecord(e1, stream));
+      auto h1 = std::chrono::steady_clock::now();
+      CK(cudaStreamSynchronize(stream));
+      float ms_b2b = 0;
+      CK(cudaEventElapsedTime(&ms_b2b, e0, e1));
+      std::vector<float> iso;
+      for (int i = 0; i < 20; ++i) {
+        sync_all();
+        CK(cudaEventRecord(e0, stream));
+        fork();
+        call();
+        join();
+        CK(cudaEventRecord(e1, stream));
+        CK(cudaStreamSynchronize(stream));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        iso.push_back(ms);
+      }
+      std::sort(iso.begin(), iso.end());
+      const double host_us = std::chrono::duration<double, std::micro>(h1 - h0).count() / iters;
+      std::printf("eager,%s,reduce_scatter_bf16_sum,%zu,%.2f,%.2f,%.2f\n", name, s, ms_b2b * 1000 / iters,
+                  iso[iso.size() / 2] * 1000, host_us);
+      std::fflush(stdout);
+      sync_all();
+    }
+  }
   for (auto c : comms) CC(cecoll_comm_destroy(c));
   return 0;
 }
