@@ -380,6 +380,9 @@ cecoll_status_t cecoll_plan_create(const cecoll_comm_t* comms, int ncomms, cecol
                                    cecoll_impl_t impl, cecoll_plan_t* out) {
   if (!comms || ncomms <= 0 || !sends || !recvs || !out) return err(CECOLL_INVALID_ARGUMENT, "null argument");
   if (!impl_ok(impl)) return err(CECOLL_INVALID_ARGUMENT, "unknown implementation");
+  if (kind != CECOLL_ALLGATHER && kind != CECOLL_ALLTOALL) return err(CECOLL_INVALID_ARGUMENT, "unknown collective");
+  for (int i = 0; i < ncomms; ++i)
+    if (!comms[i]) return err(CECOLL_INVALID_ARGUMENT, "null communicator");
   World* w = comms[0]->world;
   std::vector<CallArgs> args;
   // Streams are bound at launch; plan units are formed per (device, rank)
@@ -401,6 +404,8 @@ cecoll_status_t cecoll_plan_create_program(const cecoll_comm_t* comms, int ncomm
                                            const void* const* sends, void* const* recvs, cecoll_plan_t* out) {
   if (!comms || ncomms <= 0 || !program || !sends || !recvs || !out)
     return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  for (int i = 0; i < ncomms; ++i)
+    if (!comms[i]) return err(CECOLL_INVALID_ARGUMENT, "null communicator");
   World* w = comms[0]->world;
   std::vector<CallArgs> args;
   for (int i = 0; i < ncomms; ++i) {

@@ -106,3 +106,37 @@ def test_program_api_survives_random_arguments():
         if n <= 16:
             p.dump()
     assert ok > 50, ok
+
+
+def test_runtime_entry_points_reject_null_handles():
+    """Every runtime entry point checks its handles before touching them
+    (no CUDA needed: the checks come first): null communicators inside the
+    arrays, null plans, null outputs -> CECOLL_INVALID_ARGUMENT, no crash."""
+    import ctypes as C
+
+    L = cc.lib()
+    vp = C.c_void_p
+    null_comms = (vp * 2)(None, None)
+    bufs = (vp * 2)(None, None)
+    out = vp()
+    L.cecoll_plan_create.argtypes = [C.POINTER(vp), C.c_int, C.c_int, C.POINTER(vp), C.POINTER(vp), C.c_size_t,
+                                     C.c_int, C.POINTER(vp)]
+    assert L.cecoll_plan_create(null_comms, 2, 0, bufs, bufs, 4096, 0, C.byref(out)) == 1
+    assert L.cecoll_plan_create(null_comms, 2, 7, bufs, bufs, 4096, 0, C.byref(out)) == 1  # unknown kind
+    assert L.cecoll_plan_create_program(null_comms, 2, vp(1), bufs, bufs, C.byref(out)) == 1
+    assert L.cecoll_plan_launch(None, None) == 1
+    assert L.cecoll_plan_arm(None) == 1
+    assert L.cecoll_plan_trigger(None, None) == 1
+    assert L.cecoll_plan_disarm(None) == 1
+    assert L.cecoll_plan_destroy(None) == 1
+    assert L.cecoll_comm_destroy(None) == 1
+    code = C.c_int(0)
+    assert L.cecoll_comm_get_async_error(None, C.byref(code)) == 1
+    assert L.cecoll_mem_alloc(None, 4096, C.byref(out)) == 1
+    assert L.cecoll_mem_free(None, None) == 1
+    assert L.cecoll_register(None, None, 0) == 1
+    assert L.cecoll_deregister(None, None) == 1
+    assert L.cecoll_collective_n(0, null_comms, 2, bufs, bufs, 4096, 0, None) == 1
+    assert L.cecoll_reduce_scatter_n(null_comms, 2, bufs, bufs, 1024, 1, 0, 0, None) == 1
+    assert L.cecoll_allgather(None, None, 4096, 0, None, None) == 1
+    assert b"null" in L.cecoll_last_error()
