@@ -368,8 +368,14 @@ def run_ours(args):
         "energy": energy,
         "clocks": clocks.summary(),
     }
+    err = comms[0].async_error()  # a device-side poll timeout anywhere in the run (none expected)
+    if err is not None:
+        line["async_error"] = str(err)[:200]
     print(json.dumps(line), flush=True)
-    cc.destroy_all(comms)
+    try:
+        cc.destroy_all(comms)
+    except cc.CecollError:
+        pass  # already reported in the line
 
 
 def measure_energy(step, stream, n, s, seconds=1.5, dev=0):

@@ -45,6 +45,18 @@ AA_IMPLS = ["sm", "pcpy", "b2b", "swap", "hybrid", "pull", "prelaunch_pcpy", "pr
 HEADLINE_IMPLS = ["sm", "pcpy", "b2b", "swap", "hybrid", "pull", "hybrid@25", "hybrid@75"]
 
 STATE: dict = {}  # what the watchdog prints if a collective hangs
+ASYNC_NOTES: list = []  # device-side poll timeouts reported when a phase's world is destroyed
+
+
+def quiet_destroy(objs):
+    """Destroy communicators without raising: a device-side poll timeout that
+    a phase's world recorded (cecoll_comm_destroy's async error) is noted in
+    the line (`async_errors`) instead of ending the run before it prints."""
+    for o in objs:
+        try:
+            o.destroy()
+        except cc.CecollError as e:
+            ASYNC_NOTES.append(f"{STATE.get('phase', '?')}: {str(e)[:200]}")
 
 
 # ---------------------------------------------------------------------------
@@ -555,12 +567,17 @@ def run(args, B):
         STATE["phase"] = "experiments multicast"
         run_mc_experiment(world, rank, dev, stream, line["experiments"])
     line["config"]["wall_s"] = round(time.time() - t_start, 1)
+    err = comms[0].async_error()
+    if err is not None:
+        ASYNC_NOTES.append(f"headline world: {str(err)[:200]}")
+    if ASYNC_NOTES:
+        line["async_errors"] = ASYNC_NOTES
     if rank == 0:
         print(json.dumps(line), flush=True)
     dog.cancel()
     torch.cuda.synchronize()
     dist.barrier()
-    cc.destroy_all(comms)
+    quiet_destroy(comms)
     dist.destroy_process_group()
 
 
@@ -720,7 +737,7 @@ def sweep_pass(world, rank, dev, nccl, stream, t_start, args, rows, prelaunch):
                 print(json.dumps(row), flush=True)
     torch.cuda.synchronize()
     dist.barrier()
-    comms[0].destroy()
+    quiet_destroy(comms[:1])
     del win, exp
 
 
@@ -915,7 +932,7 @@ def run_interference(world, rank, dev, nccl, stream, args, out):
             "collective_slowdown": round(coll_with / alone, 3)}
     torch.cuda.synchronize()
     dist.barrier()
-    comms[0].destroy()
+    quiet_destroy(comms[:1])
 
 
 def run_sync_chain(world, rank, dev, stream, out):
@@ -984,7 +1001,7 @@ def run_sync_chain(world, rank, dev, stream, out):
                                  "overhead_us": round((t_chain - t_gemm - t_coll) * 1e3, 2)})
     torch.cuda.synchronize()
     dist.barrier()
-    comms[0].destroy()
+    quiet_destroy(comms[:1])
 
 
 # ---------------------------------------------------------------------------
@@ -1091,7 +1108,7 @@ def run_mc_experiment(world, rank, dev, stream, out):
         ok, err = False, str(e)[:200]
     if not all_true(ok):
         res["error"] = err or "window creation failed on another rank"
-        comms[0].destroy()
+        quiet_destroy(comms[:1])
         return
     send = torch.empty(cap, dtype=torch.uint8, device="cuda")
     exp = torch.empty(n * cap, dtype=torch.uint8, device="cuda")
@@ -1128,4 +1145,4 @@ def run_mc_experiment(world, rank, dev, stream, out):
         win.destroy()
     except Exception:  # noqa: BLE001
         pass
-    comms[0].destroy()
+    quiet_destroy(comms[:1])
