@@ -443,3 +443,40 @@ def test_plan_arm_and_trigger(kind, impl):
         res = [t.cpu().numpy() for t in recvs]
         assert O.check(kind, s, n, in_place, host_in, res) == -1, (impl, steps)
     plan.destroy()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("impl", ["sm", "pcpy", "b2b", "bcst", "prelaunch_bcst", "prelaunch_pcpy", "hybrid", "pull"])
+def test_allgather_back_to_back_without_host_sync(impl):
+    """The all-gather side of the flag-reuse stress (bcst's two-destination
+    items included): one stream per rank, random spin delays, input reload,
+    collective, copy-out, no host synchronisation until the end."""
+    import random
+
+    n, s, iters = 4, 12288 + 16, 12
+    cs = comms(n)
+    rng = random.Random("ag-" + impl)
+    streams = [torch.cuda.Stream() for _ in range(n)]
+    hosts = [[ora.splitmix_pattern(s, r, 6000 + it) for r in range(n)] for it in range(iters)]
+    inputs = [[torch.from_numpy(hosts[it][r]).cuda() for r in range(n)] for it in range(iters)]
+    sends = [torch.empty(s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    recvs = [torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    outs = [[torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)] for _ in range(iters)]
+    torch.cuda.synchronize()
+    for it in range(iters):
+        for r, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                if rng.random() < 0.5:
+                    torch.cuda._sleep(rng.randint(1000, 100000))
+                sends[r].copy_(inputs[it][r])
+        cc.all_gather(cs, sends, recvs, s, impl=impl, streams=streams)
+        for r, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                if rng.random() < 0.5:
+                    torch.cuda._sleep(rng.randint(1000, 100000))
+                outs[it][r].copy_(recvs[r])
+    torch.cuda.synchronize()
+    for it in range(iters):
+        want = np.concatenate(hosts[it])
+        for r in range(n):
+            assert np.array_equal(outs[it][r].cpu().numpy(), want), (impl, it, r)

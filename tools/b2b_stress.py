@@ -1,7 +1,7 @@
 """Repeats the back-to-back stress of tests/test_gpu_parity.py many times and
 classifies every mismatch (which iteration's bytes landed where): a
 diagnostic for flag-protocol races. Usage:
-  python tools/b2b_stress.py IMPL REPS [force]"""
+  python tools/b2b_stress.py IMPL REPS [force|plain] [allgather|alltoall]"""
 import os
 import random
 import sys
@@ -16,7 +16,13 @@ import paper_2511_06605_b200 as cc
 from oracle import oracle as ora
 
 
+KIND = sys.argv[4] if len(sys.argv) > 4 else "alltoall"
+
+
 def expected_alltoall(hosts_it, n, s):
+    if KIND == "allgather":
+        full = np.concatenate([hosts_it[j][:s] for j in range(n)])
+        return [full for _ in range(n)]
     return [np.concatenate([hosts_it[j][r * s:(r + 1) * s] for j in range(n)]) for r in range(n)]
 
 
@@ -25,9 +31,10 @@ def one(impl, rep, n=4, s=12288 + 16, iters=12, fresh=True):
     rng = random.Random(f"b2b-{impl}-{rep}")
     in_place = impl.endswith("swap")
     streams = [torch.cuda.Stream() for _ in range(n)]
-    hosts = [[ora.splitmix_pattern(n * s, r, 5000 + it) for r in range(n)] for it in range(iters)]
+    in_bytes = s if KIND == "allgather" else n * s
+    hosts = [[ora.splitmix_pattern(in_bytes, r, 5000 + it) for r in range(n)] for it in range(iters)]
     inputs = [[torch.from_numpy(hosts[it][r]).cuda() for r in range(n)] for it in range(iters)]
-    sends = [torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    sends = [torch.empty(in_bytes, dtype=torch.uint8, device="cuda") for _ in range(n)]
     recvs = sends if in_place else [torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)]
     outs = [[torch.empty(n * s, dtype=torch.uint8, device="cuda") for _ in range(n)] for _ in range(iters)]
     torch.cuda.synchronize()
@@ -37,7 +44,8 @@ def one(impl, rep, n=4, s=12288 + 16, iters=12, fresh=True):
                 if rng.random() < 0.5:
                     torch.cuda._sleep(rng.randint(1000, 100000))
                 sends[r].copy_(inputs[it][r])
-        cc.all_to_all(cs, sends, recvs, s, impl=impl, streams=streams)
+        fn = cc.all_gather if KIND == "allgather" else cc.all_to_all
+        fn(cs, sends, recvs, s, impl=impl, streams=streams)
         for r, st in enumerate(streams):
             with torch.cuda.stream(st):
                 if rng.random() < 0.5:
@@ -78,4 +86,5 @@ if __name__ == "__main__":
         if b or err or dt > 5:
             fails += 1
             print(f"rep {rep} ({dt:.1f} s) err={err}: {len(b)} bad blocks: {b[:4]}", flush=True)
-    print(f"{impl} force={os.environ.get('CECOLL_FORCE_REMOTE_SIGNALS', '0')}: {fails}/{reps} reps failed", flush=True)
+    print(f"{KIND} {impl} force={os.environ.get('CECOLL_FORCE_REMOTE_SIGNALS', '0')}: {fails}/{reps} reps failed",
+          flush=True)
