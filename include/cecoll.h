@@ -283,6 +283,12 @@ cecoll_status_t cecoll_comm_counters(cecoll_comm_t comm, int64_t out8[8]);
  * CECOLL_UNSUPPORTED wherever the node offers no multicast objects (e.g. the
  * one-GPU development boxes). Not yet executed on hardware that accepts
  * multicast objects.
+ * Reuse: the window has no ready flags (unlike the copy-engine and SM
+ * paths). A call's stores land in every rank's window as soon as that rank
+ * issues it, so every rank must have consumed the previous result (or copied
+ * it out) before any rank starts the next call on the same window (e.g. a
+ * barrier). Back-to-back calls with unchanged inputs, as in a timing loop,
+ * are safe. Completion flags are per-call epochs that only grow.
  * ------------------------------------------------------------------- */
 typedef struct cecoll_mc* cecoll_mc_t;
 cecoll_status_t cecoll_mc_window_create(cecoll_comm_t comm, size_t chunk_capacity, cecoll_mc_t* out, void** recv);
