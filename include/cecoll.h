@@ -118,7 +118,12 @@ cecoll_impl_t cecoll_select(cecoll_kind_t kind, int64_t chunk_bytes, int nranks,
  * (one "world"), and the plans built on them, are driven by one host thread
  * at a time, as with an NCCL communicator. Different worlds may be used from
  * different threads concurrently. cecoll_last_error and the group state
- * (cecoll_group_start/end) are per thread.
+ * (cecoll_group_start/end) are per thread. Eager calls never leave a gate
+ * waiting on the host, even for prelaunch_* implementations: each instance is
+ * launched after its trigger is posted. An explicit plan armed ahead is
+ * different. It blocks device-wide synchronisation and lazy module loads in
+ * every thread of the process until it is launched or disarmed (see
+ * cecoll_plan_disarm).
  * ------------------------------------------------------------------- */
 cecoll_status_t cecoll_comm_init_all(cecoll_comm_t* comms, int nranks, const int* devlist);
 /* Multi-process: one process per GPU owning one rank. `exchange` must

@@ -409,11 +409,23 @@ Status plan_launch(World* w, Plan* p, bool rearm) {
       return launch_recorded(w, p);
     return p->sm ? run_sm(w, p) : run_ce(w, p);
   }
-  // prelaunch: make sure every unit is armed, trigger all, re-arm if asked.
-  STATUS_TRY(plan_arm(w, p));
-  std::vector<cudaEvent_t> spans(p->units.size(), nullptr);
-  for (size_t i = 0; i < p->units.size(); ++i) STATUS_TRY(trigger_signal(w, p->units[i], &spans[i]));
-  for (size_t i = 0; i < p->units.size(); ++i) STATUS_TRY(trigger_wait(w, p->units[i], spans[i]));
+  // prelaunch: trigger every unit, then wait; re-arm if asked. A unit that
+  // is not armed yet (eager calls, a plan's first launch) gets its post and
+  // ready flag before its gated instance is launched: that instance never
+  // waits on the host, so no CUDA call of this thread or another (a lazy
+  // module load, a device synchronisation) can end up waiting behind a gate
+  // whose trigger it blocks.
+  const size_t nu = p->units.size();
+  std::vector<bool> was_armed(nu);
+  for (size_t i = 0; i < nu; ++i) was_armed[i] = p->units[i].armed;
+  std::vector<cudaEvent_t> spans(nu, nullptr);
+  for (size_t i = 0; i < nu; ++i) STATUS_TRY(trigger_signal(w, p->units[i], &spans[i]));
+  for (size_t i = 0; i < nu; ++i) {
+    if (was_armed[i]) continue;
+    STATUS_TRY(arm_unit(w, p->units[i]));  // consumes the post just made
+    p->units[i].armed = false;
+  }
+  for (size_t i = 0; i < nu; ++i) STATUS_TRY(trigger_wait(w, p->units[i], spans[i]));
   if (rearm) STATUS_TRY(plan_arm(w, p));
   return {};
 }

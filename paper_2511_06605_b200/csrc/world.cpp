@@ -12,6 +12,19 @@ namespace cecoll {
 
 namespace {
 
+// Zeroes device memory and waits for it on a private stream: never a
+// device-wide synchronisation, which would wait for another world's armed
+// prelaunch gate.
+Status zero_now(void* p, size_t bytes) {
+  cudaStream_t s = nullptr;
+  CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaError_t e = cudaMemsetAsync(p, 0, bytes, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  CUDA_TRY(e);
+  return {};
+}
+
 Status make_rank(World* w, int rank, int device, uint64_t* page = nullptr) {
   DeviceGuard g(device);
   // Every kernel loaded now, never lazily behind an armed gate (kernels.cu).
@@ -26,8 +39,7 @@ Status make_rank(World* w, int rank, int device, uint64_t* page = nullptr) {
     rs->owns_flags = false;
   } else {
     CUDA_TRY(cudaMalloc(&rs->flags, kFlagBytes));
-    CUDA_TRY(cudaMemset(rs->flags, 0, kFlagBytes));
-    CUDA_TRY(cudaDeviceSynchronize());
+    STATUS_TRY(zero_now(rs->flags, kFlagBytes));
   }
   w->flag_page[rank] = rs->flags;
   w->local[rank] = std::move(rs);
@@ -196,8 +208,7 @@ Status world_init_ranks(int nranks, int first, int nlocal, int device, cecoll_ex
     void* block = nullptr;
     CUDA_TRY(cudaMalloc(&block, kFlagBytes * nlocal));
     w->flag_block = block;
-    CUDA_TRY(cudaMemset(block, 0, kFlagBytes * nlocal));
-    CUDA_TRY(cudaDeviceSynchronize());
+    STATUS_TRY(zero_now(block, kFlagBytes * nlocal));
     for (int k = 0; k < nlocal; ++k)
       STATUS_TRY(make_rank(w.get(), first + k, device,
                            reinterpret_cast<uint64_t*>(static_cast<char*>(block) + k * kFlagBytes)));

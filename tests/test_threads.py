@@ -53,6 +53,14 @@ def worker(tid, iters, errors):
 
 
 def test_two_worlds_from_two_threads():
+    # torch's own kernels loaded once up front: the test is about the
+    # library's threads, not about lazy module loading
+    g = torch.Generator(device="cuda")
+    g.manual_seed(0)
+    x = torch.randint(0, 256, (N * S,), dtype=torch.uint8, device="cuda", generator=g)
+    y = torch.full((N * S,), 0xA5, dtype=torch.uint8, device="cuda")
+    torch.equal(torch.cat([x[:S], y[:S]]), torch.cat([y[:S], x[:S]]))  # loads cat, eq, all
+    torch.cuda.synchronize()
     errors = []
     threads = [threading.Thread(target=worker, args=(t, 48, errors)) for t in range(2)]
     for t in threads:
