@@ -179,6 +179,12 @@ cecoll_status_t cecoll_mem_free(cecoll_comm_t comm, void* ptr);
  * In single-process mode call once per rank inside group_start/group_end
  * (all ranks of the communicator must participate); a lone call outside a
  * group is only valid for multi-process communicators.
+ * Ordering: the collectives and plan launches of one world share its flag
+ * slots (one rdy and one done word per rank pair). Each rank's calls must
+ * therefore be ordered on the device: issue them on the same stream per
+ * rank, or order the streams with events. As with NCCL, two collectives of
+ * one world must not be in flight on unordered streams of the same rank.
+ * Every rank must also issue the world's collectives in the same order.
  * ------------------------------------------------------------------- */
 cecoll_status_t cecoll_allgather(const void* send, void* recv, size_t chunk_bytes, cecoll_impl_t impl,
                                  cecoll_comm_t comm, void* stream);
