@@ -124,6 +124,13 @@ cecoll_impl_t cecoll_select(cecoll_kind_t kind, int64_t chunk_bytes, int nranks,
  * different. It blocks device-wide synchronisation and lazy module loads in
  * every thread of the process until it is launched or disarmed (see
  * cecoll_plan_disarm).
+ * Open issue: one thread calling cudaDeviceSynchronize in a loop while
+ * another issues collectives has crashed inside the CUDA runtime on these
+ * boxes. The crash is intermittent, needs the collectives' own kernels, and
+ * does not occur with torch-only work (tools/thread_sync_probe.py,
+ * tools/torch_sync_probe.py). cecoll_comm_destroy synchronises the device.
+ * So destroy worlds, and synchronise the whole device, only while no other
+ * thread is issuing collectives.
  * ------------------------------------------------------------------- */
 cecoll_status_t cecoll_comm_init_all(cecoll_comm_t* comms, int nranks, const int* devlist);
 /* Multi-process: one process per GPU owning one rank. `exchange` must

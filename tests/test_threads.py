@@ -25,9 +25,10 @@ def expected(kind, sends):
     return [torch.cat([sends[j][r * S:(r + 1) * S] for j in range(N)]) for r in range(N)]
 
 
-def worker(tid, iters, errors):
+def worker(tid, iters, errors, worlds):
     try:
         comms = cc.Comm.init_all([0] * N)
+        worlds.append(comms)
         stream = torch.cuda.Stream()
         g = torch.Generator(device="cuda")
         g.manual_seed(1000 + tid)
@@ -46,8 +47,6 @@ def worker(tid, iters, errors):
                         errors.append((tid, it, impl, kind, r))
                         return
         stream.synchronize()
-        for c in comms:
-            c.destroy()
     except Exception as e:  # reported by the main thread
         errors.append((tid, repr(e)))
 
@@ -61,11 +60,16 @@ def test_two_worlds_from_two_threads():
     y = torch.full((N * S,), 0xA5, dtype=torch.uint8, device="cuda")
     torch.equal(torch.cat([x[:S], y[:S]]), torch.cat([y[:S], x[:S]]))  # loads cat, eq, all
     torch.cuda.synchronize()
-    errors = []
-    threads = [threading.Thread(target=worker, args=(t, 48, errors)) for t in range(2)]
+    errors, worlds = [], []
+    threads = [threading.Thread(target=worker, args=(t, 48, errors, worlds)) for t in range(2)]
     for t in threads:
         t.start()
     for t in threads:
         t.join(timeout=240)
     assert not any(t.is_alive() for t in threads), "a worker thread hung"
+    # Destroyed here, not in the workers: destroy synchronises the device,
+    # which must not overlap another thread's collectives (include/cecoll.h).
+    for comms in worlds:
+        cc.destroy_all(comms)
     assert errors == []
+
