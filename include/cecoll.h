@@ -129,8 +129,11 @@ cecoll_impl_t cecoll_select(cecoll_kind_t kind, int64_t chunk_bytes, int nranks,
  * boxes. The crash is intermittent, needs the collectives' own kernels, and
  * does not occur with torch-only work (tools/thread_sync_probe.py,
  * tools/torch_sync_probe.py). cecoll_comm_destroy synchronises the device.
- * So destroy worlds, and synchronise the whole device, only while no other
- * thread is issuing collectives.
+ * It needs the recorded command lists (cudaGraphLaunch of the library's
+ * graphs). With CECOLL_GRAPH=0, or with stream-level synchronisation in the
+ * other thread, it did not occur. So destroy worlds, and synchronise the
+ * whole device, only while no other thread is issuing collectives. A
+ * program that cannot avoid it sets CECOLL_GRAPH=0.
  * ------------------------------------------------------------------- */
 cecoll_status_t cecoll_comm_init_all(cecoll_comm_t* comms, int nranks, const int* devlist);
 /* Multi-process: one process per GPU owning one rank. `exchange` must

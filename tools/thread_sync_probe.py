@@ -1,6 +1,7 @@
 """One thread synchronises the device in a loop while another runs eager
 prelaunch collectives (tests/test_threads.py); repeated, with faulthandler.
-Usage: python -X faulthandler tools/thread_sync_probe.py [reps] [impl]"""
+Usage: python -X faulthandler tools/thread_sync_probe.py [reps] [impl]
+PROBE_SYNC=stream: the other thread synchronises an idle stream instead."""
 import faulthandler
 import os
 import sys
@@ -24,9 +25,14 @@ for rep in range(reps):
     done = threading.Event()
     errors = []
 
+    other = torch.cuda.Stream()
+
     def syncer():
         while not done.is_set():
-            torch.cuda.synchronize()
+            if os.environ.get("PROBE_SYNC") == "stream":
+                other.synchronize()
+            else:
+                torch.cuda.synchronize()
 
     def runner():
         try:
