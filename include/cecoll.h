@@ -129,11 +129,14 @@ cecoll_impl_t cecoll_select(cecoll_kind_t kind, int64_t chunk_bytes, int nranks,
  * boxes. The crash is intermittent, needs the collectives' own kernels, and
  * does not occur with torch-only work (tools/thread_sync_probe.py,
  * tools/torch_sync_probe.py). cecoll_comm_destroy synchronises the device.
- * It needs the recorded command lists (cudaGraphLaunch of the library's
- * graphs). With CECOLL_GRAPH=0, or with stream-level synchronisation in the
- * other thread, it did not occur. So destroy worlds, and synchronise the
- * whole device, only while no other thread is issuing collectives. A
- * program that cannot avoid it sets CECOLL_GRAPH=0.
+ * The cause is the recording itself. A plan's second launch captures its
+ * submission (a stream capture in progress), and a device synchronisation
+ * from another thread during that capture crashes. It does not happen with
+ * plans recorded before the race (PROBE_WARM=1), with CECOLL_GRAPH=0, or
+ * with stream-level synchronisation in the other thread. So either launch
+ * each plan twice before another thread may synchronise the device, or set
+ * CECOLL_GRAPH=0. Likewise, destroy worlds only while no other thread is
+ * issuing collectives.
  * ------------------------------------------------------------------- */
 cecoll_status_t cecoll_comm_init_all(cecoll_comm_t* comms, int nranks, const int* devlist);
 /* Multi-process: one process per GPU owning one rank. `exchange` must

@@ -1,7 +1,8 @@
 """One thread synchronises the device in a loop while another runs eager
 prelaunch collectives (tests/test_threads.py); repeated, with faulthandler.
 Usage: python -X faulthandler tools/thread_sync_probe.py [reps] [impl]
-PROBE_SYNC=stream: the other thread synchronises an idle stream instead."""
+PROBE_SYNC=stream: the other thread synchronises an idle stream instead.
+PROBE_WARM=1: every plan is recorded (launched three times) before the race."""
 import faulthandler
 import os
 import sys
@@ -21,6 +22,10 @@ for rep in range(reps):
     sends = [torch.randint(0, 256, (N * S,), dtype=torch.uint8, device="cuda") for _ in range(N)]
     recvs = [torch.empty(N * S, dtype=torch.uint8, device="cuda") for _ in range(N)]
     stream = torch.cuda.Stream()
+    if os.environ.get("PROBE_WARM") == "1":  # record every plan before the race
+        for impl in impls:
+            for _ in range(3):
+                cc.all_to_all(comms, sends, recvs, S, impl=impl, streams=stream)
     torch.cuda.synchronize()
     done = threading.Event()
     errors = []
