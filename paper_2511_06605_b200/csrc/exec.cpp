@@ -274,6 +274,15 @@ bool graph_mode_wanted(World* w, Plan* p) {
     return e && std::string(e) == "0";
   }();
   if (off || p->prelaunch || w->tracer) return false;
+  // A submission of exactly one kernel launch (the SM path with one unit and
+  // no flags) gains nothing from a graph, and skipping the recording keeps
+  // its stream out of capture mode (open issue).
+  if (p->sm && !p->hybrid && p->units.size() == 1) {
+    const Unit& u = p->units[0];
+    if (u.start.empty() && u.start_remote.empty() && u.sm_pre.empty() && u.sm_post.empty() &&
+        u.sm_post_remote.empty() && u.finish.empty())
+      return false;
+  }
   std::set<int> devs;
   for (const Unit& u : p->units) {
     if (!u.stream || u.stream == cudaStreamLegacy || u.stream == cudaStreamPerThread) return false;
