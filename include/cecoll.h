@@ -133,8 +133,10 @@ cecoll_impl_t cecoll_select(cecoll_kind_t kind, int64_t chunk_bytes, int nranks,
  * submission (a stream capture in progress), and a device synchronisation
  * from another thread during that capture crashes. It does not happen with
  * plans recorded before the race (PROBE_WARM=1), with CECOLL_GRAPH=0, or
- * with stream-level synchronisation in the other thread. So either launch
- * each plan twice before another thread may synchronise the device, or set
+ * with stream-level synchronisation in the other thread. Plans whose
+ * submission is a single kernel launch (the one-unit SM path) are never
+ * recorded, so they are not exposed. For the others, either launch each
+ * plan twice before another thread may synchronise the device, or set
  * CECOLL_GRAPH=0. Likewise, destroy worlds only while no other thread is
  * issuing collectives.
  * ------------------------------------------------------------------- */
@@ -239,8 +241,10 @@ cecoll_status_t cecoll_collective_n(cecoll_kind_t kind, const cecoll_comm_t* com
  * submission — flag operations, lanes, copies, kernels — replays as one CUDA
  * graph launched on the caller stream (one host call per collective). This
  * applies when every unit of the plan has its own device and an explicit,
- * non-capturing stream; otherwise, or with CECOLL_GRAPH=0, commands are
- * submitted one by one on every launch.
+ * non-capturing stream, and the submission is more than one call (a
+ * one-unit SM plan is a single kernel launch and is not recorded);
+ * otherwise, or with CECOLL_GRAPH=0, commands are submitted one by one on
+ * every launch.
  * ------------------------------------------------------------------- */
 cecoll_status_t cecoll_plan_create(const cecoll_comm_t* comms, int ncomms, cecoll_kind_t kind,
                                    const void* const* sends, void* const* recvs, size_t chunk_bytes,
