@@ -101,7 +101,42 @@ def main() -> None:
     with open(os.path.join(OUT, "digests.json"), "w") as f:
         json.dump(digests, f, indent=0, sort_keys=True)
     print(f"wrote {len(programs)} programs, {len(digests)} digests to {OUT}")
+    baseline_configs(ref)
+
+
+# BASELINE.json configs at their exact sizes (SURVEY.md §8 sizing): C0 all-gather
+# n=8 s=1 MiB, C1 all-to-all n=8 s=8 MiB (the bench headline), C4 all-gather
+# n=8 s=256 MiB. Every reference implementation of the collective is executed
+# (the reference's compile() + byte executor) on the seeded splitmix inputs and
+# the sha256 of every rank's output is recorded (seeds 0 and 1).
+BASELINE_CASES = [
+    ("C0", "allgather", 8, 1 << 20, (0, 1)),
+    ("C1", "alltoall", 8, 8 << 20, (0,)),
+    ("C4", "allgather", 8, 256 << 20, (0,)),
+]
+
+
+def baseline_configs(ref=None) -> None:
+    import gc
+
+    ref = ref or Reference()
+    cases = []
+    for name, kind, n, s, seeds in BASELINE_CASES:
+        for impl in IMPLS_FOR[kind]:
+            for seed in seeds:
+                res = ref.execute(kind, impl, s, n, seed)
+                cases.append({"config": name, "kind": kind, "impl": impl, "n": n, "s": s, "seed": seed,
+                              "sha256": [sha(memoryview(r)) for r in res]})
+                del res
+                gc.collect()
+                print(name, impl, seed, cases[-1]["sha256"][0][:16], flush=True)
+    with open(os.path.join(OUT, "baseline_configs.json"), "w") as f:
+        json.dump(cases, f, indent=0, sort_keys=True)
+    print(f"wrote {len(cases)} baseline-config digests to {OUT}")
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "baseline":
+        baseline_configs()
+    else:
+        main()
