@@ -123,6 +123,12 @@ def busbw(n, s, seconds):
     return (n - 1) * s / seconds / 1e9
 
 
+def bench_config():
+    """The workload, identical in both arms' lines (the driver compares the
+    `config` dicts); everything arm-specific goes under `details`."""
+    return {"workload": WORKLOAD, "ranks": NRANKS, "chunk_bytes": CHUNK}
+
+
 # ---------------------------------------------------------------------------
 # reference arm: the reference's CPU path on the host cores
 # ---------------------------------------------------------------------------
@@ -197,7 +203,8 @@ def run_reference_arm(args):
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic splitmix64 pattern",
-        "config": {"workload": WORKLOAD, "ranks": NRANKS, "chunk_bytes": CHUNK, "device": "host CPU"},
+        "config": bench_config(),
+        "details": {"device": "host CPU"},
         "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": cores, "kind": label, "sample": sample},
         "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -253,6 +260,7 @@ def run_ours(args):
         energy = None if args.no_energy else measure_energy(step, stream, n, s)
     ms = e0.elapsed_time(e1) / args.steps
     value = busbw(n, s, ms / 1e3)
+    plan_info = comms[0].last_plan_info()  # the plan the timed steps ran
 
     # Parity of the timed buffers against the definition: every chunk of every
     # rank, compared on the device (recv_j[i] = send_i[j], compiler.cpp:156-157).
@@ -272,7 +280,9 @@ def run_ours(args):
     host_out = [torch.empty(n * s, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
     for h, d in zip(host_in, sends):
         h.copy_(d)
-    e2e_steps = max(4, args.steps)
+    # Pipeline fill (the first step's inputs) and drain (the last step's
+    # results) are paid once per timed window: more steps amortise them.
+    e2e_steps = max(args.e2e_steps, args.steps)
     # Two device buffer sets so that step k's device->host copy overlaps step
     # k+1's host->device copy (PCIe is full duplex); every step still copies
     # its inputs in and its results out inside the timed region.
@@ -315,6 +325,7 @@ def run_ours(args):
     e2e_value = busbw(n, s, e2e_ms / 1e3)
     e2e_ok = all(torch.equal(host_outs[(e2e_steps - 1) % 2][j][i * s:(i + 1) * s], host_in[i][j * s:(j + 1) * s])
                  for i in range(n) for j in range(n))
+    floor_ms = pcie_floor_ms(host_in, host_outs[0], sets[0][0], sets[0][1], h2d_s, d2h_s)
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -335,15 +346,14 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic (torch.randint bytes)",
-        "config": {
-            "workload": WORKLOAD,
-            "ranks": n,
+        "config": bench_config(),
+        "details": {
             "ranks_per_gpu": n,
-            "chunk_bytes": s,
             "impl": chosen,
             "l2": "inputs larger than L2 (1 GiB touched per step vs 126 MB L2)",
             "aggregate_gbs": round(n * value, 3),
             "algbw_gbs": round(n * s / (ms / 1e3) / 1e9, 3),
+            "plan": plan_info,
         },
         "parity_ok": bool(ok),
         "roofline": {
@@ -353,6 +363,9 @@ def run_ours(args):
             "unit": "GB/s",
             "frac": round(achieved / peak, 4),
             "traffic": load_traffic(),
+            "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu "
+                              "--set full capture of this kernel (profiles/ncu_items_kernel.json), not measured "
+                              "in this run",
             "peak_source": peak_kind + " hbm_gbs (copy, read+write)",
             "algorithmic_bytes_per_launch": alg_bytes,
             "busbw_bound_gbs": round(busbw(n, s, alg_bytes / (peak * 1e9)), 1),
@@ -360,11 +373,13 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": n * n * s,
                 "d2h_bytes_per_step": n * n * s, "ms_per_step": round(e2e_ms, 3), "parity_ok": bool(e2e_ok),
+                "steps": e2e_steps,
+                "floor_ms": round(floor_ms, 3), "vs_floor": round(e2e_ms / floor_ms, 4),
+                "floor_value": round(busbw(n, s, floor_ms / 1e3), 3),
                 "pipeline": "double-buffered: H2D of step k+1 overlaps D2H of step k",
                 "bound_note": "PCIe-bound: 512 MiB host->device and 512 MiB device->host per step over one "
-                              "x16 link; both directions at once take 10.9-11.7 ms on these boxes "
-                              "(profiles/pcie_probe2_r01.txt, ce_both), so ~5.0 GB/s busBW is the floor "
-                              "for host-resident buffers on one GPU"},
+                              "x16 link. floor_ms is measured in this run: the same bytes copied both ways "
+                              "at once on the same streams with no collective (best of 3)"},
         "gpu_launches": int(round((kernels_per_step + 4 * graphs_per_step) * args.steps)),
         "energy": energy,
         "clocks": clocks.summary(),
@@ -377,6 +392,34 @@ def run_ours(args):
         cc.destroy_all(comms)
     except cc.CecollError:
         pass  # already reported in the line
+
+
+def pcie_floor_ms(host_in, host_out, dev_in, dev_out, h2d_s, d2h_s, reps=3):
+    """Per-step floor of the e2e leg: the step's host->device and
+    device->host bytes moved at the same time (full duplex) on the e2e's own
+    streams and buffers, with no collective; best of `reps` (CUDA events)."""
+    import torch
+
+    best = float("inf")
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cur = torch.cuda.current_stream()
+        e0.record(cur)
+        h2d_s.wait_event(e0)
+        d2h_s.wait_event(e0)
+        with torch.cuda.stream(h2d_s):
+            for h, d in zip(host_in, dev_in):
+                d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(d2h_s):
+            for h, d in zip(host_out, dev_out):
+                h.copy_(d, non_blocking=True)
+        cur.wait_stream(h2d_s)
+        cur.wait_stream(d2h_s)
+        e1.record(cur)
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return best
 
 
 def measure_energy(step, stream, n, s, seconds=1.5, dev=0):
@@ -458,8 +501,26 @@ def run_interference(args):
     out = {"workload": f"all-gather {n} ranks x {s >> 20} MiB bf16 shards (co-resident on 1 GPU) beside "
                        f"cuBLAS bf16 {N}^3 GEMM", "gemm_alone_ms": round(gemm_alone_ms, 4),
            "gemm_alone_tflops": round(flops / gemm_alone_ms / 1e9, 1), "impls": {}}
-    for impl in args.interference_impls.split(","):
-        plan = cc.Plan(comms, "allgather", sends, recvs, s, impl=impl)
+    host_recvs = None
+    for spec in args.interference_impls.split(","):
+        # "impl[@budget][:host]": budget = the world's SM budget (max CTAs per
+        # kernel, cecoll_comm_set_sm_budget) for this plan; ":host" = recv
+        # buffers in pinned host memory, so the copy-engine lanes run on the
+        # copy engines (device-local copies run on SMs).
+        impl, _, where = spec.partition(":")
+        impl, _, budget = impl.partition("@")
+        budget = int(budget or 0)
+        rb, sb, cs, ce = recvs, sends, s, elems
+        if where == "host":  # PCIe-bound: a smaller shard keeps the pinned footprint at n*n*chunk
+            cs = args.interference_host_chunk
+            ce = cs // 2
+            if host_recvs is None:
+                host_recvs = [torch.empty(n * ce, dtype=torch.bfloat16, pin_memory=True) for _ in range(n)]
+            rb, sb = host_recvs, [t[:ce] for t in sends]
+        comms[0].set_sm_budget(budget)
+        plan = cc.Plan(comms, "allgather", sb, rb, cs, impl=impl)
+        comms[0].set_sm_budget(0)
+        impl = spec
         # collective alone
         for _ in range(3):
             plan.launch(coll_s)
@@ -495,6 +556,10 @@ def run_interference(args):
                 break
         coll_s.synchronize()
         gemm_s.synchronize()
+        info = plan.info()
+        plan_info_summary = {"movers": [u["mover"] for u in info["units"]], "grid": [u["grid"] for u in info["units"]],
+                             "ce_lanes": [u["ce_lanes"] for u in info["units"]], "recorded": info["recorded"],
+                             "graph_fallback": info["graph_fallback"]}
         plan.destroy()
         torch.cuda.synchronize()
         window = g_start.elapsed_time(g_end)
@@ -505,7 +570,17 @@ def run_interference(args):
             coll_with = inside[0][0].elapsed_time(inside[-1][1]) / len(inside)
         else:
             coll_with = None
+        if where == "host":  # parity of the host-resident result (every rank's recv = all shards)
+            want = torch.cat([t.cpu() for t in sb])
+            parity = all(torch.equal(h, want) for h in rb)
+        else:
+            parity = all(torch.equal(rb[j][i * ce:(i + 1) * ce], sb[i]) for i in range(n) for j in range(n))
         out["impls"][impl] = {
+            "parity_ok": bool(parity),
+            "sm_budget": budget,
+            "recv": "pinned host" if where == "host" else "device",
+            "chunk_bytes": cs,
+            "plan": plan_info_summary,
             "collective_alone_ms": round(coll_alone, 4),
             "collective_with_gemm_ms": None if coll_with is None else round(coll_with, 4),
             "collective_slowdown": None if coll_with is None else round(coll_with / coll_alone, 3),
@@ -666,7 +741,48 @@ def alg_hbm_bytes(kind, impl, s, n):
 
 SWEEP_COLUMNS = ["impl", "api", "collective", "gpus", "size_bytes", "total_ns", "control_ns", "schedule_ns", "copy_ns",
                  "sync_ns", "trigger_ns", "ranks", "isolated_ns", "busbw_gbs", "hbm_gbs", "roofline_frac",
-                 "api_calls", "kernels", "graphs", "parity"]
+                 "api_calls", "kernels", "graphs", "parity", "host_ns", "traced_ns"]
+
+# Trace-event name prefix -> phase of the reference's model (sim.cpp Phase:
+# Control, Schedule, Copy, Sync, Trigger, Poll; Poll is folded into Sync as
+# in the CSV schema, sim.cpp:546-569).
+_DEVICE_PHASE = {"copy": "copy", "kernel": "copy", "sync": "sync", "poll": "sync", "trigger": "trigger"}
+_PHASE_RANK = ["copy", "trigger", "sync"]  # when device spans overlap, the data movement is on the path
+
+
+def trace_phases(events):
+    """Critical-path attribution of one traced collective (phase_breakdown,
+    sim.cpp:501-508, on a measured timeline). Every instant between the first
+    host submission and the last device command is given one phase: a device
+    command in flight (copy > trigger > sync when they overlap); else the
+    host submitting (control, or trigger for a prelaunch trigger); else
+    nothing in flight — the device waits for submitted work to start
+    (schedule: launch latency, doorbells). Returns ({phase: ns}, traced ns)."""
+    open_, spans = {}, []
+    for e in events:
+        key = (e["name"], e["pid"], e["tid"])
+        if e["ph"] == "B":
+            open_.setdefault(key, []).append(e["ts"])
+        elif open_.get(key):
+            spans.append((e["name"], e["pid"], open_[key].pop(), e["ts"]))
+    dev = [(n.split(":")[0], b, e) for n, pid, b, e in spans if pid >= 0]
+    host = [(("trigger" if n.startswith("trigger") else "control"), b, e) for n, pid, b, e in spans if pid < 0]
+    if not dev:
+        return None, 0.0
+    t0 = min([b for _, b, _ in dev] + [b for _, b, _ in host])
+    t1 = max(e for _, _, e in dev)
+    cuts = sorted({t for _, b, e in dev + host for t in (b, e) if t0 <= t <= t1} | {t0, t1})
+    out = {"control": 0.0, "schedule": 0.0, "copy": 0.0, "sync": 0.0, "trigger": 0.0}
+    for a, b in zip(cuts, cuts[1:]):
+        mid = (a + b) / 2
+        act = {_DEVICE_PHASE.get(k, "copy") for k, x, y in dev if x <= mid < y}
+        if act:
+            ph = next(p for p in _PHASE_RANK if p in act)
+        else:
+            hs = [k for k, x, y in host if x <= mid < y]
+            ph = ("trigger" if "trigger" in hs else "control") if hs else "schedule"
+        out[ph] += (b - a) * 1e3  # µs -> ns
+    return out, (t1 - t0) * 1e3
 
 
 def run_sweep(args):
@@ -750,15 +866,27 @@ def run_sweep(args):
                     stream.synchronize()
                     iso.append(e0.elapsed_time(e1))
                 iso.sort()
+                # Phase attribution from one traced, isolated collective of the
+                # same plan (recorded plans trace their replayed graph).
+                stream.synchronize()
+                with cc.Trace(comms[0]) as tr:
+                    call()
+                    stream.synchronize()
+                phases, traced_ns = trace_phases(tr.events)
                 if plan is not None:
                     plan.destroy()
                 torch.cuda.synchronize()
                 bw = busbw(n, s, total_ms / 1e3)
                 hbm = alg_hbm_bytes(kind, impl, s, n) / (total_ms / 1e3) / 1e9
+                total_ns = total_ms * 1e6
+                ph = {k: "" for k in ("control", "schedule", "copy", "sync", "trigger")}
+                if phases and traced_ns > 0:  # fractions of the traced path, applied to total_ns
+                    ph = {k: round(v / traced_ns * total_ns) for k, v in phases.items()}
                 rows.append({
                     "impl": impl, "api": args.api, "collective": kind, "gpus": 1, "size_bytes": s,
-                    "total_ns": round(total_ms * 1e6), "control_ns": round(host / iters * 1e9),
-                    "schedule_ns": "", "copy_ns": "", "sync_ns": "", "trigger_ns": "", "ranks": n,
+                    "total_ns": round(total_ns), "control_ns": ph["control"], "schedule_ns": ph["schedule"],
+                    "copy_ns": ph["copy"], "sync_ns": ph["sync"], "trigger_ns": ph["trigger"], "ranks": n,
+                    "host_ns": round(host / iters * 1e9), "traced_ns": round(traced_ns),
                     "isolated_ns": round(iso[len(iso) // 2] * 1e6), "busbw_gbs": round(bw, 3),
                     "hbm_gbs": round(hbm, 1), "roofline_frac": round(hbm / peak, 4),
                     "api_calls": round((c1["api_calls"] - c0["api_calls"]) / iters, 1),
@@ -800,6 +928,7 @@ def main():
     ap.add_argument("--algo", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-energy", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=40, help="timed steps of the end-to-end leg (at least --steps)")
     ap.add_argument("--sweep", action="store_true", help="size sweep of every implementation (CSV)")
     ap.add_argument("--ranks", type=int, default=NRANKS)
     ap.add_argument("--sweep-out", default=os.path.join(ROOT, "gpurun_out", "sweep.csv"))
@@ -808,7 +937,8 @@ def main():
                     help="sweep through the collective calls or through explicit plans")
     ap.add_argument("--interference", action="store_true", help="C4: all-gather beside a bf16 GEMM")
     ap.add_argument("--interference-chunk", type=int, default=256 << 20)
-    ap.add_argument("--interference-impls", default="sm,pcpy,b2b,prelaunch_pcpy,bcst")
+    ap.add_argument("--interference-impls", default="sm,sm@16,sm@32,sm@64,pcpy,b2b,pcpy:host,b2b:host,sm:host")
+    ap.add_argument("--interference-host-chunk", type=int, default=16 << 20)
     ap.add_argument("--interference-out", default=os.path.join(ROOT, "gpurun_out", "interference.json"))
     ap.add_argument("--gemm-iters", type=int, default=200)
     ap.add_argument("--gemm-priority", default="same", choices=["same", "high"])

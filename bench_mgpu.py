@@ -103,12 +103,12 @@ class Watchdog:
                     line.setdefault("experiments", {})["hung"] = phase
                 else:
                     line["error"] = f"watchdog: a collective did not complete (phase {phase})"
-                trials = {k: v for k, v in line["config"].get("impl_trials", {}).items() if "ms" in v}
+                trials = {k: v for k, v in line["details"].get("impl_trials", {}).items() if "ms" in v}
                 if line.get("value") is None and trials:
                     best = min(trials, key=lambda k: trials[k]["ms"])
                     line["value"] = trials[best]["busbw_gbs"]
                     line["ms_per_step"] = trials[best]["ms"]
-                    line["config"]["impl"] = best + " (from the trial phase)"
+                    line["details"]["impl"] = best + " (from the trial phase)"
                 print(json.dumps(line), flush=True)
             except Exception:  # noqa: BLE001
                 pass
@@ -220,7 +220,24 @@ def try_impl(comms, kind, impl, sends, recvs, expects, s, iters, stream):
     stream.synchronize()
     plan.disarm()
     ms = max_all(e0.elapsed_time(e1) / iters)
-    return plan, {"ms": ms}
+    return plan, {"ms": ms, "plan": plan_summary(plan)}
+
+
+def plan_summary(plan):
+    """cecoll_plan_info reduced to what a reader needs to trust the number:
+    graph fallback, recording, mover per unit, how flags between units travel."""
+    try:
+        i = plan.info()
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)[:120]}
+    return {"graph_fallback": i.get("graph_fallback", ""), "recorded": i.get("recorded"),
+            "record_note": i.get("record_note", ""), "prelaunch_folded": i.get("prelaunch_folded"),
+            "remote_signals": i.get("remote_signals"), "sm_budget": i.get("sm_budget"),
+            "movers": [u.get("mover") for u in i.get("units", [])],
+            "ce_lanes": [u.get("ce_lanes") for u in i.get("units", [])],
+            "fused_flags": [u.get("fused_flags") for u in i.get("units", [])],
+            "flag_writes_kernel": [u.get("flag_writes_kernel") for u in i.get("units", [])],
+            "flag_writes_memop": [u.get("flag_writes_memop") for u in i.get("units", [])]}
 
 
 def energy_loop(step, stream, dev, n, s, plan, seconds=1.5):
@@ -370,8 +387,9 @@ def run(args, B):
         "metric": B.METRIC, "value": None, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded torch.randint byte chunks)",
-        "config": {"workload": B.WORKLOAD, "ranks": n, "ranks_per_gpu": nlocal, "chunk_bytes": s,
-                   "l2": "inputs larger than L2 (64 MiB send + 64 MiB recv per rank)"},
+        "config": B.bench_config(),
+        "details": {"ranks_per_gpu": nlocal,
+                    "l2": "inputs larger than L2 (64 MiB send + 64 MiB recv per rank)"},
     }
     dog = Watchdog(args.mgpu_deadline, rank, lambda: line)
 
@@ -389,7 +407,7 @@ def run(args, B):
             nccl = dist.new_group(backend="nccl")
         except Exception as e:  # noqa: BLE001
             nccl_note = f"unavailable: {str(e)[:120]}"
-    line["config"]["gpus_distinct"] = distinct
+    line["details"]["gpus_distinct"] = distinct
     if rank == 0:
         line["topology"] = topology(dev, world)
 
@@ -427,7 +445,7 @@ def run(args, B):
     # --- implementation trials (consensus), then the winner -----------------
     cands = HEADLINE_IMPLS if args.algo == "auto" else [args.algo]
     trials, plans = {}, {}
-    line["config"]["impl_trials"] = trials
+    line["details"]["impl_trials"] = trials
     for impl in cands:
         plan, res = try_impl(comms, "alltoall", impl, sends, recvs, expects, s, 10, stream)
         if plan is not None:
@@ -435,7 +453,7 @@ def run(args, B):
             res["busbw_gbs"] = round(busbw(n, s, res["ms"]), 2)
             res["ms"] = round(res["ms"], 4)
         trials[impl] = res
-    line["config"]["impl_trials"] = trials
+    line["details"]["impl_trials"] = trials
     if not plans:
         line["error"] = "no implementation passed parity on every rank"
         if rank == 0:
@@ -444,8 +462,9 @@ def run(args, B):
         return
     best = min(plans, key=lambda k: trials[k]["ms"])
     best = from_rank0(best)
-    line["config"]["impl"] = best
+    line["details"]["impl"] = best
     plan = plans[best]
+    line["details"]["plan"] = trials[best].get("plan")
 
     STATE["phase"] = "headline"
     if best.endswith("swap"):
@@ -499,8 +518,8 @@ def run(args, B):
                          "region on rank 0; copy-engine copies are counted in config.ce_copies_per_step",
         "clocks": clocks.summary(),
     })
-    line["config"]["ce_copies_per_step"] = per["copies"]
-    line["config"]["api_calls_per_step"] = per["api_calls"]
+    line["details"]["ce_copies_per_step"] = per["copies"]
+    line["details"]["api_calls_per_step"] = per["api_calls"]
 
     # --- NCCL moving the same cross-GPU bytes ----------------------------------
     if nccl is not None:
@@ -566,7 +585,7 @@ def run(args, B):
     if not args.no_mgpu_experiments:
         STATE["phase"] = "experiments multicast"
         run_mc_experiment(world, rank, dev, stream, line["experiments"])
-    line["config"]["wall_s"] = round(time.time() - t_start, 1)
+    line["details"]["wall_s"] = round(time.time() - t_start, 1)
     err = comms[0].async_error()
     if err is not None:
         ASYNC_NOTES.append(f"headline world: {str(err)[:200]}")

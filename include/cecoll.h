@@ -107,6 +107,42 @@ cecoll_impl_t cecoll_reference_select(cecoll_kind_t kind, int64_t chunk_bytes);
 /* B200 selector: measured thresholds for nranks ranks on ndevices devices;
  * overridable with CECOLL_SM_MAX_BYTES. */
 cecoll_impl_t cecoll_select(cecoll_kind_t kind, int64_t chunk_bytes, int nranks, int ndevices);
+/* The selector under an SM budget (cecoll_comm_set_sm_budget): with a budget
+ * and more than one device, everything above 64 KiB chunks goes to the copy
+ * engines (per-peer lanes, no SMs); on one device the driver runs
+ * device-local copies on SMs anyway, so the budgeted SM path is kept. */
+cecoll_impl_t cecoll_select_budget(cecoll_kind_t kind, int64_t chunk_bytes, int nranks, int ndevices, int sm_budget);
+
+/* ---------------------------------------------------------------------
+ * B200 cost model (csrc/model.cpp). The reference's CostModel
+ * (cost_model.hpp:14-33) prices MI300X phases; this one prices the B200
+ * executor's structure — kernel boundaries, recorded-graph launches and
+ * parallel branches, serial memcpy nodes, the prelaunch trigger — plus three
+ * bandwidths of algorithmic HBM bytes, for n co-resident ranks on one B200.
+ * cecoll_model_fit is the reference's calibrate() (calibrate.cpp:67-181):
+ * seeded multiplicative log-normal hill-climb, deterministic given the seed,
+ * scored by mean squared log error over the measurements plus the reference's
+ * one-binary-step boundary rule on the winner grid (calibrate.cpp:44-62).
+ * Times in ns, bandwidths in bytes/s. CPU only.
+ * ------------------------------------------------------------------- */
+typedef struct {
+  double t_kernel, t_graph, t_branch, t_node, t_trigger;
+  double bw_copy, bw_fan, bw_ce, bw_lanes;
+  double folded_max_bytes, prelaunch_gain_threshold;
+} cecoll_model_t;
+void cecoll_model_default(cecoll_model_t* model);
+cecoll_status_t cecoll_model_predict(const cecoll_model_t* model, cecoll_kind_t kind, cecoll_impl_t impl,
+                                     int64_t chunk_bytes, int nranks, double* ns);
+/* winner_grid's choice at one size (sweep.cpp:186-218): the fastest of sm and
+ * the reference's six implementations, the plain variant winning a near tie
+ * with its prelaunch form. Returns -2 on error. */
+cecoll_impl_t cecoll_model_winner(const cecoll_model_t* model, cecoll_kind_t kind, int64_t chunk_bytes, int nranks);
+/* Fits *out to `count` measurements (kinds[i], impls[i], chunk_bytes[i],
+ * nranks[i] -> ns[i], device time back to back). report (optional) gets the
+ * per-boundary log. */
+cecoll_status_t cecoll_model_fit(const int* kinds, const int* impls, const int64_t* chunk_bytes, const int* nranks,
+                                 const double* ns, int count, uint64_t seed, int iterations, cecoll_model_t* out,
+                                 double* residual, char* report, size_t capacity);
 
 /* ---------------------------------------------------------------------
  * Communicators. The reference models one host process driving every GPU
@@ -160,16 +196,28 @@ cecoll_status_t cecoll_exchange_check(int nranks, int first_rank, int nlocal, in
 /* Returns the world's async error when the last communicator of a world is
  * destroyed (see cecoll_comm_get_async_error); everything is released anyway. */
 cecoll_status_t cecoll_comm_destroy(cecoll_comm_t comm);
-/* Like ncclCommGetAsyncError. Device-side flag polls give up after 20 s (the
- * reference's untriggered-poll deadlock, sim.cpp:227-242) and record it in
- * the plan's error word; collectives are asynchronous, so the failure is
- * reported here: *async_error = CECOLL_TIMEOUT (message in
+/* Like ncclCommGetAsyncError. Device-side flag polls (kernels: the SM path,
+ * fused flags, prelaunch bodies, flag kernels) give up after 20 s (the
+ * reference's untriggered-poll deadlock, sim.cpp:227-242), record it in the
+ * plan's error word and skip the data movement and signals that depended on
+ * the flag (nothing is written into a buffer its owner never released).
+ * Stream memory-operation waits (cuStreamWaitValue64: the copy-engine paths'
+ * rdy/done polls, eager and recorded) have no timeout and no error word: a
+ * peer that never signals leaves that stream waiting. Collectives are
+ * asynchronous, so a kernel-side failure is reported here: *async_error = CECOLL_TIMEOUT (message in
  * cecoll_last_error) once any plan of the communicator's world has timed
  * out, else CECOLL_SUCCESS. Sticky: a world that timed out has flags out of
  * phase and must be destroyed. Reads the error words on a private stream, so
  * it never waits for armed plans or running collectives. */
 cecoll_status_t cecoll_comm_get_async_error(cecoll_comm_t comm, cecoll_status_t* async_error);
 cecoll_status_t cecoll_comm_info(cecoll_comm_t comm, int* rank, int* nranks, int* device);
+/* Interference policy (BASELINE configs[4]: a collective beside a GEMM). Plans
+ * created after this call — explicit or behind the eager calls — launch at
+ * most max_ctas CTAs per mover / reduction kernel (0, the default: a
+ * persistent grid of 2 CTAs per SM, fastest alone), and CECOLL_IMPL_AUTO
+ * selects with cecoll_select_budget. Applies to the communicator's whole
+ * world; cached plans of another budget are not reused. */
+cecoll_status_t cecoll_comm_set_sm_budget(cecoll_comm_t comm, int max_ctas);
 
 /* Buffer registration (≙ BufferId::Input/Output being addressable on every
  * GPU, program.hpp:36). Single-process: optional no-op. Multi-process:
@@ -280,6 +328,18 @@ cecoll_status_t cecoll_plan_disarm(cecoll_plan_t plan);
 /* Destroy plans before their communicators; cecoll_comm_destroy cancels any
  * plan still armed (its handle must not be used afterwards). */
 cecoll_status_t cecoll_plan_destroy(cecoll_plan_t plan);
+/* What the plan turned into, as one JSON object: impl, prelaunch (and whether
+ * its body is a single folded kernel), graph_fallback (non-empty: the
+ * prelaunch graph could not be built and the plan runs its program without
+ * prelaunch), recorded / record_note (the recorded command list and why it
+ * is missing), sm_budget, remote_signals ("kernel" or "memop") and per unit:
+ * device, ranks, mover ("tma", "reg", "reduce", "none"), grid, ce_lanes,
+ * fused_flags, start_folded, flag_writes_memop / flag_writes_kernel. Call
+ * with json == NULL to get *length (excluding the NUL). */
+cecoll_status_t cecoll_plan_info(cecoll_plan_t plan, char* json, size_t capacity, size_t* length);
+/* The same for the cached plan behind the communicator world's latest eager
+ * collective ("{}" before the first). */
+cecoll_status_t cecoll_comm_last_plan_info(cecoll_comm_t comm, char* json, size_t capacity, size_t* length);
 
 /* Hardware timelines in the reference's trace-event format (sim.cpp:523-544,
  * export_trace_json): between trace_begin and trace_end every collective of

@@ -80,6 +80,16 @@ def build(force: bool = False) -> str:
     return LIB_PATH
 
 
+class ModelParams(C.Structure):
+    """cecoll_model_t (include/cecoll.h): the B200 cost model's parameters."""
+    _fields_ = [(k, C.c_double) for k in ("t_kernel", "t_graph", "t_branch", "t_node", "t_trigger", "bw_copy",
+                                          "bw_fan", "bw_ce", "bw_lanes", "folded_max_bytes",
+                                          "prelaunch_gain_threshold")]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 _lib = None
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
@@ -141,6 +151,16 @@ def lib():
         "cecoll_mc_allgather": ([vp, vp, sz, vp], i32),
         "cecoll_mc_handle_type": ([vp], C.c_char_p),
         "cecoll_mc_window_destroy": ([vp], i32),
+        "cecoll_plan_info": ([vp, C.c_char_p, sz, C.POINTER(sz)], i32),
+        "cecoll_comm_last_plan_info": ([vp, C.c_char_p, sz, C.POINTER(sz)], i32),
+        "cecoll_comm_set_sm_budget": ([vp, i32], i32),
+        "cecoll_select_budget": ([i32, i64, i32, i32, i32], i32),
+        "cecoll_model_default": ([C.POINTER(ModelParams)], None),
+        "cecoll_model_predict": ([C.POINTER(ModelParams), i32, i32, i64, i32, C.POINTER(C.c_double)], i32),
+        "cecoll_model_winner": ([C.POINTER(ModelParams), i32, i64, i32], i32),
+        "cecoll_model_fit": ([C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(i64), C.POINTER(C.c_int),
+                              C.POINTER(C.c_double), i32, C.c_uint64, i32, C.POINTER(ModelParams),
+                              C.POINTER(C.c_double), C.c_char_p, sz], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -162,6 +182,8 @@ EXPORTED_SYMBOLS = [
     "cecoll_comm_get_async_error", "cecoll_reduce_scatter", "cecoll_reduce_scatter_n",
     "cecoll_mem_alloc", "cecoll_mem_free", "cecoll_trace_begin", "cecoll_trace_end",
     "cecoll_mc_window_create", "cecoll_mc_allgather", "cecoll_mc_handle_type", "cecoll_mc_window_destroy",
+    "cecoll_plan_info", "cecoll_comm_last_plan_info", "cecoll_comm_set_sm_budget", "cecoll_select_budget",
+    "cecoll_model_default", "cecoll_model_predict", "cecoll_model_winner", "cecoll_model_fit",
 ]
 DTYPES = {"f32": 0, "float32": 0, "bf16": 1, "bfloat16": 1, "f16": 2, "float16": 2}
 REDOPS = {"sum": 0, "max": 1, "min": 2}
@@ -258,9 +280,59 @@ def reference_select(kind, chunk_bytes: int) -> str | None:
     return None if r < -1 else IMPL_NAMES[r]
 
 
-def select(kind, chunk_bytes: int, nranks: int, ndevices: int) -> str:
-    """The B200 selector (measured thresholds)."""
+def select(kind, chunk_bytes: int, nranks: int, ndevices: int, sm_budget: int = 0) -> str:
+    """The B200 selector (measured thresholds); with an SM budget it prefers
+    the copy engines across devices (cecoll_select_budget)."""
+    if sm_budget:
+        return IMPL_NAMES[lib().cecoll_select_budget(_kind(kind), chunk_bytes, nranks, ndevices, sm_budget)]
     return IMPL_NAMES[lib().cecoll_select(_kind(kind), chunk_bytes, nranks, ndevices)]
+
+
+class Model:
+    """The B200 cost model (csrc/model.cpp): predict the device
+    time of a collective, pick the winner at a size, fit to measurements with
+    the reference's calibrate() procedure. CPU only."""
+
+    def __init__(self, params: dict | None = None):
+        self.p = ModelParams()
+        lib().cecoll_model_default(C.byref(self.p))
+        for k, v in (params or {}).items():
+            setattr(self.p, k, float(v))
+
+    def predict_ns(self, kind, impl, chunk_bytes: int, nranks: int) -> float:
+        out = C.c_double()
+        _check(lib().cecoll_model_predict(C.byref(self.p), _kind(kind), _impl(impl), chunk_bytes, nranks,
+                                          C.byref(out)), "model_predict")
+        return out.value
+
+    def winner(self, kind, chunk_bytes: int, nranks: int) -> str:
+        return IMPL_NAMES[lib().cecoll_model_winner(C.byref(self.p), _kind(kind), chunk_bytes, nranks)]
+
+    @classmethod
+    def fit(cls, rows, seed: int = 0, iterations: int = 2000):
+        """rows: (kind, impl, chunk_bytes, nranks, ns). Returns (model, residual, report)."""
+        k = len(rows)
+        kinds = (C.c_int * k)(*[_kind(r[0]) for r in rows])
+        impls = (C.c_int * k)(*[_impl(r[1]) for r in rows])
+        sizes = (C.c_int64 * k)(*[int(r[2]) for r in rows])
+        ns_ = (C.c_int * k)(*[int(r[3]) for r in rows])
+        times = (C.c_double * k)(*[float(r[4]) for r in rows])
+        m = cls()
+        res = C.c_double()
+        rep = C.create_string_buffer(1 << 16)
+        _check(lib().cecoll_model_fit(kinds, impls, sizes, ns_, times, k, seed, iterations, C.byref(m.p),
+                                      C.byref(res), rep, len(rep)), "model_fit")
+        return m, res.value, rep.value.decode()
+
+
+def _json_out(fn, handle) -> dict:
+    import json
+
+    n = C.c_size_t()
+    _check(fn(handle, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(fn(handle, buf, n.value + 1, C.byref(n)))
+    return json.loads(buf.value.decode())
 
 
 # ---------------------------------------------------------------------------
@@ -346,6 +418,15 @@ class Comm:
 
     def mem_free(self, buf):
         _check(lib().cecoll_mem_free(self._h, _ptr(buf)), "mem_free")
+
+    def set_sm_budget(self, max_ctas: int):
+        """Plans created from now on in this world launch at most `max_ctas`
+        CTAs per kernel (0: full grid); AUTO prefers the copy engines."""
+        _check(lib().cecoll_comm_set_sm_budget(self._h, max_ctas), "comm_set_sm_budget")
+
+    def last_plan_info(self) -> dict:
+        """cecoll_comm_last_plan_info: what the latest eager collective ran."""
+        return _json_out(lib().cecoll_comm_last_plan_info, self._h)
 
     def counters(self) -> dict:
         out = (C.c_int64 * 8)()
@@ -577,6 +658,10 @@ class Plan:
     def disarm(self):
         """Cancel the armed instance (needed before torch.cuda.synchronize())."""
         _check(lib().cecoll_plan_disarm(self._h), "plan_disarm")
+
+    def info(self) -> dict:
+        """cecoll_plan_info: graph fallback, recording, movers, flag paths."""
+        return _json_out(lib().cecoll_plan_info, self._h)
 
     def destroy(self):
         if self._h is not None:

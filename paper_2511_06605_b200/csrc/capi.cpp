@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "cecoll.h"
+#include "model.hpp"
 #include "program.hpp"
 #include "runtime.hpp"
 
@@ -484,6 +485,114 @@ cecoll_status_t cecoll_trace_end(cecoll_comm_t comm, char* json, size_t capacity
   if (!json || capacity < w->trace_json.size() + 1) return CECOLL_SUCCESS;  // size query: keep the trace
   std::memcpy(json, w->trace_json.c_str(), w->trace_json.size() + 1);
   w->trace_json.clear();
+  return CECOLL_SUCCESS;
+}
+
+namespace {
+cecoll_status_t copy_out(const std::string& text, char* buf, size_t capacity, size_t* length) {
+  *length = text.size();
+  if (buf && capacity >= text.size() + 1) std::memcpy(buf, text.c_str(), text.size() + 1);
+  return CECOLL_SUCCESS;
+}
+}  // namespace
+
+cecoll_status_t cecoll_plan_info(cecoll_plan_t plan, char* json, size_t capacity, size_t* length) {
+  if (!plan || !length) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  return copy_out(plan_info(plan->world, plan->plan), json, capacity, length);
+}
+
+cecoll_status_t cecoll_comm_last_plan_info(cecoll_comm_t comm, char* json, size_t capacity, size_t* length) {
+  if (!comm || !length) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  const Plan* p = comm->world->last_plan;
+  return copy_out(p ? plan_info(comm->world, p) : std::string("{}"), json, capacity, length);
+}
+
+cecoll_status_t cecoll_comm_set_sm_budget(cecoll_comm_t comm, int max_ctas) {
+  if (!comm || max_ctas < 0) return err(CECOLL_INVALID_ARGUMENT, "null communicator or negative budget");
+  comm->world->sm_budget = max_ctas;
+  return CECOLL_SUCCESS;
+}
+
+cecoll_impl_t cecoll_select_budget(cecoll_kind_t kind, int64_t chunk_bytes, int nranks, int ndevices, int sm_budget) {
+  return static_cast<cecoll_impl_t>(select(static_cast<Kind>(kind), chunk_bytes, nranks, ndevices, sm_budget));
+}
+
+namespace {
+B200Model from_c(const cecoll_model_t* c) {
+  B200Model m;
+  m.t_kernel = c->t_kernel;
+  m.t_graph = c->t_graph;
+  m.t_branch = c->t_branch;
+  m.t_node = c->t_node;
+  m.t_trigger = c->t_trigger;
+  m.bw_copy = c->bw_copy;
+  m.bw_fan = c->bw_fan;
+  m.bw_ce = c->bw_ce;
+  m.bw_lanes = c->bw_lanes;
+  m.folded_max_bytes = c->folded_max_bytes;
+  m.prelaunch_gain_threshold = c->prelaunch_gain_threshold;
+  return m;
+}
+void to_c(const B200Model& m, cecoll_model_t* c) {
+  c->t_kernel = m.t_kernel;
+  c->t_graph = m.t_graph;
+  c->t_branch = m.t_branch;
+  c->t_node = m.t_node;
+  c->t_trigger = m.t_trigger;
+  c->bw_copy = m.bw_copy;
+  c->bw_fan = m.bw_fan;
+  c->bw_ce = m.bw_ce;
+  c->bw_lanes = m.bw_lanes;
+  c->folded_max_bytes = m.folded_max_bytes;
+  c->prelaunch_gain_threshold = m.prelaunch_gain_threshold;
+}
+}  // namespace
+
+void cecoll_model_default(cecoll_model_t* m) {
+  if (m) to_c(default_model(), m);
+}
+
+cecoll_status_t cecoll_model_predict(const cecoll_model_t* m, cecoll_kind_t kind, cecoll_impl_t impl,
+                                     int64_t chunk_bytes, int nranks, double* ns) {
+  if (!m || !ns) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  if (!impl_ok(impl) || impl == CECOLL_IMPL_AUTO) return err(CECOLL_INVALID_ARGUMENT, "unknown implementation");
+  try {
+    if (impl != CECOLL_IMPL_SM && !valid_for(static_cast<Impl>(impl), static_cast<Kind>(kind)))
+      return err(CECOLL_UNSUPPORTED, "implementation does not apply to the collective");
+    *ns = predict_ns(from_c(m), static_cast<Kind>(kind), static_cast<Impl>(impl), chunk_bytes, nranks);
+  } catch (const std::invalid_argument& e) {
+    return err(CECOLL_INVALID_ARGUMENT, e.what());
+  }
+  return CECOLL_SUCCESS;
+}
+
+cecoll_impl_t cecoll_model_winner(const cecoll_model_t* m, cecoll_kind_t kind, int64_t chunk_bytes, int nranks) {
+  if (!m) return static_cast<cecoll_impl_t>(-2);
+  try {
+    return static_cast<cecoll_impl_t>(model_winner(from_c(m), static_cast<Kind>(kind), chunk_bytes, nranks));
+  } catch (const std::invalid_argument&) {
+    return static_cast<cecoll_impl_t>(-2);
+  }
+}
+
+cecoll_status_t cecoll_model_fit(const int* kinds, const int* impls, const int64_t* chunk_bytes, const int* nranks,
+                                 const double* ns, int count, uint64_t seed, int iterations, cecoll_model_t* out,
+                                 double* residual, char* report, size_t capacity) {
+  if (!kinds || !impls || !chunk_bytes || !nranks || !ns || count < 0 || !out)
+    return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  std::vector<Measurement> meas;
+  for (int i = 0; i < count; ++i) {
+    if (impls[i] < 0 || impls[i] > CECOLL_IMPL_PULL || kinds[i] < 0 || kinds[i] > 1) continue;
+    meas.push_back({static_cast<Kind>(kinds[i]), static_cast<Impl>(impls[i]), chunk_bytes[i], nranks[i], ns[i]});
+  }
+  const FitResult r = calibrate_b200(meas, seed, iterations);
+  to_c(r.model, out);
+  if (residual) *residual = r.residual;
+  if (report && capacity) {
+    const size_t k = std::min(capacity - 1, r.report.size());
+    std::memcpy(report, r.report.data(), k);
+    report[k] = 0;
+  }
   return CECOLL_SUCCESS;
 }
 

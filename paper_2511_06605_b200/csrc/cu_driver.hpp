@@ -44,6 +44,11 @@ struct DriverApi {
   CUresult (*MemGetAllocationGranularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) =
       nullptr;
   CUresult (*DeviceGet)(CUdevice*, int) = nullptr;
+  // Explicit graph construction (exec.cpp GraphSink): stream memory operations
+  // as batch-mem-op graph nodes, in the context current on the calling thread.
+  CUresult (*GraphAddBatchMemOpNode)(CUgraphNode*, CUgraph, const CUgraphNode*, size_t,
+                                     const CUDA_BATCH_MEM_OP_NODE_PARAMS*) = nullptr;
+  CUresult (*CtxGetCurrent)(CUcontext*) = nullptr;
   bool has_multicast = false;
   bool loaded = false;
   bool has_batch_memcpy = false;

@@ -1,6 +1,7 @@
 // Executors: copy-engine lanes (pcpy / b2b / bcst / swap), the SM path,
 // prelaunch triggers, plan lifetime and the eager-call plan cache.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <set>
@@ -29,8 +30,9 @@ Status run_reduce_scatter(World* w, Impl impl, int64_t count, int dtype, int op,
   }
   if (!p) {
     STATUS_TRY(plan_create_rs(w, impl, count, dtype, op, args, &p));
-    w->plans.emplace_back(p);
+    cache_plan(w, p);
   }
+  w->last_plan = p;
   return plan_launch(w, p, false);
 }
 
@@ -46,31 +48,41 @@ const char* table_name(const ItemTable& t) {
   return "copy:copy";
 }
 
-// Traced copy submission: one call per copy, each bracketed by events.
-Status issue_copies_traced(World* w, const std::vector<Copy>& copies, cudaStream_t s, bool allow_batch, int device,
-                           int pid, int tid) {
-  if (!w->tracer) return issue_copies(w, copies, s, allow_batch);
+// Copy submission; when tracing (eager only) one call per copy, each
+// bracketed by events.
+Status issue_copies_traced(World* w, Sink& sink, const std::vector<Copy>& copies, cudaStream_t s, bool allow_batch,
+                           int device, int pid, int tid) {
+  if (!w->tracer) return sink.copies(w, copies, s, allow_batch);
   for (const Copy& c : copies) {
-    cudaEvent_t b = trace_mark(w, device, s);
-    STATUS_TRY(issue_copies(w, {c}, s, false));
-    trace_span(w, "copy:copy", pid, tid, device, b, trace_mark(w, device, s));
+    cudaEvent_t b = sink.mark(w, device, s);
+    STATUS_TRY(sink.copies(w, {c}, s, false));
+    trace_span(w, "copy:copy", pid, tid, device, b, sink.mark(w, device, s));
   }
   return {};
 }
 
 // Stream memory operations (+ the signal kernel for other devices' flags)
 // bracketed as one traced span when tracing and the batch is not empty.
-Status submit_traced(World* w, cudaStream_t s, const MemOps& ops, uint64_t** remote_tab, size_t nremote,
+Status submit_traced(World* w, Sink& sink, cudaStream_t s, const MemOps& ops, uint64_t** remote_tab, size_t nremote,
                      const char* name, int device, int pid, int tid) {
   if (ops.empty() && nremote == 0) return {};
-  cudaEvent_t b = trace_mark(w, device, s);
-  STATUS_TRY(submit(w, s, ops));
-  STATUS_TRY(signal_remote(w, remote_tab, nremote, s));
-  trace_span(w, name, pid, tid, device, b, trace_mark(w, device, s));
+  cudaEvent_t b = sink.mark(w, device, s);
+  STATUS_TRY(sink.memops(w, s, ops));
+  STATUS_TRY(signal_remote(w, sink, remote_tab, nremote, s));
+  trace_span(w, name, pid, tid, device, b, sink.mark(w, device, s));
   return {};
 }
 
-Status run_ce(World* w, Plan* p) {
+Status kernel_traced(World* w, Sink& sink, cudaStream_t s, const KernelCall& k, const std::string& name, int device,
+                     int pid, int tid) {
+  if (!k.func) return {};
+  cudaEvent_t b = sink.mark(w, device, s);
+  STATUS_TRY(sink.kernel(w, s, k));
+  trace_span(w, name, pid, tid, device, b, sink.mark(w, device, s));
+  return {};
+}
+
+Status run_ce(World* w, Plan* p, Sink& sink) {
   // Phase 1: every unit announces readiness (rdy), forks its lanes and places
   // its own chunk. Phase 2: lanes poll rdy, copy, signal done. Phase 3: units
   // poll done and join their lanes. Every poll is submitted after the signal
@@ -79,43 +91,30 @@ Status run_ce(World* w, Plan* p) {
     DeviceGuard g(u.device);
     const double h0 = trace_host_now(w);
     const int pid = u.ranks[0];
-    STATUS_TRY(issue_copies_traced(w, u.precopy, u.stream, true, u.device, pid, -1));
-    STATUS_TRY(submit_traced(w, u.stream, u.start, u.start_remote_tab, u.start_remote.size(), "sync:signal",
+    STATUS_TRY(issue_copies_traced(w, sink, u.precopy, u.stream, true, u.device, pid, -1));
+    STATUS_TRY(submit_traced(w, sink, u.stream, u.start, u.start_remote_tab, u.start_remote.size(), "sync:signal",
                              u.device, pid, -1));
-    for (int r : u.ranks) {
-      CUDA_TRY(cudaEventRecord(w->local[r]->start, u.stream));
-      ++w->counters[kCtrApiCalls];
-    }
-    STATUS_TRY(issue_copies_traced(w, u.placement, u.stream, true, u.device, pid, -1));
-    if (u.table.nitems) {  // the lanes' merged item-kernel commands (lower.cpp lower_program)
-      cudaEvent_t b = trace_mark(w, u.device, u.stream);
-      CUDA_TRY(launch_items(u.table, mover_grid_for(u.table, p->sms), u.stream));
-      ++w->counters[kCtrKernels];
-      ++w->counters[kCtrApiCalls];
-      trace_span(w, table_name(u.table), pid, -1, u.device, b, trace_mark(w, u.device, u.stream));
-    }
-    trace_host_span(w, "control", h0);
+    for (int r : u.ranks) STATUS_TRY(sink.record(w, w->local[r]->start, u.stream));
+    STATUS_TRY(issue_copies_traced(w, sink, u.placement, u.stream, true, u.device, pid, -1));
+    if (u.table.nitems)  // the lanes' merged item-kernel commands (lower.cpp lower_program)
+      STATUS_TRY(kernel_traced(w, sink, u.stream, items_call(u.table, plan_grid(p, u.table)), table_name(u.table),
+                               u.device, pid, -1));
+    sink.host_span(w, "control", h0);
   }
   for (LaneExec& l : p->lanes) {
     RankState* rs = w->local[l.rank].get();
     DeviceGuard g(rs->device);
     const double h0 = trace_host_now(w);
     cudaStream_t s = rs->lanes[l.lane];
-    CUDA_TRY(cudaStreamWaitEvent(s, rs->start, 0));
-    ++w->counters[kCtrApiCalls];
-    STATUS_TRY(submit_traced(w, s, l.pre, nullptr, 0, "poll:poll", rs->device, l.rank, l.lane));
-    STATUS_TRY(issue_copies_traced(w, l.copies, s, true, rs->device, l.rank, l.lane));
-    if (l.table.nitems) {
-      cudaEvent_t b = trace_mark(w, rs->device, s);
-      CUDA_TRY(launch_items(l.table, mover_grid_for(l.table, p->sms), s));
-      ++w->counters[kCtrKernels];
-      ++w->counters[kCtrApiCalls];
-      trace_span(w, table_name(l.table), l.rank, l.lane, rs->device, b, trace_mark(w, rs->device, s));
-    }
-    STATUS_TRY(submit_traced(w, s, l.post, nullptr, 0, "sync:signal", rs->device, l.rank, l.lane));
-    CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], s));
-    ++w->counters[kCtrApiCalls];
-    trace_host_span(w, "control", h0);
+    STATUS_TRY(sink.wait(w, s, rs->start));
+    STATUS_TRY(submit_traced(w, sink, s, l.pre, nullptr, 0, "poll:poll", rs->device, l.rank, l.lane));
+    STATUS_TRY(issue_copies_traced(w, sink, l.copies, s, true, rs->device, l.rank, l.lane));
+    if (l.table.nitems)
+      STATUS_TRY(kernel_traced(w, sink, s, items_call(l.table, plan_grid(p, l.table)), table_name(l.table), rs->device,
+                               l.rank, l.lane));
+    STATUS_TRY(submit_traced(w, sink, s, l.post, nullptr, 0, "sync:signal", rs->device, l.rank, l.lane));
+    STATUS_TRY(sink.record(w, rs->lane_done[l.lane], s));
+    sink.host_span(w, "control", h0);
   }
   for (Unit& u : p->units) {
     // Join the lanes, signal other-device destinations (one kernel), then
@@ -123,84 +122,72 @@ Status run_ce(World* w, Plan* p) {
     DeviceGuard g(u.device);
     for (const LaneExec& l : p->lanes) {
       if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) == u.ranks.end()) continue;
-      CUDA_TRY(cudaStreamWaitEvent(u.stream, w->local[l.rank]->lane_done[l.lane], 0));
-      ++w->counters[kCtrApiCalls];
+      STATUS_TRY(sink.wait(w, u.stream, w->local[l.rank]->lane_done[l.lane]));
     }
-    STATUS_TRY(submit_traced(w, u.stream, {}, u.lanes_remote_tab, u.lanes_remote.size(), "sync:signal", u.device,
-                             u.ranks[0], -1));
-    STATUS_TRY(submit_traced(w, u.stream, u.finish, nullptr, 0, "poll:poll", u.device, u.ranks[0], -1));
+    STATUS_TRY(submit_traced(w, sink, u.stream, {}, u.lanes_remote_tab, u.lanes_remote.size(), "sync:signal",
+                             u.device, u.ranks[0], -1));
+    STATUS_TRY(submit_traced(w, sink, u.stream, u.finish, nullptr, 0, "poll:poll", u.device, u.ranks[0], -1));
   }
   return {};
 }
 
-Status run_sm(World* w, Plan* p) {
+Status run_sm(World* w, Plan* p, Sink& sink) {
   for (Unit& u : p->units) {  // phase 1: readiness to sources in other units
     if (u.start_folded) {     // written by the fused kernel itself
       w->counters[kCtrFlagWrites] += u.sm_flags.npre;
       continue;
     }
     DeviceGuard g(u.device);
-    STATUS_TRY(submit_traced(w, u.stream, u.start, u.start_remote_tab, u.start_remote.size(), "sync:signal",
+    STATUS_TRY(submit_traced(w, sink, u.stream, u.start, u.start_remote_tab, u.start_remote.size(), "sync:signal",
                              u.device, u.ranks[0], -1));
   }
   for (Unit& u : p->units) {  // phase 2: wait destinations, move, signal
     DeviceGuard g(u.device);
     const double h0 = trace_host_now(w);
     const int pid = u.ranks[0];
-    if (!u.fused) STATUS_TRY(submit_traced(w, u.stream, u.sm_pre, nullptr, 0, "poll:poll", u.device, pid, -1));
+    if (!u.fused) STATUS_TRY(submit_traced(w, sink, u.stream, u.sm_pre, nullptr, 0, "poll:poll", u.device, pid, -1));
     // Hybrid: the copy-engine shares fork after the rdy polls and join
     // before the done signals.
     std::vector<const LaneExec*> forked;
     if (p->hybrid) {
       cudaEvent_t fork = w->local[u.ranks[0]]->start;
-      CUDA_TRY(cudaEventRecord(fork, u.stream));
-      ++w->counters[kCtrApiCalls];
+      STATUS_TRY(sink.record(w, fork, u.stream));
       for (const LaneExec& l : p->lanes) {
         if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) == u.ranks.end()) continue;
         RankState* rs = w->local[l.rank].get();
         cudaStream_t ls = rs->lanes[l.lane];
-        CUDA_TRY(cudaStreamWaitEvent(ls, fork, 0));
-        STATUS_TRY(issue_copies_traced(w, l.copies, ls, false, rs->device, l.rank, l.lane));
-        CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], ls));
-        w->counters[kCtrApiCalls] += 2;
+        STATUS_TRY(sink.wait(w, ls, fork));
+        STATUS_TRY(issue_copies_traced(w, sink, l.copies, ls, false, rs->device, l.rank, l.lane));
+        STATUS_TRY(sink.record(w, rs->lane_done[l.lane], ls));
         forked.push_back(&l);
       }
     }
+    const FlagSet* fs = u.fused ? &u.sm_flags : nullptr;
     if (u.table.nitems) {
-      cudaEvent_t b = trace_mark(w, u.device, u.stream);
-      CUDA_TRY(launch_items(u.table, mover_grid_for(u.table, p->sms), u.stream, u.fused ? &u.sm_flags : nullptr));
+      STATUS_TRY(kernel_traced(w, sink, u.stream, items_call(u.table, plan_grid(p, u.table), fs),
+                               std::string("kernel:") + (table_name(u.table) + 5), u.device, pid, -1));
       if (u.fused) {
         w->counters[kCtrFlagWrites] += u.sm_flags.nsig;
         w->counters[kCtrFlagWaits] += u.sm_flags.npoll;
       }
-      ++w->counters[kCtrKernels];
-      ++w->counters[kCtrApiCalls];
-      trace_span(w, std::string("kernel:") + (table_name(u.table) + 5), pid, -1, u.device, b,
-                 trace_mark(w, u.device, u.stream));
     }
     if (u.red.nitems) {
-      cudaEvent_t b = trace_mark(w, u.device, u.stream);
-      CUDA_TRY(launch_reduce(u.red, 4 * p->sms, u.stream, u.fused ? &u.sm_flags : nullptr));
+      STATUS_TRY(kernel_traced(w, sink, u.stream, reduce_call(u.red, plan_red_grid(p), fs), "kernel:reduce", u.device,
+                               pid, -1));
       if (u.fused) {
         w->counters[kCtrFlagWrites] += u.sm_flags.nsig;
         w->counters[kCtrFlagWaits] += u.sm_flags.npoll;
       }
-      ++w->counters[kCtrKernels];
-      ++w->counters[kCtrApiCalls];
-      trace_span(w, "kernel:reduce", pid, -1, u.device, b, trace_mark(w, u.device, u.stream));
     }
-    for (const LaneExec* l : forked) {
-      CUDA_TRY(cudaStreamWaitEvent(u.stream, w->local[l->rank]->lane_done[l->lane], 0));
-      ++w->counters[kCtrApiCalls];
-    }
+    for (const LaneExec* l : forked) STATUS_TRY(sink.wait(w, u.stream, w->local[l->rank]->lane_done[l->lane]));
     if (!u.fused)
-      STATUS_TRY(submit_traced(w, u.stream, u.sm_post, u.sm_post_remote_tab, u.sm_post_remote.size(), "sync:signal",
-                               u.device, pid, -1));
-    trace_host_span(w, "control", h0);
+      STATUS_TRY(submit_traced(w, sink, u.stream, u.sm_post, u.sm_post_remote_tab, u.sm_post_remote.size(),
+                               "sync:signal", u.device, pid, -1));
+    sink.host_span(w, "control", h0);
   }
   for (Unit& u : p->units) {  // phase 3: incoming chunks
     DeviceGuard g(u.device);
-    STATUS_TRY(submit_traced(w, u.stream, u.finish, nullptr, 0, "poll:poll", u.device, u.ranks[0], -1));
+    STATUS_TRY(submit_traced(w, sink, u.stream, u.finish, nullptr, 0, "poll:poll", u.device, u.ranks[0], -1));
   }
   return {};
 }
@@ -215,13 +202,24 @@ Status post_gate(Unit& u, uint64_t kind) {
   return {};
 }
 
+// Process-wide count of armed prelaunch units: device-synchronising calls
+// (cudaFree, cudaFreeHost) wait behind an armed gate, so plan memory is only
+// released while nothing is armed (release_retired).
+std::atomic<int> g_armed{0};
+
+void set_armed(Unit& u, bool armed) {
+  if (u.armed == armed) return;
+  u.armed = armed;
+  g_armed.fetch_add(armed ? 1 : -1);
+}
+
 Status arm_unit(World* w, Unit& u) {
   DeviceGuard g(u.device);
   CUDA_TRY(cudaGraphLaunch(u.exec, u.arm));
   CUDA_TRY(cudaEventRecord(u.graph_done, u.arm));
   ++w->counters[kCtrGraphLaunches];
   w->counters[kCtrApiCalls] += 2;
-  u.armed = true;
+  set_armed(u, true);
   return {};
 }
 
@@ -229,16 +227,17 @@ Status arm_unit(World* w, Unit& u) {
 // post that opens its armed graph.
 Status trigger_signal(World* w, Unit& u, cudaEvent_t* span_begin) {
   DeviceGuard g(u.device);
+  StreamSink sink;
   const double h0 = trace_host_now(w);
   const int pid = u.ranks[0];
-  STATUS_TRY(issue_copies_traced(w, u.precopy, u.stream, true, u.device, pid, -1));
+  STATUS_TRY(issue_copies_traced(w, sink, u.precopy, u.stream, true, u.device, pid, -1));
   MemOps ops = u.start;
   ops.push_back(op_write(u.ready_flag, 1));
   *span_begin = trace_mark(w, u.device, u.stream);
-  STATUS_TRY(submit_traced(w, u.stream, ops, u.start_remote_tab, u.start_remote.size(), "trigger:signal", u.device,
-                           pid, -1));
+  STATUS_TRY(submit_traced(w, sink, u.stream, ops, u.start_remote_tab, u.start_remote.size(), "trigger:signal",
+                           u.device, pid, -1));
   STATUS_TRY(post_gate(u, 1));
-  u.armed = false;
+  set_armed(u, false);
   trace_host_span(w, "trigger", h0);
   return {};
 }
@@ -248,16 +247,11 @@ Status trigger_signal(World* w, Unit& u, cudaEvent_t* span_begin) {
 // sits ahead of a signal it waits for in a shared hardware queue (§3.2).
 Status trigger_wait(World* w, Unit& u, cudaEvent_t span_begin) {
   DeviceGuard g(u.device);
+  StreamSink sink;
   const int pid = u.ranks[0];
-  if (u.nfin) {
-    cudaEvent_t pb = trace_mark(w, u.device, u.stream);
-    CUDA_TRY(launch_poll(u.fin_tab, u.nfin, u.err, u.stream));
-    ++w->counters[kCtrKernels];
-    ++w->counters[kCtrApiCalls];
-    trace_span(w, "poll:poll", pid, -1, u.device, pb, trace_mark(w, u.device, u.stream));
-  }
-  CUDA_TRY(cudaStreamWaitEvent(u.stream, u.graph_done, 0));
-  ++w->counters[kCtrApiCalls];
+  if (u.nfin)
+    STATUS_TRY(kernel_traced(w, sink, u.stream, poll_call(u.fin_tab, u.nfin, u.err), "poll:poll", u.device, pid, -1));
+  STATUS_TRY(sink.wait(w, u.stream, u.graph_done));
   // The gated graph body (polls, copies, signals) runs on the arm stream; its
   // span is taken from the trigger to its completion as seen by the caller.
   trace_span(w, "copy:graph", pid, 0, u.device, span_begin, trace_mark(w, u.device, u.stream));
@@ -267,16 +261,17 @@ Status trigger_wait(World* w, Unit& u, cudaEvent_t span_begin) {
 // Recorded command lists. A plan qualifies when every unit
 // has its own device (two units on one device keep the phase-ordered eager
 // submission, which never lets a poll block the queue of the signal it waits
-// for), its stream is an explicit, non-capturing stream, and nothing traces.
-bool graph_mode_wanted(World* w, Plan* p) {
+// for), its stream is an explicit stream that the caller is not capturing,
+// and nothing traces.
+bool graph_eligible(World* w, Plan* p) {
+  (void)w;
   static const bool off = [] {
     const char* e = std::getenv("CECOLL_GRAPH");
     return e && std::string(e) == "0";
   }();
-  if (off || p->prelaunch || w->tracer) return false;
+  if (off || p->prelaunch) return false;
   // A submission of exactly one kernel launch (the SM path with one unit and
-  // no flags) gains nothing from a graph, and skipping the recording keeps
-  // its stream out of capture mode (open issue).
+  // no flags) gains nothing from a graph.
   if (p->sm && !p->hybrid && p->units.size() == 1) {
     const Unit& u = p->units[0];
     if (u.start.empty() && u.start_remote.empty() && u.sm_pre.empty() && u.sm_post.empty() &&
@@ -304,33 +299,35 @@ void drop_recording(Plan* p) {
   p->recorded = false;
 }
 
-// Captures the plan's eager submission (run_ce / run_sm) on every unit stream
-// at once — one graph per unit; lane streams join through the start / lane_done
-// events — and instantiates the graphs. Nothing executes while recording.
+// Builds the plan's command list explicitly — the same commands run_ce /
+// run_sm submit eagerly, as memcpy, batch-mem-op and kernel nodes of one
+// graph per unit (GraphSink; the unit's lane streams map to its graph) — and
+// instantiates the graphs. Nothing executes and no stream enters capture
+// mode while recording.
 Status record_plan(World* w, Plan* p) {
   int64_t before[kNumCounters];
   for (int i = 0; i < kNumCounters; ++i) before[i] = w->counters[i];
-  size_t begun = 0;
   Status st;
+  std::vector<cudaGraph_t> graphs;
   for (Unit& u : p->units) {
-    DeviceGuard g(u.device);
-    cudaError_t e = cudaStreamBeginCapture(u.stream, cudaStreamCaptureModeThreadLocal);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaGraphCreate(&g, 0);
     if (e != cudaSuccess) {
-      st = cuda_fail(e, "cudaStreamBeginCapture", __FILE__, __LINE__);
+      st = cuda_fail(e, "cudaGraphCreate", __FILE__, __LINE__);
       break;
     }
-    ++begun;
+    u.rec_graph = g;
+    graphs.push_back(g);
   }
-  w->capturing = true;
-  if (st.ok()) st = p->sm ? run_sm(w, p) : run_ce(w, p);
-  w->capturing = false;
-  for (size_t i = 0; i < begun; ++i) {
-    Unit& u = p->units[i];
-    DeviceGuard g(u.device);
-    cudaGraph_t gph = nullptr;
-    const cudaError_t e = cudaStreamEndCapture(u.stream, &gph);
-    if (e != cudaSuccess && st.ok()) st = cuda_fail(e, "cudaStreamEndCapture", __FILE__, __LINE__);
-    u.rec_graph = gph;
+  if (st.ok()) {
+    GraphSink sink(graphs);
+    for (size_t i = 0; i < p->units.size(); ++i) {
+      Unit& u = p->units[i];
+      sink.map(u.stream, static_cast<int>(i));
+      for (int r : u.ranks)
+        for (cudaStream_t ls : w->local[r]->lanes) sink.map(ls, static_cast<int>(i));
+    }
+    st = p->sm ? run_sm(w, p, sink) : run_ce(w, p, sink);
   }
   for (Unit& u : p->units) {
     if (!st.ok()) break;
@@ -352,6 +349,50 @@ Status record_plan(World* w, Plan* p) {
   return {};
 }
 
+// A traced launch of a recorded plan (cecoll_trace_begin): the same command
+// list built once more with an event-record node around every command
+// (GraphSink::mark), launched once and released; the per-command spans then
+// show the replayed graph's timeline, not an eager stand-in.
+Status launch_traced(World* w, Plan* p) {
+  const int64_t api0 = w->counters[kCtrApiCalls];
+  std::vector<cudaGraph_t> graphs;
+  Status st;
+  for (size_t i = 0; i < p->units.size() && st.ok(); ++i) {
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaGraphCreate(&g, 0);
+    if (e != cudaSuccess) st = cuda_fail(e, "cudaGraphCreate", __FILE__, __LINE__);
+    else graphs.push_back(g);
+  }
+  if (st.ok()) {
+    GraphSink sink(graphs);
+    for (size_t i = 0; i < p->units.size(); ++i) {
+      Unit& u = p->units[i];
+      sink.map(u.stream, static_cast<int>(i));
+      for (int r : u.ranks)
+        for (cudaStream_t ls : w->local[r]->lanes) sink.map(ls, static_cast<int>(i));
+    }
+    st = p->sm ? run_sm(w, p, sink) : run_ce(w, p, sink);
+  }
+  w->counters[kCtrApiCalls] = api0;
+  for (size_t i = 0; i < graphs.size(); ++i) {
+    Unit& u = p->units[i];
+    DeviceGuard g(u.device);
+    if (st.ok()) {
+      cudaGraphExec_t exec = nullptr;
+      cudaError_t e = cudaGraphInstantiate(&exec, graphs[i], 0);
+      const double h0 = trace_host_now(w);
+      if (e == cudaSuccess) e = cudaGraphLaunch(exec, u.stream);
+      trace_host_span(w, "control", h0);
+      if (exec) cudaGraphExecDestroy(exec);  // freed once the launch completes
+      if (e != cudaSuccess) st = cuda_fail(e, "traced graph launch", __FILE__, __LINE__);
+      ++w->counters[kCtrRecordedLaunches];
+      ++w->counters[kCtrApiCalls];
+    }
+    cudaGraphDestroy(graphs[i]);
+  }
+  return st;
+}
+
 Status launch_recorded(World* w, Plan* p) {
   for (Unit& u : p->units) {
     DeviceGuard g(u.device);
@@ -363,9 +404,9 @@ Status launch_recorded(World* w, Plan* p) {
   return {};
 }
 
-bool same_call(const Plan* p, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args) {
+bool same_call(const Plan* p, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args, int budget) {
   if (p->kind != kind || p->chunk != s || p->key_rank.size() != args.size()) return false;
-  if (p->impl != impl) return false;
+  if (p->impl != impl || p->sm_budget != budget) return false;
   for (size_t i = 0; i < args.size(); ++i)
     if (p->key_rank[i] != args[i].rank || p->key_send[i] != args[i].send || p->key_recv[i] != args[i].recv ||
         p->key_stream[i] != args[i].stream)
@@ -374,6 +415,18 @@ bool same_call(const Plan* p, Kind kind, Impl impl, int64_t s, const std::vector
 }
 
 }  // namespace
+
+int armed_units() { return g_armed.load(); }
+
+int plan_grid(const Plan* p, const ItemTable& t) {
+  const int g = mover_grid_for(t, p->sms);
+  return p->sm_budget > 0 ? std::min(g, p->sm_budget) : g;
+}
+
+int plan_red_grid(const Plan* p) {
+  const int g = 4 * p->sms;
+  return p->sm_budget > 0 ? std::min(g, p->sm_budget) : g;
+}
 
 // Cancels armed instances (the next launch re-arms): after this, device-wide
 // synchronisation returns.
@@ -384,7 +437,7 @@ Status plan_disarm(World* w, Plan* p) {
     DeviceGuard g(u.device);
     STATUS_TRY(post_gate(u, 2));
     CUDA_TRY(cudaStreamSynchronize(u.arm));
-    u.armed = false;
+    set_armed(u, false);
   }
   return {};
 }
@@ -401,22 +454,24 @@ Status plan_launch(World* w, Plan* p, bool rearm) {
   if (p->inner) {  // reduce-scatter over copy engines: gather, then reduce
     for (size_t i = 0; i < p->units.size(); ++i) p->inner->units[i].stream = p->units[i].stream;
     STATUS_TRY(plan_launch(w, p->inner.get(), rearm));
+    StreamSink sink;
     for (Unit& u : p->units) {
       DeviceGuard g(u.device);
-      CUDA_TRY(launch_reduce(u.red, 4 * p->sms, u.stream));
-      ++w->counters[kCtrKernels];
-      ++w->counters[kCtrApiCalls];
+      STATUS_TRY(sink.kernel(w, u.stream, reduce_call(u.red, plan_red_grid(p))));
     }
     return {};
   }
   ++w->counters[kCtrCollectives];
   if (!p->prelaunch) {
     // First launch eager; from the second on, one recorded graph per unit.
-    const bool want = graph_mode_wanted(w, p);
-    if (p->recorded && want) return launch_recorded(w, p);
-    if (!p->recorded && want && p->launches++ >= 1 && p->record_note.empty() && record_plan(w, p).ok())
-      return launch_recorded(w, p);
-    return p->sm ? run_sm(w, p) : run_ce(w, p);
+    const int launch_no = p->launches++;
+    if (launch_no >= 1 && graph_eligible(w, p)) {
+      if (w->tracer) return launch_traced(w, p);
+      if (!p->recorded && p->record_note.empty()) record_plan(w, p);
+      if (p->recorded) return launch_recorded(w, p);
+    }
+    StreamSink sink;
+    return p->sm ? run_sm(w, p, sink) : run_ce(w, p, sink);
   }
   // prelaunch: trigger every unit, then wait; re-arm if asked. A unit that
   // is not armed yet (eager calls, a plan's first launch) gets its post and
@@ -432,7 +487,7 @@ Status plan_launch(World* w, Plan* p, bool rearm) {
   for (size_t i = 0; i < nu; ++i) {
     if (was_armed[i]) continue;
     STATUS_TRY(arm_unit(w, p->units[i]));  // consumes the post just made
-    p->units[i].armed = false;
+    set_armed(p->units[i], false);
   }
   for (size_t i = 0; i < nu; ++i) STATUS_TRY(trigger_wait(w, p->units[i], spans[i]));
   if (rearm) STATUS_TRY(plan_arm(w, p));
@@ -470,6 +525,7 @@ void note_async(World* w, const Status& s) {
 Status world_async_error(World* w) {
   if (!w->async_error.ok()) return w->async_error;
   for (auto& p : w->plans) note_async(w, plan_poll_errors(p.get()));
+  for (auto& p : w->retired) note_async(w, plan_poll_errors(p.get()));
   for (Plan* p : w->explicit_plans) note_async(w, plan_poll_errors(p));
   return w->async_error;
 }
@@ -483,7 +539,7 @@ Status plan_destroy(World* w, Plan* p) {
     if (u.armed) {
       post_gate(u, 2);  // cancel: the gate skips the body
       cudaStreamSynchronize(u.arm);
-      u.armed = false;
+      set_armed(u, false);
     }
     if (u.err) {  // kernel-side polls report timeouts here (kernels.cu poll_kernel)
       if (u.arm) cudaStreamSynchronize(u.arm);
@@ -515,15 +571,105 @@ Status plan_destroy(World* w, Plan* p) {
   return result;
 }
 
+// A plan leaving the eager cache (eviction, deregistration) is not destroyed
+// on the collective path: its release frees device and pinned memory, which
+// synchronises the device and would wait behind any armed prelaunch gate —
+// possibly one whose trigger this very thread is about to post. Retired plans
+// are released once no unit in the process is armed, or at world release.
+void retire_plan(World* w, std::unique_ptr<Plan> p) {
+  w->retired.push_back(std::move(p));
+  release_retired(w, false);
+}
+
+void release_retired(World* w, bool force) {
+  if (w->retired.empty() || (!force && armed_units() > 0)) return;
+  // plan_destroy's frees synchronise the device, so the plan's last launches
+  // have finished before its memory goes (its caller streams may be gone).
+  for (auto& p : w->retired) note_async(w, plan_destroy(w, p.get()));
+  w->retired.clear();
+}
+
+void cache_plan(World* w, Plan* p) {
+  w->plans.emplace_back(p);
+  if (w->plans.size() > kPlanCacheSize) {  // bounded cache: retire the oldest plan
+    std::unique_ptr<Plan> old = std::move(w->plans.front());
+    w->plans.erase(w->plans.begin());
+    if (w->last_plan == old.get()) w->last_plan = nullptr;
+    retire_plan(w, std::move(old));
+  }
+}
+
+namespace {
+const char* mover_name(const ItemTable& t) {
+  if (!t.nitems) return "none";
+  return t.mover == Mover::Tma ? "tma" : "reg";
+}
+}  // namespace
+
+// What a plan turned into (cecoll_plan_info): the evidence a benchmark line
+// needs to be read correctly — whether the prelaunch graph exists or the plan
+// fell back to its eager program, whether the command list is recorded (and
+// why not), which mover each unit uses and how flags between units travel.
+std::string plan_info(World* w, const Plan* p) {
+  std::string j = "{";
+  auto kv = [&](const char* k, const std::string& v, bool quote) {
+    if (j.size() > 1) j += ",";
+    j += "\"" + std::string(k) + "\":" + (quote ? "\"" + v + "\"" : v);
+  };
+  auto esc = [](std::string v) {
+    std::string o;
+    for (char c : v) {
+      if (c == '"' || c == '\\') o += '\\';
+      if (static_cast<unsigned char>(c) >= 0x20) o += c;
+    }
+    return o;
+  };
+  const char* rs = std::getenv("CECOLL_REMOTE_SIGNAL");
+  kv("impl", impl_name(p->impl), true);
+  kv("kind", p->kind == Kind::AllGather ? "allgather" : p->kind == Kind::AllToAll ? "alltoall" : "reduce_scatter",
+     true);
+  kv("chunk_bytes", std::to_string(p->chunk), false);
+  kv("prelaunch", p->prelaunch ? "true" : "false", false);
+  kv("prelaunch_folded", p->folded ? "true" : "false", false);
+  kv("graph_fallback", esc(p->graph_fallback), true);
+  kv("recorded", p->recorded ? "true" : "false", false);
+  kv("record_note", esc(p->record_note), true);
+  kv("launches", std::to_string(p->launches), false);
+  kv("sm_budget", std::to_string(p->sm_budget), false);
+  kv("remote_signals", (rs && std::string(rs) == "memop") ? "memop" : "kernel", true);
+  std::string units = "[";
+  for (size_t i = 0; i < p->units.size(); ++i) {
+    const Unit& u = p->units[i];
+    std::string ranks;
+    for (int r : u.ranks) ranks += (ranks.empty() ? "" : ",") + std::to_string(r);
+    int lanes = 0;
+    for (const LaneExec& l : p->lanes)
+      if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) != u.ranks.end() && !l.copies.empty()) ++lanes;
+    const size_t remote = u.start_remote.size() + u.sm_post_remote.size() + u.lanes_remote.size();
+    const size_t local = u.start.size() + u.sm_post.size();
+    units += std::string(i ? "," : "") + "{\"device\":" + std::to_string(u.device) + ",\"ranks\":[" + ranks +
+             "],\"mover\":\"" + (u.red.nitems ? "reduce" : mover_name(u.table)) +
+             "\",\"grid\":" + std::to_string(u.table.nitems ? plan_grid(p, u.table) : 0) +
+             ",\"ce_lanes\":" + std::to_string(lanes) + ",\"fused_flags\":" + (u.fused ? "true" : "false") +
+             ",\"start_folded\":" + (u.start_folded ? "true" : "false") +
+             ",\"flag_writes_memop\":" + std::to_string(local) +
+             ",\"flag_writes_kernel\":" + std::to_string(remote) + "}";
+  }
+  units += "]";
+  kv("units", units, false);
+  (void)w;
+  return j + "}";
+}
+
 Status run_collective(World* w, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args) {
   if (impl == Impl::Auto) {
     bool in_place = kind == Kind::AllToAll;
     for (const CallArgs& a : args) in_place &= a.send == a.recv;
-    impl = in_place ? Impl::Swap : select(kind, s, w->nranks, w->ndevices);
+    impl = in_place ? Impl::Swap : select_for(w, kind, s);
   }
   Plan* p = nullptr;
   for (auto& cand : w->plans)
-    if (same_call(cand.get(), kind, impl, s, args)) {
+    if (same_call(cand.get(), kind, impl, s, args, w->sm_budget)) {
       p = cand.get();
       break;
     }
@@ -531,16 +677,9 @@ Status run_collective(World* w, Kind kind, Impl impl, int64_t s, const std::vect
     const double h0 = trace_host_now(w);
     STATUS_TRY(plan_create(w, kind, impl, s, args, &p));
     trace_host_span(w, "control:compile", h0);
-    w->plans.emplace_back(p);
-    if (w->plans.size() > 64) {  // bounded cache: drop the oldest plan
-      for (Unit& u : w->plans.front()->units) {
-        DeviceGuard g(u.device);
-        cudaStreamSynchronize(u.stream);
-      }
-      note_async(w, plan_destroy(w, w->plans.front().get()));
-      w->plans.erase(w->plans.begin());
-    }
+    cache_plan(w, p);
   }
+  w->last_plan = p;
   // Eager calls never leave an instance armed after returning (a waiting
   // graph would block device-wide synchronisation); explicit plans do.
   return plan_launch(w, p, false);

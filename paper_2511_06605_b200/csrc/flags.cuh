@@ -17,32 +17,83 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// One flag: spin (ld.acquire.sys, 20 s bound) until *p >= 1.
-__device__ __forceinline__ void wait_flag(const uint64_t* p, uint64_t* err) {
+__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// One flag: spin (ld.acquire.sys, 20 s bound) until *p >= 1. Returns false
+// (and sets bit 0 of *err) on timeout.
+__device__ __forceinline__ bool wait_flag(const uint64_t* p, uint64_t* err) {
   const unsigned long long t0 = globaltimer();
   while (ld_acquire_sys(p) < 1) {
     if (globaltimer() - t0 > kPollTimeoutNs) {
       atomicOr(reinterpret_cast<unsigned long long*>(err), 1ull);
-      return;
+      return false;
     }
     __nanosleep(32);
   }
+  return true;
 }
 
-// Fused prologue, one full warp of a CTA (warp-level polling): CTA 0 first
-// writes the folded start signals, then lane i waits for flags i, i+32, ...
-// The closing __syncwarp orders every lane's acquire before the warp's (and,
-// after the caller's __syncthreads, the CTA's) data accesses.
-__device__ __forceinline__ void fused_wait(const FlagSet& f) {
+// Folded prelaunch gate (FlagSet::posted, one full warp of every CTA). CTA 0
+// takes the next host post and publishes it in the device word *gate; every
+// CTA reads it from there (one PCIe poller, not one per CTA). Returns true
+// for "go". *consumed is advanced by the last CTA (fused_finish).
+__device__ __forceinline__ bool folded_gate(const FlagSet& f, uint64_t* post_no) {
   const int lane = threadIdx.x & 31;
+  const uint64_t c = *reinterpret_cast<volatile uint64_t*>(f.consumed);
+  *post_no = c;
+  if (blockIdx.x == 0 && lane == 0) {
+    while (f.posted[0] <= c) __nanosleep(128);
+    const uint64_t kind = f.posted[1 + (c % 64)];
+    if (kind != 1 && kind != 2) atomicOr(reinterpret_cast<unsigned long long*>(f.err), 2ull);
+    st_release_gpu(f.gate, (c + 1) * 2 + (kind == 1 ? 1 : 0));
+  }
+  uint64_t v = 0;
+  if (lane == 0)
+    while ((v = ld_acquire_gpu(f.gate)) < (c + 1) * 2) __nanosleep(64);
+  v = __shfl_sync(0xffffffffu, v, 0);
+  return v == (c + 1) * 2 + 1;
+}
+
+// What a CTA may do after its prologue.
+enum : int { kGo = 0, kTimedOut = 1, kCancelled = 2 };
+
+// Fused prologue, one full warp of a CTA (warp-level polling): the folded
+// gate if any, then CTA 0 writes the folded start signals, then lane i waits
+// for flags i, i+32, ... The closing vote orders every lane's acquire before
+// the warp's (and, after the caller's __syncthreads, the CTA's) data
+// accesses. Returns (warp-uniform):
+//  kGo        move the data;
+//  kTimedOut  a poll gave up after 20 s: the peer never released its buffer,
+//             so nothing may be written into it — but the done signals are
+//             still written (fused_finish), so peers waiting on them (stream
+//             memory-operation waits have no bound) do not hang; the error
+//             word makes the world's failure sticky;
+//  kCancelled a cancelled prelaunch instance: no data, no signals.
+// When a skip word is set (a gate_poll kernel ran first) it decides instead.
+__device__ __forceinline__ int fused_wait(const FlagSet& f, uint64_t* post_no) {
+  const int lane = threadIdx.x & 31;
+  if (f.skip) {
+    const uint64_t sk = *reinterpret_cast<const volatile uint64_t*>(f.skip);
+    return sk == 0 ? kGo : sk == 1 ? kCancelled : kTimedOut;
+  }
+  if (f.posted && !folded_gate(f, post_no)) return kCancelled;
   if (blockIdx.x == 0)
     for (int i = lane; i < f.npre; i += 32) st_release_sys(f.pre[i], 1);
-  for (int i = lane; i < f.npoll; i += 32) wait_flag(f.polls[i], f.err);
-  __syncwarp();
+  bool ok = true;
+  for (int i = lane; i < f.npoll; i += 32) ok &= wait_flag(f.polls[i], f.err);
+  return __all_sync(0xffffffffu, ok) ? kGo : kTimedOut;
 }
 
 // Fused epilogue (thread 0 of a CTA, after the CTA's data writes are
@@ -53,16 +104,23 @@ __device__ __forceinline__ void fused_wait(const FlagSet& f) {
 // st.release.sys signals — the barrier-then-one-thread-fence pattern, no
 // fence per thread. Without signals nothing outside this unit waits on the
 // data, and the kernel boundary publishes it: no system fence at all (they
-// cost several microseconds each when every CTA issues them).
-__device__ __forceinline__ void fused_finish(const FlagSet& f) {
-  if (f.nsig) asm volatile("fence.acq_rel.sys;" ::: "memory");
+// cost several microseconds each when every CTA issues them). `state` is
+// the CTA's fused_wait result: the last CTA resets the polls only if every
+// CTA passed them, and signals unless the instance was cancelled.
+__device__ __forceinline__ void fused_finish(const FlagSet& f, int state, uint64_t post_no) {
+  if (f.nsig && state == kGo) asm volatile("fence.acq_rel.sys;" ::: "memory");
   unsigned ticket;
-  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(ticket) : "l"(f.ctr) : "memory");
-  if (ticket != gridDim.x - 1) return;
+  // tickets count up by 1 per CTA; a CTA whose poll timed out adds 1 << 20
+  // as well, so the last CTA sees whether anyone did (grids stay below 2^20)
+  const unsigned add = state == kTimedOut ? (1u << 20) + 1u : 1u;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(ticket) : "l"(f.ctr), "r"(add) : "memory");
+  if ((ticket & 0xFFFFFu) != gridDim.x - 1) return;
   *f.ctr = 0;
+  if (f.consumed) *f.consumed = post_no + 1;  // folded gate: the post is taken
+  if (state == kCancelled) return;            // uniform: every CTA read the same gate / skip word
   // Every CTA passed its polls before taking its ticket: reset them for the
   // next collective (its writers only write again after our signals).
-  for (int i = 0; i < f.npoll; ++i) *f.polls[i] = 0;
+  if (state == kGo && (ticket >> 20) == 0)
+    for (int i = 0; i < f.npoll; ++i) *f.polls[i] = 0;
   for (int i = 0; i < f.nsig; ++i) st_release_sys(f.sigs[i], 1);
 }
-

@@ -162,13 +162,19 @@ __device__ __forceinline__ int find_item(const int* first, int nitems, int tile)
 template <int kKinds, int kMinBlocks>
 __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
     reg_items_kernel(const Item* __restrict__ items, int nitems, int ntiles, FlagSet flags) {
-  if (flags.skip && *reinterpret_cast<const volatile uint64_t*>(flags.skip)) return;
   __shared__ int first[kMaxItemsSmem];
+  __shared__ int cta_state;
   for (int i = threadIdx.x; i < nitems; i += kRegThreads) first[i] = items[i].first_tile;
-  if ((flags.npoll || flags.npre) && threadIdx.x < 32) fused_wait(flags);
+  uint64_t post_no = 0;
+  if (threadIdx.x < 32) {
+    const int st = (flags.npoll || flags.npre || flags.posted || flags.skip) ? fused_wait(flags, &post_no) : kGo;
+    if (threadIdx.x == 0) cta_state = st;
+  }
   __syncthreads();
+  const int state = cta_state;
+  const bool moved = state == kGo;
   int cur = find_item(first, nitems, blockIdx.x);
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int tile = moved ? blockIdx.x : ntiles; tile < ntiles; tile += gridDim.x) {
     while (cur + 1 < nitems && first[cur + 1] <= tile) ++cur;
     const Item it = items[cur];
     const int64_t off = static_cast<int64_t>(tile - it.first_tile) * kRegTile;
@@ -177,7 +183,7 @@ __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
   }
   if (flags.ctr) {
     __syncthreads();  // every thread's stores (peer stores over NVLink included) precede thread 0's fence
-    if (threadIdx.x == 0) fused_finish(flags);
+    if (threadIdx.x == 0) fused_finish(flags, state, post_no);
   }
 }
 
@@ -195,14 +201,19 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 
 __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict__ items, int nitems, int ntiles,
                                                           int evict_first, FlagSet flags) {
-  if (flags.skip && *reinterpret_cast<const volatile uint64_t*>(flags.skip)) return;
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ int first[kMaxItemsSmem];
   for (int i = threadIdx.x; i < nitems; i += 32) first[i] = items[i].first_tile;
   __syncwarp();
-  if (flags.npoll || flags.npre) fused_wait(flags);  // the CTA is one warp
+  uint64_t post_no = 0;
+  // the CTA is one warp: fused_wait's result is already warp-uniform
+  const int state = (flags.npoll || flags.npre || flags.posted || flags.skip) ? fused_wait(flags, &post_no) : kGo;
   if (threadIdx.x != 0) return;
+  if (state != kGo) {
+    if (flags.ctr) fused_finish(flags, state, post_no);
+    return;
+  }
   for (int i = 0; i < kTmaStages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[i])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 
@@ -284,7 +295,7 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
     // The bulk stores are complete; order them (async proxy) before the
     // generic-proxy fence and ticket that publish them.
     asm volatile("fence.proxy.async.global;" ::: "memory");
-    fused_finish(flags);
+    fused_finish(flags, kGo, post_no);
   }
 }
 
@@ -348,12 +359,16 @@ __global__ void gate_poll_kernel(volatile uint64_t* posted, uint64_t* consumed, 
     if (threadIdx.x == 0) *skip = 1;
     return;
   }
+  bool ok = true;
   for (int i = threadIdx.x; i < n; i += 32) {
-    wait_flag(flags[i], err);
-    *flags[i] = 0;
+    if (wait_flag(flags[i], err)) *flags[i] = 0;
+    else ok = false;
   }
-  __syncwarp();
-  if (threadIdx.x == 0) *skip = 0;
+  // a poll that timed out keeps the mover from writing into a buffer the
+  // peer never released (skip = 2: no data, signals still written; the
+  // world's error is sticky from here on)
+  ok = __all_sync(0xffffffffu, ok);
+  if (threadIdx.x == 0) *skip = ok ? 0 : 2;
 }
 
 __global__ void __launch_bounds__(kRegThreads) mc_store_kernel(const int4* __restrict__ src, char* mc_dst,
@@ -410,36 +425,65 @@ int mover_grid_for(const ItemTable& t, int sms) {
   return mover_grid(t.mover, sms);
 }
 
-cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream, const FlagSet* fp) {
-  const FlagSet flags = fp ? *fp : FlagSet{};
-  if (t.nitems <= 0 || t.ntiles <= 0) return cudaSuccess;
-  if (t.nitems > kMaxItemsSmem) return cudaErrorInvalidValue;
+KernelCall items_call(const ItemTable& t, int grid, const FlagSet* fp) {
+  KernelCall k;
+  if (t.nitems <= 0 || t.ntiles <= 0 || t.nitems > kMaxItemsSmem) return k;
   if (grid > t.ntiles) grid = t.ntiles;
+  k.grid = dim3(grid);
   if (t.mover == Mover::Tma) {
     // The attribute is per device; set it once per device (any thread may
     // launch, so the flags are atomic; devices beyond 64 set it every time).
+    // Graph kernel nodes need it too: it is set here, before the node exists.
     static std::atomic<bool> configured[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 64 || !configured[dev].load(std::memory_order_acquire)) {
-      cudaError_t e = cudaFuncSetAttribute(tma_items_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-      if (e != cudaSuccess) return e;
+      if (cudaFuncSetAttribute(tma_items_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem) !=
+          cudaSuccess)
+        return KernelCall{};
       if (dev < 64) configured[dev].store(true, std::memory_order_release);
     }
     static const int evict_first = [] {
       const char* e = std::getenv("CECOLL_TMA_EVICT_FIRST");
       return e ? std::atoi(e) : 0;
     }();
-    tma_items_kernel<<<grid, 32, kTmaSmem, stream>>>(t.items, t.nitems, t.ntiles, evict_first, flags);
-  } else if (t.kinds == (1 << kItemCopy)) {
-    reg_items_kernel<(1 << kItemCopy), 2><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems, t.ntiles, flags);
-  } else if (!(t.kinds & ((1 << kItemSwap) | (1 << kItemFan)))) {
-    reg_items_kernel<(1 << kItemCopy) | (1 << kItemBcst), 2><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems,
-                                                                                              t.ntiles, flags);
-  } else {
-    reg_items_kernel<15, 1><<<grid, kRegThreads, 0, stream>>>(t.items, t.nitems, t.ntiles, flags);
+    k.func = reinterpret_cast<const void*>(tma_items_kernel);
+    k.block = dim3(32);
+    k.smem = kTmaSmem;
+    k.push(static_cast<const Item*>(t.items));
+    k.push(t.nitems);
+    k.push(t.ntiles);
+    k.push(evict_first);
+    k.push(fp ? *fp : FlagSet{});
+    return k;
   }
-  return cudaGetLastError();
+  if (t.kinds == (1 << kItemCopy))
+    k.func = reinterpret_cast<const void*>(reg_items_kernel<(1 << kItemCopy), 2>);
+  else if (!(t.kinds & ((1 << kItemSwap) | (1 << kItemFan))))
+    k.func = reinterpret_cast<const void*>(reg_items_kernel<(1 << kItemCopy) | (1 << kItemBcst), 2>);
+  else
+    k.func = reinterpret_cast<const void*>(reg_items_kernel<15, 1>);
+  k.block = dim3(kRegThreads);
+  k.push(static_cast<const Item*>(t.items));
+  k.push(t.nitems);
+  k.push(t.ntiles);
+  k.push(fp ? *fp : FlagSet{});
+  return k;
+}
+
+cudaError_t launch(const KernelCall& k, cudaStream_t stream) {
+  if (!k.func) return cudaSuccess;
+  void* args[12];
+  k.params(args);
+  return cudaLaunchKernel(k.func, k.grid, k.block, args, k.smem, stream);
+}
+
+cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream, const FlagSet* fp) {
+  if (t.nitems <= 0 || t.ntiles <= 0) return cudaSuccess;
+  if (t.nitems > kMaxItemsSmem) return cudaErrorInvalidValue;
+  const KernelCall k = items_call(t, grid, fp);
+  if (!k.func) return cudaErrorInvalidValue;
+  return launch(k, stream);
 }
 
 cudaError_t launch_mc_store(const char* src, char* mc_dst, int64_t bytes, uint64_t* mc_flag, uint64_t epoch,
@@ -452,28 +496,70 @@ cudaError_t launch_mc_store(const char* src, char* mc_dst, int64_t bytes, uint64
   return cudaGetLastError();
 }
 
+KernelCall poll_call(uint64_t* const* flags, int n, uint64_t* err) {
+  KernelCall k;
+  if (n <= 0) return k;
+  k.func = reinterpret_cast<const void*>(poll_kernel);
+  k.grid = dim3((n + 127) / 128);
+  k.block = dim3(128);
+  k.push(flags);
+  k.push(n);
+  k.push(err);
+  return k;
+}
+
+KernelCall signal_call(uint64_t* const* flags, int n) {
+  KernelCall k;
+  if (n <= 0) return k;
+  k.func = reinterpret_cast<const void*>(signal_kernel);
+  k.grid = dim3((n + 127) / 128);
+  k.block = dim3(128);
+  k.push(flags);
+  k.push(n);
+  return k;
+}
+
+KernelCall gate_call(volatile uint64_t* posted, uint64_t* consumed, cudaGraphConditionalHandle handle, uint64_t* err) {
+  KernelCall k;
+  k.func = reinterpret_cast<const void*>(gate_kernel);
+  k.block = dim3(32);
+  k.push(posted);
+  k.push(consumed);
+  k.push(handle);
+  k.push(err);
+  return k;
+}
+
+KernelCall gate_poll_call(volatile uint64_t* posted, uint64_t* consumed, uint64_t* const* flags, int n, uint64_t* skip,
+                          uint64_t* err) {
+  KernelCall k;
+  k.func = reinterpret_cast<const void*>(gate_poll_kernel);
+  k.block = dim3(32);
+  k.push(posted);
+  k.push(consumed);
+  k.push(flags);
+  k.push(n);
+  k.push(skip);
+  k.push(err);
+  return k;
+}
+
 cudaError_t launch_poll(uint64_t* const* flags, int n, uint64_t* err, cudaStream_t stream) {
-  if (n <= 0) return cudaSuccess;
-  poll_kernel<<<(n + 127) / 128, 128, 0, stream>>>(flags, n, err);
-  return cudaGetLastError();
+  return launch(poll_call(flags, n, err), stream);
 }
 
 cudaError_t launch_signal(uint64_t* const* flags, int n, cudaStream_t stream) {
-  if (n <= 0) return cudaSuccess;
-  signal_kernel<<<(n + 127) / 128, 128, 0, stream>>>(flags, n);
-  return cudaGetLastError();
+  return launch(signal_call(flags, n), stream);
 }
 
 cudaError_t launch_gate_poll(volatile uint64_t* posted, uint64_t* consumed, uint64_t* const* flags, int n,
                              uint64_t* skip, uint64_t* err, cudaStream_t stream) {
-  gate_poll_kernel<<<1, 32, 0, stream>>>(posted, consumed, flags, n, skip, err);
-  return cudaGetLastError();
+  return launch(gate_poll_call(posted, consumed, flags, n, skip, err), stream);
 }
 
 cudaError_t launch_gate(volatile uint64_t* posted, uint64_t* consumed, cudaGraphConditionalHandle handle,
                         uint64_t* err, cudaStream_t stream) {
-  gate_kernel<<<1, 32, 0, stream>>>(posted, consumed, handle, err);
-  return cudaGetLastError();
+  return launch(gate_call(posted, consumed, handle, err), stream);
 }
 
 // Loads every kernel of this file on the current device (and sets the TMA

@@ -4,9 +4,39 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 namespace cecoll {
+
+// A kernel launch as data: launched on a stream (eager submission) or added
+// to a graph as a kernel node (recorded command lists and prelaunch bodies
+// are built node by node, never by stream capture; exec.cpp GraphSink).
+// func == nullptr means there is nothing to launch.
+struct KernelCall {
+  const void* func = nullptr;
+  dim3 grid{1, 1, 1};
+  dim3 block{1, 1, 1};
+  unsigned smem = 0;
+  int nargs = 0;
+  unsigned used = 0;
+  unsigned short off[12] = {};
+  alignas(16) unsigned char buf[384] = {};
+
+  template <class T>
+  void push(const T& v) {
+    const unsigned o = (used + alignof(T) - 1) & ~static_cast<unsigned>(alignof(T) - 1);
+    std::memcpy(buf + o, &v, sizeof(T));
+    off[nargs++] = static_cast<unsigned short>(o);
+    used = o + sizeof(T);
+  }
+  // kernelParams for cudaLaunchKernel / cudaKernelNodeParams (pointers into buf).
+  void params(void** out) const {
+    for (int i = 0; i < nargs; ++i) out[i] = const_cast<unsigned char*>(buf + off[i]);
+  }
+};
+
+cudaError_t launch(const KernelCall& k, cudaStream_t stream);
 
 enum ItemKind : int32_t { kItemCopy = 0, kItemBcst = 1, kItemSwap = 2, kItemFan = 3 };
 
@@ -80,9 +110,20 @@ struct FlagSet {
   // Non-null: the kernel does nothing when *skip != 0 (a cancelled
   // prelaunch instance; written by the gate kernel before it).
   const uint64_t* skip = nullptr;
+  // Folded prelaunch gate (a single-kernel prelaunch body):
+  // non-null `posted` (pinned host: [0] post count, [1 + k % 64] kind of post
+  // k) makes the kernel itself the gate. Thread 0 of CTA 0 waits for the
+  // next post (number *consumed), publishes its kind in *gate (device word:
+  // (post number + 1) * 2 + go) for the other CTAs, and a "cancel" post makes
+  // every CTA skip its polls, data and signals. The last CTA advances
+  // *consumed. Requires ctr (the finish ticket).
+  volatile uint64_t* posted = nullptr;
+  uint64_t* consumed = nullptr;
+  uint64_t* gate = nullptr;
 };
 
 cudaError_t launch_items(const ItemTable& t, int grid, cudaStream_t stream, const FlagSet* flags = nullptr);
+KernelCall items_call(const ItemTable& t, int grid, const FlagSet* flags = nullptr);
 
 // Reduce-scatter reduction: dst[e] = op over srcs[0..nsrc)
 // in source order of src[e], accumulated in fp32 and rounded once (RNE) to
@@ -112,6 +153,7 @@ struct RedTable {
 
 constexpr int64_t kRedTileElems = 4096;
 cudaError_t launch_reduce(const RedTable& t, int grid, cudaStream_t stream, const FlagSet* flags = nullptr);
+KernelCall reduce_call(const RedTable& t, int grid, const FlagSet* flags = nullptr);
 
 // Flag kernels used inside recorded (prelaunch) graphs, where stream memory
 // operations are not allowed in conditional bodies.
@@ -134,6 +176,11 @@ cudaError_t launch_gate(volatile uint64_t* posted, uint64_t* consumed, cudaGraph
 //          *skip = 1 so the mover after it returns at once.
 cudaError_t launch_gate_poll(volatile uint64_t* posted, uint64_t* consumed, uint64_t* const* flags, int n,
                              uint64_t* skip, uint64_t* err, cudaStream_t stream);
+KernelCall poll_call(uint64_t* const* flags, int n, uint64_t* err);
+KernelCall signal_call(uint64_t* const* flags, int n);
+KernelCall gate_call(volatile uint64_t* posted, uint64_t* consumed, cudaGraphConditionalHandle handle, uint64_t* err);
+KernelCall gate_poll_call(volatile uint64_t* posted, uint64_t* consumed, uint64_t* const* flags, int n, uint64_t* skip,
+                          uint64_t* err);
 
 // NVLS multicast all-gather store (mcast.cpp, experimental): src (bytes, a
 // multiple of 16, 16-byte aligned) -> mc_dst with multimem.st (the switch

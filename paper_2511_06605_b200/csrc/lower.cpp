@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <set>
 #include <stdexcept>
 
@@ -225,16 +226,19 @@ bool fusion_enabled() {
 
 // SM path: the unit's rdy polls and done signals move into its item kernel.
 Status fuse_sm_flags(World* w, Plan* p) {
-  (void)w;
   if (!fusion_enabled() || p->hybrid) return {};  // hybrid: lanes need the rdy polls too
-  // With every unit on its own device (one process per GPU) the start
-  // signals fold into the kernel too: no other unit's kernel on this device
-  // can be starved by the spinning grid, so writing them at kernel start is
-  // as good as a separate submission ahead of it.
-  std::set<int> devs;
-  bool distinct = true;
-  for (const Unit& u : p->units) distinct &= devs.insert(u.device).second;
+  // When no rank outside a unit lives on its device (one process per GPU,
+  // or one unit per device in a single process) the unit's start signals
+  // fold into its kernel too: no other unit's kernel on this device can be
+  // starved by the spinning grid, so writing them at kernel start is as good
+  // as a separate submission ahead of it. The count is over every rank of the
+  // world (w->device), not only this process's units: ranks of other
+  // processes sharing the GPU (co-resident processes, MPS) have kernels that
+  // our grid could starve.
+  std::map<int, int> ranks_on;
+  for (int r = 0; r < w->nranks; ++r) ++ranks_on[w->device[r]];
   for (Unit& u : p->units) {
+    const bool distinct = ranks_on[u.device] == static_cast<int>(u.ranks.size());
     if (!u.table.nitems && !u.red.nitems) continue;  // the mover or the reduction carries them
     std::vector<uint64_t*> polls, sigs;
     for (const auto& op : u.sm_pre)
@@ -545,6 +549,8 @@ Status lower_program(World* w, Plan* p, const Addressing& ad, const std::vector<
 
 }  // namespace
 
+Impl select_for(World* w, Kind kind, int64_t s) { return select(kind, s, w->nranks, w->ndevices, w->sm_budget); }
+
 Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args, Plan** out,
                    const Program* given) {
   const int n = w->nranks;
@@ -565,13 +571,14 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
   if (impl == Impl::Auto) {
     bool in_place = kind == Kind::AllToAll;
     for (const CallArgs& a : args) in_place &= a.send == a.recv;
-    impl = in_place ? Impl::Swap : select(kind, s, n, w->ndevices);
+    impl = in_place ? Impl::Swap : select_for(w, kind, s);
   }
   if (impl != Impl::Sm && impl != Impl::Hybrid && impl != Impl::Pull && !valid_for(impl, kind))
     return fail(CECOLL_UNSUPPORTED, std::string(impl_name(impl)) + " does not apply to " +
                                          (kind == Kind::AllGather ? "allgather" : "alltoall"));
   const bool in_place_impl = base_of(impl) == Impl::Swap;
   p->impl = impl;
+  p->sm_budget = w->sm_budget;
   // Pull runs on the hybrid executor with no SM share: the SM path's flag
   // edges (r, (r+d)%n) read as "reader r, source (r+d)%n" — the source's rdy
   // means "my send is ready", the reader's done "I have read it", exactly the
@@ -734,6 +741,7 @@ Status plan_create_rs(World* w, Impl impl, int64_t count, int dtype, int op, con
   p->dtype = dtype;
   p->op = op;
   p->sm = impl == Impl::Sm;
+  p->sm_budget = w->sm_budget;
   set_key(p, args);
   if (w->multiprocess && !p->sm)
     return fail(CECOLL_UNSUPPORTED, "reduce-scatter over copy engines needs a single-process communicator");
@@ -803,8 +811,43 @@ Status plan_create_rs(World* w, Impl impl, int64_t count, int dtype, int op, con
   return {};
 }
 
-// Records one unit's lanes into a graph: [gate kernel] -> IF{ poll kernel ->
-// lanes (copies, item kernels) + placement -> signal kernel }.
+namespace {
+
+// Folded prelaunch body: the unit's mover kernel is its own
+// gate. It spins from the moment it is armed, so it must leave the device to
+// everything else: only small collectives fold (at most
+// CECOLL_FOLD_MAX_TILES_PER_CTA tiles per CTA) and the grid is capped at
+// CECOLL_FOLD_MAX_CTAS CTAs (default 32) split between the plan's units on the
+// device, within the plan's SM budget. Returns the grid, or 0 for no fold.
+int fold_grid(World* w, const Plan* p, const Unit& u) {
+  static const int max_ctas = [] {
+    const char* e = std::getenv("CECOLL_FOLD_MAX_CTAS");
+    return e ? std::atoi(e) : 32;
+  }();
+  static const int max_tiles = [] {
+    const char* e = std::getenv("CECOLL_FOLD_MAX_TILES_PER_CTA");
+    return e ? std::atoi(e) : 4;
+  }();
+  const char* off = std::getenv("CECOLL_PRELAUNCH_FOLD");
+  if ((off && std::string(off) == "0") || max_ctas <= 0) return 0;
+  int units_here = 0;
+  for (const Unit& v : p->units) units_here += v.device == u.device;
+  (void)w;
+  int cap = std::max(1, max_ctas / std::max(1, units_here));
+  if (p->sm_budget > 0) cap = std::min(cap, p->sm_budget);
+  const int grid = std::min(cap, u.table.ntiles);
+  if (grid <= 0 || static_cast<int64_t>(grid) * max_tiles < u.table.ntiles) return 0;
+  return grid;
+}
+
+}  // namespace
+
+// Builds one unit's prelaunch graph explicitly (no stream capture; GraphSink):
+//  * kernel-only body, folded: one mover kernel that takes the host post
+//    itself (FlagSet::posted) — one kernel per collective;
+//  * kernel-only body: gate_poll kernel -> mover (done signals fused);
+//  * otherwise: gate kernel -> IF{ poll kernel -> lanes (memcpy nodes, item
+//    kernels) + placement -> signal kernel }.
 Status build_graph(World* w, Plan* p, Unit& u) {
   DeviceGuard g(u.device);
   CUDA_TRY(cudaStreamCreateWithFlags(&u.arm, cudaStreamNonBlocking));
@@ -818,8 +861,9 @@ Status build_graph(World* w, Plan* p, Unit& u) {
   CUDA_TRY(cudaMemset(d, 0, 64));
   p->dev_allocs.push_back(d);
   p->dev_alloc_device.push_back(u.device);
-  u.consumed = static_cast<uint64_t*>(d);
-  u.err = static_cast<uint64_t*>(d) + 1;
+  uint64_t* words = static_cast<uint64_t*>(d);  // [0] consumed [1] err [2] ticket [3] skip [4] gate
+  u.consumed = words;
+  u.err = words + 1;
   u.ready_flag = slot(w, u.ranks[0], kSlotReady);
 
   // Polls: the unit's own readiness word plus rdy from destinations in other
@@ -844,12 +888,20 @@ Status build_graph(World* w, Plan* p, Unit& u) {
   uint64_t* posted_dev = nullptr;
   CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&posted_dev), u.posted, 0));
 
+  // Building the graph counts its commands in the world's counters; nothing
+  // is submitted, so they are restored afterwards.
+  int64_t before[kNumCounters];
+  for (int i = 0; i < kNumCounters; ++i) before[i] = w->counters[i];
+  struct Restore {
+    World* w;
+    int64_t* b;
+    ~Restore() {
+      for (int i = 0; i < kNumCounters; ++i) w->counters[i] = b[i];
+    }
+  } restore{w, before};
+
   // Kernel-only body (every chunk of the unit in its item kernel: no
-  // copy-engine lanes, no placement copies): no conditional node. A one-CTA
-  // gate_poll kernel waits for the host post and the flags (or, on cancel,
-  // sets the skip word), then the mover runs with the done signals fused in
-  // (it never spins, so it cannot hold SMs while waiting). Saves the
-  // conditional body launch and two kernel boundaries per collective.
+  // copy-engine lanes, no placement copies): no conditional node.
   // CECOLL_PRELAUNCH_COND=1 keeps the conditional form for comparison.
   bool lanes_idle = u.placement.empty();
   for (const LaneExec& l : p->lanes)
@@ -857,20 +909,31 @@ Status build_graph(World* w, Plan* p, Unit& u) {
       lanes_idle = false;
   const char* pc = std::getenv("CECOLL_PRELAUNCH_COND");
   if (lanes_idle && u.table.nitems > 0 && fusion_enabled() && !(pc && std::string(pc) == "1")) {
+    CUDA_TRY(cudaGraphCreate(&u.graph, 0));
+    GraphSink sink({u.graph});
     FlagSet f;
     f.sigs = u.sig_tab;
     f.nsig = u.nsig;
     f.err = u.err;
-    f.ctr = u.nsig ? reinterpret_cast<unsigned*>(static_cast<uint64_t*>(d) + 2) : nullptr;
-    uint64_t* skip = static_cast<uint64_t*>(d) + 3;
-    f.skip = skip;
-    CUDA_TRY(cudaStreamBeginCapture(u.arm, cudaStreamCaptureModeRelaxed));
-    cudaError_t e1 = launch_gate_poll(posted_dev, u.consumed, u.poll_tab, u.npoll, skip, u.err, u.arm);
-    cudaError_t e2 = e1 == cudaSuccess ? launch_items(u.table, mover_grid_for(u.table, p->sms), u.arm, &f) : e1;
-    const cudaError_t ec = cudaStreamEndCapture(u.arm, &u.graph);
-    CUDA_TRY(e1);
-    CUDA_TRY(e2);
-    CUDA_TRY(ec);
+    const int fg = fold_grid(w, p, u);
+    if (fg > 0) {
+      // One kernel: gate, polls (ready word + rdy), move, signals.
+      f.posted = posted_dev;
+      f.consumed = u.consumed;
+      f.gate = words + 4;
+      f.polls = u.poll_tab;
+      f.npoll = u.npoll;
+      f.ctr = reinterpret_cast<unsigned*>(words + 2);
+      p->folded = true;
+      STATUS_TRY(sink.kernel(w, u.arm, items_call(u.table, fg, &f)));
+    } else {
+      // The mover never spins here (gate_poll did the waiting), so it keeps a
+      // full grid without holding SMs while armed.
+      f.ctr = u.nsig ? reinterpret_cast<unsigned*>(words + 2) : nullptr;
+      f.skip = words + 3;
+      STATUS_TRY(sink.kernel(w, u.arm, gate_poll_call(posted_dev, u.consumed, u.poll_tab, u.npoll, words + 3, u.err)));
+      STATUS_TRY(sink.kernel(w, u.arm, items_call(u.table, plan_grid(p, u.table), &f)));
+    }
     CUDA_TRY(cudaGraphInstantiate(&u.exec, u.graph, 0));
     return {};
   }
@@ -878,19 +941,8 @@ Status build_graph(World* w, Plan* p, Unit& u) {
   CUDA_TRY(cudaGraphCreate(&u.graph, 0));
   cudaGraphConditionalHandle handle;
   CUDA_TRY(cudaGraphConditionalHandleCreate(&handle, u.graph, 0, cudaGraphCondAssignDefault));
-
-  // Root: the gate kernel.
-  CUDA_TRY(cudaStreamBeginCaptureToGraph(u.arm, u.graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  cudaError_t le = launch_gate(posted_dev, u.consumed, handle, u.err, u.arm);
-  cudaGraph_t captured = nullptr;
-  cudaError_t ec = cudaStreamEndCapture(u.arm, &captured);
-  CUDA_TRY(le);
-  CUDA_TRY(ec);
-  size_t nnodes = 0;
-  CUDA_TRY(cudaGraphGetNodes(u.graph, nullptr, &nnodes));
-  std::vector<cudaGraphNode_t> nodes(nnodes);
-  CUDA_TRY(cudaGraphGetNodes(u.graph, nodes.data(), &nnodes));
-  if (nnodes != 1) return fail(CECOLL_INTERNAL, "gate capture produced an unexpected graph");
+  GraphSink top({u.graph});
+  STATUS_TRY(top.kernel(w, u.arm, gate_call(posted_dev, u.consumed, handle, u.err)));
 
   // cudaGraphNodeParams has no default constructor (union with non-trivial
   // members): zero-initialised raw storage, as the runtime expects.
@@ -900,50 +952,36 @@ Status build_graph(World* w, Plan* p, Unit& u) {
   cp.conditional.handle = handle;
   cp.conditional.type = cudaGraphCondTypeIf;
   cp.conditional.size = 1;
-  cudaGraphNode_t if_node;
-  CUDA_TRY(cudaGraphAddNode(&if_node, u.graph, nodes.data(), 1, &cp));
+  STATUS_TRY(top.add_node(u.arm, &cp, nullptr));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
 
-  // Body: poll -> fork lanes -> join -> signal.
-  CUDA_TRY(cudaStreamBeginCaptureToGraph(u.arm, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  Status st;
-  // The body's waits stay in one-CTA poll kernels: an armed instance runs
-  // ahead of the caller stream, and a full-grid mover spinning on its flags
-  // could hold every SM that the caller's own poll kernel (on which those
-  // flags transitively depend) needs — measured as a deadlock with eight
-  // units on one GPU. The SM path fuses its flags instead (fuse_sm_flags):
-  // there everything a kernel waits for precedes it in stream order.
-  auto body_ops = [&]() -> Status {
-    CUDA_TRY(launch_poll(u.poll_tab, u.npoll, u.err, u.arm));
-    for (const Copy& c : u.placement) CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, u.arm));
-    cudaEvent_t fork;
-    CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventRecord(fork, u.arm));
-    std::vector<const LaneExec*> busy;
-    for (const LaneExec& l : p->lanes) {
-      if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) == u.ranks.end()) continue;
-      if (l.copies.empty() && !l.table.nitems) continue;  // its chunks are in the unit kernel
-      RankState* rs = w->local[l.rank].get();
-      cudaStream_t ls = rs->lanes[l.lane];
-      CUDA_TRY(cudaStreamWaitEvent(ls, fork, 0));
-      for (const Copy& c : l.copies) CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, ls));
-      if (l.table.nitems) CUDA_TRY(launch_items(l.table, mover_grid_for(l.table, p->sms), ls));
-      CUDA_TRY(cudaEventRecord(rs->lane_done[l.lane], ls));
-      busy.push_back(&l);
-    }
-    // Same-device chunks of every lane of the unit: one item kernel.
-    if (u.table.nitems) CUDA_TRY(launch_items(u.table, mover_grid_for(u.table, p->sms), u.arm));
-    for (const LaneExec* l : busy)
-      CUDA_TRY(cudaStreamWaitEvent(u.arm, w->local[l->rank]->lane_done[l->lane], 0));
-    CUDA_TRY(launch_signal(u.sig_tab, u.nsig, u.arm));
-    cudaEventDestroy(fork);
-    return {};
-  };
-  st = body_ops();
-  cudaGraph_t body_out = nullptr;
-  cudaError_t e2 = cudaStreamEndCapture(u.arm, &body_out);
-  if (!st.ok()) return st;
-  CUDA_TRY(e2);
+  // Body: poll -> fork lanes -> join -> signal. The body's waits stay in
+  // one-CTA poll kernels: an armed instance runs ahead of the caller stream,
+  // and a full-grid mover spinning on its flags could hold every SM that the
+  // caller's own poll kernel (on which those flags transitively depend)
+  // needs — measured as a deadlock with eight units on one GPU. Stream
+  // memory operations are not allowed in conditional bodies, hence kernels.
+  GraphSink sink({body});
+  STATUS_TRY(sink.kernel(w, u.arm, poll_call(u.poll_tab, u.npoll, u.err)));
+  STATUS_TRY(sink.copies(w, u.placement, u.arm, false));
+  const cudaEvent_t fork = w->local[u.ranks[0]]->start;  // an ordering key inside the graph
+  STATUS_TRY(sink.record(w, fork, u.arm));
+  std::vector<const LaneExec*> busy;
+  for (const LaneExec& l : p->lanes) {
+    if (std::find(u.ranks.begin(), u.ranks.end(), l.rank) == u.ranks.end()) continue;
+    if (l.copies.empty() && !l.table.nitems) continue;  // its chunks are in the unit kernel
+    RankState* rs = w->local[l.rank].get();
+    cudaStream_t ls = rs->lanes[l.lane];
+    STATUS_TRY(sink.wait(w, ls, fork));
+    STATUS_TRY(sink.copies(w, l.copies, ls, false));
+    STATUS_TRY(sink.kernel(w, ls, items_call(l.table, plan_grid(p, l.table))));
+    STATUS_TRY(sink.record(w, rs->lane_done[l.lane], ls));
+    busy.push_back(&l);
+  }
+  // Same-device chunks of every lane of the unit: one item kernel.
+  STATUS_TRY(sink.kernel(w, u.arm, items_call(u.table, plan_grid(p, u.table))));
+  for (const LaneExec* l : busy) STATUS_TRY(sink.wait(w, u.arm, w->local[l->rank]->lane_done[l->lane]));
+  STATUS_TRY(sink.kernel(w, u.arm, signal_call(u.sig_tab, u.nsig)));
   CUDA_TRY(cudaGraphInstantiate(&u.exec, u.graph, 0));
   return {};
 }

@@ -1,0 +1,245 @@
+// B200 cost model and its calibration — SURVEY §8(f)3.
+//
+// The reference prices a command program with a phase model
+// (CostModel, cost_model.hpp:14-33; simulate_impl, sim.cpp:183-468) whose
+// parameters describe an MI300X host driving DMA engines, and fits those
+// parameters with a seeded hill-climb (calibrate, calibrate.cpp:67-181)
+// against its paper's crossovers. On B200 the same command programs are
+// executed differently (exec.cpp): the SM path is one kernel, a copy-engine
+// program replays as one recorded graph whose lanes are parallel branches,
+// merged broadcast / swap commands are one item kernel, and a prelaunch body
+// is one or two kernels behind a trigger. This model prices exactly that
+// structure, with the terms the MI300X model lacks (kernel boundaries, graph
+// launches and branches), and calibrate() fits it to measured B200
+// latencies with the reference's procedure: multiplicative log-normal jitter
+// (σ = 0.25) on every parameter from a seeded mt19937_64, keep a candidate
+// only if it improves the score, deterministic given the seed. The score is
+// the mean squared log error over the measurements plus the reference's
+// boundary rule: a winner-grid transition that is more than one binary step
+// away from the measured one costs its distance (calibrate.cpp:44-62).
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <random>
+#include <set>
+#include <stdexcept>
+#include <tuple>
+
+#include "model.hpp"
+
+namespace cecoll {
+
+namespace {
+
+// Algorithmic HBM bytes (read + write) of one collective with co-resident
+// ranks: the program's account_traffic (verifier.cpp:281-327) plus the local
+// placement (verifier.cpp:40-44) of out-of-place programs; the SM path's
+// all-gather reads each source once (fan items).
+double hbm_bytes(Kind kind, Impl impl, int64_t s, int n) {
+  const double S = static_cast<double>(s), N = n;
+  if (impl == Impl::Sm) return kind == Kind::AllGather ? N * S + N * N * S : 2 * N * N * S;
+  // the fit prices the same programs thousands of times
+  thread_local std::map<std::tuple<int, int, int64_t, int>, double> memo;
+  const auto key = std::make_tuple(static_cast<int>(kind), static_cast<int>(impl), s, n);
+  auto it = memo.find(key);
+  if (it != memo.end()) return it->second;
+  Spec spec;
+  spec.kind = kind;
+  spec.chunk = s;
+  spec.nranks = n;
+  const Traffic t = traffic(compile(impl, spec, 32));
+  const bool swap = base_of(impl) == Impl::Swap;
+  const double b = static_cast<double>(t.read + t.write) + (swap ? 0.0 : 2 * N * S);
+  memo[key] = b;
+  return b;
+}
+
+}  // namespace
+
+B200Model default_model() { return B200Model{}; }
+
+// Device time of one collective, back to back, n ranks co-resident on one
+// B200 with one caller stream (one unit) — the configuration of
+// tools/latency.cpp and bench.py --sweep --api plan.
+double predict_ns(const B200Model& m, Kind kind, Impl impl, int64_t s, int n) {
+  const double bytes = hbm_bytes(kind, impl, s, n);
+  const Impl base = base_of(impl);
+  const double N = n;
+  const bool merged = s < (int64_t{4} << 20);  // lower.cpp: flag-free bcst / swap commands in one kernel
+  if (impl == Impl::Sm)
+    return m.t_kernel + bytes / (kind == Kind::AllGather ? m.bw_fan : m.bw_copy) * 1e9;
+  if (is_prelaunched(impl)) {
+    // one gated graph: every chunk in the unit's item kernel (one GPU)
+    const double body = bytes <= m.folded_max_bytes ? m.t_kernel : 2 * m.t_kernel;
+    const double bw = kind == Kind::AllGather && base == Impl::Bcst ? m.bw_fan : m.bw_copy;
+    return m.t_trigger + body + bytes / bw * 1e9;
+  }
+  // recorded command list: one graph per collective
+  double t = m.t_graph;
+  switch (base) {
+    case Impl::Pcpy:  // n(n-1) single-copy lanes in parallel + n placement copies
+      t += (N * (N - 1) - 1) * m.t_branch + 2 * m.t_node + bytes / m.bw_ce * 1e9;
+      break;
+    case Impl::B2b:  // n lanes of n-1 back-to-back copies + placement
+      t += (N - 1) * m.t_branch + N * m.t_node + bytes / m.bw_ce * 1e9;
+      break;
+    case Impl::Bcst: {  // broadcasts in one item kernel (or one per lane), trailing copies as memcpy nodes
+      const double lanes = merged ? 1 : N * std::floor((N - 1) / 2);
+      t += (lanes - 1 + (n % 2 == 0 ? N : 0)) * m.t_branch + m.t_kernel + m.t_node +
+           bytes / (merged ? m.bw_copy : m.bw_lanes) * 1e9;
+      break;
+    }
+    case Impl::Swap: {  // swaps in one item kernel (or one kernel per lane, concurrently)
+      const double lanes = merged ? 1 : N * (N - 1) / 2;
+      t += (lanes - 1) * m.t_branch + m.t_kernel + bytes / (merged ? m.bw_copy : m.bw_lanes) * 1e9;
+      break;
+    }
+    default:
+      throw std::invalid_argument("model: no B200 structure for this implementation");
+  }
+  return t;
+}
+
+namespace {
+
+// Winner among `cands` at size s, from a time function; the plain variant
+// wins a near tie with its prelaunch form (winner_grid, sweep.cpp:206-214).
+template <class F>
+Impl winner(const std::vector<Impl>& cands, F&& time_of, double gain_threshold) {
+  Impl best = cands.front();
+  double bt = time_of(best);
+  for (Impl c : cands) {
+    const double t = time_of(c);
+    if (t < bt) best = c, bt = t;
+  }
+  if (is_prelaunched(best)) {
+    const Impl plain = base_of(best);
+    if (std::find(cands.begin(), cands.end(), plain) != cands.end() &&
+        time_of(plain) <= bt * (1 + gain_threshold))
+      best = plain;
+  }
+  return best;
+}
+
+// First size at which the winner changes from `from` to `to` (boundary_between,
+// sweep.cpp:220-227); -1 when absent.
+int64_t boundary(const std::vector<int64_t>& sizes, const std::vector<Impl>& w, Impl from, Impl to) {
+  for (size_t i = 1; i < sizes.size(); ++i)
+    if (w[i - 1] == from && w[i] == to) return sizes[i];
+  return -1;
+}
+
+}  // namespace
+
+std::vector<Impl> model_candidates(Kind kind) {
+  if (kind == Kind::AllGather)
+    return {Impl::Sm, Impl::Pcpy, Impl::Bcst, Impl::B2b, Impl::PrelaunchPcpy, Impl::PrelaunchBcst, Impl::PrelaunchB2b};
+  return {Impl::Sm, Impl::Pcpy, Impl::Swap, Impl::B2b, Impl::PrelaunchPcpy, Impl::PrelaunchSwap, Impl::PrelaunchB2b};
+}
+
+Impl model_winner(const B200Model& m, Kind kind, int64_t s, int n) {
+  return winner(model_candidates(kind), [&](Impl c) { return predict_ns(m, kind, c, s, n); },
+                m.prelaunch_gain_threshold);
+}
+
+constexpr double kTie = 1.10;
+
+double model_score(const B200Model& m, const std::vector<Measurement>& meas, std::string* report) {
+  double err = 0;
+  int count = 0;
+  std::map<std::tuple<int, int, int64_t>, std::map<Impl, double>> grid;  // (kind, n, s) -> impl -> ns
+  for (const Measurement& x : meas) {
+    if (x.ns <= 0) continue;
+    double p;
+    try {
+      p = predict_ns(m, x.kind, x.impl, x.s, x.n);
+    } catch (const std::invalid_argument&) {
+      continue;
+    }
+    const double d = std::log(p / x.ns);
+    err += d * d;
+    ++count;
+    grid[{static_cast<int>(x.kind), x.n, x.s}][x.impl] = x.ns;
+  }
+  double penalty = count ? err / count : 0;
+  std::string log = "mean squared log error " + std::to_string(count ? err / count : 0) + " over " +
+                    std::to_string(count) + " measurements\n";
+  // Boundary rule (calibrate.cpp:44-62): every transition of the measured
+  // winner grid must appear in the model's grid within one binary step.
+  std::map<std::pair<int, int>, std::vector<int64_t>> sizes;
+  for (const auto& g : grid) sizes[{std::get<0>(g.first), std::get<1>(g.first)}].push_back(std::get<2>(g.first));
+  for (auto& kv : sizes) {
+    const Kind kind = static_cast<Kind>(kv.first.first);
+    const int n = kv.first.second;
+    std::vector<int64_t>& ss = kv.second;
+    std::sort(ss.begin(), ss.end());
+    std::vector<Impl> measured, model;
+    for (int64_t s : ss) {
+      const auto& row = grid[{kv.first.first, n, s}];
+      std::vector<Impl> cands;
+      for (const auto& e : row) cands.push_back(e.first);
+      Impl w = winner(cands, [&](Impl c) { return row.at(c); }, m.prelaunch_gain_threshold);
+      // Measured ties are noise, not crossovers: the previous size's winner
+      // stays while it is within kTie of the best here.
+      if (!measured.empty() && row.count(measured.back()) && row.at(measured.back()) <= kTie * row.at(w))
+        w = measured.back();
+      measured.push_back(w);
+      model.push_back(winner(cands, [&](Impl c) { return predict_ns(m, kind, c, s, n); }, m.prelaunch_gain_threshold));
+    }
+    for (size_t i = 1; i < ss.size(); ++i) {
+      if (measured[i - 1] == measured[i]) continue;
+      const int64_t target = ss[i];
+      const int64_t got = boundary(ss, model, measured[i - 1], measured[i]);
+      const std::string name = std::string(kind == Kind::AllGather ? "AG" : "AA") + " n=" + std::to_string(n) + " " +
+                               impl_name(measured[i - 1]) + "->" + impl_name(measured[i]);
+      if (got < 0) {
+        penalty += 4.0;
+        log += "  " + name + ": transition absent\n";
+        continue;
+      }
+      const double steps = std::abs(std::log2(static_cast<double>(got) / static_cast<double>(target)));
+      log += "  " + name + ": model " + std::to_string(got) + " measured " + std::to_string(target) + " (" +
+             std::to_string(steps) + " steps)\n";
+      penalty += std::max(0.0, steps - 1.0);
+    }
+  }
+  if (report) *report = log;
+  return penalty;
+}
+
+FitResult calibrate_b200(const std::vector<Measurement>& meas, uint64_t seed, int iterations) {
+  B200Model best = default_model();
+  std::string report;
+  double best_score = model_score(best, meas, &report);
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> jitter(0.0, 0.25);
+  B200Model current = best;
+  for (int it = 0; it < iterations; ++it) {
+    B200Model cand = current;
+    auto perturb = [&](double& v) { v *= std::exp(jitter(rng)); };
+    perturb(cand.t_kernel);
+    perturb(cand.t_graph);
+    perturb(cand.t_branch);
+    perturb(cand.t_node);
+    perturb(cand.t_trigger);
+    perturb(cand.bw_copy);
+    perturb(cand.bw_fan);
+    perturb(cand.bw_ce);
+    perturb(cand.bw_lanes);
+    std::string r;
+    const double sc = model_score(cand, meas, &r);
+    if (sc < best_score) {  // hill-climb from improvements (calibrate.cpp:150-158)
+      best_score = sc;
+      best = cand;
+      report = std::move(r);
+      current = cand;
+    }
+  }
+  FitResult out;
+  out.model = best;
+  out.residual = best_score;
+  out.report = report;
+  return out;
+}
+
+}  // namespace cecoll

@@ -556,11 +556,17 @@ Impl reference_select(Kind kind, int64_t size) {
 // (profiles/sweep_r01_plan_n8_recorded.csv). CECOLL_SM_MAX_BYTES overrides
 // the SM cutoff. (bench_mgpu.py measures every implementation per size on
 // the multi-GPU node and reports the winner grid.)
-Impl select(Kind kind, int64_t size, int nranks, int ndevices) {
+Impl select(Kind kind, int64_t size, int nranks, int ndevices, int sm_budget) {
   (void)nranks;
   int64_t sm_max;
   if (ndevices <= 1) sm_max = kind == Kind::AllGather ? INT64_MAX : (int64_t{32} << 20);
   else sm_max = int64_t{1} << 20;
+  // With an SM budget the caller keeps the SMs for its own compute: across
+  // devices every transfer above the latency regime goes to the copy engines
+  // (per-peer lanes, 0 SMs). On one device the driver itself runs
+  // device-local copies on SMs (profiles/ce_probe2_r01.txt), so the budgeted
+  // SM mover stays the choice there.
+  if (sm_budget > 0 && ndevices > 1) sm_max = int64_t{64} << 10;
   if (const char* env = std::getenv("CECOLL_SM_MAX_BYTES")) sm_max = std::atoll(env);
   if (size <= sm_max) return Impl::Sm;
   return ndevices <= 1 ? Impl::B2b : Impl::Pcpy;

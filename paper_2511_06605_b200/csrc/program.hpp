@@ -112,6 +112,6 @@ std::string validate(const Program& p, int lanes_per_rank);
 Program parse_dump(const std::string& text, Kind kind, int64_t chunk, int nranks);
 
 Impl reference_select(Kind kind, int64_t size);
-Impl select(Kind kind, int64_t size, int nranks, int ndevices);
+Impl select(Kind kind, int64_t size, int nranks, int ndevices, int sm_budget = 0);
 
 }  // namespace cecoll

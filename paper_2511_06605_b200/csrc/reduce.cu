@@ -62,10 +62,17 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const RedItem* __re
   __shared__ int first[kMaxItemsSmem];
   for (int i = threadIdx.x; i < nitems; i += kRedThreads) first[i] = items[i].first_tile;
   // Fused flags (kernels.hpp FlagSet): every source rank's send is ready.
-  if ((flags.npoll || flags.npre) && threadIdx.x < 32) fused_wait(flags);
+  __shared__ int cta_state;
+  uint64_t post_no = 0;
+  if (threadIdx.x < 32) {
+    const int st = (flags.npoll || flags.npre || flags.posted || flags.skip) ? fused_wait(flags, &post_no) : kGo;
+    if (threadIdx.x == 0) cta_state = st;
+  }
   __syncthreads();
+  const int state = cta_state;
+  const bool moved = state == kGo;
   int cur = 0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int tile = moved ? blockIdx.x : ntiles; tile < ntiles; tile += gridDim.x) {
     while (cur + 1 < nitems && first[cur + 1] <= tile) ++cur;
     const RedItem it = items[cur];
     const int64_t base = static_cast<int64_t>(tile - it.first_tile) * kRedTileElems + threadIdx.x * kElemsPerThread;
@@ -113,34 +120,47 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const RedItem* __re
   }
   if (flags.ctr) {  // every source read: tell the source ranks (last CTA)
     __syncthreads();
-    if (threadIdx.x == 0) fused_finish(flags);
+    if (threadIdx.x == 0) fused_finish(flags, state, post_no);
   }
 }
 
 template <int kDtype>
-cudaError_t launch_dtype(const RedTable& t, int grid, cudaStream_t stream, const FlagSet& f) {
-  switch (t.op) {
-    case kSum: reduce_kernel<kDtype, kSum><<<grid, kRedThreads, 0, stream>>>(t.items, t.nitems, t.ntiles, f); break;
-    case kMax: reduce_kernel<kDtype, kMax><<<grid, kRedThreads, 0, stream>>>(t.items, t.nitems, t.ntiles, f); break;
-    case kMin: reduce_kernel<kDtype, kMin><<<grid, kRedThreads, 0, stream>>>(t.items, t.nitems, t.ntiles, f); break;
-    default: return cudaErrorInvalidValue;
+const void* kernel_for(int op) {
+  switch (op) {
+    case kSum: return reinterpret_cast<const void*>(reduce_kernel<kDtype, kSum>);
+    case kMax: return reinterpret_cast<const void*>(reduce_kernel<kDtype, kMax>);
+    case kMin: return reinterpret_cast<const void*>(reduce_kernel<kDtype, kMin>);
+    default: return nullptr;
   }
-  return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_reduce(const RedTable& t, int grid, cudaStream_t stream, const FlagSet* fp) {
-  const FlagSet f = fp ? *fp : FlagSet{};
-  if (t.nitems <= 0 || t.ntiles <= 0) return cudaSuccess;
-  if (t.nitems > kMaxItemsSmem) return cudaErrorInvalidValue;
+KernelCall reduce_call(const RedTable& t, int grid, const FlagSet* fp) {
+  KernelCall k;
+  if (t.nitems <= 0 || t.ntiles <= 0 || t.nitems > kMaxItemsSmem) return k;
   if (grid > t.ntiles) grid = t.ntiles;
   switch (t.dtype) {
-    case kF32: return launch_dtype<kF32>(t, grid, stream, f);
-    case kBF16: return launch_dtype<kBF16>(t, grid, stream, f);
-    case kF16: return launch_dtype<kF16>(t, grid, stream, f);
-    default: return cudaErrorInvalidValue;
+    case kF32: k.func = kernel_for<kF32>(t.op); break;
+    case kBF16: k.func = kernel_for<kBF16>(t.op); break;
+    case kF16: k.func = kernel_for<kF16>(t.op); break;
+    default: break;
   }
+  if (!k.func) return k;
+  k.grid = dim3(grid);
+  k.block = dim3(kRedThreads);
+  k.push(static_cast<const RedItem*>(t.items));
+  k.push(t.nitems);
+  k.push(t.ntiles);
+  k.push(fp ? *fp : FlagSet{});
+  return k;
+}
+
+cudaError_t launch_reduce(const RedTable& t, int grid, cudaStream_t stream, const FlagSet* fp) {
+  if (t.nitems <= 0 || t.ntiles <= 0) return cudaSuccess;
+  const KernelCall k = reduce_call(t, grid, fp);
+  if (!k.func) return cudaErrorInvalidValue;
+  return launch(k, stream);
 }
 
 // Loads every reduction kernel on the current device (see preload_kernels,

@@ -119,6 +119,14 @@ struct World {
   std::vector<std::unique_ptr<RankState>> local;  // by rank; null if remote
   std::atomic<int64_t> counters[kNumCounters];
   std::vector<std::unique_ptr<Plan>> plans;  // eager-call plan cache
+  // Plans evicted from the cache (or dropped at deregistration) wait here
+  // until no prelaunch unit of the process is armed (exec.cpp retire_plan).
+  std::vector<std::unique_ptr<Plan>> retired;
+  // SM budget for plans created from now on (cecoll_comm_set_sm_budget): the
+  // most CTAs any mover / reduction kernel of a plan may launch (0: a full
+  // persistent grid), and the AUTO selector prefers copy-engine lanes.
+  int sm_budget = 0;
+  Plan* last_plan = nullptr;  // the cached plan of the latest eager call (cecoll_comm_last_plan_info)
   std::vector<Plan*> explicit_plans;         // cecoll_plan_create; cancelled at release
   std::vector<Window> windows;
   std::vector<int> reg_rounds;  // per local index
@@ -134,7 +142,6 @@ struct World {
   // cecoll_comm_get_async_error (a device-side flag poll timed out); sticky,
   // returned by the communicator's destroy.
   Status async_error;
-  bool capturing = false;  // record_plan in progress: no batched memcpy (not capturable)
   std::unique_ptr<Tracer> tracer;  // non-null between cecoll_trace_begin and _end
   std::string trace_json;          // last finished trace, until read through the C ABI
   World() {
@@ -225,6 +232,8 @@ struct Plan {
   int64_t hybrid_sm_bytes = 0;  // SM share of every chunk (16-byte multiple)
   bool prelaunch = false;
   int sms = 148;
+  int sm_budget = 0;              // max CTAs per kernel of this plan (0: full grid)
+  bool folded = false;            // prelaunch body is one kernel that is its own gate
   int dtype = 0, op = 0;          // reduce-scatter element type / operator
   std::unique_ptr<Plan> inner;    // reduce-scatter over copy engines: the all-to-all into staging
   std::string graph_fallback;     // why a prelaunch plan runs without its graph (empty: it has one)
@@ -282,6 +291,18 @@ Status plan_disarm(World* w, Plan* p);
 Status plan_launch(World* w, Plan* p, bool rearm);
 Status plan_destroy(World* w, Plan* p);
 Status plan_poll_errors(Plan* p);  // CECOLL_TIMEOUT if a kernel-side poll of the plan timed out
+// Plan cache and deferred release (exec.cpp).
+constexpr size_t kPlanCacheSize = 64;
+void cache_plan(World* w, Plan* p);
+void retire_plan(World* w, std::unique_ptr<Plan> p);
+void release_retired(World* w, bool force);
+int armed_units();  // prelaunch units armed in this process
+// Kernel grids under the plan's SM budget.
+int plan_grid(const Plan* p, const ItemTable& t);
+int plan_red_grid(const Plan* p);
+std::string plan_info(World* w, const Plan* p);
+// AUTO selection for the world (its device count and SM budget).
+Impl select_for(World* w, Kind kind, int64_t s);
 
 // NVLS multicast all-gather windows (mcast.cpp, experimental).
 struct McWindow;

@@ -82,11 +82,11 @@ Status issue_copies(World* w, const std::vector<Copy>& copies, cudaStream_t s, b
   const DriverApi* d = driver_api();
   // cuMemcpyBatchAsync rejects the legacy NULL stream.
   const bool legacy = s == nullptr || s == cudaStreamLegacy;
-  // cuMemcpyBatchAsync cannot be captured: inside a recording (ours or the
-  // caller's stream capture) every copy becomes its own memcpy node.
+  // cuMemcpyBatchAsync cannot be captured: inside a caller's stream capture
+  // every copy becomes its own memcpy node.
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (!legacy && copies.size() > 1) cudaStreamIsCapturing(s, &cs);
-  const bool capturing = w->capturing || cs != cudaStreamCaptureStatusNone;
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
   if (copies.size() > 1 && allow_batch && d->has_batch_memcpy && !legacy && !capturing) {
     std::vector<CUdeviceptr> dst, src;
     std::vector<size_t> sz;
@@ -127,12 +127,10 @@ Status ensure_lanes(RankState* rs, int n) {
   return {};
 }
 
-// Stream memops, then the signal kernel for other-device flags.
-Status signal_remote(World* w, uint64_t** tab, size_t n, cudaStream_t s) {
+// The signal kernel for other-device flags.
+Status signal_remote(World* w, Sink& sink, uint64_t** tab, size_t n, cudaStream_t s) {
   if (!n) return {};
-  CUDA_TRY(launch_signal(tab, static_cast<int>(n), s));
-  ++w->counters[kCtrKernels];
-  ++w->counters[kCtrApiCalls];
+  STATUS_TRY(sink.kernel(w, s, signal_call(tab, static_cast<int>(n))));
   w->counters[kCtrFlagWrites] += static_cast<int64_t>(n);
   return {};
 }

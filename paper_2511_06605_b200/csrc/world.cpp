@@ -349,8 +349,12 @@ Status world_deregister(World* w, void* ptr) {
     }
   }
   if (!found) return fail(CECOLL_NOT_REGISTERED, "cecoll_deregister: pointer is not a registered window base");
-  for (auto& p : w->plans) note_async(w, plan_destroy(w, p.get()));
-  w->plans.clear();
+  // Released later (exec.cpp retire_plan): freeing plan memory synchronises
+  // the device, which must not happen while a prelaunch gate is armed.
+  std::vector<std::unique_ptr<Plan>> drop;
+  drop.swap(w->plans);
+  w->last_plan = nullptr;
+  for (auto& p : drop) retire_plan(w, std::move(p));
   return {};
 }
 
@@ -377,6 +381,11 @@ Status world_mem_alloc(World* w, int rank, size_t bytes, void** out) {
 Status world_mem_free(World* w, void* ptr) {
   auto it = std::find_if(w->allocs.begin(), w->allocs.end(), [&](const auto& a) { return a.first == ptr; });
   if (it == w->allocs.end()) return fail(CECOLL_INVALID_ARGUMENT, "cecoll_mem_free: not a cecoll_mem_alloc pointer");
+  // cudaFree synchronises the device: behind an armed prelaunch gate (any
+  // world of the process) it would wait for a trigger that may never come.
+  if (armed_units() > 0)
+    return fail(CECOLL_INVALID_ARGUMENT,
+                "cecoll_mem_free: a prelaunch plan is armed (disarm or launch it first; cudaFree would wait for it)");
   STATUS_TRY(world_deregister(w, ptr));
   DeviceGuard g(it->second);
   CUDA_TRY(cudaFree(ptr));  // synchronises with work still reading the buffer
@@ -396,6 +405,7 @@ Status world_release(World* w) {
   // cecoll_plan handles must not be used afterwards.
   for (Plan* p : w->explicit_plans) note_async(w, plan_destroy(w, p));
   w->explicit_plans.clear();
+  release_retired(w, true);
   for (auto& rs : w->local) {
     if (!rs) continue;
     DeviceGuard g(rs->device);

@@ -100,7 +100,7 @@ def test_watchdog_prints_the_line_and_exits(phase, code, value):
         import sys, time
         sys.path.insert(0, {ROOT!r})
         import bench_mgpu as bm
-        line = {{"metric": "m", "value": {value!r}, "config": {{"impl_trials": {{
+        line = {{"metric": "m", "value": {value!r}, "config": {{}}, "details": {{"impl_trials": {{
             "sm": {{"ms": 0.2, "busbw_gbs": 300.0}}, "pcpy": {{"error": "x"}}, "b2b": {{"ms": 0.1, "busbw_gbs": 600.0}}}}}}}}
         bm.STATE["phase"] = {phase!r}
         bm.Watchdog(0.2, 0, lambda: line)
@@ -110,7 +110,7 @@ def test_watchdog_prints_the_line_and_exits(phase, code, value):
     assert r.returncode == code, r.stderr
     out = json.loads(r.stdout.strip().splitlines()[-1])
     if code == 1:  # hung before the headline: best trial so far, flagged
-        assert out["value"] == 600.0 and out["config"]["impl"].startswith("b2b")
+        assert out["value"] == 600.0 and out["details"]["impl"].startswith("b2b")
         assert "watchdog" in out["error"]
     elif value is not None:  # hung after the headline: it stands, the phase is named
         assert out["value"] == value and "nccl" in out["error"]

@@ -36,7 +36,9 @@ def test_torchrun_arm_prints_one_complete_line():
     assert "error" not in d, d.get("error")
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["parity_ok"] is True
     assert d["e2e"]["parity_ok"] is True and d["roofline"]["bound"] == "nvlink"
-    assert all("ms" in v for v in d["config"]["impl_trials"].values()), d["config"]["impl_trials"]
+    assert all("ms" in v for v in d["details"]["impl_trials"].values()), d["details"]["impl_trials"]
+    assert d["config"] == {"workload": d["config"]["workload"], "ranks": 8, "chunk_bytes": 8 << 20}
+    assert all("graph_fallback" in v["plan"] for v in d["details"]["impl_trials"].values())
     rows = [row for row in d["sweep"]["rows"] if "skipped" not in row]
     assert rows and not any(row.get("errors") for row in rows)
     assert any(k.startswith("prelaunch") for row in rows for k in row.get("us", {}))  # the late pass ran

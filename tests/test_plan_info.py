@@ -1,0 +1,83 @@
+"""cecoll_plan_info / cecoll_comm_last_plan_info: what a plan turned into
+(the fields every bench line carries, so a number cannot be misread: a
+prelaunch plan that fell back to eager, a command list that is not recorded,
+the mover and the flag path of every unit)."""
+import pytest
+
+import paper_2511_06605_b200 as cc
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+N = 8
+
+
+@pytest.fixture(scope="module")
+def comms():
+    cs = cc.Comm.init_all([0] * N)
+    yield cs
+    cc.destroy_all(cs)
+
+
+def _bufs(s, kind="alltoall"):
+    in_bytes = s if kind == "allgather" else N * s
+    return ([torch.randint(0, 256, (in_bytes,), dtype=torch.uint8, device="cuda") for _ in range(N)],
+            [torch.zeros(N * s, dtype=torch.uint8, device="cuda") for _ in range(N)])
+
+
+def test_single_unit_sm_is_one_kernel_not_recorded(comms):
+    sends, recvs = _bufs(4096)
+    st = torch.cuda.Stream()
+    for _ in range(3):
+        cc.all_to_all(comms, sends, recvs, 4096, impl="sm", streams=st)
+    info = comms[0].last_plan_info()
+    assert info["impl"] == "sm" and not info["recorded"] and info["record_note"] == ""
+    assert len(info["units"]) == 1 and info["units"][0]["mover"] in ("tma", "reg")
+    assert info["units"][0]["ranks"] == list(range(N))
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("impl", ["pcpy", "b2b", "hybrid"])
+def test_copy_engine_plans_record_from_the_second_launch(comms, impl):
+    sends, recvs = _bufs(65536)
+    st = torch.cuda.Stream()
+    cc.all_to_all(comms, sends, recvs, 65536, impl=impl, streams=st)
+    assert not comms[0].last_plan_info()["recorded"]
+    cc.all_to_all(comms, sends, recvs, 65536, impl=impl, streams=st)
+    info = comms[0].last_plan_info()
+    assert info["recorded"] and info["record_note"] == "", info
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("impl,s,folded", [("prelaunch_b2b", 4096, True), ("prelaunch_swap", 4096, True),
+                                           ("prelaunch_pcpy", 8 << 20, False)])
+def test_prelaunch_plans_report_their_body(comms, impl, s, folded):
+    sends, recvs = _bufs(s)
+    if impl.endswith("swap"):
+        recvs = sends
+    plan = cc.Plan(comms, "alltoall", sends, recvs, s, impl=impl)
+    info = plan.info()
+    assert info["prelaunch"] and info["graph_fallback"] == ""
+    assert info["prelaunch_folded"] == folded, info
+    plan.launch(torch.cuda.current_stream())
+    torch.cuda.current_stream().synchronize()
+    plan.destroy()
+    torch.cuda.synchronize()
+
+
+def test_sm_budget_caps_the_grid(comms):
+    sends, recvs = _bufs(8 << 20)
+    comms[0].set_sm_budget(16)
+    try:
+        plan = cc.Plan(comms, "alltoall", sends, recvs, 8 << 20, impl="sm")
+        info = plan.info()
+        assert info["sm_budget"] == 16 and info["units"][0]["grid"] == 16
+        plan.launch(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        for i in range(N):
+            for j in range(N):
+                s = 8 << 20
+                assert torch.equal(recvs[j][i * s:(i + 1) * s], sends[i][j * s:(j + 1) * s])
+        plan.destroy()
+    finally:
+        comms[0].set_sm_budget(0)

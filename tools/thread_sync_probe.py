@@ -2,7 +2,10 @@
 prelaunch collectives (tests/test_threads.py); repeated, with faulthandler.
 Usage: python -X faulthandler tools/thread_sync_probe.py [reps] [impl]
 PROBE_SYNC=stream: the other thread synchronises an idle stream instead.
-PROBE_WARM=1: every plan is recorded (launched three times) before the race."""
+PROBE_WARM=1: every plan is recorded (launched three times) before the race.
+Exit status: 0 clean; 3 a thread hung; 4 an error or a parity failure; a
+signal (e.g. -11) if the process crashed. tests/test_thread_sync.py runs it
+cold (no warming) for the recorded and prelaunch implementations."""
 import faulthandler
 import os
 import sys
@@ -62,4 +65,6 @@ for rep in range(reps):
         faulthandler.dump_traceback(all_threads=True)
         os._exit(3)
     cc.destroy_all(comms)
+    if errors or not ok:
+        sys.exit(4)
 print("done", flush=True)
