@@ -642,7 +642,7 @@ def run_e2e(comms, plans, best, sets, expects, s, n, nlocal, stream, args):
                 h.copy_(d, non_blocking=True)
         out_done[b].record(d2h_s)
 
-    steps = max(4, args.steps)
+    steps = max(getattr(args, "e2e_steps", 40), args.steps)
     for k in range(2):
         step(k)
     d2h_s.synchronize()
@@ -652,21 +652,37 @@ def run_e2e(comms, plans, best, sets, expects, s, n, nlocal, stream, args):
     torch.cuda.synchronize()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # cold window (pipeline empty at the start, drained at the end), then a
+    # steady window (pipeline full at both edges) as in bench.py
     e0.record(h2d_s)
-    for k in range(steps):
+    k = 0
+    for _ in range(steps):
         step(k)
+        k += 1
     e1.record(d2h_s)
+    for _ in range(2):
+        step(k)
+        k += 1
+    s0.record(d2h_s)
+    for _ in range(steps):
+        step(k)
+        k += 1
+    s1.record(d2h_s)
     d2h_s.synchronize()
     stream.synchronize()
     for p in e2e_plans:
         p.disarm()
     torch.cuda.synchronize()
-    ms = max_all(e0.elapsed_time(e1) / steps)
-    last = host_outs[(steps - 1) % 2]
+    cold = max_all(e0.elapsed_time(e1) / steps)
+    ms = max_all(s0.elapsed_time(s1) / steps)
+    last = host_outs[(k - 1) % 2]
     ok = all_true(all(bool(torch.equal(h.cuda(), e)) for h, e in zip(last, expects)))
     e2e_plans[1].destroy()
     return {"value": round(busbw(n, s, ms), 3), "unit": "GB/s", "h2d_bytes_per_step": n * n * s,
-            "d2h_bytes_per_step": n * n * s, "ms_per_step": round(ms, 3), "parity_ok": ok,
+            "d2h_bytes_per_step": n * n * s, "ms_per_step": round(ms, 3), "parity_ok": ok, "steps": steps,
+            "window": "steady state (pipeline full at both edges)", "cold_ms_per_step": round(cold, 3),
+            "cold_value": round(busbw(n, s, cold), 3),
             "pipeline": "double-buffered: H2D of step k+1 overlaps D2H of step k; each GPU copies its "
                         f"{nlocal} ranks' buffers over its own PCIe link; bytes are whole-job"}
 

@@ -127,7 +127,8 @@ cecoll_impl_t cecoll_select_budget(cecoll_kind_t kind, int64_t chunk_bytes, int 
  * ------------------------------------------------------------------- */
 typedef struct {
   double t_kernel, t_graph, t_branch, t_node, t_trigger;
-  double bw_copy, bw_fan, bw_ce, bw_lanes;
+  double bw_copy, bw_fan, bw_ce, bw_lanes, bw_swap;
+  double l2_boost, l2_bytes; /* bandwidth factor when the buffers fit in L2 */
   double folded_max_bytes, prelaunch_gain_threshold;
 } cecoll_model_t;
 void cecoll_model_default(cecoll_model_t* model);
@@ -160,21 +161,11 @@ cecoll_status_t cecoll_model_fit(const int* kinds, const int* impls, const int64
  * different. It blocks device-wide synchronisation and lazy module loads in
  * every thread of the process until it is launched or disarmed (see
  * cecoll_plan_disarm).
- * Open issue: one thread calling cudaDeviceSynchronize in a loop while
- * another issues collectives has crashed inside the CUDA runtime on these
- * boxes. The crash is intermittent, needs the collectives' own kernels, and
- * does not occur with torch-only work (tools/thread_sync_probe.py,
- * tools/torch_sync_probe.py). cecoll_comm_destroy synchronises the device.
- * The cause is the recording itself. A plan's second launch captures its
- * submission (a stream capture in progress), and a device synchronisation
- * from another thread during that capture crashes. It does not happen with
- * plans recorded before the race (PROBE_WARM=1), with CECOLL_GRAPH=0, or
- * with stream-level synchronisation in the other thread. Plans whose
- * submission is a single kernel launch (the one-unit SM path) are never
- * recorded, so they are not exposed. For the others, either launch each
- * plan twice before another thread may synchronise the device, or set
- * CECOLL_GRAPH=0. Likewise, destroy worlds only while no other thread is
- * issuing collectives.
+ * Recorded command lists and prelaunch graphs are built node by node (no
+ * stream capture), so a device-wide synchronisation in another thread can
+ * run at any time, including while a plan records (tests/test_thread_sync.py;
+ * round 1's capture-based recording crashed in that race). Destroy a world
+ * only while no other thread is issuing collectives on it.
  * ------------------------------------------------------------------- */
 cecoll_status_t cecoll_comm_init_all(cecoll_comm_t* comms, int nranks, const int* devlist);
 /* Multi-process: one process per GPU owning one rank. `exchange` must
@@ -282,10 +273,11 @@ cecoll_status_t cecoll_collective_n(cecoll_kind_t kind, const cecoll_comm_t* com
 /* ---------------------------------------------------------------------
  * Explicit prelaunch plans (≙ apply_prelaunch, compiler.cpp:267-285, and the
  * producer→collective sync chain, sim.cpp:475-499). A plan binds the ranks'
- * buffers once, records the command lists as CUDA graphs gated by trigger
+ * buffers once, builds the command lists as CUDA graphs gated by trigger
  * polls, and keeps one instance armed ahead of the trigger.
  * Plans of the other implementations (and the cached plans behind the eager
- * calls) are recorded too: from their second launch on, each unit's whole
+ * calls) are recorded too (built explicitly, node by node — never by stream
+ * capture): from their second launch on, each unit's whole
  * submission — flag operations, lanes, copies, kernels — replays as one CUDA
  * graph launched on the caller stream (one host call per collective). This
  * applies when every unit of the plan has its own device and an explicit,

@@ -83,7 +83,8 @@ def build(force: bool = False) -> str:
 class ModelParams(C.Structure):
     """cecoll_model_t (include/cecoll.h): the B200 cost model's parameters."""
     _fields_ = [(k, C.c_double) for k in ("t_kernel", "t_graph", "t_branch", "t_node", "t_trigger", "bw_copy",
-                                          "bw_fan", "bw_ce", "bw_lanes", "folded_max_bytes",
+                                          "bw_fan", "bw_ce", "bw_lanes", "bw_swap", "l2_boost", "l2_bytes",
+                                          "folded_max_bytes",
                                           "prelaunch_gain_threshold")]
 
     def as_dict(self) -> dict:

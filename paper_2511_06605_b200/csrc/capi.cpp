@@ -529,6 +529,9 @@ B200Model from_c(const cecoll_model_t* c) {
   m.bw_fan = c->bw_fan;
   m.bw_ce = c->bw_ce;
   m.bw_lanes = c->bw_lanes;
+  m.bw_swap = c->bw_swap;
+  m.l2_boost = c->l2_boost;
+  m.l2_bytes = c->l2_bytes;
   m.folded_max_bytes = c->folded_max_bytes;
   m.prelaunch_gain_threshold = c->prelaunch_gain_threshold;
   return m;
@@ -543,6 +546,9 @@ void to_c(const B200Model& m, cecoll_model_t* c) {
   c->bw_fan = m.bw_fan;
   c->bw_ce = m.bw_ce;
   c->bw_lanes = m.bw_lanes;
+  c->bw_swap = m.bw_swap;
+  c->l2_boost = m.l2_boost;
+  c->l2_bytes = m.l2_bytes;
   c->folded_max_bytes = m.folded_max_bytes;
   c->prelaunch_gain_threshold = m.prelaunch_gain_threshold;
 }

@@ -215,6 +215,24 @@ void set_armed(Unit& u, bool armed) {
 
 Status arm_unit(World* w, Unit& u) {
   DeviceGuard g(u.device);
+  const uint64_t instance = u.instances++;
+  if (u.fold_node) {  // the folded kernel waits for post number `instance`
+    KernelCall& k = u.fold_call;
+    FlagSet f;
+    std::memcpy(&f, k.buf + k.off[k.nargs - 1], sizeof(f));
+    f.post_no = instance;
+    std::memcpy(k.buf + k.off[k.nargs - 1], &f, sizeof(f));
+    void* args[12];
+    k.params(args);
+    cudaKernelNodeParams kp;
+    std::memset(&kp, 0, sizeof(kp));
+    kp.func = const_cast<void*>(k.func);
+    kp.gridDim = k.grid;
+    kp.blockDim = k.block;
+    kp.sharedMemBytes = k.smem;
+    kp.kernelParams = args;
+    CUDA_TRY(cudaGraphExecKernelNodeSetParams(u.exec, u.fold_node, &kp));
+  }
   CUDA_TRY(cudaGraphLaunch(u.exec, u.arm));
   CUDA_TRY(cudaEventRecord(u.graph_done, u.arm));
   ++w->counters[kCtrGraphLaunches];

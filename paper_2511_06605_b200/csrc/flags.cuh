@@ -45,29 +45,52 @@ __device__ __forceinline__ bool wait_flag(const uint64_t* p, uint64_t* err) {
   return true;
 }
 
-// Folded prelaunch gate (FlagSet::posted, one full warp of every CTA). CTA 0
-// takes the next host post and publishes it in the device word *gate; every
-// CTA reads it from there (one PCIe poller, not one per CTA). Returns true
-// for "go". *consumed is advanced by the last CTA (fused_finish).
-__device__ __forceinline__ bool folded_gate(const FlagSet& f, uint64_t* post_no) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t c = *reinterpret_cast<volatile uint64_t*>(f.consumed);
-  *post_no = c;
-  if (blockIdx.x == 0 && lane == 0) {
-    while (f.posted[0] <= c) __nanosleep(128);
-    const uint64_t kind = f.posted[1 + (c % 64)];
-    if (kind != 1 && kind != 2) atomicOr(reinterpret_cast<unsigned long long*>(f.err), 2ull);
-    st_release_gpu(f.gate, (c + 1) * 2 + (kind == 1 ? 1 : 0));
-  }
-  uint64_t v = 0;
-  if (lane == 0)
-    while ((v = ld_acquire_gpu(f.gate)) < (c + 1) * 2) __nanosleep(64);
-  v = __shfl_sync(0xffffffffu, v, 0);
-  return v == (c + 1) * 2 + 1;
-}
-
 // What a CTA may do after its prologue.
 enum : int { kGo = 0, kTimedOut = 1, kCancelled = 2 };
+
+// Folded prelaunch gate (FlagSet::posted, one full warp of every CTA). CTA 0
+// alone takes host post number f.post_no (one PCIe poller), writes the folded
+// start signals, polls the flags (one set of system-scope pollers) and resets
+// them — their writers only write again after this instance completes or
+// signals — then publishes the outcome in the device word *gate =
+// (post_no + 1) * 4 + state; every other CTA waits for that word (device
+// scope). CTA 0's system-scope acquire of the flags followed by its release of
+// the gate word orders the flag writers' data before every CTA's accesses.
+__device__ __forceinline__ int folded_gate(const FlagSet& f) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t c = f.post_no;
+  const uint64_t base = (c + 1) * 4;
+  int state;
+  if (blockIdx.x == 0) {
+    uint64_t kind = 0;
+    if (lane == 0) {
+      while (f.posted[0] <= c) __nanosleep(128);
+      kind = f.posted[1 + (c % 64)];
+      if (kind != 1 && kind != 2) atomicOr(reinterpret_cast<unsigned long long*>(f.err), 2ull);
+    }
+    kind = __shfl_sync(0xffffffffu, kind, 0);
+    if (kind != 1) {
+      state = kCancelled;
+    } else {
+      for (int i = lane; i < f.npre; i += 32) st_release_sys(f.pre[i], 1);
+      bool ok = true;
+      for (int i = lane; i < f.npoll; i += 32) {
+        const bool got = wait_flag(f.polls[i], f.err);
+        if (got) *f.polls[i] = 0;
+        ok &= got;
+      }
+      state = __all_sync(0xffffffffu, ok) ? kGo : kTimedOut;
+    }
+    if (lane == 0) st_release_gpu(f.gate, base + state);
+  } else {
+    uint64_t v = 0;
+    if (lane == 0)
+      while ((v = ld_acquire_gpu(f.gate)) < base) __nanosleep(64);
+    v = __shfl_sync(0xffffffffu, v, 0);
+    state = static_cast<int>(v - base);
+  }
+  return state;
+}
 
 // Fused prologue, one full warp of a CTA (warp-level polling): the folded
 // gate if any, then CTA 0 writes the folded start signals, then lane i waits
@@ -82,13 +105,13 @@ enum : int { kGo = 0, kTimedOut = 1, kCancelled = 2 };
 //             word makes the world's failure sticky;
 //  kCancelled a cancelled prelaunch instance: no data, no signals.
 // When a skip word is set (a gate_poll kernel ran first) it decides instead.
-__device__ __forceinline__ int fused_wait(const FlagSet& f, uint64_t* post_no) {
+__device__ __forceinline__ int fused_wait(const FlagSet& f) {
   const int lane = threadIdx.x & 31;
   if (f.skip) {
     const uint64_t sk = *reinterpret_cast<const volatile uint64_t*>(f.skip);
     return sk == 0 ? kGo : sk == 1 ? kCancelled : kTimedOut;
   }
-  if (f.posted && !folded_gate(f, post_no)) return kCancelled;
+  if (f.posted) return folded_gate(f);
   if (blockIdx.x == 0)
     for (int i = lane; i < f.npre; i += 32) st_release_sys(f.pre[i], 1);
   bool ok = true;
@@ -107,7 +130,7 @@ __device__ __forceinline__ int fused_wait(const FlagSet& f, uint64_t* post_no) {
 // cost several microseconds each when every CTA issues them). `state` is
 // the CTA's fused_wait result: the last CTA resets the polls only if every
 // CTA passed them, and signals unless the instance was cancelled.
-__device__ __forceinline__ void fused_finish(const FlagSet& f, int state, uint64_t post_no) {
+__device__ __forceinline__ void fused_finish(const FlagSet& f, int state) {
   if (f.nsig && state == kGo) asm volatile("fence.acq_rel.sys;" ::: "memory");
   unsigned ticket;
   // tickets count up by 1 per CTA; a CTA whose poll timed out adds 1 << 20
@@ -116,11 +139,11 @@ __device__ __forceinline__ void fused_finish(const FlagSet& f, int state, uint64
   asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(ticket) : "l"(f.ctr), "r"(add) : "memory");
   if ((ticket & 0xFFFFFu) != gridDim.x - 1) return;
   *f.ctr = 0;
-  if (f.consumed) *f.consumed = post_no + 1;  // folded gate: the post is taken
-  if (state == kCancelled) return;            // uniform: every CTA read the same gate / skip word
+  if (state == kCancelled) return;  // uniform: every CTA read the same gate / skip word
   // Every CTA passed its polls before taking its ticket: reset them for the
-  // next collective (its writers only write again after our signals).
-  if (state == kGo && (ticket >> 20) == 0)
+  // next collective (its writers only write again after our signals). A
+  // folded gate has reset them already.
+  if (state == kGo && (ticket >> 20) == 0 && !f.posted)
     for (int i = 0; i < f.npoll; ++i) *f.polls[i] = 0;
   for (int i = 0; i < f.nsig; ++i) st_release_sys(f.sigs[i], 1);
 }

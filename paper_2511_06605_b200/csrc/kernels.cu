@@ -165,9 +165,8 @@ __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
   __shared__ int first[kMaxItemsSmem];
   __shared__ int cta_state;
   for (int i = threadIdx.x; i < nitems; i += kRegThreads) first[i] = items[i].first_tile;
-  uint64_t post_no = 0;
   if (threadIdx.x < 32) {
-    const int st = (flags.npoll || flags.npre || flags.posted || flags.skip) ? fused_wait(flags, &post_no) : kGo;
+    const int st = (flags.npoll || flags.npre || flags.posted || flags.skip) ? fused_wait(flags) : kGo;
     if (threadIdx.x == 0) cta_state = st;
   }
   __syncthreads();
@@ -183,7 +182,7 @@ __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
   }
   if (flags.ctr) {
     __syncthreads();  // every thread's stores (peer stores over NVLink included) precede thread 0's fence
-    if (threadIdx.x == 0) fused_finish(flags, state, post_no);
+    if (threadIdx.x == 0) fused_finish(flags, state);
   }
 }
 
@@ -206,12 +205,11 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
   __shared__ int first[kMaxItemsSmem];
   for (int i = threadIdx.x; i < nitems; i += 32) first[i] = items[i].first_tile;
   __syncwarp();
-  uint64_t post_no = 0;
   // the CTA is one warp: fused_wait's result is already warp-uniform
-  const int state = (flags.npoll || flags.npre || flags.posted || flags.skip) ? fused_wait(flags, &post_no) : kGo;
+  const int state = (flags.npoll || flags.npre || flags.posted || flags.skip) ? fused_wait(flags) : kGo;
   if (threadIdx.x != 0) return;
   if (state != kGo) {
-    if (flags.ctr) fused_finish(flags, state, post_no);
+    if (flags.ctr) fused_finish(flags, state);
     return;
   }
   for (int i = 0; i < kTmaStages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[i])));
@@ -295,7 +293,7 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
     // The bulk stores are complete; order them (async proxy) before the
     // generic-proxy fence and ticket that publish them.
     asm volatile("fence.proxy.async.global;" ::: "memory");
-    fused_finish(flags, kGo, post_no);
+    fused_finish(flags, kGo);
   }
 }
 

@@ -107,18 +107,20 @@ struct FlagSet {
   int nsig = 0;
   unsigned* ctr = nullptr;
   uint64_t* err = nullptr;
-  // Non-null: the kernel does nothing when *skip != 0 (a cancelled
-  // prelaunch instance; written by the gate kernel before it).
+  // Non-null: written by a gate_poll kernel before the mover — 0 move, 1 a
+  // cancelled prelaunch instance (no data, no signals), 2 a poll timed out
+  // (no data, signals still written).
   const uint64_t* skip = nullptr;
   // Folded prelaunch gate (a single-kernel prelaunch body):
   // non-null `posted` (pinned host: [0] post count, [1 + k % 64] kind of post
-  // k) makes the kernel itself the gate. Thread 0 of CTA 0 waits for the
-  // next post (number *consumed), publishes its kind in *gate (device word:
-  // (post number + 1) * 2 + go) for the other CTAs, and a "cancel" post makes
-  // every CTA skip its polls, data and signals. The last CTA advances
-  // *consumed. Requires ctr (the finish ticket).
+  // k) makes the kernel itself the gate for post number `post_no` (set per
+  // instance when it is armed: instance i consumes post i). CTA 0 waits for
+  // the post, writes the start signals, polls and resets the flags, and
+  // publishes the outcome in *gate (device word: (post_no + 1) * 4 + state)
+  // for the other CTAs; a "cancel" post makes every CTA skip data and
+  // signals. No finish ticket unless there are signals.
   volatile uint64_t* posted = nullptr;
-  uint64_t* consumed = nullptr;
+  uint64_t post_no = 0;
   uint64_t* gate = nullptr;
 };
 

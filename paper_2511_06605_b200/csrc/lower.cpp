@@ -828,8 +828,10 @@ int fold_grid(World* w, const Plan* p, const Unit& u) {
     const char* e = std::getenv("CECOLL_FOLD_MAX_TILES_PER_CTA");
     return e ? std::atoi(e) : 4;
   }();
-  const char* off = std::getenv("CECOLL_PRELAUNCH_FOLD");
-  if ((off && std::string(off) == "0") || max_ctas <= 0) return 0;
+  // Off by default: measured slower than gate_poll -> mover on one B200
+  // (profiles/prelaunch_fold_ab_r02.csv); CECOLL_PRELAUNCH_FOLD=1 enables.
+  const char* on = std::getenv("CECOLL_PRELAUNCH_FOLD");
+  if (!(on && std::string(on) == "1") || max_ctas <= 0) return 0;
   int units_here = 0;
   for (const Unit& v : p->units) units_here += v.device == u.device;
   (void)w;
@@ -917,15 +919,17 @@ Status build_graph(World* w, Plan* p, Unit& u) {
     f.err = u.err;
     const int fg = fold_grid(w, p, u);
     if (fg > 0) {
-      // One kernel: gate, polls (ready word + rdy), move, signals.
+      // One kernel: gate, polls (ready word + rdy), move, signals. Its post
+      // number is set per instance at arm time (exec.cpp arm_unit).
       f.posted = posted_dev;
-      f.consumed = u.consumed;
       f.gate = words + 4;
       f.polls = u.poll_tab;
       f.npoll = u.npoll;
-      f.ctr = reinterpret_cast<unsigned*>(words + 2);
+      f.ctr = u.nsig ? reinterpret_cast<unsigned*>(words + 2) : nullptr;
       p->folded = true;
-      STATUS_TRY(sink.kernel(w, u.arm, items_call(u.table, fg, &f)));
+      u.fold_call = items_call(u.table, fg, &f);
+      STATUS_TRY(sink.kernel(w, u.arm, u.fold_call));
+      u.fold_node = sink.tail(u.arm).front();
     } else {
       // The mover never spins here (gate_poll did the waiting), so it keeps a
       // full grid without holding SMs while armed.

@@ -24,6 +24,9 @@ struct B200Model {
   double bw_fan = 5.9e12;   // SM mover, fan / broadcast items (write-bound)
   double bw_ce = 6.0e12;    // driver memcpy nodes (device-local copies run on SMs on one GPU)
   double bw_lanes = 6.3e12; // one item kernel per lane, running concurrently (chunks >= 4 MiB)
+  double bw_swap = 6.3e12;  // in-place swap items in one register-mover kernel (merged / prelaunch)
+  double l2_boost = 1.3;    // every bandwidth, when the collective's buffers fit in L2
+  double l2_bytes = 96.0 * (1 << 20);  // that footprint (126 MB L2, fixed, not fitted)
   double folded_max_bytes = 8.0 * (1 << 20);  // prelaunch bodies up to this traffic are one folded kernel
   double prelaunch_gain_threshold = 0.002;    // winner_grid's tie-break (cost_model.hpp:30)
 };

@@ -63,9 +63,8 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const RedItem* __re
   for (int i = threadIdx.x; i < nitems; i += kRedThreads) first[i] = items[i].first_tile;
   // Fused flags (kernels.hpp FlagSet): every source rank's send is ready.
   __shared__ int cta_state;
-  uint64_t post_no = 0;
   if (threadIdx.x < 32) {
-    const int st = (flags.npoll || flags.npre || flags.posted || flags.skip) ? fused_wait(flags, &post_no) : kGo;
+    const int st = (flags.npoll || flags.npre || flags.posted || flags.skip) ? fused_wait(flags) : kGo;
     if (threadIdx.x == 0) cta_state = st;
   }
   __syncthreads();
@@ -120,7 +119,7 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const RedItem* __re
   }
   if (flags.ctr) {  // every source read: tell the source ranks (last CTA)
     __syncthreads();
-    if (threadIdx.x == 0) fused_finish(flags, state, post_no);
+    if (threadIdx.x == 0) fused_finish(flags, state);
   }
 }
 

@@ -207,6 +207,12 @@ struct Unit {
   uint64_t* ready_flag = nullptr;  // device word the caller stream writes
   bool armed = false;
   uint64_t posts = 0;
+  // Folded prelaunch body (lower.cpp fold): the single kernel node and its
+  // launch descriptor; each armed instance gets the number of the post it
+  // consumes (instance i consumes post i) through its kernel parameters.
+  cudaGraphNode_t fold_node = nullptr;
+  KernelCall fold_call;
+  uint64_t instances = 0;
   // Recorded command list of a non-prelaunch plan (exec.cpp record_plan):
   // the unit's whole submission (flags, lanes, copies, kernels) as one graph.
   cudaGraph_t rec_graph = nullptr;

@@ -49,18 +49,34 @@ def test_copy_engine_plans_record_from_the_second_launch(comms, impl):
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("impl,s,folded", [("prelaunch_b2b", 4096, True), ("prelaunch_swap", 4096, True),
-                                           ("prelaunch_pcpy", 8 << 20, False)])
-def test_prelaunch_plans_report_their_body(comms, impl, s, folded):
+@pytest.mark.parametrize("fold", ["0", "1"])
+@pytest.mark.parametrize("impl,s,small", [("prelaunch_b2b", 4096, True), ("prelaunch_swap", 4096, True),
+                                          ("prelaunch_pcpy", 8 << 20, False)])
+def test_prelaunch_plans_report_their_body(comms, impl, s, small, fold, monkeypatch):
+    """The folded single-kernel body is opt-in (CECOLL_PRELAUNCH_FOLD=1) and
+    only for small collectives; every launch is byte-checked, three times
+    (instances consume posts 0, 1, 2 through their kernel parameters)."""
+    monkeypatch.setenv("CECOLL_PRELAUNCH_FOLD", fold)
     sends, recvs = _bufs(s)
     if impl.endswith("swap"):
         recvs = sends
     plan = cc.Plan(comms, "alltoall", sends, recvs, s, impl=impl)
     info = plan.info()
     assert info["prelaunch"] and info["graph_fallback"] == ""
-    assert info["prelaunch_folded"] == folded, info
-    plan.launch(torch.cuda.current_stream())
-    torch.cuda.current_stream().synchronize()
+    assert info["prelaunch_folded"] == (small and fold == "1"), info
+    st = torch.cuda.current_stream()
+    # Results are compared on the host: while the next instance is armed, a
+    # torch kernel launched for the first time in the process would wait
+    # behind the armed gate for its lazy module load (DESIGN.md §3.2).
+    host_sends = [t.cpu() for t in sends]
+    for it in range(3):
+        want = None
+        if not impl.endswith("swap"):
+            want = [torch.cat([host_sends[j][r * s:(r + 1) * s] for j in range(N)]) for r in range(N)]
+        plan.launch(st)
+        st.synchronize()  # the next instance is armed: no device-wide sync
+        if want is not None:
+            assert all(torch.equal(a.cpu(), b) for a, b in zip(recvs, want)), (impl, it)
     plan.destroy()
     torch.cuda.synchronize()
 

@@ -27,8 +27,8 @@ import paper_2511_06605_b200 as cc  # noqa: E402
 
 MODEL_IMPLS = {"sm", "pcpy", "b2b", "bcst", "swap", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_bcst",
                "prelaunch_swap"}
-DEFAULT_LATENCY = ["profiles/latency_r02_n8.csv", "profiles/latency_r01_n2_final.csv"]
-DEFAULT_SWEEP = ["profiles/sweep_r01_plan_n8_final.csv", "profiles/sweep_r01_plan_n4.csv",
+DEFAULT_LATENCY = ["profiles/latency_r02_n8.csv", "profiles/latency_r02_n2.csv"]
+DEFAULT_SWEEP = ["profiles/sweep_r02_plan_n8.csv", "profiles/sweep_r01_plan_n4.csv",
                  "profiles/sweep_r01_plan_n2_final.csv"]
 SWEEP_MIN = 4 << 20
 
@@ -98,7 +98,7 @@ def main():
     ap.add_argument("--latency", nargs="*", default=DEFAULT_LATENCY)
     ap.add_argument("--sweep", nargs="*", default=DEFAULT_SWEEP)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--iterations", type=int, default=3000)
+    ap.add_argument("--iterations", type=int, default=20000)
     args = ap.parse_args()
     rows, sources = load_rows(args.latency, args.sweep)
     default = cc.Model()
