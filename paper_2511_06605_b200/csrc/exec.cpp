@@ -289,8 +289,16 @@ bool graph_eligible(World* w, Plan* p) {
   }();
   if (off || p->prelaunch) return false;
   // A submission of exactly one kernel launch (the SM path with one unit and
-  // no flags) gains nothing from a graph.
-  if (p->sm && !p->hybrid && p->units.size() == 1) {
+  // no flags) is recorded too: on the round-2 boxes a one-node graph launch
+  // costs the host 1.3 µs against 3-5 µs for the direct launch
+  // (profiles/latency_r02_n8.csv: swap's recorded single kernel vs sm), and
+  // back-to-back small collectives are host-bound. CECOLL_RECORD_SINGLE=0
+  // keeps such plans on direct launches.
+  static const bool single_off = [] {
+    const char* e = std::getenv("CECOLL_RECORD_SINGLE");
+    return e && std::string(e) == "0";
+  }();
+  if (single_off && p->sm && !p->hybrid && p->units.size() == 1) {
     const Unit& u = p->units[0];
     if (u.start.empty() && u.start_remote.empty() && u.sm_pre.empty() && u.sm_post.empty() &&
         u.sm_post_remote.empty() && u.finish.empty())

@@ -25,13 +25,18 @@ def _bufs(s, kind="alltoall"):
             [torch.zeros(N * s, dtype=torch.uint8, device="cuda") for _ in range(N)])
 
 
-def test_single_unit_sm_is_one_kernel_not_recorded(comms):
+def test_single_unit_sm_is_one_kernel_recorded(comms):
+    """One kernel per collective, replayed as a one-node graph from the second
+    launch (cheaper on the host than a direct launch, exec.cpp graph_eligible)."""
     sends, recvs = _bufs(4096)
     st = torch.cuda.Stream()
+    c0 = comms[0].counters()
     for _ in range(3):
         cc.all_to_all(comms, sends, recvs, 4096, impl="sm", streams=st)
+    c1 = comms[0].counters()
     info = comms[0].last_plan_info()
-    assert info["impl"] == "sm" and not info["recorded"] and info["record_note"] == ""
+    assert info["impl"] == "sm" and info["recorded"] and info["record_note"] == ""
+    assert c1["kernels"] - c0["kernels"] == 3 and c1["recorded_launches"] - c0["recorded_launches"] == 2
     assert len(info["units"]) == 1 and info["units"][0]["mover"] in ("tma", "reg")
     assert info["units"][0]["ranks"] == list(range(N))
     torch.cuda.synchronize()

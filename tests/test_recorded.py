@@ -56,8 +56,8 @@ def test_eager_calls_replay_recorded_lists(kind, impl, n):
             assert O.check(kind, s, n, in_place, host, res) == -1, (kind, impl, it)
         c1 = comms[0].counters()
         # first call eager, calls 2..5 replay one recorded graph (one unit);
-        # the one-unit SM path is a single kernel launch and is not recorded
-        assert c1["recorded_launches"] - c0["recorded_launches"] == (0 if impl == "sm" else 4)
+        # the one-unit SM path too (a one-node graph)
+        assert c1["recorded_launches"] - c0["recorded_launches"] == 4
         assert c1["collectives"] - c0["collectives"] == 5
     finally:
         torch.cuda.synchronize()
