@@ -192,13 +192,21 @@ Status run_sm(World* w, Plan* p, Sink& sink) {
   return {};
 }
 
-Status post_gate(Unit& u, uint64_t kind) {
-  const uint64_t k = u.posts++;
-  volatile uint64_t* posted = u.posted;
-  posted[1 + (k % 64)] = kind;
-  __atomic_thread_fence(__ATOMIC_SEQ_CST);
-  posted[0] = k + 1;
-  __atomic_thread_fence(__ATOMIC_SEQ_CST);
+// Cancels a unit's armed instance: writes "cancel" (2) into its trigger word
+// from a private stream (the caller's stream may be anywhere; the arm stream
+// is held by the spinning gate), then waits for the instance to finish — its
+// gate takes the word and skips the body.
+Status cancel_armed(World* w, Unit& u) {
+  cudaStream_t s = nullptr;
+  CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  Status st = submit(w, s, MemOps{op_write(u.ready_flag, 2)});
+  if (st.ok()) {
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) st = cuda_fail(e, "cancel write", __FILE__, __LINE__);
+  }
+  cudaStreamDestroy(s);
+  STATUS_TRY(st);
+  CUDA_TRY(cudaStreamSynchronize(u.arm));
   return {};
 }
 
@@ -241,8 +249,9 @@ Status arm_unit(World* w, Unit& u) {
   return {};
 }
 
-// Trigger phase 1 (signals): the unit's start / ready writes and the host
-// post that opens its armed graph.
+// Trigger phase 1 (signals): the unit's start signals and its trigger word
+// (ready = 1), written by the caller stream: the armed graph's gate opens when
+// the caller stream reaches this point (stream-ordered behind the producer).
 Status trigger_signal(World* w, Unit& u, cudaEvent_t* span_begin) {
   DeviceGuard g(u.device);
   StreamSink sink;
@@ -254,7 +263,6 @@ Status trigger_signal(World* w, Unit& u, cudaEvent_t* span_begin) {
   *span_begin = trace_mark(w, u.device, u.stream);
   STATUS_TRY(submit_traced(w, sink, u.stream, ops, u.start_remote_tab, u.start_remote.size(), "trigger:signal",
                            u.device, pid, -1));
-  STATUS_TRY(post_gate(u, 1));
   set_armed(u, false);
   trace_host_span(w, "trigger", h0);
   return {};
@@ -461,8 +469,7 @@ Status plan_disarm(World* w, Plan* p) {
   for (Unit& u : p->units) {
     if (!u.armed) continue;
     DeviceGuard g(u.device);
-    STATUS_TRY(post_gate(u, 2));
-    CUDA_TRY(cudaStreamSynchronize(u.arm));
+    STATUS_TRY(cancel_armed(w, u));
     set_armed(u, false);
   }
   return {};
@@ -563,8 +570,8 @@ Status plan_destroy(World* w, Plan* p) {
   for (Unit& u : p->units) {
     DeviceGuard g(u.device);
     if (u.armed) {
-      post_gate(u, 2);  // cancel: the gate skips the body
-      cudaStreamSynchronize(u.arm);
+      const Status c = cancel_armed(w, u);  // the gate skips the body
+      if (!c.ok() && result.ok()) result = c;
       set_armed(u, false);
     }
     if (u.err) {  // kernel-side polls report timeouts here (kernels.cu poll_kernel)
@@ -581,12 +588,10 @@ Status plan_destroy(World* w, Plan* p) {
       cudaStreamDestroy(u.arm);
     }
     if (u.graph_done) cudaEventDestroy(u.graph_done);
-    if (u.posted) cudaFreeHost(u.posted);
     u.exec = nullptr;
     u.graph = nullptr;
     u.arm = nullptr;
     u.graph_done = nullptr;
-    u.posted = nullptr;
     u.err = nullptr;
   }
   for (size_t i = 0; i < p->dev_allocs.size(); ++i) {

@@ -48,33 +48,45 @@ __device__ __forceinline__ bool wait_flag(const uint64_t* p, uint64_t* err) {
 // What a CTA may do after its prologue.
 enum : int { kGo = 0, kTimedOut = 1, kCancelled = 2 };
 
-// Folded prelaunch gate (FlagSet::posted, one full warp of every CTA). CTA 0
-// alone takes host post number f.post_no (one PCIe poller), writes the folded
-// start signals, polls the flags (one set of system-scope pollers) and resets
+// The trigger word of a prelaunch unit (its ready slot): the caller stream
+// writes 1 ("go") when it triggers the unit; a cancel writes 2 from a private
+// stream (exec.cpp cancel_armed). No bound: an armed instance waits as long
+// as its caller leaves it armed. The word is taken by resetting it to 0 (the
+// next trigger is only written after this instance completes). Polling device
+// memory keeps PCIe reads of host memory off the trigger's critical path
+// (round 1's gate read a host post first: ~2 us of every prelaunch
+// collective, tools/prelaunch_probe.cu).
+__device__ __forceinline__ uint64_t take_trigger(uint64_t* p, uint64_t* err) {
+  uint64_t v;
+  while ((v = ld_acquire_sys(p)) == 0) __nanosleep(32);
+  *p = 0;
+  if (v != 1 && v != 2) atomicOr(reinterpret_cast<unsigned long long*>(err), 2ull);
+  return v;
+}
+
+// Folded prelaunch gate (FlagSet::fold, one full warp of every CTA). CTA 0
+// alone takes the unit's trigger word (f.polls[0]), writes the folded start
+// signals, polls the other flags (one set of system-scope pollers) and resets
 // them — their writers only write again after this instance completes or
 // signals — then publishes the outcome in the device word *gate =
-// (post_no + 1) * 4 + state; every other CTA waits for that word (device
-// scope). CTA 0's system-scope acquire of the flags followed by its release of
-// the gate word orders the flag writers' data before every CTA's accesses.
+// (post_no + 1) * 4 + state, post_no being the instance's number (set when it
+// is armed); every other CTA waits for that word (device scope). CTA 0's
+// system-scope acquire of the flags followed by its release of the gate word
+// orders the flag writers' data before every CTA's accesses.
 __device__ __forceinline__ int folded_gate(const FlagSet& f) {
   const int lane = threadIdx.x & 31;
-  const uint64_t c = f.post_no;
-  const uint64_t base = (c + 1) * 4;
+  const uint64_t base = (f.post_no + 1) * 4;
   int state;
   if (blockIdx.x == 0) {
     uint64_t kind = 0;
-    if (lane == 0) {
-      while (f.posted[0] <= c) __nanosleep(128);
-      kind = f.posted[1 + (c % 64)];
-      if (kind != 1 && kind != 2) atomicOr(reinterpret_cast<unsigned long long*>(f.err), 2ull);
-    }
+    if (lane == 0) kind = take_trigger(f.polls[0], f.err);
     kind = __shfl_sync(0xffffffffu, kind, 0);
     if (kind != 1) {
       state = kCancelled;
     } else {
       for (int i = lane; i < f.npre; i += 32) st_release_sys(f.pre[i], 1);
       bool ok = true;
-      for (int i = lane; i < f.npoll; i += 32) {
+      for (int i = 1 + lane; i < f.npoll; i += 32) {
         const bool got = wait_flag(f.polls[i], f.err);
         if (got) *f.polls[i] = 0;
         ok &= got;
@@ -111,7 +123,7 @@ __device__ __forceinline__ int fused_wait(const FlagSet& f) {
     const uint64_t sk = *reinterpret_cast<const volatile uint64_t*>(f.skip);
     return sk == 0 ? kGo : sk == 1 ? kCancelled : kTimedOut;
   }
-  if (f.posted) return folded_gate(f);
+  if (f.fold) return folded_gate(f);
   if (blockIdx.x == 0)
     for (int i = lane; i < f.npre; i += 32) st_release_sys(f.pre[i], 1);
   bool ok = true;
@@ -143,7 +155,7 @@ __device__ __forceinline__ void fused_finish(const FlagSet& f, int state) {
   // Every CTA passed its polls before taking its ticket: reset them for the
   // next collective (its writers only write again after our signals). A
   // folded gate has reset them already.
-  if (state == kGo && (ticket >> 20) == 0 && !f.posted)
+  if (state == kGo && (ticket >> 20) == 0 && !f.fold)
     for (int i = 0; i < f.npoll; ++i) *f.polls[i] = 0;
   for (int i = 0; i < f.nsig; ++i) st_release_sys(f.sigs[i], 1);
 }

@@ -51,6 +51,14 @@ CUstreamBatchMemOpParams op_wait(uint64_t* addr, uint64_t v);
 void add_poll(MemOps& ops, uint64_t* addr);
 // cuStreamBatchMemOp in batches of at most 255 operations.
 Status submit(World* w, cudaStream_t s, const MemOps& ops);
+// Writes a plan table (src, or zeros when src is null) into device memory of
+// the current device and returns once the bytes have landed: on a private
+// per-device stream, synchronised. Plain cudaMemcpy from pageable memory may
+// return before its DMA completes and cudaMemset is asynchronous, both on the
+// legacy stream that the callers' non-blocking streams do not wait for — a
+// plan's first kernel could read the table before it is written (seen once
+// in eight fresh two-process runs, tools/pull_race_probe.py).
+Status write_device(void* dst, const void* src, size_t bytes);
 // Copy commands: one cuMemcpyBatchAsync (allow_batch, non-legacy stream) or
 // one cudaMemcpyAsync per copy.
 Status issue_copies(World* w, const std::vector<Copy>& copies, cudaStream_t s, bool allow_batch);

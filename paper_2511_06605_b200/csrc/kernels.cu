@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
   __shared__ int cta_state;
   for (int i = threadIdx.x; i < nitems; i += kRegThreads) first[i] = items[i].first_tile;
   if (threadIdx.x < 32) {
-    const int st = (flags.npoll || flags.npre || flags.posted || flags.skip) ? fused_wait(flags) : kGo;
+    const int st = (flags.npoll || flags.npre || flags.fold || flags.skip) ? fused_wait(flags) : kGo;
     if (threadIdx.x == 0) cta_state = st;
   }
   __syncthreads();
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
   for (int i = threadIdx.x; i < nitems; i += 32) first[i] = items[i].first_tile;
   __syncwarp();
   // the CTA is one warp: fused_wait's result is already warp-uniform
-  const int state = (flags.npoll || flags.npre || flags.posted || flags.skip) ? fused_wait(flags) : kGo;
+  const int state = (flags.npoll || flags.npre || flags.fold || flags.skip) ? fused_wait(flags) : kGo;
   if (threadIdx.x != 0) return;
   if (state != kGo) {
     if (flags.ctr) fused_finish(flags, state);
@@ -323,42 +323,27 @@ __global__ void signal_kernel(uint64_t* const* flags, int n) {
   st_release_sys(flags[i], 1);
 }
 
-// Gate of a recorded prelaunch graph. The host posts triggers/cancels into
-// pinned memory: posted[0] is a monotonic count, posted[1 + k % 64] the kind
-// of post k (1 = go, 2 = cancel). `consumed` (device memory) counts the posts
-// already taken by earlier instances; instances run one at a time on the arm
-// stream, so the read-modify-write needs no atomics.
-__global__ void gate_kernel(volatile uint64_t* posted, uint64_t* consumed, cudaGraphConditionalHandle handle,
-                            uint64_t* err) {
+// Gate of a recorded prelaunch graph with a conditional body: takes the
+// unit's trigger word (take_trigger, flags.cuh) and opens the body on "go".
+__global__ void gate_kernel(uint64_t* trigger, cudaGraphConditionalHandle handle, uint64_t* err) {
   if (threadIdx.x != 0) return;
-  const uint64_t c = *consumed;
-  while (posted[0] <= c) __nanosleep(256);
-  const uint64_t kind = posted[1 + (c % 64)];
-  *consumed = c + 1;
-  __threadfence_system();
-  if (kind != 1 && kind != 2) atomicOr(reinterpret_cast<unsigned long long*>(err), 2ull);
+  const uint64_t kind = take_trigger(trigger, err);
   cudaGraphSetConditional(handle, kind == 1 ? 1u : 0u);
 }
 
-__global__ void gate_poll_kernel(volatile uint64_t* posted, uint64_t* consumed, uint64_t* const* flags, int n,
-                                 uint64_t* skip, uint64_t* err) {
-  // Lane 0 takes the host post; on "go" the warp polls the flags in
-  // parallel (lane i: flags i, i+32, ...) and resets them.
+__global__ void gate_poll_kernel(uint64_t* const* flags, int n, uint64_t* skip, uint64_t* err) {
+  // flags[0] is the unit's trigger word: lane 0 takes it; on "go" the warp
+  // polls the other flags in parallel (lane i: flags 1+i, 33+i, ...) and
+  // resets them.
   __shared__ uint64_t kind;
-  if (threadIdx.x == 0) {
-    const uint64_t c = *consumed;
-    while (posted[0] <= c) __nanosleep(256);
-    kind = posted[1 + (c % 64)];
-    *consumed = c + 1;
-    if (kind != 1 && kind != 2) atomicOr(reinterpret_cast<unsigned long long*>(err), 2ull);
-  }
+  if (threadIdx.x == 0) kind = take_trigger(flags[0], err);
   __syncwarp();
   if (kind != 1) {
     if (threadIdx.x == 0) *skip = 1;
     return;
   }
   bool ok = true;
-  for (int i = threadIdx.x; i < n; i += 32) {
+  for (int i = 1 + threadIdx.x; i < n; i += 32) {
     if (wait_flag(flags[i], err)) *flags[i] = 0;
     else ok = false;
   }
@@ -517,24 +502,20 @@ KernelCall signal_call(uint64_t* const* flags, int n) {
   return k;
 }
 
-KernelCall gate_call(volatile uint64_t* posted, uint64_t* consumed, cudaGraphConditionalHandle handle, uint64_t* err) {
+KernelCall gate_call(uint64_t* trigger, cudaGraphConditionalHandle handle, uint64_t* err) {
   KernelCall k;
   k.func = reinterpret_cast<const void*>(gate_kernel);
   k.block = dim3(32);
-  k.push(posted);
-  k.push(consumed);
+  k.push(trigger);
   k.push(handle);
   k.push(err);
   return k;
 }
 
-KernelCall gate_poll_call(volatile uint64_t* posted, uint64_t* consumed, uint64_t* const* flags, int n, uint64_t* skip,
-                          uint64_t* err) {
+KernelCall gate_poll_call(uint64_t* const* flags, int n, uint64_t* skip, uint64_t* err) {
   KernelCall k;
   k.func = reinterpret_cast<const void*>(gate_poll_kernel);
   k.block = dim3(32);
-  k.push(posted);
-  k.push(consumed);
   k.push(flags);
   k.push(n);
   k.push(skip);
@@ -548,16 +529,6 @@ cudaError_t launch_poll(uint64_t* const* flags, int n, uint64_t* err, cudaStream
 
 cudaError_t launch_signal(uint64_t* const* flags, int n, cudaStream_t stream) {
   return launch(signal_call(flags, n), stream);
-}
-
-cudaError_t launch_gate_poll(volatile uint64_t* posted, uint64_t* consumed, uint64_t* const* flags, int n,
-                             uint64_t* skip, uint64_t* err, cudaStream_t stream) {
-  return launch(gate_poll_call(posted, consumed, flags, n, skip, err), stream);
-}
-
-cudaError_t launch_gate(volatile uint64_t* posted, uint64_t* consumed, cudaGraphConditionalHandle handle,
-                        uint64_t* err, cudaStream_t stream) {
-  return launch(gate_call(posted, consumed, handle, err), stream);
 }
 
 // Loads every kernel of this file on the current device (and sets the TMA

@@ -91,7 +91,7 @@ Status upload_items(Plan* p, int device, std::vector<HostItem>& host, ItemTable*
     for (const HostItem& h : host) flat.insert(flat.end(), h.fan.begin(), h.fan.end());
     void* d = nullptr;
     CUDA_TRY(cudaMalloc(&d, sizeof(char*) * flat.size()));
-    CUDA_TRY(cudaMemcpy(d, flat.data(), sizeof(char*) * flat.size(), cudaMemcpyHostToDevice));
+    STATUS_TRY(write_device(d, flat.data(), sizeof(char*) * flat.size()));
     p->dev_allocs.push_back(d);
     p->dev_alloc_device.push_back(device);
     fan_dev = static_cast<char**>(d);
@@ -114,7 +114,7 @@ Status upload_items(Plan* p, int device, std::vector<HostItem>& host, ItemTable*
   if (tiles > INT32_MAX) return fail(CECOLL_INVALID_ARGUMENT, "collective too large for one launch");
   void* d = nullptr;
   CUDA_TRY(cudaMalloc(&d, sizeof(Item) * items.size()));
-  CUDA_TRY(cudaMemcpy(d, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice));
+  STATUS_TRY(write_device(d, items.data(), sizeof(Item) * items.size()));
   p->dev_allocs.push_back(d);
   p->dev_alloc_device.push_back(device);
   out->items = static_cast<Item*>(d);
@@ -129,7 +129,7 @@ Status upload_ptrs(Plan* p, int device, const std::vector<uint64_t*>& ptrs, uint
   DeviceGuard g(device);
   void* d = nullptr;
   CUDA_TRY(cudaMalloc(&d, sizeof(uint64_t*) * ptrs.size()));
-  CUDA_TRY(cudaMemcpy(d, ptrs.data(), sizeof(uint64_t*) * ptrs.size(), cudaMemcpyHostToDevice));
+  STATUS_TRY(write_device(d, ptrs.data(), sizeof(uint64_t*) * ptrs.size()));
   p->dev_allocs.push_back(d);
   p->dev_alloc_device.push_back(device);
   *out = static_cast<uint64_t**>(d);
@@ -208,7 +208,7 @@ Status alloc_fused_words(Plan* p, int device, uint64_t** err, unsigned** ctr) {
   DeviceGuard g(device);
   void* d = nullptr;
   CUDA_TRY(cudaMalloc(&d, 64));
-  CUDA_TRY(cudaMemset(d, 0, 64));
+  STATUS_TRY(write_device(d, nullptr, 64));
   p->dev_allocs.push_back(d);
   p->dev_alloc_device.push_back(device);
   *err = static_cast<uint64_t*>(d);
@@ -681,7 +681,7 @@ Status upload_red(Plan* p, int device, std::vector<RedItem>& items, const std::v
   for (const auto& v : srcs) flat.insert(flat.end(), v.begin(), v.end());
   void* d = nullptr;
   CUDA_TRY(cudaMalloc(&d, sizeof(char*) * flat.size()));
-  CUDA_TRY(cudaMemcpy(d, flat.data(), sizeof(char*) * flat.size(), cudaMemcpyHostToDevice));
+  STATUS_TRY(write_device(d, flat.data(), sizeof(char*) * flat.size()));
   p->dev_allocs.push_back(d);
   p->dev_alloc_device.push_back(device);
   int64_t tiles = 0;
@@ -695,7 +695,7 @@ Status upload_red(Plan* p, int device, std::vector<RedItem>& items, const std::v
   if (tiles > INT32_MAX) return fail(CECOLL_INVALID_ARGUMENT, "reduce-scatter too large for one launch");
   void* t = nullptr;
   CUDA_TRY(cudaMalloc(&t, sizeof(RedItem) * items.size()));
-  CUDA_TRY(cudaMemcpy(t, items.data(), sizeof(RedItem) * items.size(), cudaMemcpyHostToDevice));
+  STATUS_TRY(write_device(t, items.data(), sizeof(RedItem) * items.size()));
   p->dev_allocs.push_back(t);
   p->dev_alloc_device.push_back(device);
   out->items = static_cast<RedItem*>(t);
@@ -845,31 +845,29 @@ int fold_grid(World* w, const Plan* p, const Unit& u) {
 }  // namespace
 
 // Builds one unit's prelaunch graph explicitly (no stream capture; GraphSink):
-//  * kernel-only body, folded: one mover kernel that takes the host post
-//    itself (FlagSet::posted) — one kernel per collective;
+//  * kernel-only body, folded: one mover kernel that takes the trigger word
+//    itself (FlagSet::fold) — one kernel per collective;
 //  * kernel-only body: gate_poll kernel -> mover (done signals fused);
 //  * otherwise: gate kernel -> IF{ poll kernel -> lanes (memcpy nodes, item
 //    kernels) + placement -> signal kernel }.
+// Every form is triggered by the unit's trigger word (its ready slot), which
+// the caller stream writes; no host memory is read on the trigger path.
 Status build_graph(World* w, Plan* p, Unit& u) {
   DeviceGuard g(u.device);
   CUDA_TRY(cudaStreamCreateWithFlags(&u.arm, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&u.graph_done, cudaEventDisableTiming));
-  void* host = nullptr;
-  CUDA_TRY(cudaHostAlloc(&host, 4096, cudaHostAllocMapped | cudaHostAllocPortable));
-  std::memset(host, 0, 4096);
-  u.posted = static_cast<uint64_t*>(host);
   void* d = nullptr;
   CUDA_TRY(cudaMalloc(&d, 64));
-  CUDA_TRY(cudaMemset(d, 0, 64));
+  STATUS_TRY(write_device(d, nullptr, 64));
   p->dev_allocs.push_back(d);
   p->dev_alloc_device.push_back(u.device);
-  uint64_t* words = static_cast<uint64_t*>(d);  // [0] consumed [1] err [2] ticket [3] skip [4] gate
-  u.consumed = words;
+  uint64_t* words = static_cast<uint64_t*>(d);  // [0] trigger [1] err [2] ticket [3] skip [4] gate
   u.err = words + 1;
-  u.ready_flag = slot(w, u.ranks[0], kSlotReady);
+  u.ready_flag = words;
 
-  // Polls: the unit's own readiness word plus rdy from destinations in other
-  // units; signals: done to those destinations (from the lanes' memops).
+  // Polls: the unit's trigger word first (the gate takes it), then rdy from
+  // destinations in other units; signals: done to those destinations (from
+  // the lanes' memops).
   std::vector<uint64_t*> polls{u.ready_flag}, sigs, fins;
   for (const LaneExec& le : p->lanes) {
     if (std::find(u.ranks.begin(), u.ranks.end(), le.rank) == u.ranks.end()) continue;
@@ -886,9 +884,6 @@ Status build_graph(World* w, Plan* p, Unit& u) {
   STATUS_TRY(upload_ptrs(p, u.device, polls, &u.poll_tab));
   STATUS_TRY(upload_ptrs(p, u.device, sigs, &u.sig_tab));
   STATUS_TRY(upload_ptrs(p, u.device, fins, &u.fin_tab));
-
-  uint64_t* posted_dev = nullptr;
-  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&posted_dev), u.posted, 0));
 
   // Building the graph counts its commands in the world's counters; nothing
   // is submitted, so they are restored afterwards.
@@ -919,9 +914,9 @@ Status build_graph(World* w, Plan* p, Unit& u) {
     f.err = u.err;
     const int fg = fold_grid(w, p, u);
     if (fg > 0) {
-      // One kernel: gate, polls (ready word + rdy), move, signals. Its post
-      // number is set per instance at arm time (exec.cpp arm_unit).
-      f.posted = posted_dev;
+      // One kernel: gate (trigger word), polls (rdy), move, signals. Its
+      // instance number is set per instance at arm time (exec.cpp arm_unit).
+      f.fold = 1;
       f.gate = words + 4;
       f.polls = u.poll_tab;
       f.npoll = u.npoll;
@@ -935,7 +930,7 @@ Status build_graph(World* w, Plan* p, Unit& u) {
       // full grid without holding SMs while armed.
       f.ctr = u.nsig ? reinterpret_cast<unsigned*>(words + 2) : nullptr;
       f.skip = words + 3;
-      STATUS_TRY(sink.kernel(w, u.arm, gate_poll_call(posted_dev, u.consumed, u.poll_tab, u.npoll, words + 3, u.err)));
+      STATUS_TRY(sink.kernel(w, u.arm, gate_poll_call(u.poll_tab, u.npoll, words + 3, u.err)));
       STATUS_TRY(sink.kernel(w, u.arm, items_call(u.table, plan_grid(p, u.table), &f)));
     }
     CUDA_TRY(cudaGraphInstantiate(&u.exec, u.graph, 0));
@@ -946,7 +941,7 @@ Status build_graph(World* w, Plan* p, Unit& u) {
   cudaGraphConditionalHandle handle;
   CUDA_TRY(cudaGraphConditionalHandleCreate(&handle, u.graph, 0, cudaGraphCondAssignDefault));
   GraphSink top({u.graph});
-  STATUS_TRY(top.kernel(w, u.arm, gate_call(posted_dev, u.consumed, handle, u.err)));
+  STATUS_TRY(top.kernel(w, u.arm, gate_call(u.ready_flag, handle, u.err)));
 
   // cudaGraphNodeParams has no default constructor (union with non-trivial
   // members): zero-initialised raw storage, as the runtime expects.
@@ -966,7 +961,7 @@ Status build_graph(World* w, Plan* p, Unit& u) {
   // needs — measured as a deadlock with eight units on one GPU. Stream
   // memory operations are not allowed in conditional bodies, hence kernels.
   GraphSink sink({body});
-  STATUS_TRY(sink.kernel(w, u.arm, poll_call(u.poll_tab, u.npoll, u.err)));
+  STATUS_TRY(sink.kernel(w, u.arm, poll_call(u.poll_tab + 1, u.npoll - 1, u.err)));  // [0]: the gate's
   STATUS_TRY(sink.copies(w, u.placement, u.arm, false));
   const cudaEvent_t fork = w->local[u.ranks[0]]->start;  // an ordering key inside the graph
   STATUS_TRY(sink.record(w, fork, u.arm));

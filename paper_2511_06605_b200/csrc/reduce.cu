@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const RedItem* __re
   // Fused flags (kernels.hpp FlagSet): every source rank's send is ready.
   __shared__ int cta_state;
   if (threadIdx.x < 32) {
-    const int st = (flags.npoll || flags.npre || flags.posted || flags.skip) ? fused_wait(flags) : kGo;
+    const int st = (flags.npoll || flags.npre || flags.fold || flags.skip) ? fused_wait(flags) : kGo;
     if (threadIdx.x == 0) cta_state = st;
   }
   __syncthreads();

@@ -45,7 +45,6 @@ constexpr int kMaxLanes = 32;
 // Flag page layout (u64 slots).
 constexpr int kSlotRdy = 0;             // rdy[j], j < kMaxRanks
 constexpr int kSlotDone = kMaxRanks;    // done[i]
-constexpr int kSlotReady = 2 * kMaxRanks;  // unit-ready word of a prelaunch graph
 constexpr size_t kFlagBytes = 4096;
 
 // World::counters (exported by cecoll_comm_counters in this order).
@@ -197,19 +196,19 @@ struct Unit {
   cudaGraphExec_t exec = nullptr;
   cudaStream_t arm = nullptr;
   cudaEvent_t graph_done = nullptr;
-  uint64_t* posted = nullptr;      // pinned host: [0] count, [1..64] kinds
-  uint64_t* consumed = nullptr;    // device
   uint64_t* err = nullptr;         // device
   uint64_t** poll_tab = nullptr;   // device array of flag pointers
   uint64_t** sig_tab = nullptr;
   uint64_t** fin_tab = nullptr;
   int npoll = 0, nsig = 0, nfin = 0;
-  uint64_t* ready_flag = nullptr;  // device word the caller stream writes
+  // Trigger word (device memory owned by the plan, one per unit, so armed
+  // plans never share one): the caller stream writes 1 to trigger, a cancel
+  // writes 2 from a private stream; the gate takes it.
+  uint64_t* ready_flag = nullptr;
   bool armed = false;
-  uint64_t posts = 0;
   // Folded prelaunch body (lower.cpp fold): the single kernel node and its
-  // launch descriptor; each armed instance gets the number of the post it
-  // consumes (instance i consumes post i) through its kernel parameters.
+  // launch descriptor; each armed instance gets its instance number through
+  // its kernel parameters.
   cudaGraphNode_t fold_node = nullptr;
   KernelCall fold_call;
   uint64_t instances = 0;

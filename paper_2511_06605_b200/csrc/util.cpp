@@ -2,6 +2,8 @@
 // the executors.
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "internal.hpp"
 
@@ -74,6 +76,31 @@ Status submit(World* w, cudaStream_t s, const MemOps& ops) {
     }
     ++w->counters[kCtrApiCalls];
     i += count;
+  }
+  return {};
+}
+
+Status write_device(void* dst, const void* src, size_t bytes) {
+  if (!bytes) return {};
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> streams;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  cudaStream_t s = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = streams.find(dev);
+    if (it == streams.end()) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      streams[dev] = s;
+    } else {
+      s = it->second;
+    }
+    // one writer at a time per device stream (the synchronise below is
+    // per call)
+    if (src) CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    else CUDA_TRY(cudaMemsetAsync(dst, 0, bytes, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
   }
   return {};
 }
