@@ -276,8 +276,12 @@ def run_ours(args):
     graphs_per_step = (c1["graph_launches"] - c0["graph_launches"]) / args.steps
 
     # e2e: pinned host inputs -> HBM -> collective -> HBM -> pinned host results.
-    host_in = [torch.empty(n * s, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
-    host_out = [torch.empty(n * s, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
+    # Every rank's buffer is a row of one [n, n*s] tensor (host and device), so
+    # each direction of a step is ONE 512 MiB copy: one large DMA per direction
+    # runs the PCIe link closer to its duplex peak than eight 64 MiB copies
+    # (10.93 vs 11.36 ms, gpurun_out/pcie5 / pcie_probe4, profiles/pcie_r02.txt).
+    host_in_all = torch.empty((n, n * s), dtype=torch.uint8, pin_memory=True)
+    host_in = list(host_in_all.unbind(0))
     for h, d in zip(host_in, sends):
         h.copy_(d)
     # Pipeline fill (the first step's inputs) and drain (the last step's
@@ -286,8 +290,11 @@ def run_ours(args):
     # Two device buffer sets so that step k's device->host copy overlaps step
     # k+1's host->device copy (PCIe is full duplex); every step still copies
     # its inputs in and its results out inside the timed region.
-    sets = [(sends, recvs), ([torch.empty_like(t) for t in sends], [torch.empty_like(t) for t in recvs])]
-    host_outs = [host_out, [torch.empty(n * s, dtype=torch.uint8, pin_memory=True) for _ in range(n)]]
+    dev_sets = [(torch.empty((n, n * s), dtype=torch.uint8, device="cuda"),
+                 torch.empty((n, n * s), dtype=torch.uint8, device="cuda")) for _ in range(2)]
+    sets = [(list(a.unbind(0)), list(b.unbind(0))) for a, b in dev_sets]
+    host_out_all = [torch.empty((n, n * s), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    host_outs = [list(h.unbind(0)) for h in host_out_all]
     h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
     in_ready = [torch.cuda.Event() for _ in range(2)]
     coll_done = [torch.cuda.Event() for _ in range(2)]
@@ -300,8 +307,7 @@ def run_ours(args):
         sd, rv = sets[b]
         h2d_s.wait_event(coll_done[b])  # collective k-2 has read sd
         with torch.cuda.stream(h2d_s):
-            for h, d in zip(host_in, sd):
-                d.copy_(h, non_blocking=True)
+            dev_sets[b][0].copy_(host_in_all, non_blocking=True)
         in_ready[b].record(h2d_s)
         stream.wait_event(in_ready[b])
         stream.wait_event(out_done[b])  # results k-2 have left rv
@@ -309,8 +315,7 @@ def run_ours(args):
         coll_done[b].record(stream)
         d2h_s.wait_event(coll_done[b])
         with torch.cuda.stream(d2h_s):
-            for h, d in zip(host_outs[b], rv):
-                h.copy_(d, non_blocking=True)
+            host_out_all[b].copy_(dev_sets[b][1], non_blocking=True)
         out_done[b].record(d2h_s)
 
     for k in range(2):
@@ -344,7 +349,7 @@ def run_ours(args):
     e2e_value = busbw(n, s, e2e_ms / 1e3)
     e2e_ok = all(torch.equal(host_outs[(k - 1) % 2][j][i * s:(i + 1) * s], host_in[i][j * s:(j + 1) * s])
                  for i in range(n) for j in range(n))
-    floor_ms = pcie_floor_ms(host_in, host_outs[0], sets[0][0], sets[0][1], h2d_s, d2h_s)
+    floor_ms = pcie_floor_ms([host_in_all], [host_out_all[0]], [dev_sets[0][0]], [dev_sets[0][1]], h2d_s, d2h_s)
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -397,7 +402,8 @@ def run_ours(args):
                 "cold_value": round(busbw(n, s, cold_ms / 1e3), 3),
                 "floor_ms": round(floor_ms, 3), "vs_floor": round(e2e_ms / floor_ms, 4),
                 "floor_value": round(busbw(n, s, floor_ms / 1e3), 3),
-                "pipeline": "double-buffered: H2D of step k+1 overlaps D2H of step k",
+                "pipeline": "double-buffered: H2D of step k+1 overlaps D2H of step k; one 512 MiB copy per "
+                            "direction per step (the ranks' buffers are rows of one [n, n*s] tensor)",
                 "bound_note": "PCIe-bound: 512 MiB host->device and 512 MiB device->host per step over one "
                               "x16 link. floor_ms is measured in this run: the same bytes copied both ways "
                               "at once on the same streams with no collective (best of 3)"},
