@@ -116,13 +116,16 @@ __device__ __forceinline__ int folded_gate(const FlagSet& f) {
 //             memory-operation waits have no bound) do not hang; the error
 //             word makes the world's failure sticky;
 //  kCancelled a cancelled prelaunch instance: no data, no signals.
-// When a skip word is set (a gate_poll kernel ran first) it decides instead.
-__device__ __forceinline__ int fused_wait(const FlagSet& f) {
+// When a skip word is set (a gate_poll kernel ran first) it decides instead;
+// the kernels read it at entry (read_skip), in parallel with their table
+// loads, and pass the value in.
+__device__ __forceinline__ uint64_t read_skip(const FlagSet& f) {
+  return f.skip ? *reinterpret_cast<const volatile uint64_t*>(f.skip) : 0;
+}
+
+__device__ __forceinline__ int fused_wait(const FlagSet& f, uint64_t sk) {
   const int lane = threadIdx.x & 31;
-  if (f.skip) {
-    const uint64_t sk = *reinterpret_cast<const volatile uint64_t*>(f.skip);
-    return sk == 0 ? kGo : sk == 1 ? kCancelled : kTimedOut;
-  }
+  if (f.skip) return sk == 0 ? kGo : sk == 1 ? kCancelled : kTimedOut;
   if (f.fold) return folded_gate(f);
   if (blockIdx.x == 0)
     for (int i = lane; i < f.npre; i += 32) st_release_sys(f.pre[i], 1);

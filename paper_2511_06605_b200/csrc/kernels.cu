@@ -164,9 +164,10 @@ __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
     reg_items_kernel(const Item* __restrict__ items, int nitems, int ntiles, FlagSet flags) {
   __shared__ int first[kMaxItemsSmem];
   __shared__ int cta_state;
+  const uint64_t sk = threadIdx.x < 32 ? read_skip(flags) : 0;
   for (int i = threadIdx.x; i < nitems; i += kRegThreads) first[i] = items[i].first_tile;
   if (threadIdx.x < 32) {
-    const int st = (flags.npoll || flags.npre || flags.fold || flags.skip) ? fused_wait(flags) : kGo;
+    const int st = (flags.npoll || flags.npre || flags.fold || flags.skip) ? fused_wait(flags, sk) : kGo;
     if (threadIdx.x == 0) cta_state = st;
   }
   __syncthreads();
@@ -203,10 +204,11 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ int first[kMaxItemsSmem];
+  const uint64_t sk = read_skip(flags);
   for (int i = threadIdx.x; i < nitems; i += 32) first[i] = items[i].first_tile;
   __syncwarp();
   // the CTA is one warp: fused_wait's result is already warp-uniform
-  const int state = (flags.npoll || flags.npre || flags.fold || flags.skip) ? fused_wait(flags) : kGo;
+  const int state = (flags.npoll || flags.npre || flags.fold || flags.skip) ? fused_wait(flags, sk) : kGo;
   if (threadIdx.x != 0) return;
   if (state != kGo) {
     if (flags.ctr) fused_finish(flags, state);

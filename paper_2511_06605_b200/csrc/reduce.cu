@@ -60,11 +60,12 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const RedItem* __re
   constexpr int kVecElems = 16 / static_cast<int>(sizeof(T));            // elements per 16-byte vector
   constexpr int kVecs = kElemsPerThread / kVecElems;                       // vectors per thread
   __shared__ int first[kMaxItemsSmem];
+  const uint64_t sk = threadIdx.x < 32 ? read_skip(flags) : 0;
   for (int i = threadIdx.x; i < nitems; i += kRedThreads) first[i] = items[i].first_tile;
   // Fused flags (kernels.hpp FlagSet): every source rank's send is ready.
   __shared__ int cta_state;
   if (threadIdx.x < 32) {
-    const int st = (flags.npoll || flags.npre || flags.fold || flags.skip) ? fused_wait(flags) : kGo;
+    const int st = (flags.npoll || flags.npre || flags.fold || flags.skip) ? fused_wait(flags, sk) : kGo;
     if (threadIdx.x == 0) cta_state = st;
   }
   __syncthreads();

@@ -283,14 +283,15 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(dtab, &pt, sizeof(pt), cudaMemcpyHostToDevice));
     const int smem = static_cast<int>(chunk);
     CK(cudaFuncSetAttribute(tma_param_mover, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    for (int variant = 0; variant < 3; ++variant) {
-      if (variant == 2 && chunk > 128 * 1024) continue;
+    for (int variant = 0; variant < 4; ++variant) {
+      if (variant >= 2 && chunk > 128 * 1024) continue;
       cudaGraph_t g;
       cudaGraphExec_t ge;
       CK(cudaStreamBeginCapture(as, cudaStreamCaptureModeRelaxed));
       if (variant == 0) table_mover<<<kChunks, 256, 0, as>>>(dtab);
       if (variant == 1) param_mover<<<kChunks, 256, 0, as>>>(pt);
       if (variant == 2) tma_param_mover<<<kChunks, 32, smem, as>>>(pt);
+      if (variant == 3) tma_param_mover<<<kChunks, 32, 128 * 1024, as>>>(pt);
       CK(cudaStreamEndCapture(as, &g));
       CK(cudaGraphInstantiate(&ge, g, 0));
       for (int rep = 0; rep < 2; ++rep) {
@@ -301,8 +302,10 @@ int main(int argc, char** argv) {
         auto t1 = clk::now();
         CK(cudaEventRecord(e1, cs));
         if (rep)
-          report(variant == 0 ? "(g) table in global, 1 CTA/item" : variant == 1 ? "(h) table in params, 1 CTA/item"
-                                                                               : "(i) TMA, table in params, 1 warp/item",
+          report(variant == 0   ? "(g) table in global, 1 CTA/item"
+                 : variant == 1 ? "(h) table in params, 1 CTA/item"
+                 : variant == 2 ? "(i) TMA, table in params, 1 warp/item"
+                                : "(j) as (i) with 128 KiB dynamic smem",
                  hus(t0, t1));
       }
     }
