@@ -680,7 +680,9 @@ std::string plan_info(World* w, const Plan* p) {
     const size_t local = u.start.size() + u.sm_post.size();
     units += std::string(i ? "," : "") + "{\"device\":" + std::to_string(u.device) + ",\"ranks\":[" + ranks +
              "],\"mover\":\"" + (u.red.nitems ? "reduce" : mover_name(u.table)) +
-             "\",\"grid\":" + std::to_string(u.table.nitems ? plan_grid(p, u.table) : 0) +
+             "\",\"grid\":" + std::to_string(u.table.nitems ? std::min(plan_grid(p, u.table), u.table.ntiles) : 0) +
+             ",\"tile_bytes\":" + std::to_string(u.table.nitems ? u.table.tile : 0) +
+             ",\"tiles\":" + std::to_string(u.table.ntiles) +
              ",\"ce_lanes\":" + std::to_string(lanes) + ",\"fused_flags\":" + (u.fused ? "true" : "false") +
              ",\"start_folded\":" + (u.start_folded ? "true" : "false") +
              ",\"flag_writes_memop\":" + std::to_string(local) +

@@ -9,6 +9,8 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
+#include <string>
+#include <vector>
 
 #include "kernels.hpp"
 
@@ -191,16 +193,21 @@ __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
 // TMA bulk mover (copy items, 16-byte aligned, sizes multiple of 16)
 // ---------------------------------------------------------------------------
 
-constexpr int kTmaStages = 4;
+#ifndef CECOLL_TMA_STAGES
+#define CECOLL_TMA_STAGES 4
+#endif
+constexpr int kTmaStages = CECOLL_TMA_STAGES;
 constexpr int kTmaTile = 32 * 1024;
 constexpr int kTmaSmem = kTmaStages * kTmaTile;
+// CTAs of the TMA mover resident per SM (228 KiB of shared memory per SM)
+constexpr int kTmaPerSm = (228 * 1024) / (kTmaSmem + 8 * 1024);
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
 __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict__ items, int nitems, int ntiles,
-                                                          int evict_first, FlagSet flags) {
+                                                          int tile_bytes, int evict_first, FlagSet flags) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ int first[kMaxItemsSmem];
@@ -224,12 +231,12 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
     const int tile = blockIdx.x + k * gridDim.x;
     while (cur + 1 < nitems && first[cur + 1] <= tile) ++cur;
     const Item& it = items[cur];
-    const int64_t off = static_cast<int64_t>(tile - it.first_tile) * kTmaTile;
+    const int64_t off = static_cast<int64_t>(tile - it.first_tile) * tile_bytes;
     const int64_t rem = it.bytes - off;
     *src = it.src + off;
     *item = cur;
     *off_out = off;
-    *bytes = static_cast<uint32_t>(rem < kTmaTile ? rem : kTmaTile);
+    *bytes = static_cast<uint32_t>(rem < tile_bytes ? rem : tile_bytes);
   };
   // L2 policy of the bulk copies. Evict-first helped the isolated mover by
   // 1-5% at 1-8 MiB chunks (profiles/copy_bench2_r01.txt) but cost 3-4% in
@@ -381,9 +388,24 @@ __global__ void __launch_bounds__(kRegThreads) mc_store_kernel(const int4* __res
 
 int64_t mover_tile_bytes(Mover m) { return m == Mover::Tma ? kTmaTile : kRegTile; }
 
-int64_t tiles_for(int64_t bytes, Mover m) {
-  const int64_t t = mover_tile_bytes(m);
-  return (bytes + t - 1) / t;
+int table_tile(Mover m, const std::vector<int64_t>& sizes, int sms) {
+  if (m != Mover::Tma) return static_cast<int>(kRegTile);
+  static const bool fixed = [] {
+    const char* e = std::getenv("CECOLL_TMA_FIXED_TILE");
+    return e && std::string(e) == "1";
+  }();
+  if (fixed) return kTmaTile;
+  // The smallest tile (1 KiB steps, at least 4 KiB) that still gives every
+  // resident CTA at most one tile: at these sizes parallelism wins over
+  // pipelining inside a CTA (tools/latency: a 64 KiB all-gather 8.2 -> 4.1
+  // us). Tables that need more than one wave at 32 KiB keep 32 KiB tiles.
+  const int64_t slots = int64_t{kTmaPerSm} * sms;
+  for (int64_t t = 4096; t < kTmaTile; t += 1024) {
+    int64_t n = 0;
+    for (int64_t b : sizes) n += (b + t - 1) / t;
+    if (n <= slots) return static_cast<int>(t);
+  }
+  return kTmaTile;
 }
 
 // Default: a persistent grid of 2 CTAs per SM (fastest alone; the TMA ring
@@ -407,6 +429,9 @@ int mover_grid_for(const ItemTable& t, int sms) {
     return e ? std::atoi(e) : 0;
   }();
   if (per_cta > 0) return (t.ntiles + per_cta - 1) / per_cta;
+  // a table tiled below 32 KiB is small: one wave of resident CTAs
+  if (t.mover == Mover::Tma && t.tile > 0 && t.tile < kTmaTile)
+    return std::min(mover_grid(t.mover, sms), kTmaPerSm * sms);
   return mover_grid(t.mover, sms);
 }
 
@@ -438,6 +463,7 @@ KernelCall items_call(const ItemTable& t, int grid, const FlagSet* fp) {
     k.push(static_cast<const Item*>(t.items));
     k.push(t.nitems);
     k.push(t.ntiles);
+    k.push(t.tile > 0 ? t.tile : kTmaTile);
     k.push(evict_first);
     k.push(fp ? *fp : FlagSet{});
     return k;

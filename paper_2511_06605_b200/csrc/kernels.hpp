@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace cecoll {
@@ -76,13 +77,19 @@ struct ItemTable {
   int ntiles = 0;
   Mover mover = Mover::Reg;
   int kinds = 1;  // bitmask of (1 << ItemKind) present
+  int tile = 0;   // bytes per tile (0: the mover's default)
 };
 
 constexpr int kMaxItemsSmem = 1024;
 
 int64_t mover_tile_bytes(Mover m);
-// Tiles of one item under mover m.
-int64_t tiles_for(int64_t bytes, Mover m);
+// Tile size of a table of items of `sizes` bytes on a device with `sms` SMs:
+// the register mover uses 64 KiB tiles; the TMA mover the smallest tile (4-32
+// KiB) that leaves at most one tile per resident CTA, or 32 KiB tiles on its
+// persistent grid when even those need more than one wave.
+int table_tile(Mover m, const std::vector<int64_t>& sizes, int sms);
+// Tiles of one item of `bytes` at `tile` bytes per tile.
+inline int64_t tiles_of(int64_t bytes, int tile) { return (bytes + tile - 1) / tile; }
 // Grid that fills the device for mover m (multiple of the SM count).
 int mover_grid(Mover m, int sms);
 // Grid for one table (honours CECOLL_SM_TILES_PER_CTA).

@@ -96,13 +96,16 @@ Status upload_items(Plan* p, int device, std::vector<HostItem>& host, ItemTable*
     p->dev_alloc_device.push_back(device);
     fan_dev = static_cast<char**>(d);
   }
+  std::vector<int64_t> sizes;
+  for (const HostItem& h : host) sizes.push_back(h.item.bytes);
+  out->tile = table_tile(out->mover, sizes, p->sms);
   std::vector<Item> items;
   int64_t tiles = 0;
   size_t fan_at = 0;
   for (HostItem& h : host) {
     Item it = h.item;
     it.first_tile = static_cast<int32_t>(tiles);
-    tiles += tiles_for(it.bytes, out->mover);
+    tiles += tiles_of(it.bytes, out->tile);
     if (it.kind == kItemFan) {
       it.fan = fan_dev + fan_at;
       it.nfan = static_cast<int32_t>(h.fan.size());
@@ -642,10 +645,10 @@ Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<
       if (src != dst) u.placement.push_back({dst, src, s});
     }
 
+  p->sms = device_sms(p->units[0].device);  // tile sizes depend on it (upload_items)
   if (p->hybrid) STATUS_TRY(lower_hybrid(w, p, kind, s, ad));
   else if (p->sm) STATUS_TRY(lower_sm(w, p, kind, s, ad));
   else STATUS_TRY(lower_program(w, p, ad, unit_of, in_place_impl));
-  p->sms = device_sms(p->units[0].device);
   STATUS_TRY(split_remote(w, p));
   if (p->sm) STATUS_TRY(fuse_sm_flags(w, p));
   if (p->prelaunch)

@@ -102,3 +102,25 @@ def test_sm_budget_caps_the_grid(comms):
         plan.destroy()
     finally:
         comms[0].set_sm_budget(0)
+
+
+@pytest.mark.parametrize("kind,s,tile,tiles", [
+    ("allgather", 65536, 4096, 128),        # 8 fan items: smallest tile leaving <= 1 tile per SM
+    ("allgather", 262144, 15360, 144),      # 8 x ceil(256 KiB / 15 KiB) = 144 <= 148
+    ("alltoall", 65536, 32768, 128),        # 64 items x 2 tiles already fit one wave
+    ("alltoall", 8 << 20, 32768, 64 * 256),  # the headline: 32 KiB tiles on the persistent grid
+])
+def test_tma_tile_size_follows_the_table(comms, kind, s, tile, tiles):
+    """kernels.cu table_tile: one tile per resident CTA while the table fits one
+    wave (a 64 KiB all-gather 8.2 -> 4.1 us per collective), 32 KiB tiles on
+    the persistent grid above."""
+    sends, recvs = _bufs(s, kind)
+    fn = cc.all_gather if kind == "allgather" else cc.all_to_all
+    fn(comms, sends, recvs, s, impl="sm", streams=torch.cuda.Stream())
+    u = comms[0].last_plan_info()["units"][0]
+    assert u["mover"] == "tma" and u["tile_bytes"] == tile and u["tiles"] == tiles, u
+    assert u["grid"] == min(tiles, 296), u
+    ok = all(torch.equal(recvs[j][i * s:(i + 1) * s], sends[i] if kind == "allgather" else sends[i][j * s:(j + 1) * s])
+             for i in range(N) for j in range(N))
+    assert ok
+    torch.cuda.synchronize()

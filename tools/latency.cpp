@@ -80,7 +80,7 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  const size_t max_s = 1 << 20;
+  const size_t max_s = std::getenv("LAT_MAX") ? std::strtoull(std::getenv("LAT_MAX"), nullptr, 0) : size_t(1) << 20;
   std::vector<void*> send(n), recv(n);
   for (int r = 0; r < n; ++r) {
     CK(cudaMalloc(&send[r], n * max_s));
