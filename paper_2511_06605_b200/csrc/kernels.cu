@@ -163,11 +163,15 @@ __device__ __forceinline__ int find_item(const int* first, int nitems, int tile)
 
 template <int kKinds, int kMinBlocks>
 __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
-    reg_items_kernel(const Item* __restrict__ items, int nitems, int ntiles, FlagSet flags) {
+    reg_items_kernel(const Item* __restrict__ items, int nitems, int ntiles, int uniform, FlagSet flags) {
+  // uniform > 0: every item has `uniform` tiles, so tile t belongs to item
+  // t / uniform and the first-tile prefix (a global load round trip before
+  // any data moves) is not needed.
   __shared__ int first[kMaxItemsSmem];
   __shared__ int cta_state;
   const uint64_t sk = threadIdx.x < 32 ? read_skip(flags) : 0;
-  for (int i = threadIdx.x; i < nitems; i += kRegThreads) first[i] = items[i].first_tile;
+  if (!uniform)
+    for (int i = threadIdx.x; i < nitems; i += kRegThreads) first[i] = items[i].first_tile;
   if (threadIdx.x < 32) {
     const int st = (flags.npoll || flags.npre || flags.fold || flags.skip) ? fused_wait(flags, sk) : kGo;
     if (threadIdx.x == 0) cta_state = st;
@@ -175,9 +179,11 @@ __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
   __syncthreads();
   const int state = cta_state;
   const bool moved = state == kGo;
-  int cur = find_item(first, nitems, blockIdx.x);
+  int cur = uniform ? 0 : find_item(first, nitems, blockIdx.x);
   for (int tile = moved ? blockIdx.x : ntiles; tile < ntiles; tile += gridDim.x) {
-    while (cur + 1 < nitems && first[cur + 1] <= tile) ++cur;
+    if (uniform) cur = tile / uniform;
+    else
+      while (cur + 1 < nitems && first[cur + 1] <= tile) ++cur;
     const Item it = items[cur];
     const int64_t off = static_cast<int64_t>(tile - it.first_tile) * kRegTile;
     const int64_t rem = it.bytes - off;
@@ -207,12 +213,14 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 }
 
 __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict__ items, int nitems, int ntiles,
-                                                          int tile_bytes, int evict_first, FlagSet flags) {
+                                                          int tile_bytes, int uniform, int evict_first,
+                                                          FlagSet flags) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ int first[kMaxItemsSmem];
   const uint64_t sk = read_skip(flags);
-  for (int i = threadIdx.x; i < nitems; i += 32) first[i] = items[i].first_tile;
+  if (!uniform)  // see reg_items_kernel
+    for (int i = threadIdx.x; i < nitems; i += 32) first[i] = items[i].first_tile;
   __syncwarp();
   // the CTA is one warp: fused_wait's result is already warp-uniform
   const int state = (flags.npoll || flags.npre || flags.fold || flags.skip) ? fused_wait(flags, sk) : kGo;
@@ -225,11 +233,13 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 
   const int mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  int cur = find_item(first, nitems, blockIdx.x);
+  int cur = uniform ? 0 : find_item(first, nitems, blockIdx.x);
   // Tile k of this CTA is global tile blockIdx.x + k * gridDim.x.
   auto locate = [&](int k, const char** src, int* item, int64_t* off_out, uint32_t* bytes) {
     const int tile = blockIdx.x + k * gridDim.x;
-    while (cur + 1 < nitems && first[cur + 1] <= tile) ++cur;
+    if (uniform) cur = tile / uniform;
+    else
+      while (cur + 1 < nitems && first[cur + 1] <= tile) ++cur;
     const Item& it = items[cur];
     const int64_t off = static_cast<int64_t>(tile - it.first_tile) * tile_bytes;
     const int64_t rem = it.bytes - off;
@@ -464,6 +474,7 @@ KernelCall items_call(const ItemTable& t, int grid, const FlagSet* fp) {
     k.push(t.nitems);
     k.push(t.ntiles);
     k.push(t.tile > 0 ? t.tile : kTmaTile);
+    k.push(t.uniform);
     k.push(evict_first);
     k.push(fp ? *fp : FlagSet{});
     return k;
@@ -478,6 +489,7 @@ KernelCall items_call(const ItemTable& t, int grid, const FlagSet* fp) {
   k.push(static_cast<const Item*>(t.items));
   k.push(t.nitems);
   k.push(t.ntiles);
+  k.push(t.uniform);
   k.push(fp ? *fp : FlagSet{});
   return k;
 }

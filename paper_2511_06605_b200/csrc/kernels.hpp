@@ -77,7 +77,8 @@ struct ItemTable {
   int ntiles = 0;
   Mover mover = Mover::Reg;
   int kinds = 1;  // bitmask of (1 << ItemKind) present
-  int tile = 0;   // bytes per tile (0: the mover's default)
+  int tile = 0;     // bytes per tile (0: the mover's default)
+  int uniform = 0;  // tiles per item when every item has the same count, else 0
 };
 
 constexpr int kMaxItemsSmem = 1024;

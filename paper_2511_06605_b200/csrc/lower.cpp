@@ -123,6 +123,10 @@ Status upload_items(Plan* p, int device, std::vector<HostItem>& host, ItemTable*
   out->items = static_cast<Item*>(d);
   out->nitems = static_cast<int>(items.size());
   out->ntiles = static_cast<int>(tiles);
+  const int64_t per = tiles_of(items[0].bytes, out->tile);
+  bool uniform = per > 0;
+  for (const Item& it : items) uniform &= tiles_of(it.bytes, out->tile) == per;
+  out->uniform = uniform ? static_cast<int>(per) : 0;
   return {};
 }
 

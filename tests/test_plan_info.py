@@ -117,6 +117,7 @@ def test_tma_tile_size_follows_the_table(comms, kind, s, tile, tiles):
     sends, recvs = _bufs(s, kind)
     fn = cc.all_gather if kind == "allgather" else cc.all_to_all
     fn(comms, sends, recvs, s, impl="sm", streams=torch.cuda.Stream())
+    torch.cuda.synchronize()
     u = comms[0].last_plan_info()["units"][0]
     assert u["mover"] == "tma" and u["tile_bytes"] == tile and u["tiles"] == tiles, u
     assert u["grid"] == min(tiles, 296), u

@@ -199,6 +199,47 @@ __global__ void tma_param_mover(const __grid_constant__ ParamTable t) {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// (k)-(m): the library TMA mover's ingredients added one at a time to (i):
+// template flags: table in global memory, createpolicy + L2 cache hints,
+// a 4-stage mbarrier ring with 128 KiB of dynamic shared memory.
+template <bool kGlobal, bool kHint, bool kRing>
+__global__ void tma_variant(const __grid_constant__ ParamTable t, const ProbeItem* items) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t bars[4];
+  if (threadIdx.x != 0) return;
+  const ProbeItem it = kGlobal ? items[blockIdx.x] : t.it[blockIdx.x];
+  const int nb = kRing ? 4 : 1;
+  for (int i = 0; i < nb; ++i)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bars[i]))));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[0]));
+  const uint32_t r = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
+  const uint32_t bytes = static_cast<uint32_t>(it.bytes);
+  uint64_t policy = 0;
+  if (kHint) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  if (kHint)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(r),
+                 "l"(it.src), "r"(bytes), "r"(b), "l"(policy)
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(r),
+                 "l"(it.src), "r"(bytes), "r"(b)
+                 : "memory");
+  asm volatile("{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}" ::"r"(b),
+               "r"(0)
+               : "memory");
+  if (kHint)
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(it.dst), "r"(r),
+                 "r"(bytes), "l"(policy)
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(it.dst), "r"(r), "r"(bytes)
+                 : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main(int argc, char** argv) {
   const size_t chunk = argc > 1 ? std::strtoull(argv[1], nullptr, 0) : 4096;
   const int iters = argc > 2 ? std::atoi(argv[2]) : 2000;
@@ -307,6 +348,36 @@ int main(int argc, char** argv) {
                  : variant == 2 ? "(i) TMA, table in params, 1 warp/item"
                                 : "(j) as (i) with 128 KiB dynamic smem",
                  hus(t0, t1));
+      }
+    }
+    // (k)-(m)
+    {
+      auto kk = tma_variant<true, false, false>;
+      auto kl = tma_variant<true, true, false>;
+      auto km = tma_variant<true, true, true>;
+      CK(cudaFuncSetAttribute(km, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
+      for (int variant = 0; variant < 3 && chunk <= 32 * 1024; ++variant) {
+        cudaGraph_t g;
+        cudaGraphExec_t ge;
+        CK(cudaStreamBeginCapture(as, cudaStreamCaptureModeRelaxed));
+        if (variant == 0) kk<<<kChunks, 32, smem, as>>>(pt, dtab);
+        if (variant == 1) kl<<<kChunks, 32, smem, as>>>(pt, dtab);
+        if (variant == 2) km<<<kChunks, 32, 128 * 1024, as>>>(pt, dtab);
+        CK(cudaStreamEndCapture(as, &g));
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        for (int rep = 0; rep < 2; ++rep) {
+          reset();
+          CK(cudaEventRecord(e0, cs));
+          auto t0 = clk::now();
+          for (int i = 0; i < iters; ++i) CK(cudaGraphLaunch(ge, cs));
+          auto t1 = clk::now();
+          CK(cudaEventRecord(e1, cs));
+          if (rep)
+            report(variant == 0   ? "(k) (i) + table in global"
+                   : variant == 1 ? "(l) (k) + L2 cache hints"
+                                  : "(m) (l) + 4 mbarriers, 128 KiB smem",
+                   hus(t0, t1));
+        }
       }
     }
   }
