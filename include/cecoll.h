@@ -273,18 +273,22 @@ cecoll_status_t cecoll_collective_n(cecoll_kind_t kind, const cecoll_comm_t* com
 /* ---------------------------------------------------------------------
  * Explicit prelaunch plans (≙ apply_prelaunch, compiler.cpp:267-285, and the
  * producer→collective sync chain, sim.cpp:475-499). A plan binds the ranks'
- * buffers once, builds the command lists as CUDA graphs gated by trigger
- * polls, and keeps one instance armed ahead of the trigger.
+ * buffers once, builds the command lists as CUDA graphs gated on a per-unit
+ * device trigger word, and keeps one instance armed ahead of the trigger.
+ * The trigger is stream-ordered: cecoll_plan_launch has each caller stream
+ * write the word (a stream memory operation), so the armed instance starts
+ * when that stream reaches the call — behind a producer kernel queued before
+ * it, with no host round trip.
  * Plans of the other implementations (and the cached plans behind the eager
  * calls) are recorded too (built explicitly, node by node — never by stream
  * capture): from their second launch on, each unit's whole
  * submission — flag operations, lanes, copies, kernels — replays as one CUDA
  * graph launched on the caller stream (one host call per collective). This
  * applies when every unit of the plan has its own device and an explicit,
- * non-capturing stream, and the submission is more than one call (a
- * one-unit SM plan is a single kernel launch and is not recorded);
- * otherwise, or with CECOLL_GRAPH=0, commands are submitted one by one on
- * every launch.
+ * non-capturing stream (a one-unit SM plan, a single kernel, is recorded too:
+ * a one-node graph launch costs the host less than the direct launch;
+ * CECOLL_RECORD_SINGLE=0 opts out); otherwise, or with CECOLL_GRAPH=0,
+ * commands are submitted one by one on every launch.
  * ------------------------------------------------------------------- */
 cecoll_status_t cecoll_plan_create(const cecoll_comm_t* comms, int ncomms, cecoll_kind_t kind,
                                    const void* const* sends, void* const* recvs, size_t chunk_bytes,
@@ -294,8 +298,8 @@ cecoll_status_t cecoll_plan_create(const cecoll_comm_t* comms, int ncomms, cecol
 cecoll_status_t cecoll_plan_create_program(const cecoll_comm_t* comms, int ncomms, cecoll_program_t program,
                                            const void* const* sends, void* const* recvs, cecoll_plan_t* out);
 /* Trigger the armed instance from each rank's stream (streams[i] for
- * comms[i]; NULL entries = host trigger) and make each stream wait for
- * completion; re-arms the next instance off the critical path. */
+ * comms[i]; NULL entries = the legacy default stream) and make each stream
+ * wait for completion; re-arms the next instance off the critical path. */
 cecoll_status_t cecoll_plan_launch(cecoll_plan_t plan, void* const* streams);
 /* The two halves of cecoll_plan_launch, for callers that schedule the arming
  * themselves (SURVEY §8(b) plan_arm / plan_trigger). cecoll_plan_arm launches

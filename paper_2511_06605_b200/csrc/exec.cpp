@@ -192,20 +192,17 @@ Status run_sm(World* w, Plan* p, Sink& sink) {
   return {};
 }
 
-// Cancels a unit's armed instance: writes "cancel" (2) into its trigger word
-// from a private stream (the caller's stream may be anywhere; the arm stream
-// is held by the spinning gate), then waits for the instance to finish — its
-// gate takes the word and skips the body.
+// Cancels a unit's armed instance: raises the unit's cancel count in pinned
+// host memory (no stream: a stream memory operation could land in the same
+// hardware queue as the armed graph and wait behind it forever — round 2's
+// first version did, and an 8-rank latency run hung in plan_destroy), then
+// waits for the instance to finish; its gate sees the raise and skips the
+// body.
 Status cancel_armed(World* w, Unit& u) {
-  cudaStream_t s = nullptr;
-  CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  Status st = submit(w, s, MemOps{op_write(u.ready_flag, 2)});
-  if (st.ok()) {
-    const cudaError_t e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) st = cuda_fail(e, "cancel write", __FILE__, __LINE__);
-  }
-  cudaStreamDestroy(s);
-  STATUS_TRY(st);
+  (void)w;
+  volatile uint64_t* c = u.cancel_host;
+  *c = ++u.cancels;
+  __atomic_thread_fence(__ATOMIC_SEQ_CST);
   CUDA_TRY(cudaStreamSynchronize(u.arm));
   return {};
 }
@@ -223,24 +220,6 @@ void set_armed(Unit& u, bool armed) {
 
 Status arm_unit(World* w, Unit& u) {
   DeviceGuard g(u.device);
-  const uint64_t instance = u.instances++;
-  if (u.fold_node) {  // the folded kernel waits for post number `instance`
-    KernelCall& k = u.fold_call;
-    FlagSet f;
-    std::memcpy(&f, k.buf + k.off[k.nargs - 1], sizeof(f));
-    f.post_no = instance;
-    std::memcpy(k.buf + k.off[k.nargs - 1], &f, sizeof(f));
-    void* args[12];
-    k.params(args);
-    cudaKernelNodeParams kp;
-    std::memset(&kp, 0, sizeof(kp));
-    kp.func = const_cast<void*>(k.func);
-    kp.gridDim = k.grid;
-    kp.blockDim = k.block;
-    kp.sharedMemBytes = k.smem;
-    kp.kernelParams = args;
-    CUDA_TRY(cudaGraphExecKernelNodeSetParams(u.exec, u.fold_node, &kp));
-  }
   CUDA_TRY(cudaGraphLaunch(u.exec, u.arm));
   CUDA_TRY(cudaEventRecord(u.graph_done, u.arm));
   ++w->counters[kCtrGraphLaunches];
@@ -588,6 +567,8 @@ Status plan_destroy(World* w, Plan* p) {
       cudaStreamDestroy(u.arm);
     }
     if (u.graph_done) cudaEventDestroy(u.graph_done);
+    if (u.cancel_host) cudaFreeHost(u.cancel_host);
+    u.cancel_host = nullptr;
     u.exec = nullptr;
     u.graph = nullptr;
     u.arm = nullptr;

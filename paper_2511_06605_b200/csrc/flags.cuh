@@ -48,38 +48,59 @@ __device__ __forceinline__ bool wait_flag(const uint64_t* p, uint64_t* err) {
 // What a CTA may do after its prologue.
 enum : int { kGo = 0, kTimedOut = 1, kCancelled = 2 };
 
-// The trigger word of a prelaunch unit (its ready slot): the caller stream
-// writes 1 ("go") when it triggers the unit; a cancel writes 2 from a private
-// stream (exec.cpp cancel_armed). No bound: an armed instance waits as long
-// as its caller leaves it armed. The word is taken by resetting it to 0 (the
-// next trigger is only written after this instance completes). Polling device
-// memory keeps PCIe reads of host memory off the trigger's critical path
-// (round 1's gate read a host post first: ~2 us of every prelaunch
-// collective, tools/prelaunch_probe.cu).
-__device__ __forceinline__ uint64_t take_trigger(uint64_t* p, uint64_t* err) {
+// Trigger of a prelaunch unit. The caller stream writes 1 ("go") into the
+// unit's device trigger word when it triggers the unit; the gate spins on
+// that word and takes it by resetting it to 0 (the next trigger is only
+// written after this instance completes). A cancel comes from the host
+// without any stream (a stream could share a hardware queue with the armed
+// graph and never run): the host raises a count in pinned memory
+// (`cancel`, exec.cpp cancel_armed) and the gate compares it with the count
+// it has already honoured (`seen`, device) once every 256 polls — PCIe reads
+// of host memory stay off the go path (round 1's gate read a host post on
+// every trigger: ~2 us per prelaunch collective, tools/prelaunch_probe.cu).
+// No bound: an armed instance waits as long as its caller leaves it armed.
+// Returns 1 (go) or 2 (cancel).
+__device__ __forceinline__ uint64_t take_trigger(uint64_t* p, const volatile uint64_t* cancel, uint64_t* seen,
+                                                 uint64_t* err) {
   uint64_t v;
-  while ((v = ld_acquire_sys(p)) == 0) __nanosleep(32);
+  for (unsigned i = 1;; ++i) {
+    v = ld_acquire_sys(p);
+    if (v) break;
+    if ((i & 255) == 0) {
+      const uint64_t c = *cancel;
+      if (c > *seen) {
+        *seen = c;
+        return 2;
+      }
+    }
+    __nanosleep(32);
+  }
   *p = 0;
-  if (v != 1 && v != 2) atomicOr(reinterpret_cast<unsigned long long*>(err), 2ull);
+  if (v != 1) atomicOr(reinterpret_cast<unsigned long long*>(err), 2ull);
   return v;
 }
 
-// Folded prelaunch gate (FlagSet::fold, one full warp of every CTA). CTA 0
+// Folded prelaunch gate (FlagSet::epoch, one full warp of every CTA). CTA 0
 // alone takes the unit's trigger word (f.polls[0]), writes the folded start
 // signals, polls the other flags (one set of system-scope pollers) and resets
 // them — their writers only write again after this instance completes or
 // signals — then publishes the outcome in the device word *gate =
-// (post_no + 1) * 4 + state, post_no being the instance's number (set when it
-// is armed); every other CTA waits for that word (device scope). CTA 0's
-// system-scope acquire of the flags followed by its release of the gate word
-// orders the flag writers' data before every CTA's accesses.
+// (epoch + 1) * 4 + state; every other CTA waits for that word (device
+// scope). *epoch counts completed instances: instances run one at a time on
+// the unit's arm stream and the previous one's last CTA advanced it, so every
+// CTA of this instance reads the same value (no per-instance kernel
+// parameters, so arming is a plain graph launch). CTA 0's system-scope
+// acquire of the flags followed by its release of the gate word orders the
+// flag writers' data before every CTA's accesses.
 __device__ __forceinline__ int folded_gate(const FlagSet& f) {
   const int lane = threadIdx.x & 31;
-  const uint64_t base = (f.post_no + 1) * 4;
+  uint64_t base = 0;
+  if (lane == 0) base = (*reinterpret_cast<const volatile uint64_t*>(f.epoch) + 1) * 4;
+  base = __shfl_sync(0xffffffffu, base, 0);
   int state;
   if (blockIdx.x == 0) {
     uint64_t kind = 0;
-    if (lane == 0) kind = take_trigger(f.polls[0], f.err);
+    if (lane == 0) kind = take_trigger(f.polls[0], f.cancel, f.seen, f.err);
     kind = __shfl_sync(0xffffffffu, kind, 0);
     if (kind != 1) {
       state = kCancelled;
@@ -126,7 +147,7 @@ __device__ __forceinline__ uint64_t read_skip(const FlagSet& f) {
 __device__ __forceinline__ int fused_wait(const FlagSet& f, uint64_t sk) {
   const int lane = threadIdx.x & 31;
   if (f.skip) return sk == 0 ? kGo : sk == 1 ? kCancelled : kTimedOut;
-  if (f.fold) return folded_gate(f);
+  if (f.epoch) return folded_gate(f);
   if (blockIdx.x == 0)
     for (int i = lane; i < f.npre; i += 32) st_release_sys(f.pre[i], 1);
   bool ok = true;
@@ -154,11 +175,12 @@ __device__ __forceinline__ void fused_finish(const FlagSet& f, int state) {
   asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(ticket) : "l"(f.ctr), "r"(add) : "memory");
   if ((ticket & 0xFFFFFu) != gridDim.x - 1) return;
   *f.ctr = 0;
+  if (f.epoch) *f.epoch += 1;       // a folded body: this instance is complete
   if (state == kCancelled) return;  // uniform: every CTA read the same gate / skip word
   // Every CTA passed its polls before taking its ticket: reset them for the
   // next collective (its writers only write again after our signals). A
   // folded gate has reset them already.
-  if (state == kGo && (ticket >> 20) == 0 && !f.fold)
+  if (state == kGo && (ticket >> 20) == 0 && !f.epoch)
     for (int i = 0; i < f.npoll; ++i) *f.polls[i] = 0;
   for (int i = 0; i < f.nsig; ++i) st_release_sys(f.sigs[i], 1);
 }

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
   if (!uniform)
     for (int i = threadIdx.x; i < nitems; i += kRegThreads) first[i] = items[i].first_tile;
   if (threadIdx.x < 32) {
-    const int st = (flags.npoll || flags.npre || flags.fold || flags.skip) ? fused_wait(flags, sk) : kGo;
+    const int st = (flags.npoll || flags.npre || flags.epoch || flags.skip) ? fused_wait(flags, sk) : kGo;
     if (threadIdx.x == 0) cta_state = st;
   }
   __syncthreads();
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
     for (int i = threadIdx.x; i < nitems; i += 32) first[i] = items[i].first_tile;
   __syncwarp();
   // the CTA is one warp: fused_wait's result is already warp-uniform
-  const int state = (flags.npoll || flags.npre || flags.fold || flags.skip) ? fused_wait(flags, sk) : kGo;
+  const int state = (flags.npoll || flags.npre || flags.epoch || flags.skip) ? fused_wait(flags, sk) : kGo;
   if (threadIdx.x != 0) return;
   if (state != kGo) {
     if (flags.ctr) fused_finish(flags, state);
@@ -344,18 +344,20 @@ __global__ void signal_kernel(uint64_t* const* flags, int n) {
 
 // Gate of a recorded prelaunch graph with a conditional body: takes the
 // unit's trigger word (take_trigger, flags.cuh) and opens the body on "go".
-__global__ void gate_kernel(uint64_t* trigger, cudaGraphConditionalHandle handle, uint64_t* err) {
+__global__ void gate_kernel(uint64_t* trigger, const volatile uint64_t* cancel, uint64_t* seen,
+                            cudaGraphConditionalHandle handle, uint64_t* err) {
   if (threadIdx.x != 0) return;
-  const uint64_t kind = take_trigger(trigger, err);
+  const uint64_t kind = take_trigger(trigger, cancel, seen, err);
   cudaGraphSetConditional(handle, kind == 1 ? 1u : 0u);
 }
 
-__global__ void gate_poll_kernel(uint64_t* const* flags, int n, uint64_t* skip, uint64_t* err) {
+__global__ void gate_poll_kernel(uint64_t* const* flags, int n, const volatile uint64_t* cancel, uint64_t* seen,
+                                 uint64_t* skip, uint64_t* err) {
   // flags[0] is the unit's trigger word: lane 0 takes it; on "go" the warp
   // polls the other flags in parallel (lane i: flags 1+i, 33+i, ...) and
   // resets them.
   __shared__ uint64_t kind;
-  if (threadIdx.x == 0) kind = take_trigger(flags[0], err);
+  if (threadIdx.x == 0) kind = take_trigger(flags[0], cancel, seen, err);
   __syncwarp();
   if (kind != 1) {
     if (threadIdx.x == 0) *skip = 1;
@@ -542,22 +544,28 @@ KernelCall signal_call(uint64_t* const* flags, int n) {
   return k;
 }
 
-KernelCall gate_call(uint64_t* trigger, cudaGraphConditionalHandle handle, uint64_t* err) {
+KernelCall gate_call(uint64_t* trigger, const volatile uint64_t* cancel, uint64_t* seen,
+                     cudaGraphConditionalHandle handle, uint64_t* err) {
   KernelCall k;
   k.func = reinterpret_cast<const void*>(gate_kernel);
   k.block = dim3(32);
   k.push(trigger);
+  k.push(cancel);
+  k.push(seen);
   k.push(handle);
   k.push(err);
   return k;
 }
 
-KernelCall gate_poll_call(uint64_t* const* flags, int n, uint64_t* skip, uint64_t* err) {
+KernelCall gate_poll_call(uint64_t* const* flags, int n, const volatile uint64_t* cancel, uint64_t* seen,
+                          uint64_t* skip, uint64_t* err) {
   KernelCall k;
   k.func = reinterpret_cast<const void*>(gate_poll_kernel);
   k.block = dim3(32);
   k.push(flags);
   k.push(n);
+  k.push(cancel);
+  k.push(seen);
   k.push(skip);
   k.push(err);
   return k;

@@ -120,15 +120,16 @@ struct FlagSet {
   // (no data, signals still written).
   const uint64_t* skip = nullptr;
   // Folded prelaunch gate (a single-kernel prelaunch body):
-  // fold != 0 makes the kernel itself the gate of instance number `post_no`
-  // (set per instance when it is armed). polls[0] is then the unit's trigger
+  // a non-null `epoch` (device word: instances of this body completed so far)
+  // makes the kernel itself the gate. polls[0] is then the unit's trigger
   // word (1 go, 2 cancel; flags.cuh take_trigger). CTA 0 takes the trigger,
   // writes the start signals, polls and resets the other flags, and
-  // publishes the outcome in *gate (device word: (post_no + 1) * 4 + state)
-  // for the other CTAs; a cancel makes every CTA skip data and signals. No
-  // finish ticket unless there are signals.
-  int fold = 0;
-  uint64_t post_no = 0;
+  // publishes the outcome in *gate (device word: (epoch + 1) * 4 + state)
+  // for the other CTAs; a cancel makes every CTA skip data and signals. The
+  // last CTA (finish ticket, always present here) advances *epoch.
+  uint64_t* epoch = nullptr;
+  const volatile uint64_t* cancel = nullptr;  // host cancel count (flags.cuh take_trigger)
+  uint64_t* seen = nullptr;                   // cancels honoured (device)
   uint64_t* gate = nullptr;
 };
 
@@ -170,8 +171,9 @@ KernelCall reduce_call(const RedTable& t, int grid, const FlagSet* flags = nullp
 //  poll:   every flags[i] >= 1, then reset to 0 (ld.acquire.sys spin with a
 //          globaltimer bound; on timeout *err |= 1 and the kernel exits).
 //  signal: flags[i] = 1 with st.release.sys after a system-scope fence.
-//  gate:   take the unit's trigger word (1 go, 2 cancel; flags.cuh
-//          take_trigger): "go" opens the conditional body, "cancel" skips it.
+//  gate:   take the unit's trigger (flags.cuh take_trigger: the device
+//          trigger word, or a host cancel): "go" opens the conditional body,
+//          "cancel" skips it.
 // Load every kernel of the library on the current device (called at world
 // init for each device; see kernels.cu).
 cudaError_t preload_kernels();
@@ -179,13 +181,15 @@ cudaError_t preload_reduce_kernels();
 cudaError_t launch_poll(uint64_t* const* flags, int n, uint64_t* err, cudaStream_t stream);
 cudaError_t launch_signal(uint64_t* const* flags, int n, cudaStream_t stream);
 //  gate_poll: the gate of a kernel-only prelaunch body (no conditional node):
-//          takes the trigger word flags[0]; on "go" polls flags[1..n) (>= 1,
+//          takes the trigger (word flags[0]); on "go" polls flags[1..n) (>= 1,
 //          reset to 0, as poll) and writes *skip = 0; on "cancel" writes
 //          *skip = 1 so the mover after it returns at once.
 KernelCall poll_call(uint64_t* const* flags, int n, uint64_t* err);
 KernelCall signal_call(uint64_t* const* flags, int n);
-KernelCall gate_call(uint64_t* trigger, cudaGraphConditionalHandle handle, uint64_t* err);
-KernelCall gate_poll_call(uint64_t* const* flags, int n, uint64_t* skip, uint64_t* err);
+KernelCall gate_call(uint64_t* trigger, const volatile uint64_t* cancel, uint64_t* seen,
+                     cudaGraphConditionalHandle handle, uint64_t* err);
+KernelCall gate_poll_call(uint64_t* const* flags, int n, const volatile uint64_t* cancel, uint64_t* seen,
+                          uint64_t* skip, uint64_t* err);
 
 // NVLS multicast all-gather store (mcast.cpp, experimental): src (bytes, a
 // multiple of 16, 16-byte aligned) -> mc_dst with multimem.st (the switch

@@ -868,9 +868,15 @@ Status build_graph(World* w, Plan* p, Unit& u) {
   STATUS_TRY(write_device(d, nullptr, 64));
   p->dev_allocs.push_back(d);
   p->dev_alloc_device.push_back(u.device);
-  uint64_t* words = static_cast<uint64_t*>(d);  // [0] trigger [1] err [2] ticket [3] skip [4] gate
+  uint64_t* words = static_cast<uint64_t*>(d);  // [0] trigger [1] err [2] ticket [3] skip [4] gate [5] epoch [6] seen
   u.err = words + 1;
   u.ready_flag = words;
+  void* host = nullptr;
+  CUDA_TRY(cudaHostAlloc(&host, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(host, 0, 64);
+  u.cancel_host = static_cast<uint64_t*>(host);
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&u.cancel_dev), host, 0));
+  uint64_t* const seen = words + 6;
 
   // Polls: the unit's trigger word first (the gate takes it), then rdy from
   // destinations in other units; signals: done to those destinations (from
@@ -921,23 +927,23 @@ Status build_graph(World* w, Plan* p, Unit& u) {
     f.err = u.err;
     const int fg = fold_grid(w, p, u);
     if (fg > 0) {
-      // One kernel: gate (trigger word), polls (rdy), move, signals. Its
-      // instance number is set per instance at arm time (exec.cpp arm_unit).
-      f.fold = 1;
+      // One kernel: gate (trigger word), polls (rdy), move, signals; its
+      // last CTA advances the instance count the next instance gates on.
+      f.epoch = words + 5;
+      f.cancel = u.cancel_dev;
+      f.seen = seen;
       f.gate = words + 4;
       f.polls = u.poll_tab;
       f.npoll = u.npoll;
-      f.ctr = u.nsig ? reinterpret_cast<unsigned*>(words + 2) : nullptr;
+      f.ctr = reinterpret_cast<unsigned*>(words + 2);
       p->folded = true;
-      u.fold_call = items_call(u.table, fg, &f);
-      STATUS_TRY(sink.kernel(w, u.arm, u.fold_call));
-      u.fold_node = sink.tail(u.arm).front();
+      STATUS_TRY(sink.kernel(w, u.arm, items_call(u.table, fg, &f)));
     } else {
       // The mover never spins here (gate_poll did the waiting), so it keeps a
       // full grid without holding SMs while armed.
       f.ctr = u.nsig ? reinterpret_cast<unsigned*>(words + 2) : nullptr;
       f.skip = words + 3;
-      STATUS_TRY(sink.kernel(w, u.arm, gate_poll_call(u.poll_tab, u.npoll, words + 3, u.err)));
+      STATUS_TRY(sink.kernel(w, u.arm, gate_poll_call(u.poll_tab, u.npoll, u.cancel_dev, seen, words + 3, u.err)));
       STATUS_TRY(sink.kernel(w, u.arm, items_call(u.table, plan_grid(p, u.table), &f)));
     }
     CUDA_TRY(cudaGraphInstantiate(&u.exec, u.graph, 0));
@@ -948,7 +954,7 @@ Status build_graph(World* w, Plan* p, Unit& u) {
   cudaGraphConditionalHandle handle;
   CUDA_TRY(cudaGraphConditionalHandleCreate(&handle, u.graph, 0, cudaGraphCondAssignDefault));
   GraphSink top({u.graph});
-  STATUS_TRY(top.kernel(w, u.arm, gate_call(u.ready_flag, handle, u.err)));
+  STATUS_TRY(top.kernel(w, u.arm, gate_call(u.ready_flag, u.cancel_dev, seen, handle, u.err)));
 
   // cudaGraphNodeParams has no default constructor (union with non-trivial
   // members): zero-initialised raw storage, as the runtime expects.

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const RedItem* __re
   // Fused flags (kernels.hpp FlagSet): every source rank's send is ready.
   __shared__ int cta_state;
   if (threadIdx.x < 32) {
-    const int st = (flags.npoll || flags.npre || flags.fold || flags.skip) ? fused_wait(flags, sk) : kGo;
+    const int st = (flags.npoll || flags.npre || flags.epoch || flags.skip) ? fused_wait(flags, sk) : kGo;
     if (threadIdx.x == 0) cta_state = st;
   }
   __syncthreads();

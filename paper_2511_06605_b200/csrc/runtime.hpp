@@ -202,16 +202,15 @@ struct Unit {
   uint64_t** fin_tab = nullptr;
   int npoll = 0, nsig = 0, nfin = 0;
   // Trigger word (device memory owned by the plan, one per unit, so armed
-  // plans never share one): the caller stream writes 1 to trigger, a cancel
-  // writes 2 from a private stream; the gate takes it.
+  // plans never share one): the caller stream writes 1 to trigger; the gate
+  // takes it.
   uint64_t* ready_flag = nullptr;
+  // Cancels: a count in pinned host memory (written by the host, no stream)
+  // and its device alias; the gate honours each raise once.
+  uint64_t* cancel_host = nullptr;
+  uint64_t* cancel_dev = nullptr;
+  uint64_t cancels = 0;
   bool armed = false;
-  // Folded prelaunch body (lower.cpp fold): the single kernel node and its
-  // launch descriptor; each armed instance gets its instance number through
-  // its kernel parameters.
-  cudaGraphNode_t fold_node = nullptr;
-  KernelCall fold_call;
-  uint64_t instances = 0;
   // Recorded command list of a non-prelaunch plan (exec.cpp record_plan):
   // the unit's whole submission (flags, lanes, copies, kernels) as one graph.
   cudaGraph_t rec_graph = nullptr;

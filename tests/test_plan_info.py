@@ -115,6 +115,7 @@ def test_tma_tile_size_follows_the_table(comms, kind, s, tile, tiles):
     wave (a 64 KiB all-gather 8.2 -> 4.1 us per collective), 32 KiB tiles on
     the persistent grid above."""
     sends, recvs = _bufs(s, kind)
+    torch.cuda.synchronize()  # the inputs are written on the default stream
     fn = cc.all_gather if kind == "allgather" else cc.all_to_all
     fn(comms, sends, recvs, s, impl="sm", streams=torch.cuda.Stream())
     torch.cuda.synchronize()
