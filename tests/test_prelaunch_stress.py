@@ -41,7 +41,8 @@ SCRIPT = textwrap.dedent("""
                     plan = cc.Plan(comms, kind, recvs if swap else sends, recvs, s, impl=impl)
                     for _ in range(3):
                         plan.launch(streams)
-                    torch.cuda.synchronize() if not swap else None
+                    # armed now: no device-wide synchronisation before the
+                    # destroy (cecoll.h cecoll_plan_disarm)
                     plan.destroy()  # armed: the cancel path
                     fn = cc.all_gather if kind == "allgather" else cc.all_to_all
                     for _ in range(3):
