@@ -40,7 +40,6 @@ const DriverApi* driver_api() {
     ok &= load("cuGetErrorString", api.GetErrorString);
     ok &= load("cuGraphAddBatchMemOpNode", api.GraphAddBatchMemOpNode);
     ok &= load("cuCtxGetCurrent", api.CtxGetCurrent);
-    api.has_batch_memcpy = load("cuMemcpyBatchAsync", api.MemcpyBatchAsync);
     bool mc = load("cuMulticastCreate", api.MulticastCreate);
     mc &= load("cuMulticastGetGranularity", api.MulticastGetGranularity);
     mc &= load("cuMulticastAddDevice", api.MulticastAddDevice);

@@ -3,9 +3,9 @@
 // libcecoll links cudart statically and never links libcuda, so the shared
 // library loads (and its CPU-side planner runs) on a machine without a GPU
 // driver. The stream memory operations (cuStreamWaitValue64 /
-// cuStreamWriteValue64 / cuStreamBatchMemOp) and cuMemcpyBatchAsync have no
-// cudart equivalent; they are looked up once with
-// cudaGetDriverEntryPointByVersion the first time a communicator is created.
+// cuStreamWriteValue64 / cuStreamBatchMemOp) have no cudart equivalent;
+// they are looked up once with cudaGetDriverEntryPointByVersion the first
+// time a communicator is created.
 #pragma once
 
 #include <cuda.h>
@@ -19,8 +19,6 @@ struct DriverApi {
   CUresult (*StreamWaitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned) = nullptr;
   CUresult (*StreamWriteValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned) = nullptr;
   CUresult (*StreamBatchMemOp)(CUstream, unsigned, CUstreamBatchMemOpParams*, unsigned) = nullptr;
-  CUresult (*MemcpyBatchAsync)(CUdeviceptr*, CUdeviceptr*, size_t*, size_t, CUmemcpyAttributes*,
-                               size_t*, size_t, size_t*, CUstream) = nullptr;
   CUresult (*DeviceGetAttribute)(int*, CUdevice_attribute, CUdevice) = nullptr;
   CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
   CUresult (*MulticastCreate)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*) = nullptr;
@@ -51,7 +49,6 @@ struct DriverApi {
   CUresult (*CtxGetCurrent)(CUcontext*) = nullptr;
   bool has_multicast = false;
   bool loaded = false;
-  bool has_batch_memcpy = false;
 };
 
 // Returns the process-wide table, loading it on first use. Returns nullptr

@@ -50,12 +50,12 @@ const char* table_name(const ItemTable& t) {
 
 // Copy submission; when tracing (eager only) one call per copy, each
 // bracketed by events.
-Status issue_copies_traced(World* w, Sink& sink, const std::vector<Copy>& copies, cudaStream_t s, bool allow_batch,
+Status issue_copies_traced(World* w, Sink& sink, const std::vector<Copy>& copies, cudaStream_t s,
                            int device, int pid, int tid) {
-  if (!w->tracer) return sink.copies(w, copies, s, allow_batch);
+  if (!w->tracer) return sink.copies(w, copies, s);
   for (const Copy& c : copies) {
     cudaEvent_t b = sink.mark(w, device, s);
-    STATUS_TRY(sink.copies(w, {c}, s, false));
+    STATUS_TRY(sink.copies(w, {c}, s));
     trace_span(w, "copy:copy", pid, tid, device, b, sink.mark(w, device, s));
   }
   return {};
@@ -91,11 +91,11 @@ Status run_ce(World* w, Plan* p, Sink& sink) {
     DeviceGuard g(u.device);
     const double h0 = trace_host_now(w);
     const int pid = u.ranks[0];
-    STATUS_TRY(issue_copies_traced(w, sink, u.precopy, u.stream, true, u.device, pid, -1));
+    STATUS_TRY(issue_copies_traced(w, sink, u.precopy, u.stream, u.device, pid, -1));
     STATUS_TRY(submit_traced(w, sink, u.stream, u.start, u.start_remote_tab, u.start_remote.size(), "sync:signal",
                              u.device, pid, -1));
     for (int r : u.ranks) STATUS_TRY(sink.record(w, w->local[r]->start, u.stream));
-    STATUS_TRY(issue_copies_traced(w, sink, u.placement, u.stream, true, u.device, pid, -1));
+    STATUS_TRY(issue_copies_traced(w, sink, u.placement, u.stream, u.device, pid, -1));
     if (u.table.nitems)  // the lanes' merged item-kernel commands (lower.cpp lower_program)
       STATUS_TRY(kernel_traced(w, sink, u.stream, items_call(u.table, plan_grid(p, u.table)), table_name(u.table),
                                u.device, pid, -1));
@@ -108,7 +108,7 @@ Status run_ce(World* w, Plan* p, Sink& sink) {
     cudaStream_t s = rs->lanes[l.lane];
     STATUS_TRY(sink.wait(w, s, rs->start));
     STATUS_TRY(submit_traced(w, sink, s, l.pre, nullptr, 0, "poll:poll", rs->device, l.rank, l.lane));
-    STATUS_TRY(issue_copies_traced(w, sink, l.copies, s, true, rs->device, l.rank, l.lane));
+    STATUS_TRY(issue_copies_traced(w, sink, l.copies, s, rs->device, l.rank, l.lane));
     if (l.table.nitems)
       STATUS_TRY(kernel_traced(w, sink, s, items_call(l.table, plan_grid(p, l.table)), table_name(l.table), rs->device,
                                l.rank, l.lane));
@@ -157,7 +157,7 @@ Status run_sm(World* w, Plan* p, Sink& sink) {
         RankState* rs = w->local[l.rank].get();
         cudaStream_t ls = rs->lanes[l.lane];
         STATUS_TRY(sink.wait(w, ls, fork));
-        STATUS_TRY(issue_copies_traced(w, sink, l.copies, ls, false, rs->device, l.rank, l.lane));
+        STATUS_TRY(issue_copies_traced(w, sink, l.copies, ls, rs->device, l.rank, l.lane));
         STATUS_TRY(sink.record(w, rs->lane_done[l.lane], ls));
         forked.push_back(&l);
       }
@@ -236,7 +236,7 @@ Status trigger_signal(World* w, Unit& u, cudaEvent_t* span_begin) {
   StreamSink sink;
   const double h0 = trace_host_now(w);
   const int pid = u.ranks[0];
-  STATUS_TRY(issue_copies_traced(w, sink, u.precopy, u.stream, true, u.device, pid, -1));
+  STATUS_TRY(issue_copies_traced(w, sink, u.precopy, u.stream, u.device, pid, -1));
   MemOps ops = u.start;
   ops.push_back(op_write(u.ready_flag, 1));
   *span_begin = trace_mark(w, u.device, u.stream);

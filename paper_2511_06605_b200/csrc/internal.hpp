@@ -59,9 +59,8 @@ Status submit(World* w, cudaStream_t s, const MemOps& ops);
 // plan's first kernel could read the table before it is written (seen once
 // in eight fresh two-process runs, tools/pull_race_probe.py).
 Status write_device(void* dst, const void* src, size_t bytes);
-// Copy commands: one cuMemcpyBatchAsync (allow_batch, non-legacy stream) or
-// one cudaMemcpyAsync per copy.
-Status issue_copies(World* w, const std::vector<Copy>& copies, cudaStream_t s, bool allow_batch);
+// Copy commands: one cudaMemcpyAsync per copy, in order on stream s.
+Status issue_copies(World* w, const std::vector<Copy>& copies, cudaStream_t s);
 Status ensure_lanes(RankState* rs, int n);
 // Where an executor's commands go (sink.cpp): StreamSink
 // submits them to their streams now; GraphSink adds them as explicit nodes of
@@ -73,7 +72,7 @@ class Sink {
   virtual ~Sink() = default;
   virtual bool graph() const = 0;
   virtual Status memops(World* w, cudaStream_t s, const MemOps& ops) = 0;
-  virtual Status copies(World* w, const std::vector<Copy>& c, cudaStream_t s, bool allow_batch) = 0;
+  virtual Status copies(World* w, const std::vector<Copy>& c, cudaStream_t s) = 0;
   virtual Status kernel(World* w, cudaStream_t s, const KernelCall& k) = 0;
   virtual Status record(World* w, cudaEvent_t e, cudaStream_t s) = 0;
   virtual Status wait(World* w, cudaStream_t s, cudaEvent_t e) = 0;
@@ -88,7 +87,7 @@ class StreamSink : public Sink {
  public:
   bool graph() const override { return false; }
   Status memops(World* w, cudaStream_t s, const MemOps& ops) override;
-  Status copies(World* w, const std::vector<Copy>& c, cudaStream_t s, bool allow_batch) override;
+  Status copies(World* w, const std::vector<Copy>& c, cudaStream_t s) override;
   Status kernel(World* w, cudaStream_t s, const KernelCall& k) override;
   Status record(World* w, cudaEvent_t e, cudaStream_t s) override;
   Status wait(World* w, cudaStream_t s, cudaEvent_t e) override;
@@ -103,7 +102,7 @@ class GraphSink : public Sink {
   void map(cudaStream_t s, int graph);
   bool graph() const override { return true; }
   Status memops(World* w, cudaStream_t s, const MemOps& ops) override;
-  Status copies(World* w, const std::vector<Copy>& c, cudaStream_t s, bool allow_batch) override;
+  Status copies(World* w, const std::vector<Copy>& c, cudaStream_t s) override;
   Status kernel(World* w, cudaStream_t s, const KernelCall& k) override;
   Status record(World* w, cudaEvent_t e, cudaStream_t s) override;
   Status wait(World* w, cudaStream_t s, cudaEvent_t e) override;

@@ -975,7 +975,7 @@ Status build_graph(World* w, Plan* p, Unit& u) {
   // memory operations are not allowed in conditional bodies, hence kernels.
   GraphSink sink({body});
   STATUS_TRY(sink.kernel(w, u.arm, poll_call(u.poll_tab + 1, u.npoll - 1, u.err)));  // [0]: the gate's
-  STATUS_TRY(sink.copies(w, u.placement, u.arm, false));
+  STATUS_TRY(sink.copies(w, u.placement, u.arm));
   const cudaEvent_t fork = w->local[u.ranks[0]]->start;  // an ordering key inside the graph
   STATUS_TRY(sink.record(w, fork, u.arm));
   std::vector<const LaneExec*> busy;
@@ -985,7 +985,7 @@ Status build_graph(World* w, Plan* p, Unit& u) {
     RankState* rs = w->local[l.rank].get();
     cudaStream_t ls = rs->lanes[l.lane];
     STATUS_TRY(sink.wait(w, ls, fork));
-    STATUS_TRY(sink.copies(w, l.copies, ls, false));
+    STATUS_TRY(sink.copies(w, l.copies, ls));
     STATUS_TRY(sink.kernel(w, ls, items_call(l.table, plan_grid(p, l.table))));
     STATUS_TRY(sink.record(w, rs->lane_done[l.lane], ls));
     busy.push_back(&l);

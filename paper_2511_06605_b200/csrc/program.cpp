@@ -548,7 +548,7 @@ Impl reference_select(Kind kind, int64_t size) {
 // B200 selector (the winner_grid analog, sweep.cpp:186-218). One device
 // (co-resident ranks), from profiles/sweep_r01_*.csv: the SM path wins every
 // all-gather size (fan items read each source once) and all-to-all up to
-// 16 MiB chunks; above that the driver's batched copies (b2b) are ~5%
+// 16 MiB chunks; above that the driver's back-to-back copies (b2b) are ~5%
 // faster. Several devices: not measured in round 1 — the SM path for
 // latency-bound chunks, per-peer copies (copy engines over NVLink, one lane
 // per peer) above; their plans replay as recorded graphs (exec.cpp), which

@@ -21,8 +21,8 @@ namespace cecoll {
 
 Status StreamSink::memops(World* w, cudaStream_t s, const MemOps& ops) { return submit(w, s, ops); }
 
-Status StreamSink::copies(World* w, const std::vector<Copy>& c, cudaStream_t s, bool allow_batch) {
-  return issue_copies(w, c, s, allow_batch);
+Status StreamSink::copies(World* w, const std::vector<Copy>& c, cudaStream_t s) {
+  return issue_copies(w, c, s);
 }
 
 Status StreamSink::kernel(World* w, cudaStream_t s, const KernelCall& k) {
@@ -118,8 +118,8 @@ Status GraphSink::memops(World* w, cudaStream_t s, const MemOps& ops) {
   return {};
 }
 
-Status GraphSink::copies(World* w, const std::vector<Copy>& c, cudaStream_t s, bool allow_batch) {
-  (void)allow_batch;  // a recorded lane keeps its copies back to back as a chain of memcpy nodes
+Status GraphSink::copies(World* w, const std::vector<Copy>& c, cudaStream_t s) {
+  // a recorded lane keeps its copies back to back as a chain of memcpy nodes
   Tail& t = tail_of(s);
   for (const Copy& cp : c) {
     cudaGraphNode_t node = nullptr;

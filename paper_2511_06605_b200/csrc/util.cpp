@@ -105,34 +105,10 @@ Status write_device(void* dst, const void* src, size_t bytes) {
   return {};
 }
 
-Status issue_copies(World* w, const std::vector<Copy>& copies, cudaStream_t s, bool allow_batch) {
-  const DriverApi* d = driver_api();
-  // cuMemcpyBatchAsync rejects the legacy NULL stream.
-  const bool legacy = s == nullptr || s == cudaStreamLegacy;
-  // cuMemcpyBatchAsync cannot be captured: inside a caller's stream capture
-  // every copy becomes its own memcpy node.
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (!legacy && copies.size() > 1) cudaStreamIsCapturing(s, &cs);
-  const bool capturing = cs != cudaStreamCaptureStatusNone;
-  if (copies.size() > 1 && allow_batch && d->has_batch_memcpy && !legacy && !capturing) {
-    std::vector<CUdeviceptr> dst, src;
-    std::vector<size_t> sz;
-    for (const Copy& c : copies) {
-      dst.push_back(reinterpret_cast<CUdeviceptr>(c.dst));
-      src.push_back(reinterpret_cast<CUdeviceptr>(c.src));
-      sz.push_back(static_cast<size_t>(c.bytes));
-    }
-    CUmemcpyAttributes attr;
-    std::memset(&attr, 0, sizeof(attr));
-    attr.srcAccessOrder = CU_MEMCPY_SRC_ACCESS_ORDER_STREAM;
-    attr.flags = CU_MEMCPY_FLAG_PREFER_OVERLAP_WITH_COMPUTE;
-    size_t idx = 0, fail_idx = 0;
-    CU_TRY(d->MemcpyBatchAsync(dst.data(), src.data(), sz.data(), copies.size(), &attr, &idx, 1, &fail_idx,
-                               reinterpret_cast<CUstream>(s)));
-    w->counters[kCtrCopies] += static_cast<int64_t>(copies.size());
-    ++w->counters[kCtrApiCalls];
-    return {};
-  }
+Status issue_copies(World* w, const std::vector<Copy>& copies, cudaStream_t s) {
+  // One cudaMemcpyAsync per copy: a b2b lane's n-1 copies go out back to back
+  // on its stream (the driver's batched-copy entry point is not used: it
+  // faulted the GPU on this pool, profiles/README.md).
   for (const Copy& c : copies) {
     CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, static_cast<size_t>(c.bytes), cudaMemcpyDefault, s));
     ++w->counters[kCtrCopies];
