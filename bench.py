@@ -640,7 +640,9 @@ def run_sweep_rs(args):
         s = count * 2
         sends = [torch.randn(n * count, device="cuda").to(torch.bfloat16) for _ in range(n)]
         recvs = [torch.empty(count, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
-        for impl in ("sm", "pcpy", "b2b", "prelaunch_pcpy"):
+        torch.cuda.synchronize()  # inputs written on torch's stream, collectives on `stream`
+        for impl in [i for i in ("sm", "pcpy", "b2b", "prelaunch_pcpy")
+                     if not args.sweep_impls or i in args.sweep_impls.split(",")]:
             def call():
                 cc.reduce_scatter(comms, sends, recvs, count, dtype="bf16", op="sum", impl=impl, streams=stream)
 
@@ -830,10 +832,15 @@ def run_sweep(args):
     stream = torch.cuda.Stream()
     rows = []
     sizes = [4096 << (2 * k) for k in range(10)]  # 4 KiB .. 1 GiB
+    if args.sweep_sizes:
+        sizes = [int(float(x)) for x in args.sweep_sizes.split(",")]
     out_path = args.sweep_out
     O = ora.Oracle()
-    for kind in ("allgather", "alltoall"):
+    kinds = args.sweep_kinds.split(",") if args.sweep_kinds else ["allgather", "alltoall"]
+    for kind in kinds:
         impls = ["sm", "hybrid", "pull"] + cc.IMPLS_FOR[kind]
+        if args.sweep_impls:
+            impls = [i for i in impls if i in args.sweep_impls.split(",")]
         for s in sizes:
             in_bytes = s if kind == "allgather" else n * s
             if n * (in_bytes + n * s) > args.max_bytes:
@@ -847,6 +854,10 @@ def run_sweep(args):
                     rb = work
                 else:
                     work, rb = sends, recvs
+                # the inputs (and clones) are written on torch's stream; the
+                # collective runs on `stream` (the caller orders them, as with
+                # NCCL): without this a 2 GiB randint can still be running
+                torch.cuda.synchronize()
                 fn = cc.all_gather if kind == "allgather" else cc.all_to_all
                 plan = None
                 if args.api == "plan":
@@ -960,6 +971,9 @@ def main():
     ap.add_argument("--ranks", type=int, default=NRANKS)
     ap.add_argument("--sweep-out", default=os.path.join(ROOT, "gpurun_out", "sweep.csv"))
     ap.add_argument("--max-bytes", type=float, default=96e9)
+    ap.add_argument("--sweep-impls", default="", help="comma list: only these implementations")
+    ap.add_argument("--sweep-kinds", default="", help="comma list: allgather,alltoall")
+    ap.add_argument("--sweep-sizes", default="", help="comma list of per-peer chunk bytes")
     ap.add_argument("--api", default="eager", choices=["eager", "plan"],
                     help="sweep through the collective calls or through explicit plans")
     ap.add_argument("--interference", action="store_true", help="C4: all-gather beside a bf16 GEMM")

@@ -130,6 +130,13 @@ typedef struct {
   double bw_copy, bw_fan, bw_ce, bw_lanes, bw_swap;
   double l2_boost, l2_bytes; /* bandwidth factor when the buffers fit in L2 */
   double folded_max_bytes, prelaunch_gain_threshold;
+  /* SM mover tables larger than one wave of 32 KiB tiles on one CTA per SM
+   * (stream_min_bytes, fixed): pipeline fill and drain of the short-lived
+   * CTAs (kernels.cu TmaPolicy), added once per collective */
+  double t_stream, stream_min_bytes;
+  /* in-place swap items whose buffers fit in L2: their writes land on lines
+   * the same items just read, so they gain more than l2_boost */
+  double l2_boost_swap;
 } cecoll_model_t;
 void cecoll_model_default(cecoll_model_t* model);
 cecoll_status_t cecoll_model_predict(const cecoll_model_t* model, cecoll_kind_t kind, cecoll_impl_t impl,

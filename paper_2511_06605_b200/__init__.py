@@ -85,7 +85,8 @@ class ModelParams(C.Structure):
     _fields_ = [(k, C.c_double) for k in ("t_kernel", "t_graph", "t_branch", "t_node", "t_trigger", "bw_copy",
                                           "bw_fan", "bw_ce", "bw_lanes", "bw_swap", "l2_boost", "l2_bytes",
                                           "folded_max_bytes",
-                                          "prelaunch_gain_threshold")]
+                                          "prelaunch_gain_threshold", "t_stream", "stream_min_bytes",
+                                          "l2_boost_swap")]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

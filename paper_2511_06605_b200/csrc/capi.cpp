@@ -534,6 +534,9 @@ B200Model from_c(const cecoll_model_t* c) {
   m.l2_bytes = c->l2_bytes;
   m.folded_max_bytes = c->folded_max_bytes;
   m.prelaunch_gain_threshold = c->prelaunch_gain_threshold;
+  m.t_stream = c->t_stream;
+  m.stream_min_bytes = c->stream_min_bytes;
+  m.l2_boost_swap = c->l2_boost_swap;
   return m;
 }
 void to_c(const B200Model& m, cecoll_model_t* c) {
@@ -551,6 +554,9 @@ void to_c(const B200Model& m, cecoll_model_t* c) {
   c->l2_bytes = m.l2_bytes;
   c->folded_max_bytes = m.folded_max_bytes;
   c->prelaunch_gain_threshold = m.prelaunch_gain_threshold;
+  c->t_stream = m.t_stream;
+  c->stream_min_bytes = m.stream_min_bytes;
+  c->l2_boost_swap = m.l2_boost_swap;
 }
 }  // namespace
 

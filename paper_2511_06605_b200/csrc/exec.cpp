@@ -172,7 +172,7 @@ Status run_sm(World* w, Plan* p, Sink& sink) {
       }
     }
     if (u.red.nitems) {
-      STATUS_TRY(kernel_traced(w, sink, u.stream, reduce_call(u.red, plan_red_grid(p), fs), "kernel:reduce", u.device,
+      STATUS_TRY(kernel_traced(w, sink, u.stream, reduce_call(u.red, plan_red_grid(p, u.red), fs), "kernel:reduce", u.device,
                                pid, -1));
       if (u.fused) {
         w->counters[kCtrFlagWrites] += u.sm_flags.nsig;
@@ -436,8 +436,18 @@ int plan_grid(const Plan* p, const ItemTable& t) {
   return p->sm_budget > 0 ? std::min(g, p->sm_budget) : g;
 }
 
-int plan_red_grid(const Plan* p) {
-  const int g = 4 * p->sms;
+// Reduction kernel grid: ceil(tiles / 2) short-lived CTAs, at least 4 per SM
+// (the TMA mover's shape policy, kernels.cu TmaPolicy). With four sources'
+// loads in flight (reduce.cu) 16-256 MiB chunks went from 0.89-0.95 of the
+// copy peak (persistent grid, one source at a time) to 1.0-1.06
+// (profiles/tma_shape_r02.md); CECOLL_RED_TPC=0 restores the persistent grid.
+int plan_red_grid(const Plan* p, const RedTable& t) {
+  static const int tpc = [] {
+    const char* e = std::getenv("CECOLL_RED_TPC");
+    return e ? std::atoi(e) : 2;
+  }();
+  int g = 4 * p->sms;
+  if (tpc > 0) g = std::max(g, std::min((t.ntiles + tpc - 1) / tpc, kMaxGrid));
   return p->sm_budget > 0 ? std::min(g, p->sm_budget) : g;
 }
 
@@ -469,7 +479,7 @@ Status plan_launch(World* w, Plan* p, bool rearm) {
     StreamSink sink;
     for (Unit& u : p->units) {
       DeviceGuard g(u.device);
-      STATUS_TRY(sink.kernel(w, u.stream, reduce_call(u.red, plan_red_grid(p))));
+      STATUS_TRY(sink.kernel(w, u.stream, reduce_call(u.red, plan_red_grid(p, u.red))));
     }
     return {};
   }

@@ -203,15 +203,23 @@ __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
 #define CECOLL_TMA_STAGES 4
 #endif
 constexpr int kTmaStages = CECOLL_TMA_STAGES;
-constexpr int kTmaTile = 32 * 1024;
+constexpr int kTmaTile = 32 * 1024;  // largest tile
 constexpr int kTmaSmem = kTmaStages * kTmaTile;
-// CTAs of the TMA mover resident per SM (228 KiB of shared memory per SM)
-constexpr int kTmaPerSm = (228 * 1024) / (kTmaSmem + 8 * 1024);
+// The ring is sized per launch (kTmaStages x the table's tile). CTAs of the
+// TMA mover resident per SM at a tile size: 228 KiB of shared memory per SM,
+// 1 KiB reserved per CTA, the kernel's static shared memory (the mbarriers
+// and the first-tile table), at most 32 CTAs per SM.
+constexpr int kTmaStaticSmem = kTmaStages * 8 + kMaxItemsSmem * 4 + 256;  // ptxas: 4224 B
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// kLag 0: a stage is refilled as soon as its own stores have read it
+// (wait_group.read 0); kLag 1: the previous iteration's stage is refilled
+// after the current stores are issued (wait_group.read 1), so one tile's
+// stores are always in flight while the next load is issued.
+template <int kLag>
 __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict__ items, int nitems, int ntiles,
                                                           int tile_bytes, int uniform, int evict_first,
                                                           FlagSet flags) {
@@ -262,7 +270,7 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
-            "r"(smem_addr(ring + stage * kTmaTile)),
+            "r"(smem_addr(ring + stage * tile_bytes)),
         "l"(src), "r"(bytes), "r"(bar), "l"(policy)
         : "memory");
   };
@@ -286,7 +294,7 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
         : "memory");
     phase ^= 1u << st;
     const Item& it = items[sitem[st]];
-    const uint32_t from = smem_addr(ring + st * kTmaTile);
+    const uint32_t from = smem_addr(ring + st * tile_bytes);
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
                      it.dst + soff[st]),
                  "r"(from), "r"(nbytes[st]), "l"(policy)
@@ -298,12 +306,24 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
                      "r"(from), "r"(nbytes[st]), "l"(policy)
                      : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    if (issued < mine) {
-      // The stage is refilled once its store has finished reading it.
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    if (kLag == 0) {
+      if (issued < mine) {
+        // The stage is refilled once its store has finished reading it.
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        const char* src;
+        locate(issued, &src, &sitem[st], &soff[st], &nbytes[st]);
+        load(st, src, nbytes[st]);
+        ++issued;
+      }
+    } else if (k >= 1 && issued < mine) {
+      // Tile `issued` goes to stage issued % kTmaStages == (k - 1) % kTmaStages,
+      // whose stores (issued last iteration) have read it once every group
+      // but the newest has.
+      const int pst = (k - 1) % kTmaStages;
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       const char* src;
-      locate(issued, &src, &sitem[st], &soff[st], &nbytes[st]);
-      load(st, src, nbytes[st]);
+      locate(issued, &src, &sitem[pst], &soff[pst], &nbytes[pst]);
+      load(pst, src, nbytes[pst]);
       ++issued;
     }
   }
@@ -400,50 +420,107 @@ __global__ void __launch_bounds__(kRegThreads) mc_store_kernel(const int4* __res
 
 int64_t mover_tile_bytes(Mover m) { return m == Mover::Tma ? kTmaTile : kRegTile; }
 
-int table_tile(Mover m, const std::vector<int64_t>& sizes, int sms) {
+namespace {
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+// TMA mover shape (tools/fan_probe.cu, tools/r2_tma_ab.sh,
+// profiles/tma_shape_r02.md):
+//  * one-wave tables: the smallest tile that leaves one tile per CTA, with
+//    one resident CTA per SM counted (CECOLL_TMA_ONEWAVE_RES=0 counts the
+//    residency at each tile size instead);
+//  * larger copy tables (all-to-all): 16 KiB tiles, 2 tiles per CTA;
+//  * larger fan tables (all-gather: one read, n writes): 8 KiB tiles, one
+//    tile per CTA.
+// Short-lived CTAs, the hardware block scheduler refilling the SMs, beat a
+// persistent grid that walks each CTA through a strided band of tiles: the
+// 8-rank all-to-all at 16-256 MiB chunks 0.95 -> 1.07-1.09 of the measured
+// copy peak, the headline 64 x 8 MiB 0.163 -> 0.161 ms, the all-gather fan
+// at 16-256 MiB 0.89-0.90 -> 0.99-1.02. (Round 1's shape — 32 KiB tiles on
+// 2 waves of one CTA per SM — is CECOLL_TMA_TILE=32768 CECOLL_TMA_TPC=0.)
+// CECOLL_TMA_{TILE,WAVES,LAG,TPC} override the copy shape,
+// CECOLL_TMA_FAN_{TILE,WAVES,LAG,TPC} the fan shape (TPC 0: WAVES waves of
+// resident CTAs instead of tiles per CTA).
+struct TmaShape {
+  int tile, waves, lag;
+  int tpc;  // > 0: ceil(tiles / tpc) CTAs (tiles per CTA) instead of `waves`
+};
+struct TmaPolicy {
+  bool onewave_res1 = env_int("CECOLL_TMA_ONEWAVE_RES", 1) == 1;
+  TmaShape copy{env_int("CECOLL_TMA_TILE", 16384), env_int("CECOLL_TMA_WAVES", 2), env_int("CECOLL_TMA_LAG", 0),
+                env_int("CECOLL_TMA_TPC", 2)};
+  TmaShape fan{env_int("CECOLL_TMA_FAN_TILE", 8192), env_int("CECOLL_TMA_FAN_WAVES", 4),
+               env_int("CECOLL_TMA_FAN_LAG", 1), env_int("CECOLL_TMA_FAN_TPC", 1)};
+  bool fixed = env_int("CECOLL_TMA_FIXED_TILE", 0) == 1;
+  const TmaShape& shape(bool has_fan) const { return has_fan ? fan : copy; }
+};
+const TmaPolicy& tma_policy() {
+  static const TmaPolicy p;
+  return p;
+}
+int clamp_tile(int t) {
+  t = (t / 1024) * 1024;
+  return t < 4096 ? 4096 : (t > kTmaTile ? kTmaTile : t);
+}
+}  // namespace
+
+int tma_resident(int tile) {
+  const int per = (228 * 1024) / (kTmaStages * tile + kTmaStaticSmem + 1024);
+  return per < 1 ? 1 : (per > 32 ? 32 : per);
+}
+
+int table_tile(Mover m, const std::vector<int64_t>& sizes, int sms, int budget, bool has_fan) {
   if (m != Mover::Tma) return static_cast<int>(kRegTile);
-  static const bool fixed = [] {
-    const char* e = std::getenv("CECOLL_TMA_FIXED_TILE");
-    return e && std::string(e) == "1";
-  }();
-  if (fixed) return kTmaTile;
+  const TmaPolicy& pol = tma_policy();
+  if (pol.fixed) return kTmaTile;
   // The smallest tile (1 KiB steps, at least 4 KiB) that still gives every
   // resident CTA at most one tile: at these sizes parallelism wins over
   // pipelining inside a CTA (tools/latency: a 64 KiB all-gather 8.2 -> 4.1
-  // us). Tables that need more than one wave at 32 KiB keep 32 KiB tiles.
-  const int64_t slots = int64_t{kTmaPerSm} * sms;
-  for (int64_t t = 4096; t < kTmaTile; t += 1024) {
+  // us). An SM budget caps the CTAs that count.
+  for (int t = 4096; t <= kTmaTile; t += 1024) {
+    int64_t slots = int64_t{pol.onewave_res1 ? 1 : tma_resident(t)} * sms;
+    if (budget > 0) slots = std::min<int64_t>(slots, budget);
     int64_t n = 0;
     for (int64_t b : sizes) n += (b + t - 1) / t;
-    if (n <= slots) return static_cast<int>(t);
+    if (n <= slots) return t;
   }
-  return kTmaTile;
+  // Streaming tables. A budgeted plan keeps the largest ring (most bytes in
+  // flight per CTA it is allowed).
+  if (budget > 0) return kTmaTile;
+  return clamp_tile(pol.shape(has_fan).tile);
 }
 
-// Default: a persistent grid of 2 CTAs per SM (fastest alone; the TMA ring
-// holds 128 KiB of shared memory per CTA). Beside compute, the mover's SM
-// footprint is a policy: CECOLL_SM_GRID=<ctas> caps the grid (SM budget),
-// CECOLL_SM_TILES_PER_CTA=<k> launches short-lived CTAs of k tiles so the
-// block scheduler can interleave a higher-priority stream's CTAs
+// Register mover: a persistent grid of 2 CTAs per SM. TMA mover: ceil(tiles
+// / tpc) CTAs of the table's shape (TmaPolicy; a one-wave table launches one
+// CTA per tile: items_call caps the grid at the tile count). Beside compute, the mover's SM footprint is a policy: the
+// plan's SM budget (cecoll_comm_set_sm_budget) or CECOLL_SM_GRID=<ctas> caps
+// the grid, CECOLL_SM_TILES_PER_CTA=<k> launches short-lived CTAs of k tiles
+// so the block scheduler can interleave a higher-priority stream's CTAs
 // (profiles/interference_r01.json).
 int mover_grid(Mover m, int sms) {
   (void)m;
-  static const int cap = [] {
-    const char* e = std::getenv("CECOLL_SM_GRID");
-    return e ? std::atoi(e) : 0;
-  }();
+  static const int cap = env_int("CECOLL_SM_GRID", 0);
   return cap > 0 ? cap : 2 * sms;
 }
 
 int mover_grid_for(const ItemTable& t, int sms) {
-  static const int per_cta = [] {
-    const char* e = std::getenv("CECOLL_SM_TILES_PER_CTA");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (per_cta > 0) return (t.ntiles + per_cta - 1) / per_cta;
-  // a table tiled below 32 KiB is small: one wave of resident CTAs
-  if (t.mover == Mover::Tma && t.tile > 0 && t.tile < kTmaTile)
-    return std::min(mover_grid(t.mover, sms), kTmaPerSm * sms);
+  static const int per_cta = env_int("CECOLL_SM_TILES_PER_CTA", 0);
+  if (per_cta > 0) return std::min((t.ntiles + per_cta - 1) / per_cta, kMaxGrid);
+  if (t.mover == Mover::Tma) {
+    static const int cap = env_int("CECOLL_SM_GRID", 0);
+    const TmaPolicy& pol = tma_policy();
+    const int tile = t.tile > 0 ? t.tile : kTmaTile;
+    const TmaShape& sh = pol.shape(t.kinds & (1 << kItemFan));
+    const int64_t one_wave = int64_t{tma_resident(tile)} * sms;
+    int64_t g = std::max(1, sh.waves) * one_wave;
+    // a table that fits one wave keeps one tile per CTA (items_call caps the
+    // grid at the tile count); larger ones get ceil(tiles / tpc) CTAs
+    if (sh.tpc > 0 && t.ntiles > one_wave) g = (t.ntiles + sh.tpc - 1) / sh.tpc;
+    // fused_finish counts CTAs in 20 bits (flags.cuh): larger tables loop
+    g = std::min<int64_t>(g, kMaxGrid);
+    return cap > 0 ? std::min<int>(cap, static_cast<int>(g)) : static_cast<int>(g);
+  }
   return mover_grid(t.mover, sms);
 }
 
@@ -460,8 +537,10 @@ KernelCall items_call(const ItemTable& t, int grid, const FlagSet* fp) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 64 || !configured[dev].load(std::memory_order_acquire)) {
-      if (cudaFuncSetAttribute(tma_items_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem) !=
-          cudaSuccess)
+      if (cudaFuncSetAttribute(tma_items_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem) !=
+              cudaSuccess ||
+          cudaFuncSetAttribute(tma_items_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem) !=
+              cudaSuccess)
         return KernelCall{};
       if (dev < 64) configured[dev].store(true, std::memory_order_release);
     }
@@ -469,9 +548,10 @@ KernelCall items_call(const ItemTable& t, int grid, const FlagSet* fp) {
       const char* e = std::getenv("CECOLL_TMA_EVICT_FIRST");
       return e ? std::atoi(e) : 0;
     }();
-    k.func = reinterpret_cast<const void*>(tma_items_kernel);
+    const bool lag = tma_policy().shape(t.kinds & (1 << kItemFan)).lag == 1;
+    k.func = lag ? reinterpret_cast<const void*>(tma_items_kernel<1>) : reinterpret_cast<const void*>(tma_items_kernel<0>);
     k.block = dim3(32);
-    k.smem = kTmaSmem;
+    k.smem = kTmaStages * (t.tile > 0 ? t.tile : kTmaTile);
     k.push(static_cast<const Item*>(t.items));
     k.push(t.nitems);
     k.push(t.ntiles);
@@ -593,7 +673,8 @@ cudaError_t preload_kernels() {
       reinterpret_cast<const void*>(reg_items_kernel<(1 << kItemCopy), 2>),
       reinterpret_cast<const void*>(reg_items_kernel<(1 << kItemCopy) | (1 << kItemBcst), 2>),
       reinterpret_cast<const void*>(reg_items_kernel<15, 1>),
-      reinterpret_cast<const void*>(tma_items_kernel),
+      reinterpret_cast<const void*>(tma_items_kernel<0>),
+      reinterpret_cast<const void*>(tma_items_kernel<1>),
       reinterpret_cast<const void*>(poll_kernel),
       reinterpret_cast<const void*>(signal_kernel),
       reinterpret_cast<const void*>(gate_kernel),
@@ -604,7 +685,9 @@ cudaError_t preload_kernels() {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
   }
-  return cudaFuncSetAttribute(tma_items_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+  cudaError_t e = cudaFuncSetAttribute(tma_items_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(tma_items_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
 }
 
 }  // namespace cecoll

@@ -65,8 +65,8 @@ constexpr int kMaxFan = 32;
 //  Reg: 512-thread CTAs, 64 KiB tiles staged through registers (eight 16-byte
 //       loads in flight per thread), any alignment, any item kind.
 //  Tma: copy / fan tables whose items are 16-byte aligned with sizes that
-//       are multiples of 16: one elected thread per CTA streams 32 KiB tiles
-//       through a 4-stage shared-memory ring with cp.async.bulk
+//       are multiples of 16: one elected thread per CTA streams 4-32 KiB
+//       tiles through a 4-stage shared-memory ring with cp.async.bulk
 //       (global->shared on an mbarrier, shared->global as a bulk group; a
 //       fan tile is loaded once and stored once per destination).
 enum class Mover : int { Reg = 0, Tma = 1 };
@@ -82,13 +82,19 @@ struct ItemTable {
 };
 
 constexpr int kMaxItemsSmem = 1024;
+// Largest grid of an item or reduction kernel: fused_finish's tickets count
+// CTAs in 20 bits (flags.cuh); CTAs past the grid loop over further tiles.
+constexpr int kMaxGrid = 1 << 19;
 
 int64_t mover_tile_bytes(Mover m);
-// Tile size of a table of items of `sizes` bytes on a device with `sms` SMs:
-// the register mover uses 64 KiB tiles; the TMA mover the smallest tile (4-32
-// KiB) that leaves at most one tile per resident CTA, or 32 KiB tiles on its
-// persistent grid when even those need more than one wave.
-int table_tile(Mover m, const std::vector<int64_t>& sizes, int sms);
+// Tile size of a table of items of `sizes` bytes on a device with `sms` SMs
+// (budget: the plan's SM budget in CTAs, 0 = none): the register mover uses
+// 64 KiB tiles; the TMA mover the smallest tile (4-32 KiB) that leaves at
+// most one tile per resident CTA, else its streaming tile (kernels.cu
+// TmaPolicy; 32 KiB under a budget).
+int table_tile(Mover m, const std::vector<int64_t>& sizes, int sms, int budget = 0, bool has_fan = false);
+// CTAs of the TMA mover resident per SM when its ring holds `tile`-byte stages.
+int tma_resident(int tile);
 // Tiles of one item of `bytes` at `tile` bytes per tile.
 inline int64_t tiles_of(int64_t bytes, int tile) { return (bytes + tile - 1) / tile; }
 // Grid that fills the device for mover m (multiple of the SM count).

@@ -98,7 +98,7 @@ Status upload_items(Plan* p, int device, std::vector<HostItem>& host, ItemTable*
   }
   std::vector<int64_t> sizes;
   for (const HostItem& h : host) sizes.push_back(h.item.bytes);
-  out->tile = table_tile(out->mover, sizes, p->sms);
+  out->tile = table_tile(out->mover, sizes, p->sms, p->sm_budget, (kinds & (1 << kItemFan)) != 0);
   std::vector<Item> items;
   int64_t tiles = 0;
   size_t fan_at = 0;

@@ -73,20 +73,23 @@ double predict_ns(const B200Model& m_in, Kind kind, Impl impl, int64_t s, int n)
     m.bw_fan *= m.l2_boost;
     m.bw_ce *= m.l2_boost;
     m.bw_lanes *= m.l2_boost;
-    m.bw_swap *= m.l2_boost;
+    m.bw_swap *= m.l2_boost_swap;
   }
   const double bytes = hbm_bytes(kind, impl, s, n);
   const Impl base = base_of(impl);
   const double N = n;
   const bool merged = s < (int64_t{4} << 20);  // lower.cpp: flag-free bcst / swap commands in one kernel
+  // the SM mover's table: copy items (n·n·s) or fan items (n·s source bytes)
+  const double table = kind == Kind::AllGather && impl == Impl::Sm ? N * S : N * N * S;
+  const double stream = table > m.stream_min_bytes ? m.t_stream : 0.0;
   if (impl == Impl::Sm)
-    return m.t_kernel + bytes / (kind == Kind::AllGather ? m.bw_fan : m.bw_copy) * 1e9;
+    return m.t_kernel + stream + bytes / (kind == Kind::AllGather ? m.bw_fan : m.bw_copy) * 1e9;
   if (is_prelaunched(impl)) {
     // one gated graph: every chunk in the unit's item kernel (one GPU)
     const double body = bytes <= m.folded_max_bytes ? m.t_kernel : 2 * m.t_kernel;
     // the unit's one item kernel: TMA copy items, or register-mover swap items
     const double bw = base == Impl::Swap ? m.bw_swap : m.bw_copy;
-    return m.t_trigger + body + bytes / bw * 1e9;
+    return m.t_trigger + body + (base == Impl::Swap ? 0.0 : stream) + bytes / bw * 1e9;
   }
   // recorded command list: one graph per collective
   double t = m.t_graph;
@@ -188,15 +191,37 @@ double model_score(const B200Model& m, const std::vector<Measurement>& meas, std
     std::vector<int64_t>& ss = kv.second;
     std::sort(ss.begin(), ss.end());
     std::vector<Impl> measured, model;
-    for (int64_t s : ss) {
+    for (size_t k = 0; k < ss.size(); ++k) {
+      const int64_t s = ss[k];
       const auto& row = grid[{kv.first.first, n, s}];
       std::vector<Impl> cands;
       for (const auto& e : row) cands.push_back(e.first);
       Impl w = winner(cands, [&](Impl c) { return row.at(c); }, m.prelaunch_gain_threshold);
       // Measured ties are noise, not crossovers: the previous size's winner
-      // stays while it is within kTie of the best here.
+      // stays while it is within kTie of the best here. At the smallest size
+      // a tie goes to the tied implementation that stays within kTie of the
+      // best over the most consecutive sizes (an exact 4 KiB tie between two
+      // one-kernel programs is not a crossover either).
       if (!measured.empty() && row.count(measured.back()) && row.at(measured.back()) <= kTie * row.at(w))
         w = measured.back();
+      if (measured.empty()) {
+        auto run = [&](Impl c) {
+          size_t j = k;
+          for (; j < ss.size(); ++j) {
+            const auto& r = grid[{kv.first.first, n, ss[j]}];
+            double best = 1e300;
+            for (const auto& e : r) best = std::min(best, e.second);
+            if (!r.count(c) || r.at(c) > kTie * best) break;
+          }
+          return j - k;
+        };
+        size_t best_run = run(w);
+        for (Impl c : cands)
+          if (row.at(c) <= kTie * row.at(w) && run(c) > best_run) {
+            best_run = run(c);
+            w = c;
+          }
+      }
       measured.push_back(w);
       model.push_back(winner(cands, [&](Impl c) { return predict_ns(m, kind, c, s, n); }, m.prelaunch_gain_threshold));
     }
@@ -242,6 +267,8 @@ FitResult calibrate_b200(const std::vector<Measurement>& meas, uint64_t seed, in
     perturb(cand.bw_lanes);
     perturb(cand.bw_swap);
     perturb(cand.l2_boost);
+    perturb(cand.t_stream);
+    perturb(cand.l2_boost_swap);
     std::string r;
     const double sc = model_score(cand, meas, &r);
     if (sc < best_score) {  // hill-climb from improvements (calibrate.cpp:150-158)

@@ -29,6 +29,9 @@ struct B200Model {
   double l2_bytes = 96.0 * (1 << 20);  // that footprint (126 MB L2, fixed, not fitted)
   double folded_max_bytes = 8.0 * (1 << 20);  // prelaunch bodies up to this traffic are one folded kernel
   double prelaunch_gain_threshold = 0.002;    // winner_grid's tie-break (cost_model.hpp:30)
+  double t_stream = 3000;  // device: fill / drain of an SM mover table beyond one wave
+  double stream_min_bytes = 148.0 * 32768;  // one wave: 32 KiB tiles, one CTA per SM (fixed, not fitted)
+  double l2_boost_swap = 1.3;  // bw_swap's factor when the buffers fit in L2 (in-place: writes hit read lines)
 };
 
 struct Measurement {

@@ -546,20 +546,22 @@ Impl reference_select(Kind kind, int64_t size) {
 }
 
 // B200 selector (the winner_grid analog, sweep.cpp:186-218). One device
-// (co-resident ranks), from profiles/sweep_r01_*.csv: the SM path wins every
-// all-gather size (fan items read each source once) and all-to-all up to
-// 16 MiB chunks; above that the driver's back-to-back copies (b2b) are ~5%
-// faster. Several devices: not measured in round 1 — the SM path for
-// latency-bound chunks, per-peer copies (copy engines over NVLink, one lane
-// per peer) above; their plans replay as recorded graphs (exec.cpp), which
-// beat the gated prelaunch graphs at every measured size on one GPU
-// (profiles/sweep_r01_plan_n8_recorded.csv). CECOLL_SM_MAX_BYTES overrides
-// the SM cutoff. (bench_mgpu.py measures every implementation per size on
-// the multi-GPU node and reports the winner grid.)
+// (co-resident ranks), from profiles/latency_r02_n{8,2}_final.csv and
+// profiles/sweep_r02_plan_n{8,2}_final.csv: the SM path wins or ties every
+// size of both collectives since the mover runs short-lived CTAs (kernels.cu
+// TmaPolicy; round 1's persistent grid lost to the driver's back-to-back
+// copies, b2b, by ~5% above 16 MiB all-to-all chunks). Several devices: not
+// measured yet — the SM path for latency-bound chunks, per-peer copies (copy
+// engines over NVLink, one lane per peer) above; their plans replay as
+// recorded graphs (exec.cpp), which beat the gated prelaunch graphs at every
+// measured size on one GPU (profiles/sweep_r01_plan_n8_recorded.csv).
+// CECOLL_SM_MAX_BYTES overrides the SM cutoff. (bench_mgpu.py measures every
+// implementation per size on the multi-GPU node and reports the winner grid.)
 Impl select(Kind kind, int64_t size, int nranks, int ndevices, int sm_budget) {
   (void)nranks;
   int64_t sm_max;
-  if (ndevices <= 1) sm_max = kind == Kind::AllGather ? INT64_MAX : (int64_t{32} << 20);
+  (void)kind;
+  if (ndevices <= 1) sm_max = INT64_MAX;
   else sm_max = int64_t{1} << 20;
   // With an SM budget the caller keeps the SMs for its own compute: across
   // devices every transfer above the latency regime goes to the copy engines

@@ -7,7 +7,7 @@
 //
 // Roofline: HBM (or NVLink for peer sources): per output element nsrc reads
 // and one write. Each thread owns 16 consecutive elements of a 4096-element
-// tile and issues all of a source's 16-byte loads before folding them.
+// tile and issues four sources' 16-byte loads before folding them.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -52,6 +52,11 @@ __device__ __forceinline__ float fold(float acc, float x) {
   return (x < acc) ? x : acc;
 }
 
+// Sources whose loads are in flight together: 4 (with 2 tiles per CTA,
+// exec.cpp plan_red_grid, 16-256 MiB chunks 0.89-0.95 -> 1.0-1.06 of the copy
+// peak; 8 sources at once drop to 0.41-0.50, profiles/tma_shape_r02.md).
+constexpr int kBatch = 4;
+
 template <int kDtype, int kOp>
 __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const RedItem* __restrict__ items, int nitems,
                                                               int ntiles, FlagSet flags) {
@@ -80,20 +85,30 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const RedItem* __re
     float acc[kElemsPerThread];
     const bool full = base + kElemsPerThread <= it.elems;
     if (it.vec && full) {
-      for (int s = 0; s < it.nsrc; ++s) {
-        const int4* p = reinterpret_cast<const int4*>(it.srcs[s] + base * sizeof(T));
-        int4 v[kVecs];
+      // kBatch sources' loads in flight before any is folded (the fold order
+      // stays source 0, 1, ..., n-1)
+      for (int s0 = 0; s0 < it.nsrc; s0 += kBatch) {
+        int4 v[kBatch][kVecs];
 #pragma unroll
-        for (int k = 0; k < kVecs; ++k) v[k] = __ldg(p + k);
+        for (int b = 0; b < kBatch; ++b)
+          if (s0 + b < it.nsrc) {
+            const int4* p = reinterpret_cast<const int4*>(it.srcs[s0 + b] + base * sizeof(T));
 #pragma unroll
-        for (int k = 0; k < kVecs; ++k) {
-          const T* x = reinterpret_cast<const T*>(&v[k]);
-#pragma unroll
-          for (int e = 0; e < kVecElems; ++e) {
-            const float f = E::to_f(x[e]);
-            acc[k * kVecElems + e] = s == 0 ? f : fold<kOp>(acc[k * kVecElems + e], f);
+            for (int k = 0; k < kVecs; ++k) v[b][k] = __ldg(p + k);
           }
-        }
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b)
+          if (s0 + b < it.nsrc) {
+#pragma unroll
+            for (int k = 0; k < kVecs; ++k) {
+              const T* x = reinterpret_cast<const T*>(&v[b][k]);
+#pragma unroll
+              for (int e = 0; e < kVecElems; ++e) {
+                const float f = E::to_f(x[e]);
+                acc[k * kVecElems + e] = s0 + b == 0 ? f : fold<kOp>(acc[k * kVecElems + e], f);
+              }
+            }
+          }
       }
       int4 out[kVecs];
 #pragma unroll
@@ -168,11 +183,9 @@ cudaError_t launch_reduce(const RedTable& t, int grid, cudaStream_t stream, cons
 cudaError_t preload_reduce_kernels() {
   cudaFuncAttributes a;
   const void* fns[] = {
-      reinterpret_cast<const void*>(reduce_kernel<kF32, kSum>),  reinterpret_cast<const void*>(reduce_kernel<kF32, kMax>),
-      reinterpret_cast<const void*>(reduce_kernel<kF32, kMin>),  reinterpret_cast<const void*>(reduce_kernel<kBF16, kSum>),
-      reinterpret_cast<const void*>(reduce_kernel<kBF16, kMax>), reinterpret_cast<const void*>(reduce_kernel<kBF16, kMin>),
-      reinterpret_cast<const void*>(reduce_kernel<kF16, kSum>),  reinterpret_cast<const void*>(reduce_kernel<kF16, kMax>),
-      reinterpret_cast<const void*>(reduce_kernel<kF16, kMin>),
+      kernel_for<kF32>(kSum),  kernel_for<kF32>(kMax),  kernel_for<kF32>(kMin),
+      kernel_for<kBF16>(kSum), kernel_for<kBF16>(kMax), kernel_for<kBF16>(kMin),
+      kernel_for<kF16>(kSum),  kernel_for<kF16>(kMax),  kernel_for<kF16>(kMin),
   };
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);

@@ -303,7 +303,7 @@ void release_retired(World* w, bool force);
 int armed_units();  // prelaunch units armed in this process
 // Kernel grids under the plan's SM budget.
 int plan_grid(const Plan* p, const ItemTable& t);
-int plan_red_grid(const Plan* p);
+int plan_red_grid(const Plan* p, const RedTable& t);
 std::string plan_info(World* w, const Plan* p);
 // AUTO selection for the world (its device count and SM budget).
 Impl select_for(World* w, Kind kind, int64_t s);

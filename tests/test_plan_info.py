@@ -104,16 +104,18 @@ def test_sm_budget_caps_the_grid(comms):
         comms[0].set_sm_budget(0)
 
 
-@pytest.mark.parametrize("kind,s,tile,tiles", [
-    ("allgather", 65536, 4096, 128),        # 8 fan items: smallest tile leaving <= 1 tile per SM
-    ("allgather", 262144, 15360, 144),      # 8 x ceil(256 KiB / 15 KiB) = 144 <= 148
-    ("alltoall", 65536, 32768, 128),        # 64 items x 2 tiles already fit one wave
-    ("alltoall", 8 << 20, 32768, 64 * 256),  # the headline: 32 KiB tiles on the persistent grid
+@pytest.mark.parametrize("kind,s,tile,tiles,grid", [
+    ("allgather", 65536, 4096, 128, 128),         # 8 fan items: smallest tile leaving <= 1 tile per SM
+    ("allgather", 262144, 15360, 144, 144),       # 8 x ceil(256 KiB / 15 KiB) = 144 <= 148
+    ("alltoall", 65536, 32768, 128, 128),         # 64 items x 2 tiles already fit one wave
+    ("alltoall", 8 << 20, 16384, 64 * 512, 64 * 256),  # the headline: 16 KiB tiles, 2 tiles per CTA
+    ("allgather", 8 << 20, 8192, 8 * 1024, 8 * 1024),  # fan: 8 KiB tiles, one tile per CTA
 ])
-def test_tma_tile_size_follows_the_table(comms, kind, s, tile, tiles):
-    """kernels.cu table_tile: one tile per resident CTA while the table fits one
-    wave (a 64 KiB all-gather 8.2 -> 4.1 us per collective), 32 KiB tiles on
-    the persistent grid above."""
+def test_tma_tile_size_follows_the_table(comms, kind, s, tile, tiles, grid):
+    """kernels.cu table_tile / mover_grid_for: one tile per CTA while the table
+    fits one wave of one CTA per SM (a 64 KiB all-gather 8.2 -> 4.1 us per
+    collective); above, short-lived CTAs of the table kind's shape (copy: 16
+    KiB tiles, 2 per CTA; fan: 8 KiB tiles, 1 per CTA)."""
     sends, recvs = _bufs(s, kind)
     torch.cuda.synchronize()  # the inputs are written on the default stream
     fn = cc.all_gather if kind == "allgather" else cc.all_to_all
@@ -121,7 +123,7 @@ def test_tma_tile_size_follows_the_table(comms, kind, s, tile, tiles):
     torch.cuda.synchronize()
     u = comms[0].last_plan_info()["units"][0]
     assert u["mover"] == "tma" and u["tile_bytes"] == tile and u["tiles"] == tiles, u
-    assert u["grid"] == min(tiles, 296), u
+    assert u["grid"] == grid, u
     ok = all(torch.equal(recvs[j][i * s:(i + 1) * s], sends[i] if kind == "allgather" else sends[i][j * s:(j + 1) * s])
              for i in range(N) for j in range(N))
     assert ok

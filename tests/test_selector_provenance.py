@@ -4,9 +4,9 @@ cecoll_select picks for an out-of-place collective is within 10% (plus one
 ~2 µs device-time step) of the fastest out-of-place implementation — the analogue of the reference's own
 check that its table matches the simulated winners (acceptance.cpp:85-87).
 Latency regime (chunks <= 1 MiB): device time per collective from C++
-(tools/latency.cpp, profiles/latency_r01_n{8,2}_final.csv) — the Python
+(tools/latency.cpp, profiles/latency_r02_n{8,2}_final.csv) — the Python
 sweep is host-bound there. Bandwidth regime: the plan sweep
-(profiles/sweep_r01_plan_n{8,2}_final.csv). CPU only: reads the files."""
+(profiles/sweep_r02_plan_n{8,2}_final.csv). CPU only: reads the files."""
 import csv
 import os
 
@@ -17,17 +17,17 @@ import paper_2511_06605_b200 as cc
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 TOL = 1.10
 # Back-to-back device times of small collectives come in steps of ~2.05 µs
-# (profiles/latency_r01_n*_final.csv: 4.11, 6.15, 8.20 ...): one step of slack.
+# (profiles/latency_r02_n*_final.csv: 4.11, 6.15, 8.20 ...): one step of slack.
 SLACK_US = 2.1
 
 
 def _grid(n):
     t = {}
-    with open(os.path.join(ROOT, "profiles", f"latency_r01_n{n}_final.csv")) as f:
+    with open(os.path.join(ROOT, "profiles", f"latency_r02_n{n}_final.csv")) as f:
         for r in csv.DictReader(f):
             if r["api"] == "plan" and not r["impl"].endswith("swap"):
                 t.setdefault((r["collective"], int(r["size_bytes"])), {})[r["impl"]] = float(r["device_us_b2b"])
-    with open(os.path.join(ROOT, "profiles", f"sweep_r01_plan_n{n}_final.csv")) as f:
+    with open(os.path.join(ROOT, "profiles", f"sweep_r02_plan_n{n}_final.csv")) as f:
         for r in csv.DictReader(f):
             s = int(r["size_bytes"])
             if r.get("api") != "plan" or r["parity"] != "True" or r["impl"].endswith("swap") or s <= 1 << 20:
@@ -47,7 +47,8 @@ def test_selector_within_tolerance_of_measured_winner(n):
         assert pick in times, (kind, s, pick)
         best = min(times.values())
         assert times[pick] <= TOL * best + SLACK_US, (kind, s, pick, times)
-    # the table in words: the SM path everywhere for all-gather, up to 32 MiB
-    # for all-to-all, the driver's copies above
+    # the table in words: the SM path everywhere on one device (round 1: the
+    # driver's copies above 32 MiB all-to-all chunks, before the mover's
+    # short-lived CTAs)
     assert cc.select("allgather", 1 << 28, n, 1) == "sm"
-    assert cc.select("alltoall", 1 << 28, n, 1) == "b2b"
+    assert cc.select("alltoall", 1 << 28, n, 1) == "sm"

@@ -27,9 +27,10 @@ import paper_2511_06605_b200 as cc  # noqa: E402
 
 MODEL_IMPLS = {"sm", "pcpy", "b2b", "bcst", "swap", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_bcst",
                "prelaunch_swap"}
-DEFAULT_LATENCY = ["profiles/latency_r02_n8.csv", "profiles/latency_r02_n2.csv"]
-DEFAULT_SWEEP = ["profiles/sweep_r02_plan_n8.csv", "profiles/sweep_r01_plan_n4.csv",
-                 "profiles/sweep_r01_plan_n2_final.csv"]
+DEFAULT_LATENCY = ["profiles/latency_r02_n8_final.csv", "profiles/latency_r02_n4_final.csv",
+                   "profiles/latency_r02_n2_final.csv"]
+DEFAULT_SWEEP = ["profiles/sweep_r02_plan_n8_final.csv", "profiles/sweep_r02_plan_n4_final.csv",
+                 "profiles/sweep_r02_plan_n2_final.csv"]
 SWEEP_MIN = 4 << 20
 
 

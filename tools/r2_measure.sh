@@ -9,6 +9,7 @@ run() { local name=$1; shift; local t0=$(date +%s); timeout "$@"; echo "== $name
 [ -z "$SKIP_LAT" ] && run lat_n8 300 tools/latency 8 300 0 > gpurun_out/${tag}_lat_n8.csv
 [ -z "$SKIP_LAT" ] && run lat_n2 300 tools/latency 2 300 0 > gpurun_out/${tag}_lat_n2.csv
 [ -z "$SKIP_SWEEP" ] && run sweep_n8 900 python bench.py --sweep --api plan --ranks 8 --sweep-out gpurun_out/${tag}_sweep_n8.csv > gpurun_out/${tag}_sweep_n8.log 2>&1
+[ -z "$SKIP_SWEEP" ] && run sweep_n2 900 python bench.py --sweep --api plan --ranks 2 --sweep-out gpurun_out/${tag}_sweep_n2.csv > gpurun_out/${tag}_sweep_n2.log 2>&1
 [ -z "$SKIP_INTF" ] && run interference 900 python bench.py --interference --gemm-iters 100 --interference-out gpurun_out/${tag}_interference.json > gpurun_out/${tag}_interference.log 2>&1
 [ -z "$SKIP_SYNC" ] && run sync_chain 600 python bench.py --sync-chain --sync-out gpurun_out/${tag}_sync_chain.json > gpurun_out/${tag}_sync_chain.log 2>&1
 [ -z "$SKIP_RS" ] && run sweep_rs 600 python bench.py --sweep-rs --sweep-out gpurun_out/${tag}_sweep_rs.csv > gpurun_out/${tag}_sweep_rs.log 2>&1
