@@ -582,6 +582,9 @@ def run(args, B):
         STATE["prefix"] = "experiments-grade sweep: "  # a hang here leaves the main line standing
         sweep_pass(world, rank, dev, nccl, stream, t_start, args, line["sweep"]["rows"], prelaunch=True)
         STATE["prefix"] = ""
+    if not args.no_mgpu_experiments and from_rank0(time.time() - t_start < args.mgpu_budget + 240):
+        STATE["phase"] = "experiments tune"
+        run_tune_experiment(world, rank, dev, stream, line["experiments"])
     if not args.no_mgpu_experiments:
         STATE["phase"] = "experiments multicast"
         run_mc_experiment(world, rank, dev, stream, line["experiments"])
@@ -1122,6 +1125,35 @@ def run_experiments(comms, sets, n, s, my_ranks, stream, out):
                 else:
                     os.environ[k] = v
         out[f"{name}/{kind}"] = res
+
+
+def run_tune_experiment(world, rank, dev, stream, out):
+    """cecoll_tune on the node (csrc/tune.cpp): one rank per GPU, every
+    applicable implementation at 4 KiB-16 MiB chunks, device time max over
+    ranks and processes; the measured winner grid that replaces the static
+    multi-device guess in program.cpp select. Reports the
+    installed table, every candidate's time, and whether every process
+    installed the same table."""
+    res = {}
+    out["tune"] = res
+    comms = cc.Comm.init_ranks(world, rank, 1, dev, cc.torch_exchange())
+    try:
+        t0 = time.time()
+        cc.tune(comms, max_chunk=16 << 20, streams=stream)
+        table = comms[0].tuned_table()
+        tables = [None] * world
+        dist.all_gather_object(tables, table)
+        res["seconds"] = round(time.time() - t0, 1)
+        res["table"] = [f"{k} {s} {i}" for k, s, i in table]
+        res["same_on_every_rank"] = all(t == table for t in tables)
+        res["us"] = {f"{k} {s}": v["us"] for (k, s), v in comms[0].tune_report().items()}
+        res["static"] = {f"{k} {s}": cc.select(k, s, world, world) for k, s, _ in table}
+    except Exception as e:  # noqa: BLE001
+        res["error"] = str(e)[:200]
+    finally:
+        torch.cuda.synchronize()
+        dist.barrier()
+        quiet_destroy(comms)
 
 
 def run_mc_experiment(world, rank, dev, stream, out):

@@ -217,6 +217,33 @@ cecoll_status_t cecoll_comm_info(cecoll_comm_t comm, int* rank, int* nranks, int
  * world; cached plans of another budget are not reused. */
 cecoll_status_t cecoll_comm_set_sm_budget(cecoll_comm_t comm, int max_ctas);
 
+/* Measured selector (csrc/tune.cpp; the reference's run_sweep + winner_grid,
+ * sweep.cpp:71-218, executed on this machine). Times every applicable
+ * all-gather and all-to-all implementation (sm, pcpy, b2b, bcst, hybrid,
+ * pull, prelaunch_*) at 4 KiB x 4^k chunks up to max_chunk_bytes (0: 64 MiB)
+ * on scratch buffers, device time per collective back to back, max over
+ * ranks; picks the winner per size (the plain variant wins a near tie with
+ * its prelaunch form, prelaunch_gain_threshold; the static selector's choice
+ * keeps a tie within 3%) and installs the table: CECOLL_IMPL_AUTO on this
+ * world then uses the nearest tuned size (log scale) while no SM budget is
+ * set. comms: every local communicator of one world (all ranks of a
+ * cecoll_comm_init_all world; a process's own ranks otherwise — every
+ * process calls it with the same max_chunk_bytes, and the times are agreed
+ * through the init exchange so every rank installs the same table).
+ * streams: one per comm, or NULL for one private stream per device. Needs
+ * 2 * nranks * max_chunk_bytes of device memory per rank while it runs;
+ * refused while a prelaunch plan is armed. Collective, blocking. */
+cecoll_status_t cecoll_tune(const cecoll_comm_t* comms, int n, int64_t max_chunk_bytes, void* const* streams);
+/* The installed table as text, one "<allgather|alltoall> <chunk_bytes> <impl>"
+ * line per tuned size; *len = bytes needed (with the terminating NUL). */
+cecoll_status_t cecoll_tune_table(cecoll_comm_t comm, char* buf, size_t cap, size_t* len);
+/* The last cecoll_tune's measurements: per kind and size, every candidate's
+ * device µs per collective (-1: rejected) and the winner, one line each. */
+cecoll_status_t cecoll_tune_report(cecoll_comm_t comm, char* buf, size_t cap, size_t* len);
+/* Installs a table in that text form (e.g. saved from an earlier run on the
+ * same node; load the same text on every process); "" clears it. */
+cecoll_status_t cecoll_tune_load(cecoll_comm_t comm, const char* text);
+
 /* Buffer registration (≙ BufferId::Input/Output being addressable on every
  * GPU, program.hpp:36). Single-process: optional no-op. Multi-process:
  * collective (each process registers its local ranks in the same order);

@@ -156,6 +156,10 @@ def lib():
         "cecoll_plan_info": ([vp, C.c_char_p, sz, C.POINTER(sz)], i32),
         "cecoll_comm_last_plan_info": ([vp, C.c_char_p, sz, C.POINTER(sz)], i32),
         "cecoll_comm_set_sm_budget": ([vp, i32], i32),
+        "cecoll_tune": ([C.POINTER(vp), i32, i64, C.POINTER(vp)], i32),
+        "cecoll_tune_table": ([vp, C.c_char_p, sz, C.POINTER(sz)], i32),
+        "cecoll_tune_load": ([vp, C.c_char_p], i32),
+        "cecoll_tune_report": ([vp, C.c_char_p, sz, C.POINTER(sz)], i32),
         "cecoll_select_budget": ([i32, i64, i32, i32, i32], i32),
         "cecoll_model_default": ([C.POINTER(ModelParams)], None),
         "cecoll_model_predict": ([C.POINTER(ModelParams), i32, i32, i64, i32, C.POINTER(C.c_double)], i32),
@@ -186,6 +190,7 @@ EXPORTED_SYMBOLS = [
     "cecoll_mc_window_create", "cecoll_mc_allgather", "cecoll_mc_handle_type", "cecoll_mc_window_destroy",
     "cecoll_plan_info", "cecoll_comm_last_plan_info", "cecoll_comm_set_sm_budget", "cecoll_select_budget",
     "cecoll_model_default", "cecoll_model_predict", "cecoll_model_winner", "cecoll_model_fit",
+    "cecoll_tune", "cecoll_tune_table", "cecoll_tune_load", "cecoll_tune_report",
 ]
 DTYPES = {"f32": 0, "float32": 0, "bf16": 1, "bfloat16": 1, "f16": 2, "float16": 2}
 REDOPS = {"sum": 0, "max": 1, "min": 2}
@@ -426,6 +431,39 @@ class Comm:
         CTAs per kernel (0: full grid); AUTO prefers the copy engines."""
         _check(lib().cecoll_comm_set_sm_budget(self._h, max_ctas), "comm_set_sm_budget")
 
+    def tuned_table(self) -> list:
+        """cecoll_tune_table: the world's measured winner grid as
+        [(kind, chunk_bytes, impl), ...] (empty: the static selector)."""
+        n = C.c_size_t()
+        _check(lib().cecoll_tune_table(self._h, None, 0, C.byref(n)), "tune_table")
+        buf = C.create_string_buffer(n.value)
+        _check(lib().cecoll_tune_table(self._h, buf, n.value, C.byref(n)), "tune_table")
+        rows = []
+        for line in buf.value.decode().splitlines():
+            kind, s, impl = line.split()
+            rows.append((kind, int(s), impl))
+        return rows
+
+    def tune_report(self) -> dict:
+        """cecoll_tune_report: {(kind, chunk_bytes): {"us": {impl: µs}, "winner": impl}}."""
+        n = C.c_size_t()
+        _check(lib().cecoll_tune_report(self._h, None, 0, C.byref(n)), "tune_report")
+        buf = C.create_string_buffer(n.value)
+        _check(lib().cecoll_tune_report(self._h, buf, n.value, C.byref(n)), "tune_report")
+        out = {}
+        for line in buf.value.decode().splitlines():
+            head, win = line.split(" -> ")
+            parts = head.split()
+            us = {k: float(v) for k, v in (p.split("=") for p in parts[2:])}
+            out[(parts[0], int(parts[1]))] = {"us": us, "winner": win}
+        return out
+
+    def load_tuned(self, rows):
+        """cecoll_tune_load: install a table ([(kind, chunk_bytes, impl)] or
+        its text form); an empty one clears it."""
+        text = rows if isinstance(rows, str) else "".join(f"{k} {s} {i}\n" for k, s, i in rows)
+        _check(lib().cecoll_tune_load(self._h, text.encode()), "tune_load")
+
     def last_plan_info(self) -> dict:
         """cecoll_comm_last_plan_info: what the latest eager collective ran."""
         return _json_out(lib().cecoll_comm_last_plan_info, self._h)
@@ -522,6 +560,20 @@ class Trace:
 
         with open(path, "w") as f:
             json.dump(self.events, f, indent=1)
+
+
+def tune(comms: Sequence[Comm], max_chunk: int = 64 << 20, streams=None):
+    """cecoll_tune: measure every applicable implementation on this machine
+    (4 KiB x 4^k chunks up to max_chunk) and let AUTO use the winners. Pass
+    every local communicator of the world (every process calls it)."""
+    n = len(comms)
+    hs = (C.c_void_p * n)(*[c._h for c in comms])
+    ss = None
+    if streams is not None:
+        if not isinstance(streams, (list, tuple)):
+            streams = [streams] * n
+        ss = (C.c_void_p * n)(*[_stream(s) for s in streams])
+    _check(lib().cecoll_tune(hs, n, max_chunk, ss), "tune")
 
 
 def destroy_all(comms: Sequence[Comm]):

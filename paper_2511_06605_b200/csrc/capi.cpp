@@ -3,11 +3,13 @@
 // CECOLL_UNSUPPORTED and the message is kept for cecoll_last_error().
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "cecoll.h"
+#include "internal.hpp"
 #include "model.hpp"
 #include "program.hpp"
 #include "runtime.hpp"
@@ -218,6 +220,73 @@ cecoll_impl_t cecoll_reference_select(cecoll_kind_t kind, int64_t chunk_bytes) {
 
 cecoll_impl_t cecoll_select(cecoll_kind_t kind, int64_t chunk_bytes, int nranks, int ndevices) {
   return static_cast<cecoll_impl_t>(select(static_cast<Kind>(kind), chunk_bytes, nranks, ndevices));
+}
+
+cecoll_status_t cecoll_tune(const cecoll_comm_t* comms, int n, int64_t max_chunk_bytes, void* const* streams) {
+  if (!comms || n <= 0 || !comms[0] || !comms[0]->world) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  if (g_group_depth > 0) return err(CECOLL_INVALID_ARGUMENT, "cecoll_tune: not inside a group");
+  World* w = comms[0]->world;
+  std::vector<int> ranks;
+  for (int i = 0; i < n; ++i) {
+    if (!comms[i] || comms[i]->world != w) return err(CECOLL_INVALID_ARGUMENT, "cecoll_tune: communicators of one world");
+    ranks.push_back(comms[i]->rank);
+  }
+  if (static_cast<int>(ranks.size()) != (w->multiprocess ? w->nlocal : w->nranks))
+    return err(CECOLL_INVALID_ARGUMENT, "cecoll_tune: pass every local communicator of the world");
+  std::vector<cudaStream_t> ss(ranks.size(), nullptr);
+  std::map<int, cudaStream_t> own;  // one private stream per device
+  for (size_t k = 0; k < ranks.size(); ++k) {
+    if (streams && streams[k]) {
+      ss[k] = static_cast<cudaStream_t>(streams[k]);
+      continue;
+    }
+    const int dev = w->device[ranks[k]];
+    if (!own.count(dev)) {
+      DeviceGuard g(dev);
+      cudaStream_t s = nullptr;
+      if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
+        return err(CECOLL_CUDA_ERROR, "cecoll_tune: stream creation failed");
+      own[dev] = s;
+    }
+    ss[k] = own[dev];
+  }
+  std::string report;
+  Status s = world_tune(w, ranks, max_chunk_bytes, ss, &report);
+  for (auto& kv : own) {
+    DeviceGuard g(kv.first);
+    cudaStreamSynchronize(kv.second);
+    cudaStreamDestroy(kv.second);
+  }
+  return st(s);
+}
+
+cecoll_status_t cecoll_tune_table(cecoll_comm_t comm, char* buf, size_t cap, size_t* len) {
+  if (!comm || !comm->world) return err(CECOLL_INVALID_ARGUMENT, "null communicator");
+  const std::string t = tuned_text(comm->world);
+  if (len) *len = t.size() + 1;
+  if (buf && cap) {
+    const size_t m = std::min(cap - 1, t.size());
+    std::memcpy(buf, t.data(), m);
+    buf[m] = 0;
+  }
+  return CECOLL_SUCCESS;
+}
+
+cecoll_status_t cecoll_tune_report(cecoll_comm_t comm, char* buf, size_t cap, size_t* len) {
+  if (!comm || !comm->world) return err(CECOLL_INVALID_ARGUMENT, "null communicator");
+  const std::string& t = comm->world->tune_report;
+  if (len) *len = t.size() + 1;
+  if (buf && cap) {
+    const size_t m = std::min(cap - 1, t.size());
+    std::memcpy(buf, t.data(), m);
+    buf[m] = 0;
+  }
+  return CECOLL_SUCCESS;
+}
+
+cecoll_status_t cecoll_tune_load(cecoll_comm_t comm, const char* text) {
+  if (!comm || !comm->world || !text) return err(CECOLL_INVALID_ARGUMENT, "null argument");
+  return st(tuned_load(comm->world, text));
 }
 
 cecoll_status_t cecoll_comm_init_all(cecoll_comm_t* comms, int nranks, const int* devlist) {

@@ -556,7 +556,13 @@ Status lower_program(World* w, Plan* p, const Addressing& ad, const std::vector<
 
 }  // namespace
 
-Impl select_for(World* w, Kind kind, int64_t s) { return select(kind, s, w->nranks, w->ndevices, w->sm_budget); }
+Impl select_for(World* w, Kind kind, int64_t s) {
+  if (w->sm_budget == 0) {  // a budget changes the preference: the static policy decides
+    const Impl t = tuned_select(w, kind, s);
+    if (t != Impl::Auto) return t;
+  }
+  return select(kind, s, w->nranks, w->ndevices, w->sm_budget);
+}
 
 Status plan_create(World* w, Kind kind, Impl impl, int64_t s, const std::vector<CallArgs>& args, Plan** out,
                    const Program* given) {

@@ -125,6 +125,11 @@ struct World {
   // most CTAs any mover / reduction kernel of a plan may launch (0: a full
   // persistent grid), and the AUTO selector prefers copy-engine lanes.
   int sm_budget = 0;
+  // Measured winner grid (cecoll_tune / cecoll_tune_load, tune.cpp): per
+  // collective kind, ascending (chunk bytes, implementation); when present
+  // and no SM budget is set it drives CECOLL_IMPL_AUTO for this world.
+  std::map<int, std::vector<std::pair<int64_t, Impl>>> tuned;
+  std::string tune_report;  // the last cecoll_tune's measurements, one line per size
   Plan* last_plan = nullptr;  // the cached plan of the latest eager call (cecoll_comm_last_plan_info)
   std::vector<Plan*> explicit_plans;         // cecoll_plan_create; cancelled at release
   std::vector<Window> windows;
@@ -307,6 +312,16 @@ int plan_red_grid(const Plan* p, const RedTable& t);
 std::string plan_info(World* w, const Plan* p);
 // AUTO selection for the world (its device count and SM budget).
 Impl select_for(World* w, Kind kind, int64_t s);
+
+// tune.cpp: the measured winner grid. world_tune sweeps every applicable
+// implementation over 4 KiB x 4^k chunks up to max_chunk on the local ranks
+// `ranks` (streams[k] for ranks[k]) and installs the table; tuned_select
+// returns Impl::Auto when the world has no table for `kind`.
+Status world_tune(World* w, const std::vector<int>& ranks, int64_t max_chunk, const std::vector<cudaStream_t>& streams,
+                  std::string* report);
+Impl tuned_select(const World* w, Kind kind, int64_t s);
+std::string tuned_text(const World* w);
+Status tuned_load(World* w, const std::string& text);
 
 // NVLS multicast all-gather windows (mcast.cpp, experimental).
 struct McWindow;
