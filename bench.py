@@ -660,9 +660,9 @@ def run_sweep_rs(args):
             hbm = n * (n + 1) * s / (ms / 1e3) / 1e9
             # the bytes this form must move: the SM path reads every rank's
             # chunk in place (n(n+1)s); the copy-engine forms first gather
-            # the n^2 chunks into staging (read + write) and the reduction
-            # reads them back (3n^2 s + n s)
-            own = n * (n + 1) * s if impl == "sm" else (3 * n * n + n) * s
+            # the n(n-1) remote chunks into staging (read + write) and the
+            # reduction reads n chunks per rank and writes one ((3n^2 - n)s)
+            own = n * (n + 1) * s if impl == "sm" else (3 * n * n - n) * s
             row = {"impl": impl, "collective": "reduce_scatter_bf16_sum", "ranks": n, "size_bytes": s,
                    "total_ns": round(ms * 1e6), "busbw_gbs": round(busbw(n, s, ms / 1e3), 3),
                    "hbm_gbs": round(hbm, 1), "roofline_frac": round(hbm / peak, 4),

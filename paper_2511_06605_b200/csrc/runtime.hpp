@@ -286,8 +286,10 @@ Status run_collective(World* w, Kind kind, Impl impl, int64_t chunk, const std::
 
 // `given`: execute this program (e.g. parsed from the reference's
 // dump_program text) instead of compiling one.
+// `no_placement`: skip the local-slot placement copies (the reduce-scatter's
+// copy-engine gather reads each rank's own chunk in place).
 Status plan_create(World* w, Kind kind, Impl impl, int64_t chunk, const std::vector<CallArgs>& args, Plan** out,
-                   const Program* given = nullptr);
+                   const Program* given = nullptr, bool no_placement = false);
 // Reduce-scatter: count elements of `dtype` per rank chunk.
 // impl Sm: one kernel per unit reads every rank's chunk (peer loads over
 // NVLink); pcpy / b2b / prelaunch_*: an all-to-all over the copy engines into
