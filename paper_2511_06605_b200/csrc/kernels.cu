@@ -169,6 +169,8 @@ __global__ void __launch_bounds__(kRegThreads, kMinBlocks)
   // any data moves) is not needed.
   __shared__ int first[kMaxItemsSmem];
   __shared__ int cta_state;
+  // no-op unless launched behind a programmatic edge (see gate_poll_kernel)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint64_t sk = threadIdx.x < 32 ? read_skip(flags) : 0;
   if (!uniform)
     for (int i = threadIdx.x; i < nitems; i += kRegThreads) first[i] = items[i].first_tile;
@@ -226,6 +228,7 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ int first[kMaxItemsSmem];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // see reg_items_kernel
   const uint64_t sk = read_skip(flags);
   if (!uniform)  // see reg_items_kernel
     for (int i = threadIdx.x; i < nitems; i += 32) first[i] = items[i].first_tile;
@@ -392,6 +395,10 @@ __global__ void gate_poll_kernel(uint64_t* const* flags, int n, const volatile u
   // peer never released (skip = 2: no data, signals still written; the
   // world's error is sticky from here on)
   ok = __all_sync(0xffffffffu, ok);
+  // A mover behind a programmatic edge (CECOLL_PRELAUNCH_PDL=1) may launch
+  // now; it still waits (griddepcontrol.wait) until this grid has finished
+  // and its skip word is visible.
+  asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x == 0) *skip = ok ? 0 : 2;
 }
 

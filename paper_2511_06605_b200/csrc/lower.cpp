@@ -953,6 +953,21 @@ Status build_graph(World* w, Plan* p, Unit& u) {
       f.skip = words + 3;
       STATUS_TRY(sink.kernel(w, u.arm, gate_poll_call(u.poll_tab, u.npoll, u.cancel_dev, seen, words + 3, u.err)));
       STATUS_TRY(sink.kernel(w, u.arm, items_call(u.table, plan_grid(p, u.table), &f)));
+      // CECOLL_PRELAUNCH_PDL=1: the gate -> mover edge becomes programmatic,
+      // so the mover's CTAs launch while the gate finishes (tools/pdl_probe.cu)
+      const char* pdl = std::getenv("CECOLL_PRELAUNCH_PDL");
+      if (pdl && std::string(pdl) == "1") {
+        size_t ne = 1;
+        cudaGraphNode_t from = nullptr, to = nullptr;
+        CUDA_TRY(cudaGraphGetEdges(u.graph, &from, &to, &ne));
+        if (ne == 1) {
+          CUDA_TRY(cudaGraphRemoveDependencies(u.graph, &from, &to, 1));
+          cudaGraphEdgeData ed = {};
+          ed.from_port = cudaGraphKernelNodePortProgrammatic;
+          ed.type = cudaGraphDependencyTypeProgrammatic;
+          CUDA_TRY(cudaGraphAddDependencies_v2(u.graph, &from, &to, &ed, 1));
+        }
+      }
     }
     CUDA_TRY(cudaGraphInstantiate(&u.exec, u.graph, 0));
     return {};
