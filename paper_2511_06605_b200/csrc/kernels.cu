@@ -437,7 +437,10 @@ int env_int(const char* name, int dflt) {
 //  * one-wave tables: the smallest tile that leaves one tile per CTA, with
 //    one resident CTA per SM counted (CECOLL_TMA_ONEWAVE_RES=0 counts the
 //    residency at each tile size instead);
-//  * larger copy tables (all-to-all): 16 KiB tiles, 2 tiles per CTA;
+//  * larger copy tables (all-to-all): 16 KiB tiles, 3 tiles per CTA up to
+//    16384 tiles (256 MiB of chunks), 2 above (tools/latency with LAT_MIN /
+//    LAT_STEP: 256 KiB 8.2 -> 6.2 us, 1 MiB 25.8 -> 24.6, 4 MiB 85.6 -> 83.9;
+//    2 per CTA stays 1-2% faster from the headline's 32768 tiles up);
 //  * larger fan tables (all-gather: one read, n writes): 8 KiB tiles, one
 //    tile per CTA.
 // Short-lived CTAs, the hardware block scheduler refilling the SMs, beat a
@@ -452,11 +455,13 @@ int env_int(const char* name, int dflt) {
 struct TmaShape {
   int tile, waves, lag;
   int tpc;  // > 0: ceil(tiles / tpc) CTAs (tiles per CTA) instead of `waves`
+  int tpc_small = 0, small_tiles = 0;  // tables of at most small_tiles tiles: tpc_small per CTA
 };
 struct TmaPolicy {
   bool onewave_res1 = env_int("CECOLL_TMA_ONEWAVE_RES", 1) == 1;
   TmaShape copy{env_int("CECOLL_TMA_TILE", 16384), env_int("CECOLL_TMA_WAVES", 2), env_int("CECOLL_TMA_LAG", 0),
-                env_int("CECOLL_TMA_TPC", 2)};
+                env_int("CECOLL_TMA_TPC", 2), env_int("CECOLL_TMA_TPC_SMALL", 3),
+                env_int("CECOLL_TMA_SMALL_TILES", 16384)};
   TmaShape fan{env_int("CECOLL_TMA_FAN_TILE", 8192), env_int("CECOLL_TMA_FAN_WAVES", 4),
                env_int("CECOLL_TMA_FAN_LAG", 1), env_int("CECOLL_TMA_FAN_TPC", 1)};
   bool fixed = env_int("CECOLL_TMA_FIXED_TILE", 0) == 1;
@@ -523,7 +528,10 @@ int mover_grid_for(const ItemTable& t, int sms) {
     int64_t g = std::max(1, sh.waves) * one_wave;
     // a table that fits one wave keeps one tile per CTA (items_call caps the
     // grid at the tile count); larger ones get ceil(tiles / tpc) CTAs
-    if (sh.tpc > 0 && t.ntiles > one_wave) g = (t.ntiles + sh.tpc - 1) / sh.tpc;
+    if (sh.tpc > 0 && t.ntiles > one_wave) {
+      const int tpc = sh.tpc_small > 0 && t.ntiles <= sh.small_tiles ? sh.tpc_small : sh.tpc;
+      g = (t.ntiles + tpc - 1) / tpc;
+    }
     // fused_finish counts CTAs in 20 bits (flags.cuh): larger tables loop
     g = std::min<int64_t>(g, kMaxGrid);
     return cap > 0 ? std::min<int>(cap, static_cast<int>(g)) : static_cast<int>(g);

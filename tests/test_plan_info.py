@@ -108,6 +108,7 @@ def test_sm_budget_caps_the_grid(comms):
     ("allgather", 65536, 4096, 128, 128),         # 8 fan items: smallest tile leaving <= 1 tile per SM
     ("allgather", 262144, 15360, 144, 144),       # 8 x ceil(256 KiB / 15 KiB) = 144 <= 148
     ("alltoall", 65536, 32768, 128, 128),         # 64 items x 2 tiles already fit one wave
+    ("alltoall", 1 << 20, 16384, 64 * 64, 1366),        # up to 16384 tiles: 3 tiles per CTA
     ("alltoall", 8 << 20, 16384, 64 * 512, 64 * 256),  # the headline: 16 KiB tiles, 2 tiles per CTA
     ("allgather", 8 << 20, 8192, 8 * 1024, 8 * 1024),  # fan: 8 KiB tiles, one tile per CTA
 ])
@@ -115,7 +116,8 @@ def test_tma_tile_size_follows_the_table(comms, kind, s, tile, tiles, grid):
     """kernels.cu table_tile / mover_grid_for: one tile per CTA while the table
     fits one wave of one CTA per SM (a 64 KiB all-gather 8.2 -> 4.1 us per
     collective); above, short-lived CTAs of the table kind's shape (copy: 16
-    KiB tiles, 2 per CTA; fan: 8 KiB tiles, 1 per CTA)."""
+    KiB tiles, 3 per CTA up to 16384 tiles and 2 above; fan: 8 KiB tiles, 1
+    per CTA)."""
     sends, recvs = _bufs(s, kind)
     torch.cuda.synchronize()  # the inputs are written on the default stream
     fn = cc.all_gather if kind == "allgather" else cc.all_to_all

@@ -2,6 +2,7 @@
 // (no Python in the loop): the library's own control cost per collective.
 //
 //   tools/latency [nranks] [iters] [per_rank_streams] [impl-filter]
+//     (env LAT_MIN / LAT_MAX / LAT_STEP: size grid, default 4 KiB..1 MiB x4)
 //     (GPU box; ranks co-resident on GPU 0; per_rank_streams=1 gives every
 //      rank its own stream: one unit per rank, flags between all of them)
 //
@@ -81,6 +82,9 @@ int main(int argc, char** argv) {
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   const size_t max_s = std::getenv("LAT_MAX") ? std::strtoull(std::getenv("LAT_MAX"), nullptr, 0) : size_t(1) << 20;
+  // LAT_MIN / LAT_STEP: first size and multiplier of the size grid (4 KiB, x4)
+  const size_t min_s = std::getenv("LAT_MIN") ? std::strtoull(std::getenv("LAT_MIN"), nullptr, 0) : size_t(4096);
+  const size_t step = std::getenv("LAT_STEP") ? std::strtoull(std::getenv("LAT_STEP"), nullptr, 0) : size_t(4);
   std::vector<void*> send(n), recv(n);
   for (int r = 0; r < n; ++r) {
     CK(cudaMalloc(&send[r], n * max_s));
@@ -91,7 +95,7 @@ int main(int argc, char** argv) {
   const char* names[] = {"sm", "pcpy", "b2b", "bcst", "swap", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_bcst",
                          "prelaunch_swap", "hybrid", "pull"};
   for (int kind = 0; kind < 2; ++kind) {
-    for (size_t s = 4096; s <= max_s; s *= 4) {
+    for (size_t s = min_s; s <= max_s; s *= step) {
       for (const char* name : names) {
         if (!only.empty() && only != name) continue;
         const cecoll_impl_t impl = cecoll_parse_impl(name);
@@ -150,7 +154,7 @@ int main(int argc, char** argv) {
   }
   // Reduce-scatter (bf16 sum, eager collective call): chunk s bytes per rank.
   const char* rs_names[] = {"sm", "pcpy", "b2b", "prelaunch_pcpy"};
-  for (size_t s = 4096; s <= max_s; s *= 4) {
+  for (size_t s = min_s; s <= max_s; s *= step) {
     for (const char* name : rs_names) {
       if (!only.empty() && only != name) continue;
       const cecoll_impl_t impl = cecoll_parse_impl(name);
