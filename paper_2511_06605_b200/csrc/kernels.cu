@@ -536,6 +536,17 @@ int mover_grid_for(const ItemTable& t, int sms) {
     g = std::min<int64_t>(g, kMaxGrid);
     return cap > 0 ? std::min<int>(cap, static_cast<int>(g)) : static_cast<int>(g);
   }
+  // Register mover: one 64 KiB tile per CTA (at least the persistent grid's
+  // CTA count), the TMA mover's finding again: forced onto aligned tables
+  // (CECOLL_MOVER=reg) it goes from 0.83 / 0.91 of the copy peak (all-gather
+  // / all-to-all, 64 MiB chunks, persistent 2 CTAs per SM) to 0.99 / 1.06,
+  // and prelaunch_bcst's broadcast items from 0.86 to 0.99-1.02 at 16-64 MiB
+  // (profiles/reg_shape_r02.txt). Tables with in-place swap items keep the
+  // persistent grid (1-3% faster there). CECOLL_REG_TPC=k sets k tiles per
+  // CTA; 0 restores the persistent grid everywhere.
+  static const int reg_tpc = env_int("CECOLL_REG_TPC", 1);
+  if (reg_tpc > 0 && !(t.kinds & (1 << kItemSwap)))
+    return std::max(mover_grid(t.mover, sms), std::min((t.ntiles + reg_tpc - 1) / reg_tpc, kMaxGrid));
   return mover_grid(t.mover, sms);
 }
 
