@@ -241,6 +241,23 @@ double model_score(const B200Model& m, const std::vector<Measurement>& meas, std
              std::to_string(steps) + " steps)\n";
       penalty += std::max(0.0, steps - 1.0);
     }
+    // The converse (round 2): a transition of the model's grid that the
+    // measured grid does not have within one step is a spurious crossover —
+    // the reference's rule only looks one way, and a fit could flip to a
+    // loser and back between two measured sizes at no cost.
+    for (size_t i = 1; i < ss.size(); ++i) {
+      if (model[i - 1] == model[i]) continue;
+      const int64_t got = boundary(ss, measured, model[i - 1], model[i]);
+      const std::string name = std::string(kind == Kind::AllGather ? "AG" : "AA") + " n=" + std::to_string(n) + " " +
+                               impl_name(model[i - 1]) + "->" + impl_name(model[i]);
+      if (got < 0) {
+        penalty += 4.0;
+        log += "  " + name + ": spurious model transition at " + std::to_string(ss[i]) + "\n";
+        continue;
+      }
+      const double steps = std::abs(std::log2(static_cast<double>(got) / static_cast<double>(ss[i])));
+      penalty += std::max(0.0, steps - 1.0);
+    }
   }
   if (report) *report = log;
   return penalty;
