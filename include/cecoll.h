@@ -211,8 +211,8 @@ cecoll_status_t cecoll_comm_get_async_error(cecoll_comm_t comm, cecoll_status_t*
 cecoll_status_t cecoll_comm_info(cecoll_comm_t comm, int* rank, int* nranks, int* device);
 /* Interference policy (BASELINE configs[4]: a collective beside a GEMM). Plans
  * created after this call — explicit or behind the eager calls — launch at
- * most max_ctas CTAs per mover / reduction kernel (0, the default: a
- * persistent grid of 2 CTAs per SM, fastest alone), and CECOLL_IMPL_AUTO
+ * most max_ctas CTAs per mover / reduction kernel (0, the default: the
+ * movers' own grids, short-lived CTAs, fastest alone), and CECOLL_IMPL_AUTO
  * selects with cecoll_select_budget. Applies to the communicator's whole
  * world; cached plans of another budget are not reused. */
 cecoll_status_t cecoll_comm_set_sm_budget(cecoll_comm_t comm, int max_ctas);
