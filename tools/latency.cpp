@@ -6,7 +6,8 @@
 //     (GPU box; ranks co-resident on GPU 0; per_rank_streams=1 gives every
 //      rank its own stream: one unit per rank, flags between all of them)
 //
-// Prints CSV: api,impl,collective,size_bytes,device_us_b2b,device_us_isolated,host_us
+// Prints CSV: api,impl,collective,size_bytes,device_us_b2b,device_us_isolated (median of 50),host_us,
+// isolated_p10_us,isolated_p90_us (median plus p10 / p90)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -91,7 +92,7 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&recv[r], n * max_s));
     CK(cudaMemset(send[r], r, n * max_s));
   }
-  std::printf("api,impl,collective,size_bytes,device_us_b2b,device_us_isolated,host_us\n");
+  std::printf("api,impl,collective,size_bytes,device_us_b2b,device_us_isolated,host_us,isolated_p10_us,isolated_p90_us\n");
   const char* names[] = {"sm", "pcpy", "b2b", "bcst", "swap", "prelaunch_pcpy", "prelaunch_b2b", "prelaunch_bcst",
                          "prelaunch_swap", "hybrid", "pull"};
   for (int kind = 0; kind < 2; ++kind) {
@@ -128,7 +129,7 @@ int main(int argc, char** argv) {
           float ms_b2b = 0;
           CK(cudaEventElapsedTime(&ms_b2b, e0, e1));
           std::vector<float> iso;
-          for (int i = 0; i < 20; ++i) {
+          for (int i = 0; i < 50; ++i) {
             sync_all();
             CK(cudaEventRecord(e0, stream));
             fork();
@@ -142,9 +143,9 @@ int main(int argc, char** argv) {
           }
           std::sort(iso.begin(), iso.end());
           const double host_us = std::chrono::duration<double, std::micro>(h1 - h0).count() / iters;
-          std::printf("%s,%s,%s,%zu,%.2f,%.2f,%.2f\n", api == 0 ? "plan" : "eager", name,
+          std::printf("%s,%s,%s,%zu,%.2f,%.2f,%.2f,%.2f,%.2f\n", api == 0 ? "plan" : "eager", name,
                       kind == 0 ? "allgather" : "alltoall", s, ms_b2b * 1000 / iters, iso[iso.size() / 2] * 1000,
-                      host_us);
+                      host_us, iso[iso.size() / 10] * 1000, iso[iso.size() * 9 / 10] * 1000);
           std::fflush(stdout);
           if (plan) CC(cecoll_plan_destroy(plan));
           sync_all();
@@ -176,7 +177,7 @@ int main(int argc, char** argv) {
       float ms_b2b = 0;
       CK(cudaEventElapsedTime(&ms_b2b, e0, e1));
       std::vector<float> iso;
-      for (int i = 0; i < 20; ++i) {
+      for (int i = 0; i < 50; ++i) {
         sync_all();
         CK(cudaEventRecord(e0, stream));
         fork();
@@ -190,8 +191,8 @@ int main(int argc, char** argv) {
       }
       std::sort(iso.begin(), iso.end());
       const double host_us = std::chrono::duration<double, std::micro>(h1 - h0).count() / iters;
-      std::printf("eager,%s,reduce_scatter_bf16_sum,%zu,%.2f,%.2f,%.2f\n", name, s, ms_b2b * 1000 / iters,
-                  iso[iso.size() / 2] * 1000, host_us);
+      std::printf("eager,%s,reduce_scatter_bf16_sum,%zu,%.2f,%.2f,%.2f,%.2f,%.2f\n", name, s, ms_b2b * 1000 / iters,
+                  iso[iso.size() / 2] * 1000, host_us, iso[iso.size() / 10] * 1000, iso[iso.size() * 9 / 10] * 1000);
       std::fflush(stdout);
       sync_all();
     }
