@@ -438,7 +438,7 @@ int env_int(const char* name, int dflt) {
 //    one resident CTA per SM counted (CECOLL_TMA_ONEWAVE_RES=0 counts the
 //    residency at each tile size instead);
 //  * larger copy tables (all-to-all): 16 KiB tiles, 3 tiles per CTA up to
-//    16384 tiles (256 MiB of chunks), 2 above (tools/latency with LAT_MIN /
+//    16384 tiles (a 256 MiB table), 2 above (tools/latency with LAT_MIN /
 //    LAT_STEP: 256 KiB 8.2 -> 6.2 us, 1 MiB 25.8 -> 24.6, 4 MiB 85.6 -> 83.9;
 //    2 per CTA stays 1-2% faster from the headline's 32768 tiles up);
 //  * larger fan tables (all-gather: one read, n writes): 8 KiB tiles, one
@@ -503,13 +503,14 @@ int table_tile(Mover m, const std::vector<int64_t>& sizes, int sms, int budget, 
   return clamp_tile(pol.shape(has_fan).tile);
 }
 
-// Register mover: a persistent grid of 2 CTAs per SM. TMA mover: ceil(tiles
-// / tpc) CTAs of the table's shape (TmaPolicy; a one-wave table launches one
-// CTA per tile: items_call caps the grid at the tile count). Beside compute, the mover's SM footprint is a policy: the
-// plan's SM budget (cecoll_comm_set_sm_budget) or CECOLL_SM_GRID=<ctas> caps
-// the grid, CECOLL_SM_TILES_PER_CTA=<k> launches short-lived CTAs of k tiles
-// so the block scheduler can interleave a higher-priority stream's CTAs
-// (profiles/interference_r01.json).
+// Grids. TMA mover: ceil(tiles / tpc) CTAs of the table's shape (TmaPolicy;
+// a one-wave table launches one CTA per tile: items_call caps the grid at the
+// tile count). Register mover: one tile per CTA, or a persistent 2 CTAs per
+// SM for swap tables (mover_grid). Beside compute, the mover's SM footprint
+// is a policy: the plan's SM budget (cecoll_comm_set_sm_budget) or
+// CECOLL_SM_GRID=<ctas> caps the grid, CECOLL_SM_TILES_PER_CTA=<k> launches
+// short-lived CTAs of k tiles so the block scheduler can interleave a
+// higher-priority stream's CTAs (profiles/interference_r01.json).
 int mover_grid(Mover m, int sms) {
   (void)m;
   static const int cap = env_int("CECOLL_SM_GRID", 0);
