@@ -546,7 +546,8 @@ int mover_grid_for(const ItemTable& t, int sms) {
   // persistent grid (1-3% faster there). CECOLL_REG_TPC=k sets k tiles per
   // CTA; 0 restores the persistent grid everywhere.
   static const int reg_tpc = env_int("CECOLL_REG_TPC", 1);
-  if (reg_tpc > 0 && !(t.kinds & (1 << kItemSwap)))
+  static const int reg_cap = env_int("CECOLL_SM_GRID", 0);  // a process-wide cap wins
+  if (reg_tpc > 0 && reg_cap <= 0 && !(t.kinds & (1 << kItemSwap)))
     return std::max(mover_grid(t.mover, sms), std::min((t.ntiles + reg_tpc - 1) / reg_tpc, kMaxGrid));
   return mover_grid(t.mover, sms);
 }
