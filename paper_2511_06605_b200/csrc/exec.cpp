@@ -238,10 +238,17 @@ Status trigger_signal(World* w, Unit& u, cudaEvent_t* span_begin) {
   const int pid = u.ranks[0];
   STATUS_TRY(issue_copies_traced(w, sink, u.precopy, u.stream, u.device, pid, -1));
   MemOps ops = u.start;
-  ops.push_back(op_write(u.ready_flag, 1));
+  // CECOLL_TRIGGER_KERNEL=1: the trigger word is written by a one-thread
+  // signal kernel instead of a stream memory operation (A/B).
+  static const bool kernel_trigger = [] {
+    const char* e = std::getenv("CECOLL_TRIGGER_KERNEL");
+    return e && std::string(e) == "1";
+  }();
+  if (!kernel_trigger) ops.push_back(op_write(u.ready_flag, 1));
   *span_begin = trace_mark(w, u.device, u.stream);
   STATUS_TRY(submit_traced(w, sink, u.stream, ops, u.start_remote_tab, u.start_remote.size(), "trigger:signal",
                            u.device, pid, -1));
+  if (kernel_trigger) STATUS_TRY(sink.kernel(w, u.stream, signal_call(u.ready_tab, 1)));
   set_armed(u, false);
   trace_host_span(w, "trigger", h0);
   return {};

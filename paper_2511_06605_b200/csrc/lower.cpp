@@ -879,6 +879,7 @@ Status build_graph(World* w, Plan* p, Unit& u) {
   uint64_t* words = static_cast<uint64_t*>(d);  // [0] trigger [1] err [2] ticket [3] skip [4] gate [5] epoch [6] seen
   u.err = words + 1;
   u.ready_flag = words;
+  STATUS_TRY(upload_ptrs(p, u.device, {u.ready_flag}, &u.ready_tab));
   void* host = nullptr;
   CUDA_TRY(cudaHostAlloc(&host, 64, cudaHostAllocMapped | cudaHostAllocPortable));
   std::memset(host, 0, 64);

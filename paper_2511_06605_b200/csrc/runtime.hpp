@@ -210,6 +210,7 @@ struct Unit {
   // plans never share one): the caller stream writes 1 to trigger; the gate
   // takes it.
   uint64_t* ready_flag = nullptr;
+  uint64_t** ready_tab = nullptr;  // {ready_flag} in device memory (CECOLL_TRIGGER_KERNEL=1)
   // Cancels: a count in pinned host memory (written by the host, no stream)
   // and its device alias; the gate honours each raise once.
   uint64_t* cancel_host = nullptr;
