@@ -404,8 +404,9 @@ def run_ours(args):
                 "floor_value": round(busbw(n, s, floor_ms / 1e3), 3),
                 "pipeline": "double-buffered: H2D of step k+1 overlaps D2H of step k; one 512 MiB copy per "
                             "direction per step (the ranks' buffers are rows of one [n, n*s] tensor)",
-                "bound_note": "PCIe-bound: 512 MiB host->device and 512 MiB device->host per step over one "
-                              "x16 link. floor_ms is measured in this run: the same bytes copied both ways "
+                "bound_note": "host-bound: 512 MiB host->device and 512 MiB device->host per step over one "
+                              "x16 link, i.e. 1 GiB of host memory traffic per step, the same the CPU arm "
+                              "moves (profiles/host_mem_probe_r02.txt). floor_ms is measured in this run: the same bytes copied both ways "
                               "at once on the same streams with no collective, 6 steps back to back, per "
                               "step (best of 3 loops)"},
         "gpu_launches": int(round((kernels_per_step + 4 * graphs_per_step) * args.steps)),
