@@ -582,6 +582,9 @@ def run(args, B):
         STATE["prefix"] = "experiments-grade sweep: "  # a hang here leaves the main line standing
         sweep_pass(world, rank, dev, nccl, stream, t_start, args, line["sweep"]["rows"], prelaunch=True)
         STATE["prefix"] = ""
+    if not args.no_mgpu_experiments and from_rank0(time.time() - t_start < args.mgpu_budget + 220):
+        STATE["phase"] = "experiments ce share"
+        run_ce_share_experiment(world, rank, dev, line["experiments"])
     if not args.no_mgpu_experiments and from_rank0(time.time() - t_start < args.mgpu_budget + 240):
         STATE["phase"] = "experiments tune"
         run_tune_experiment(world, rank, dev, stream, line["experiments"])
@@ -1125,6 +1128,55 @@ def run_experiments(comms, sets, n, s, my_ranks, stream, out):
                 else:
                     os.environ[k] = v
         out[f"{name}/{kind}"] = res
+
+
+def run_ce_share_experiment(world, rank, dev, out):
+    """Copy-engine sharing over NVLink (the reference models
+    max-min fair flows, sim.cpp:124-179): rank 0 releases k peer copies of
+    64 MiB at once (one stream each) from its GPU to k peers, and k copies to
+    one peer, and records each copy's completion. On the one-GPU boxes the
+    host link serialises same-direction copies (profiles/ce_share_r02.json);
+    this measures the same on NVLink. The other ranks wait at the barrier."""
+    res = {}
+    out["ce_share_nvlink"] = res
+    try:
+        ng = torch.cuda.device_count()
+        if rank == 0 and ng >= 2:
+            n = 64 << 20
+            src = torch.empty(n, dtype=torch.uint8, device=f"cuda:{dev}")
+            cases = {f"{k}_peers": [(dev + 1 + i) % ng for i in range(k)] for k in (1, 2, 4, ng - 1) if k <= ng - 1}
+            cases["4_to_one_peer"] = [(dev + 1) % ng] * 4
+            for name, peers in cases.items():
+                dsts = [torch.empty(n, dtype=torch.uint8, device=f"cuda:{p}") for p in peers]
+                streams = [torch.cuda.Stream(device=dev) for _ in peers]
+                best = None
+                for _ in range(3):
+                    torch.cuda.synchronize(dev)
+                    go = torch.cuda.Event(enable_timing=True)
+                    ends = [torch.cuda.Event(enable_timing=True) for _ in peers]
+                    gate = torch.cuda.Stream(device=dev)
+                    with torch.cuda.stream(gate):
+                        torch.cuda._sleep(2_000_000)
+                        go.record(gate)
+                    for d, s, e in zip(dsts, streams, ends):
+                        s.wait_event(go)
+                        with torch.cuda.stream(s):
+                            d.copy_(src, non_blocking=True)
+                            e.record(s)
+                    for s in streams:
+                        s.synchronize()
+                    t = [go.elapsed_time(e) for e in ends]
+                    if best is None or max(t) < max(best):
+                        best = t
+                res[name] = {"peers": peers, "done_ms": [round(x, 3) for x in best],
+                             "aggregate_gbs": round(len(peers) * n / max(best) / 1e6, 1),
+                             "single_copy_gbs": round(n / min(best) / 1e6, 1)}
+                del dsts
+    except Exception as e:  # noqa: BLE001
+        res["error"] = str(e)[:200]
+    finally:
+        torch.cuda.synchronize()
+        dist.barrier()
 
 
 def run_tune_experiment(world, rank, dev, stream, out):
