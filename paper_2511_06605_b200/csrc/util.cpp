@@ -108,7 +108,7 @@ Status write_device(void* dst, const void* src, size_t bytes) {
 Status issue_copies(World* w, const std::vector<Copy>& copies, cudaStream_t s) {
   // One cudaMemcpyAsync per copy: a b2b lane's n-1 copies go out back to back
   // on its stream (the driver's batched-copy entry point is not used: it
-  // faulted the GPU on this pool, profiles/README.md).
+  // faulted GPUs on the round-2 pool).
   for (const Copy& c : copies) {
     CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, static_cast<size_t>(c.bytes), cudaMemcpyDefault, s));
     ++w->counters[kCtrCopies];
