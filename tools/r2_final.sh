@@ -9,4 +9,4 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${ta
 timeout 500 python bench.py > gpurun_out/${tag}_bench.log 2>&1; echo bench=$? >> gpurun_out/${tag}_bench.log
 timeout 500 python bench.py --impl reference > gpurun_out/${tag}_ref.log 2>&1; echo ref=$? >> gpurun_out/${tag}_ref.log
 tail -n 2 gpurun_out/${tag}_tests.log; tail -n 2 gpurun_out/${tag}_smoke.log; grep '^{' gpurun_out/${tag}_bench.log | cut -c1-300; tail -n 1 gpurun_out/${tag}_ref.log
-[ -z "$SKIP_MEASURE" ] && bash tools/r2_measure.sh ${tag}
+if [ -z "$SKIP_MEASURE" ]; then bash tools/r2_measure.sh ${tag}; fi
