@@ -130,3 +130,25 @@ def test_tma_tile_size_follows_the_table(comms, kind, s, tile, tiles, grid):
              for i in range(N) for j in range(N))
     assert ok
     torch.cuda.synchronize()
+
+
+def test_grid_cap_loops_over_the_remaining_tiles(comms):
+    """A table of more tiles than kMaxGrid CTAs (2^19: fused_finish counts CTAs
+    in 20 bits) launches the capped grid and every CTA loops over its further
+    tiles: an all-gather of 1 GiB chunks is 2^20 fan tiles of 8 KiB."""
+    s = 1 << 30
+    sends = [torch.randint(0, 256, (s,), dtype=torch.uint8, device="cuda") for _ in range(N)]
+    recvs = [torch.empty(N * s, dtype=torch.uint8, device="cuda") for _ in range(N)]
+    try:
+        torch.cuda.synchronize()
+        cc.all_gather(comms, sends, recvs, s, impl="sm", streams=torch.cuda.Stream())
+        torch.cuda.synchronize()
+        u = comms[0].last_plan_info()["units"][0]
+        assert u["tiles"] == 8 * (s // 8192) and u["grid"] == 1 << 19, u
+        for j in range(N):
+            for i in range(N):
+                assert torch.equal(recvs[j][i * s:(i + 1) * s], sends[i]), (i, j)
+    finally:
+        del sends, recvs
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
