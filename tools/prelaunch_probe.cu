@@ -418,6 +418,47 @@ int main(int argc, char** argv) {
                hus(t0, t1));
     }
   }
+  // (b2) two gated graphs alternating on two arm streams (own ready words):
+  // the instance for collective i+1 is already spinning while i runs.
+  {
+    cudaStream_t as2;
+    CK(cudaStreamCreateWithFlags(&as2, cudaStreamNonBlocking));
+    cudaStream_t arm[2] = {as, as2};
+    uint64_t* rdy[2] = {ready, words + 48};
+    cudaEvent_t gd[2];
+    CK(cudaEventCreateWithFlags(&gd[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&gd[1], cudaEventDisableTiming));
+    cudaGraphExec_t ge[2];
+    for (int k = 0; k < 2; ++k) {
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(arm[k], cudaStreamCaptureModeRelaxed));
+      gate<<<1, 32, 0, arm[k]>>>(rdy[k]);
+      mover<<<grid, 512, 0, arm[k]>>>(src, dst, nvec);
+      CK(cudaStreamEndCapture(arm[k], &g));
+      CK(cudaGraphInstantiate(&ge[k], g, 0));
+    }
+    for (int rep = 0; rep < 2; ++rep) {
+      reset();
+      for (int k = 0; k < 2; ++k) {
+        CK(cudaGraphLaunch(ge[k], arm[k]));
+        CK(cudaEventRecord(gd[k], arm[k]));
+      }
+      CK(cudaEventRecord(e0, cs));
+      auto t0 = clk::now();
+      for (int i = 0; i < iters; ++i) {
+        const int k = i & 1;
+        CD(cuStreamWriteValue64(cs, reinterpret_cast<CUdeviceptr>(rdy[k]), 1, 0));
+        CK(cudaStreamWaitEvent(cs, gd[k], 0));
+        if (i + 2 < iters) {
+          CK(cudaGraphLaunch(ge[k], arm[k]));
+          CK(cudaEventRecord(gd[k], arm[k]));
+        }
+      }
+      auto t1 = clk::now();
+      CK(cudaEventRecord(e1, cs));
+      if (rep) report("(b2) two gated graphs alternating", hus(t0, t1));
+    }
+  }
   // (d) self-gated mover (one kernel per collective), caller memop write +
   // memop wait
   for (int rep = 0; rep < 2; ++rep) {
