@@ -1,6 +1,7 @@
 """The C ABI driven from C++ alone across processes (tools/mp_selftest.cpp):
 forked processes exchange blobs through shared memory, register a
-library-owned window and run every implementation, byte-checked."""
+library-owned window and run every implementation, byte-checked, then run
+cecoll_tune and check that every process installed the same table."""
 import os
 import shutil
 import subprocess
@@ -31,4 +32,5 @@ def test_cpp_processes_every_implementation(nprocs, chunk):
     r = subprocess.run([EXE, str(nprocs), str(chunk)], capture_output=True, text=True, timeout=500)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "all implementations bit-exact" in r.stdout
-    assert r.stdout.count("PASS") >= 14 and "FAIL" not in r.stdout
+    assert r.stdout.count("PASS") >= 15 and "FAIL" not in r.stdout
+    assert "tune      same table      PASS" in r.stdout  # cecoll_tune from C, agreed across processes

@@ -15,6 +15,7 @@
 #include <unistd.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -137,6 +138,32 @@ int child(Ctx c, int64_t s) {
       }
       failures += ok ? 0 : 1;
     }
+  }
+  // Measured selection from C (cecoll_tune, csrc/tune.cpp): every process
+  // must install the same table (times agreed through the exchange).
+  {
+    bool ok = cecoll_tune(&comm, 1, 65536, nullptr) == CECOLL_SUCCESS;
+    std::string table;
+    if (ok) {
+      size_t len = 0;
+      cecoll_tune_table(comm, nullptr, 0, &len);
+      table.assign(len, '\0');
+      cecoll_tune_table(comm, &table[0], len, &len);
+      table.resize(std::strlen(table.c_str()));
+    } else {
+      std::fprintf(stderr, "rank %d: tune: %s\n", c.rank, cecoll_last_error());
+    }
+    uint64_t h = 1469598103934665603ull;  // FNV-1a of the table text
+    for (char ch : table) h = (h ^ static_cast<uint8_t>(ch)) * 1099511628211ull;
+    std::vector<uint64_t> all(static_cast<size_t>(n));
+    exchange(&c, &h, sizeof(h), all.data());
+    for (uint64_t x : all) ok &= x == all[0];
+    ok &= std::count(table.begin(), table.end(), '\n') == 6;  // 4, 16, 64 KiB for both collectives
+    if (c.rank == 0) {
+      std::printf("%-9s %-15s %s\n", "tune", "same table", ok ? "PASS" : "FAIL");
+      std::fflush(stdout);
+    }
+    failures += ok ? 0 : 1;
   }
   CK(cudaStreamDestroy(stream));
   cecoll_mem_free(comm, win);
