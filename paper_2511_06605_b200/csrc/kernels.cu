@@ -222,8 +222,11 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 // after the current stores are issued (wait_group.read 1), so one tile's
 // stores are always in flight while the next load is issued.
 template <int kLag>
+// opts: bit 0 L2 evict-first, bit 1 a swap table (every item kItemSwap: a
+// stage holds both sides of the exchange, tile_bytes each, and its stores
+// write them crosswise).
 __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict__ items, int nitems, int ntiles,
-                                                          int tile_bytes, int uniform, int evict_first,
+                                                          int tile_bytes, int uniform, int opts,
                                                           FlagSet flags) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
@@ -243,6 +246,8 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
   for (int i = 0; i < kTmaStages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[i])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 
+  const bool swp = opts & 2;
+  const int stride = swp ? 2 * tile_bytes : tile_bytes;  // bytes of ring per stage
   const int mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   int cur = uniform ? 0 : find_item(first, nitems, blockIdx.x);
   // Tile k of this CTA is global tile blockIdx.x + k * gridDim.x.
@@ -264,19 +269,28 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
   // the bench step (profiles/tma_hint_ab_r01.txt), so evict-normal is the
   // default; CECOLL_TMA_EVICT_FIRST=1 selects evict-first.
   uint64_t policy;
-  if (evict_first)
+  if (opts & 1)
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
   else
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
-  auto load = [&](int stage, const char* src, uint32_t bytes) {
+  // src2: the other side of a swap item (loaded behind src in the stage)
+  auto load = [&](int stage, const char* src, uint32_t bytes, const char* src2) {
     const uint32_t bar = smem_addr(&full[stage]);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(swp ? 2 * bytes : bytes)
+                 : "memory");
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
-            "r"(smem_addr(ring + stage * tile_bytes)),
+            "r"(smem_addr(ring + stage * stride)),
         "l"(src), "r"(bytes), "r"(bar), "l"(policy)
         : "memory");
+    if (swp)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+              "r"(smem_addr(ring + stage * stride + tile_bytes)),
+          "l"(src2), "r"(bytes), "r"(bar), "l"(policy)
+          : "memory");
   };
+  auto other = [&](int item, int64_t off) -> const char* { return swp ? items[item].dst + off : nullptr; };
   int sitem[kTmaStages];
   int64_t soff[kTmaStages];
   uint32_t nbytes[kTmaStages];
@@ -284,7 +298,7 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
   for (; issued < kTmaStages && issued < mine; ++issued) {
     const char* src;
     locate(issued, &src, &sitem[issued], &soff[issued], &nbytes[issued]);
-    load(issued, src, nbytes[issued]);
+    load(issued, src, nbytes[issued], other(sitem[issued], soff[issued]));
   }
   uint32_t phase = 0;
   for (int k = 0; k < mine; ++k) {
@@ -297,11 +311,16 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
         : "memory");
     phase ^= 1u << st;
     const Item& it = items[sitem[st]];
-    const uint32_t from = smem_addr(ring + st * tile_bytes);
+    const uint32_t from = smem_addr(ring + st * stride);
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
                      it.dst + soff[st]),
                  "r"(from), "r"(nbytes[st]), "l"(policy)
                  : "memory");
+    if (swp)  // the exchange's other half: what was at dst goes to src
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                       const_cast<char*>(it.src) + soff[st]),
+                   "r"(from + tile_bytes), "r"(nbytes[st]), "l"(policy)
+                   : "memory");
     if (it.kind == kItemFan)
       for (int f = 1; f < it.nfan; ++f)
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
@@ -315,7 +334,7 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         const char* src;
         locate(issued, &src, &sitem[st], &soff[st], &nbytes[st]);
-        load(st, src, nbytes[st]);
+        load(st, src, nbytes[st], other(sitem[st], soff[st]));
         ++issued;
       }
     } else if (k >= 1 && issued < mine) {
@@ -326,7 +345,7 @@ __global__ void __launch_bounds__(32, 1) tma_items_kernel(const Item* __restrict
       asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       const char* src;
       locate(issued, &src, &sitem[pst], &soff[pst], &nbytes[pst]);
-      load(pst, src, nbytes[pst]);
+      load(pst, src, nbytes[pst], other(sitem[pst], soff[pst]));
       ++issued;
     }
   }
@@ -482,9 +501,21 @@ int tma_resident(int tile) {
   return per < 1 ? 1 : (per > 32 ? 32 : per);
 }
 
-int table_tile(Mover m, const std::vector<int64_t>& sizes, int sms, int budget, bool has_fan) {
+int table_tile(Mover m, const std::vector<int64_t>& sizes, int sms, int budget, bool has_fan, bool swap) {
   if (m != Mover::Tma) return static_cast<int>(kRegTile);
   const TmaPolicy& pol = tma_policy();
+  if (swap) {
+    // a stage holds both sides: the tile is half the copy tables' ring stage
+    // (one-wave tables: the smallest tile leaving one tile per CTA, as below)
+    for (int t = 4096; t <= kTmaTile / 2; t += 1024) {
+      int64_t slots = int64_t{pol.onewave_res1 ? 1 : tma_resident(2 * t)} * sms;
+      if (budget > 0) slots = std::min<int64_t>(slots, budget);
+      int64_t n = 0;
+      for (int64_t b : sizes) n += (b + t - 1) / t;
+      if (n <= slots) return t;
+    }
+    return budget > 0 ? kTmaTile / 2 : std::min(kTmaTile / 2, clamp_tile(pol.copy.tile) / 2);
+  }
   if (pol.fixed) return kTmaTile;
   // The smallest tile (1 KiB steps, at least 4 KiB) that still gives every
   // resident CTA at most one tile: at these sizes parallelism wins over
@@ -523,7 +554,7 @@ int mover_grid_for(const ItemTable& t, int sms) {
   if (t.mover == Mover::Tma) {
     static const int cap = env_int("CECOLL_SM_GRID", 0);
     const TmaPolicy& pol = tma_policy();
-    const int tile = t.tile > 0 ? t.tile : kTmaTile;
+    const int tile = (t.tile > 0 ? t.tile : kTmaTile) * (t.kinds == (1 << kItemSwap) ? 2 : 1);
     const TmaShape& sh = pol.shape(t.kinds & (1 << kItemFan));
     const int64_t one_wave = int64_t{tma_resident(tile)} * sms;
     int64_t g = std::max(1, sh.waves) * one_wave;
@@ -577,15 +608,16 @@ KernelCall items_call(const ItemTable& t, int grid, const FlagSet* fp) {
       return e ? std::atoi(e) : 0;
     }();
     const bool lag = tma_policy().shape(t.kinds & (1 << kItemFan)).lag == 1;
+    const bool swp = t.kinds == (1 << kItemSwap);
     k.func = lag ? reinterpret_cast<const void*>(tma_items_kernel<1>) : reinterpret_cast<const void*>(tma_items_kernel<0>);
     k.block = dim3(32);
-    k.smem = kTmaStages * (t.tile > 0 ? t.tile : kTmaTile);
+    k.smem = kTmaStages * (t.tile > 0 ? t.tile : kTmaTile) * (swp ? 2 : 1);
     k.push(static_cast<const Item*>(t.items));
     k.push(t.nitems);
     k.push(t.ntiles);
     k.push(t.tile > 0 ? t.tile : kTmaTile);
     k.push(t.uniform);
-    k.push(evict_first);
+    k.push((evict_first ? 1 : 0) | (swp ? 2 : 0));
     k.push(fp ? *fp : FlagSet{});
     return k;
   }

@@ -64,9 +64,10 @@ constexpr int kMaxFan = 32;
 // Which kernel moves a table:
 //  Reg: 512-thread CTAs, 64 KiB tiles staged through registers (eight 16-byte
 //       loads in flight per thread), any alignment, any item kind.
-//  Tma: copy / fan tables whose items are 16-byte aligned with sizes that
-//       are multiples of 16: one elected thread per CTA streams 4-32 KiB
-//       tiles through a 4-stage shared-memory ring with cp.async.bulk
+//  Tma: copy / fan tables and pure swap tables whose items are 16-byte
+//       aligned with sizes that are multiples of 16: one elected thread per
+//       CTA streams 4-32 KiB tiles (swap: both sides of a 4-16 KiB exchange
+//       per stage) through a 4-stage shared-memory ring with cp.async.bulk
 //       (global->shared on an mbarrier, shared->global as a bulk group; a
 //       fan tile is loaded once and stored once per destination).
 enum class Mover : int { Reg = 0, Tma = 1 };
@@ -92,7 +93,8 @@ int64_t mover_tile_bytes(Mover m);
 // 64 KiB tiles; the TMA mover the smallest tile (4-32 KiB) that leaves at
 // most one tile per resident CTA, else its streaming tile (kernels.cu
 // TmaPolicy; 32 KiB under a budget).
-int table_tile(Mover m, const std::vector<int64_t>& sizes, int sms, int budget = 0, bool has_fan = false);
+int table_tile(Mover m, const std::vector<int64_t>& sizes, int sms, int budget = 0, bool has_fan = false,
+               bool swap = false);
 // CTAs of the TMA mover resident per SM when its ring holds `tile`-byte stages.
 int tma_resident(int tile);
 // Tiles of one item of `bytes` at `tile` bytes per tile.

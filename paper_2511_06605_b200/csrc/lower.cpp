@@ -77,10 +77,14 @@ Status upload_items(Plan* p, int device, std::vector<HostItem>& host, ItemTable*
     kinds |= 1 << it.kind;
     uintptr_t a = reinterpret_cast<uintptr_t>(it.src) | reinterpret_cast<uintptr_t>(it.dst);
     for (char* f : h.fan) a |= reinterpret_cast<uintptr_t>(f);
-    tma &= (it.kind == kItemCopy || it.kind == kItemFan) && (a & 15) == 0 && (it.bytes & 15) == 0 &&
-           (!h.remote || peer_tma);
+    tma &= (it.kind == kItemCopy || it.kind == kItemFan || it.kind == kItemSwap) && (a & 15) == 0 &&
+           (it.bytes & 15) == 0 && (!h.remote || peer_tma);
     nfan += h.fan.size();
   }
+  // Swap items take the TMA mover only as a pure swap table (a stage holds
+  // both sides of the exchange); CECOLL_TMA_SWAP=0 keeps them on registers.
+  const char* ts = std::getenv("CECOLL_TMA_SWAP");
+  if ((kinds & (1 << kItemSwap)) && (kinds != (1 << kItemSwap) || (ts && std::string(ts) == "0"))) tma = false;
   const char* env = std::getenv("CECOLL_MOVER");
   if (env && std::string(env) == "reg") tma = false;
   out->mover = tma ? Mover::Tma : Mover::Reg;
@@ -98,7 +102,8 @@ Status upload_items(Plan* p, int device, std::vector<HostItem>& host, ItemTable*
   }
   std::vector<int64_t> sizes;
   for (const HostItem& h : host) sizes.push_back(h.item.bytes);
-  out->tile = table_tile(out->mover, sizes, p->sms, p->sm_budget, (kinds & (1 << kItemFan)) != 0);
+  out->tile = table_tile(out->mover, sizes, p->sms, p->sm_budget, (kinds & (1 << kItemFan)) != 0,
+                         kinds == (1 << kItemSwap));
   std::vector<Item> items;
   int64_t tiles = 0;
   size_t fan_at = 0;
