@@ -245,8 +245,17 @@ double model_score(const B200Model& m, const std::vector<Measurement>& meas, std
     // measured grid does not have within one step is a spurious crossover —
     // the reference's rule only looks one way, and a fit could flip to a
     // loser and back between two measured sizes at no cost.
+    auto tied = [&](size_t idx, Impl c) {  // c within kTie of the measured best at ss[idx]
+      const auto& row = grid[{kv.first.first, n, ss[idx]}];
+      double best = 1e300;
+      for (const auto& e : row) best = std::min(best, e.second);
+      return row.count(c) && row.at(c) <= kTie * best;
+    };
     for (size_t i = 1; i < ss.size(); ++i) {
       if (model[i - 1] == model[i]) continue;
+      // switching between two implementations the measurements tie on (either
+      // side of the switch) is a tie resolution, not a crossover
+      if (tied(i - 1, model[i]) || tied(i, model[i - 1])) continue;
       const int64_t got = boundary(ss, measured, model[i - 1], model[i]);
       const std::string name = std::string(kind == Kind::AllGather ? "AG" : "AA") + " n=" + std::to_string(n) + " " +
                                impl_name(model[i - 1]) + "->" + impl_name(model[i]);
